@@ -1,0 +1,123 @@
+/*
+ * fzb200.h -- C ABI of the B200 (sm_100a) FZModules hot path.
+ *
+ * Plain pointers, sizes and a cudaStream_t passed as void*; no torch types.
+ * Every entry point is asynchronous on `stream` and returns 0 or a negative
+ * FZB_E_* launch/argument error.  Data-dependent failures (corrupt streams,
+ * malformed codes, ...) are OR-ed as FZB_ERR_* bits into a caller-provided
+ * device status word (uint32_t*), which the host reads once per pipeline
+ * run and maps 1:1 onto the reference's FZError classes.
+ *
+ * Each function names the reference routine it replaces (fzpipe,
+ * /root/reference/pkg/src/fzpipe).  The reference is Python + numba; these
+ * are the calls its stage dispatchers (pipeline.py:269-297, 415-436) would
+ * bind through ctypes -- see INTEGRATION.md.
+ *
+ * Device layout conventions: quantization codes are u16 (radius <= 32768,
+ * the bitshuffle limit of encode.py:336-337); outlier flags are a u32
+ * bitmap with bit (t & 31) of word t >> 5; eb_abs lives in device memory
+ * (double*) so no host sync is needed between min/max and the predictor.
+ */
+#ifndef FZB200_H
+#define FZB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FZB_API __attribute__((visibility("default")))
+
+/* negative return codes (argument / launch errors) */
+#define FZB_E_WORKSPACE (-1001) /* workspace too small */
+#define FZB_E_RADIUS (-1002)    /* radius outside [1, 32768] (RadiusTooLarge) */
+#define FZB_E_ARG (-1003)       /* invalid argument */
+
+FZB_API int fzb_abi_version(void);
+
+/* ---- a1: bound resolution (pipeline.py:360-364, core.py:155-170) ------- */
+/* Exact f32 min/max of d_in[0..n) -> d_lohi[0..1]; sets FZB_ERR_NONFINITE. */
+FZB_API size_t fzb_minmax_workspace_bytes(uint64_t n);
+FZB_API int fzb_minmax_f32(const float *d_in, uint64_t n, float *d_lohi, void *d_ws, size_t ws_bytes,
+                           uint32_t *d_status, void *stream);
+/* d_eb = eb_mode ? magnitude * (hi - lo) : magnitude, in f64 exactly as core.py:167. */
+FZB_API int fzb_resolve_bound(const float *d_lohi, int eb_mode, double magnitude, double *d_eb, void *stream);
+
+/* ---- a2-a4: Lorenzo (predict.py:93-144, 221-253) ------------------------ */
+FZB_API size_t fzb_lorenzo_workspace_bytes(uint32_t n0, uint32_t n1, uint32_t n2);
+/* codes u16[n]; d_bitmap u32[ceil(n/32)] zeroed by caller; outliers set bits. */
+FZB_API int fzb_lorenzo_encode_f32(const float *d_in, uint32_t n0, uint32_t n1, uint32_t n2, const double *d_eb,
+                                   uint32_t radius, uint16_t *d_codes, uint32_t *d_bitmap, void *d_ws,
+                                   size_t ws_bytes, void *stream);
+/* d_recon holds the outlier values (fzb_outlier_scatter) and is completed in place. */
+FZB_API int fzb_lorenzo_decode_f32(const uint16_t *d_codes, const uint32_t *d_bitmap, float *d_recon, uint32_t n0,
+                                   uint32_t n1, uint32_t n2, const double *d_eb, uint32_t radius, void *d_ws,
+                                   size_t ws_bytes, void *stream);
+
+/* ---- a5-a6: G-Interp (predict.py:147-201, 270-344) ---------------------- */
+/* d_recon: f32[n] workspace (encode) / output (decode); d_anchors f32[prod((d-1)/stride+1)]. */
+FZB_API int fzb_interp_encode_f32(const float *d_in, uint32_t n0, uint32_t n1, uint32_t n2, const double *d_eb,
+                                  uint32_t radius, uint32_t anchor_stride, const double *h_weights4,
+                                  uint16_t *d_codes, float *d_recon, uint32_t *d_bitmap, float *d_anchors,
+                                  void *stream);
+FZB_API int fzb_interp_decode_f32(const uint16_t *d_codes, const uint32_t *d_bitmap, const float *d_anchors,
+                                  float *d_recon, uint32_t n0, uint32_t n1, uint32_t n2, const double *d_eb,
+                                  uint32_t radius, uint32_t anchor_stride, const double *h_weights4, void *stream);
+
+/* ---- outliers (predict.py:212-214, pipeline.py:300-304, 402-412) ------- */
+FZB_API size_t fzb_outlier_workspace_bytes(uint64_t n);
+/* bitmap -> sorted u64 indices + f32 values (gathered from d_in); *d_count = k. */
+FZB_API int fzb_outlier_compact(const uint32_t *d_bitmap, uint64_t n, const float *d_in, uint64_t *d_idx,
+                                float *d_vals, uint64_t *d_count, void *d_ws, size_t ws_bytes, void *stream);
+/* Scatter k outliers into d_recon + d_bitmap (zeroed by caller) and check the
+ * QuantOutput invariants (core.py:207-215) against d_codes. */
+FZB_API int fzb_outlier_scatter(const uint64_t *d_idx, const float *d_vals, uint64_t k, uint64_t n,
+                                const uint16_t *d_codes, uint32_t radius, float *d_recon, uint32_t *d_bitmap,
+                                uint32_t *d_status, void *stream);
+
+/* ---- a7: histogram (encode.py:79-111) ----------------------------------- */
+/* d_bins u64[nbins] is zeroed here; codes >= nbins set FZB_ERR_CODE_RANGE. */
+FZB_API int fzb_histogram(const uint16_t *d_codes, uint64_t n, uint32_t nbins, uint64_t *d_bins,
+                          uint32_t *d_status, void *stream);
+
+/* ---- a8: codebook (encode.py:118-217) ----------------------------------- */
+FZB_API size_t fzb_huffman_build_workspace_bytes(uint32_t nsym);
+/* Length-limited (32) package-merge with the reference's tie-breaking,
+ * canonical codewords, and d_bit_count = sum(bins * len). */
+FZB_API int fzb_huffman_build(const uint64_t *d_bins, uint32_t nsym, uint8_t *d_lengths, uint32_t *d_codewords,
+                              uint64_t *d_bit_count, void *d_ws, size_t ws_bytes, void *stream);
+
+/* ---- a9: Huffman encode (encode.py:220-231, 279-291) -------------------- */
+FZB_API size_t fzb_huffman_encode_workspace_bytes(uint64_t n);
+/* MSB-first stream written as d_out bytes (capacity out_cap >= ceil(bits/8)
+ * rounded up to 4); sets FZB_ERR_HF_MISMATCH if the packed length differs
+ * from *d_bit_count. */
+FZB_API int fzb_huffman_encode(const uint16_t *d_codes, uint64_t n, const uint8_t *d_lengths,
+                               const uint32_t *d_codewords, uint32_t nsym, const uint64_t *d_bit_count,
+                               uint8_t *d_out, uint64_t out_cap, void *d_ws, size_t ws_bytes, uint32_t *d_status,
+                               void *stream);
+
+/* ---- a10: Huffman decode (encode.py:234-317) ----------------------------- */
+FZB_API size_t fzb_huffman_decode_workspace_bytes(uint64_t nbytes, uint32_t nsym);
+FZB_API int fzb_huffman_decode(const uint8_t *d_stream, uint64_t nbytes, uint64_t n, const uint8_t *d_lengths,
+                               uint32_t nsym, uint16_t *d_codes, void *d_ws, size_t ws_bytes, uint32_t *d_status,
+                               void *stream);
+
+/* ---- a11-a12: bitshuffle (encode.py:324-391) ----------------------------- */
+FZB_API size_t fzb_bitshuffle_workspace_bytes(uint64_t n);
+/* d_bitmap: nblocks*16 bytes; d_payload: capacity nblocks*128 words; *d_nwords = payload words. */
+FZB_API int fzb_bitshuffle_encode(const uint16_t *d_codes, uint64_t n, uint8_t *d_bitmap, uint32_t *d_payload,
+                                  uint64_t *d_nwords, void *d_ws, size_t ws_bytes, void *stream);
+FZB_API int fzb_bitshuffle_decode(const uint8_t *d_bitmap, const uint32_t *d_payload, uint64_t payload_words,
+                                  uint64_t n, uint32_t radius, uint16_t *d_codes, void *d_ws, size_t ws_bytes,
+                                  uint32_t *d_status, void *stream);
+
+/* ---- utilities ----------------------------------------------------------- */
+FZB_API int fzb_fill_u16(uint16_t *d_dst, uint64_t n, uint16_t value, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FZB200_H */

@@ -1,0 +1,663 @@
+// huffman.cu -- canonical, length-limited Huffman codec for sm_100a.
+//
+// Reference: fzpipe encode.py:118-317.
+//  * build: package-merge (limit 32) with the reference's (weight, symbol)
+//    tie-breaking (encode.py:174-213), run by one CTA.  Coin trees are not
+//    materialised: every merged list's selected items form a prefix, so a
+//    leaf's length is the number of levels whose selected prefix contains
+//    it; only "is this merged slot a leaf" bytes per level are stored.
+//    Each level's merge is done by parallel rank search (merge path) when
+//    the package list is sorted by (weight, tiebreak) -- it always was in
+//    every histogram we tried -- with a serial two-head merge fallback that
+//    reproduces heapq.merge exactly otherwise.
+//  * encode: per-thread bit lengths -> CTA totals -> scan -> every thread
+//    writes its big-endian 32-bit words (interior words with plain stores,
+//    the two boundary words with atomicOr), i.e. the MSB-first byte stream
+//    of encode.py:220-231.
+//  * decode: the single unchunked stream (no sync index) is decoded with a
+//    self-synchronising scheme: 1024-bit subsequences, iterate "start =
+//    end of predecessor" to a fixed point (Huffman codes resynchronise in a
+//    few bits), scan the symbol counts, then decode+write.  A 12-bit LUT
+//    short-cuts the canonical first_code/limit walk of encode.py:234-276;
+//    truncation / invalid-code / trailing / padding checks reproduce
+//    encode.py:299-316 exactly.
+#include "common.cuh"
+
+namespace {
+
+constexpr int MAXLEN = 32;
+constexpr int BT = 1024;  // build threads
+
+struct BuildWS {
+    unsigned long long *bw, *pw, *mw;  // base / packages / merged weights
+    uint32_t *bs, *pt, *mt;            // base symbols / package tiebreaks / merged tiebreaks
+    uint8_t* isbase;                   // [MAXLEN][2m] leaf marks per merged list
+};
+
+FZB_DEV bool key_less(unsigned long long wa, uint32_t ta, unsigned long long wb, uint32_t tb) {
+    return wa < wb || (wa == wb && ta < tb);
+}
+
+__global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long long* __restrict__ bins, uint32_t nsym,
+                                                           uint8_t* __restrict__ lengths, uint32_t* __restrict__ cw,
+                                                           unsigned long long* __restrict__ bit_count, BuildWS ws) {
+    __shared__ uint32_t tmp[33];
+    __shared__ unsigned long long tmp64[33];
+    __shared__ uint32_t s_m, s_unsorted;
+    __shared__ long long s_nb[MAXLEN + 1];
+    __shared__ uint32_t s_cnt[MAXLEN + 1];
+    __shared__ unsigned long long s_first[MAXLEN + 1];
+    const int tid = threadIdx.x;
+
+    // 1. compact used symbols (symbol order) and zero outputs
+    uint32_t carry = 0;
+    for (uint32_t s0 = 0; s0 < nsym; s0 += BT) {
+        const uint32_t s = s0 + tid;
+        const bool used = s < nsym && bins[s] != 0;
+        if (s < nsym) { lengths[s] = 0; cw[s] = 0; }
+        uint32_t tot;
+        const uint32_t p = block_exclusive_scan(used ? 1u : 0u, tmp, &tot);
+        if (used) { ws.bw[carry + p] = bins[s]; ws.bs[carry + p] = s; }
+        carry += tot;
+    }
+    if (tid == 0) s_m = carry;
+    __syncthreads();
+    const uint32_t m = s_m;
+    if (m == 0) {
+        if (tid == 0) *bit_count = 0;
+        return;
+    }
+    if (m == 1) {
+        if (tid == 0) {
+            lengths[ws.bs[0]] = 1;
+            cw[ws.bs[0]] = 0;
+            *bit_count = ws.bw[0];
+        }
+        return;
+    }
+    // 2. bitonic sort of (w, s) over the next power of two (pad = max key)
+    uint32_t np2 = 1;
+    while (np2 < m) np2 <<= 1;
+    for (uint32_t q = m + tid; q < np2; q += BT) { ws.bw[q] = ~0ull; ws.bs[q] = 0xFFFFFFFFu; }
+    __syncthreads();
+    for (uint32_t k = 2; k <= np2; k <<= 1)
+        for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+            for (uint32_t q = tid; q < np2; q += BT) {
+                const uint32_t ixj = q ^ jj;
+                if (ixj > q) {
+                    const bool up = (q & k) == 0;
+                    const unsigned long long wa = ws.bw[q], wb = ws.bw[ixj];
+                    const uint32_t ta = ws.bs[q], tb2 = ws.bs[ixj];
+                    const bool gt = key_less(wb, tb2, wa, ta);
+                    if (gt == up) {
+                        ws.bw[q] = wb; ws.bs[q] = tb2;
+                        ws.bw[ixj] = wa; ws.bs[ixj] = ta;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    // 3. levels.  M_0 = base.
+    for (uint32_t q = tid; q < m; q += BT) { ws.mw[q] = ws.bw[q]; ws.mt[q] = ws.bs[q]; ws.isbase[q] = 1; }
+    uint32_t mlen = m;
+    __syncthreads();
+    for (int l = 1; l < MAXLEN; l++) {
+        const uint32_t npk = mlen / 2;
+        for (uint32_t q = tid; q < npk; q += BT) {
+            ws.pw[q] = ws.mw[2 * q] + ws.mw[2 * q + 1];
+            ws.pt[q] = ws.mt[2 * q];
+        }
+        if (tid == 0) s_unsorted = 0;
+        __syncthreads();
+        for (uint32_t q = tid; q + 1 < npk; q += BT)
+            if (key_less(ws.pw[q + 1], ws.pt[q + 1], ws.pw[q], ws.pt[q])) s_unsorted = 1;
+        __syncthreads();
+        uint8_t* ib = ws.isbase + (size_t)l * 2 * m;
+        if (!s_unsorted) {
+            for (uint32_t q = tid; q < m; q += BT) {  // base item q: count packages < it
+                const unsigned long long w = ws.bw[q];
+                const uint32_t t = ws.bs[q];
+                uint32_t lo = 0, hi = npk;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (key_less(ws.pw[mid], ws.pt[mid], w, t)) lo = mid + 1; else hi = mid;
+                }
+                ws.mw[q + lo] = w; ws.mt[q + lo] = t; ib[q + lo] = 1;
+            }
+            for (uint32_t q = tid; q < npk; q += BT) {  // package q: count bases < it
+                const unsigned long long w = ws.pw[q];
+                const uint32_t t = ws.pt[q];
+                uint32_t lo = 0, hi = m;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (key_less(ws.bw[mid], ws.bs[mid], w, t)) lo = mid + 1; else hi = mid;
+                }
+                ws.mw[q + lo] = w; ws.mt[q + lo] = t; ib[q + lo] = 0;
+            }
+        } else if (tid == 0) {  // heapq.merge(base, level): two heads, base first unless package < base
+            uint32_t i = 0, j = 0, o = 0;
+            while (i < m || j < npk) {
+                if (j >= npk || (i < m && !key_less(ws.pw[j], ws.pt[j], ws.bw[i], ws.bs[i]))) {
+                    ws.mw[o] = ws.bw[i]; ws.mt[o] = ws.bs[i]; ib[o++] = 1; i++;
+                } else {
+                    ws.mw[o] = ws.pw[j]; ws.mt[o] = ws.pt[j]; ib[o++] = 0; j++;
+                }
+            }
+        }
+        mlen = m + npk;
+        __syncthreads();
+    }
+    // 4. selected prefixes, top level down
+    long long L = 2 * ((long long)m - 1);
+    for (int l = MAXLEN - 1; l >= 1; l--) {
+        const uint8_t* ib = ws.isbase + (size_t)l * 2 * m;
+        uint32_t c = 0;
+        for (long long q = tid; q < L; q += BT) c += ib[q];
+        uint32_t tot;
+        block_exclusive_scan(c, tmp, &tot);
+        if (tid == 0) s_nb[l] = tot;
+        L = 2 * (L - (long long)tot);
+    }
+    if (tid == 0) s_nb[0] = L;
+    __syncthreads();
+    // 5. lengths and bit count
+    unsigned long long bits = 0;
+    for (uint32_t q = tid; q < m; q += BT) {
+        int len = 0;
+        for (int l = 0; l < MAXLEN; l++) len += (long long)q < s_nb[l];
+        lengths[ws.bs[q]] = (uint8_t)len;
+        bits += ws.bw[q] * (unsigned long long)len;
+    }
+    unsigned long long btot;
+    block_exclusive_scan64(bits, tmp64, &btot);
+    if (tid == 0) *bit_count = btot;
+    __syncthreads();
+    // 6. canonical codewords by (length, symbol)  (encode.py:155-171)
+    if (tid <= MAXLEN) s_cnt[tid] = 0;
+    __syncthreads();
+    for (uint32_t s = tid; s < nsym; s += BT)
+        if (lengths[s]) atomicAdd(&s_cnt[lengths[s]], 1u);
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long code = 0;
+        s_first[0] = 0;
+        for (int l = 1; l <= MAXLEN; l++) {
+            code = (code + (l > 1 ? s_cnt[l - 1] : 0)) << 1;
+            s_first[l] = code;
+        }
+        for (int l = 0; l <= MAXLEN; l++) s_cnt[l] = 0;  // reuse as running rank
+    }
+    __syncthreads();
+    if (tid < 32) {
+        const int lane = tid;
+        for (uint32_t s0 = 0; s0 < nsym; s0 += 32) {
+            const uint32_t s = s0 + lane;
+            const int len = s < nsym ? lengths[s] : 0;
+            const unsigned peers = __match_any_sync(0xffffffffu, len);
+            const uint32_t rank = __popc(peers & lanemask_lt());
+            if (len) cw[s] = (uint32_t)(s_first[len] + s_cnt[len] + rank);
+            __syncwarp();
+            if (len && rank == 0) s_cnt[len] += __popc(peers);
+            __syncwarp();
+        }
+    }
+}
+
+// ------------------------------------------------------------------ encode
+constexpr int HE_THREADS = 256;
+constexpr int HE_PER = 16;                     // codes per thread
+constexpr int HE_CHUNK = HE_THREADS * HE_PER;  // codes per CTA
+
+FZB_DEV void load16(const uint16_t* __restrict__ codes, uint64_t n, uint64_t base, uint32_t c[HE_PER]) {
+    if (base + HE_PER <= n) {
+        const uint4* p = reinterpret_cast<const uint4*>(codes + base);
+        const uint4 a = __ldg(p), b = __ldg(p + 1);
+        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int e = 0; e < 8; e++) { c[2 * e] = w[e] & 0xFFFFu; c[2 * e + 1] = w[e] >> 16; }
+    } else {
+#pragma unroll
+        for (int e = 0; e < HE_PER; e++) c[e] = (base + e < n) ? (uint32_t)codes[base + e] : 0xFFFFFFFFu;
+    }
+}
+
+__global__ void __launch_bounds__(HE_THREADS) hf_count_kernel(const uint16_t* __restrict__ codes, uint64_t n,
+                                                              const uint8_t* __restrict__ lengths, uint32_t nsym,
+                                                              unsigned long long* __restrict__ cta_bits) {
+    __shared__ unsigned long long tmp[33];
+    const uint64_t base = ((uint64_t)blockIdx.x * HE_THREADS + threadIdx.x) * HE_PER;
+    uint32_t c[HE_PER];
+    load16(codes, n, base, c);
+    unsigned long long b = 0;
+#pragma unroll
+    for (int e = 0; e < HE_PER; e++)
+        if (c[e] < nsym) b += __ldg(lengths + c[e]);
+    unsigned long long tot;
+    block_exclusive_scan64(b, tmp, &tot);
+    if (threadIdx.x == 0) cta_bits[blockIdx.x] = tot;
+}
+
+__global__ void scan_u64_kernel(const unsigned long long* __restrict__ x, uint64_t m,
+                                unsigned long long* __restrict__ offs, unsigned long long* __restrict__ tot) {
+    __shared__ unsigned long long tmp[33];
+    unsigned long long carry = 0;
+    for (uint64_t b0 = 0; b0 < m; b0 += blockDim.x) {
+        const uint64_t q = b0 + threadIdx.x;
+        const unsigned long long v = q < m ? x[q] : 0ull;
+        unsigned long long t;
+        const unsigned long long p = block_exclusive_scan64(v, tmp, &t);
+        if (q < m) offs[q] = carry + p;
+        carry += t;
+    }
+    if (threadIdx.x == 0) *tot = carry;
+}
+
+__global__ void hf_zero_kernel(uint32_t* __restrict__ out, const unsigned long long* __restrict__ bits,
+                               uint64_t cap_words) {
+    uint64_t words = (*bits + 31) / 32;
+    if (words > cap_words) words = cap_words;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < words; q += stride) out[q] = 0;
+}
+
+__global__ void hf_check_kernel(const unsigned long long* __restrict__ got, const unsigned long long* __restrict__ want,
+                                uint32_t* __restrict__ status) {
+    if (*got != *want) set_err(status, FZB_ERR_HF_MISMATCH);
+}
+
+FZB_DEV uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+__global__ void __launch_bounds__(HE_THREADS) hf_write_kernel(const uint16_t* __restrict__ codes, uint64_t n,
+                                                              const uint8_t* __restrict__ lengths,
+                                                              const uint32_t* __restrict__ cwords, uint32_t nsym,
+                                                              const unsigned long long* __restrict__ cta_off,
+                                                              const unsigned long long* __restrict__ want_bits,
+                                                              uint32_t* __restrict__ out, uint64_t cap_words) {
+    __shared__ unsigned long long tmp[33];
+    const uint64_t base = ((uint64_t)blockIdx.x * HE_THREADS + threadIdx.x) * HE_PER;
+    uint32_t c[HE_PER];
+    load16(codes, n, base, c);
+    uint32_t len[HE_PER], cwv[HE_PER];
+    unsigned long long b = 0;
+#pragma unroll
+    for (int e = 0; e < HE_PER; e++) {
+        len[e] = 0; cwv[e] = 0;
+        if (c[e] < nsym) { len[e] = __ldg(lengths + c[e]); cwv[e] = __ldg(cwords + c[e]); }
+        b += len[e];
+    }
+    const unsigned long long o = cta_off[blockIdx.x] + block_exclusive_scan64(b, tmp, nullptr);
+    if (b == 0) return;
+    uint64_t w = o >> 5;
+    int filled = (int)(o & 31);
+    unsigned long long acc = 0;  // MSB-aligned pending bits of word w
+    bool first = true;
+#pragma unroll
+    for (int e = 0; e < HE_PER; e++) {
+        const int l = (int)len[e];
+        if (l == 0) continue;
+        // place l bits right after `filled` bits (acc holds up to 64)
+        acc |= ((unsigned long long)cwv[e] << (64 - l)) >> filled;
+        filled += l;
+        if (filled >= 32) {
+            const uint32_t word = (uint32_t)(acc >> 32);
+            if (w < cap_words) {
+                if (first) atomicOr(out + w, bswap32(word));
+                else out[w] = bswap32(word);
+            }
+            first = false;
+            acc <<= 32;
+            filled -= 32;
+            w++;
+        }
+    }
+    if (filled > 0 && w < cap_words) atomicOr(out + w, bswap32((uint32_t)(acc >> 32)));
+}
+
+// ------------------------------------------------------------------ decode
+constexpr int LUT_BITS = 12;
+constexpr int SUB = 1024;  // bits per decode subsequence
+constexpr int HD_THREADS = 128;
+
+struct DecTables {
+    long long first_code[MAXLEN + 2];
+    long long first_idx[MAXLEN + 2];
+    long long limit[MAXLEN + 2];
+    int maxlen;
+    int pad;
+};
+
+__global__ void hf_tables_kernel(const uint8_t* __restrict__ lengths, uint32_t nsym, DecTables* __restrict__ T,
+                                 uint16_t* __restrict__ sym_sorted, uint32_t* __restrict__ lut) {
+    __shared__ uint32_t cnt[MAXLEN + 1];
+    __shared__ uint32_t run[MAXLEN + 1];
+    __shared__ long long s_fc[MAXLEN + 2], s_fi[MAXLEN + 2];
+    const int tid = threadIdx.x;
+    if (tid <= MAXLEN) { cnt[tid] = 0; run[tid] = 0; }
+    __syncthreads();
+    for (uint32_t s = tid; s < nsym; s += blockDim.x)
+        if (lengths[s] && lengths[s] <= MAXLEN) atomicAdd(&cnt[lengths[s]], 1u);
+    for (uint32_t q = tid; q < (1u << LUT_BITS); q += blockDim.x) lut[q] = 0;
+    __syncthreads();
+    if (tid == 0) {
+        int maxlen = 0;
+        for (int l = 1; l <= MAXLEN; l++) if (cnt[l]) maxlen = l;
+        long long code = 0, idx = 0;
+        for (int l = 0; l <= MAXLEN + 1; l++) { T->first_code[l] = 0; T->first_idx[l] = 0; T->limit[l] = 0; }
+        for (int l = 1; l <= maxlen; l++) {  // encode.py:265-273
+            code <<= 1;
+            T->first_code[l] = code; s_fc[l] = code;
+            T->first_idx[l] = idx; s_fi[l] = idx;
+            T->limit[l] = code + cnt[l];
+            code += cnt[l];
+            idx += cnt[l];
+        }
+        T->maxlen = maxlen;
+    }
+    __syncthreads();
+    // sym_sorted in (len, sym) order + LUT for short codes
+    if (tid < 32) {
+        const int lane = tid;
+        for (uint32_t s0 = 0; s0 < nsym; s0 += 32) {
+            const uint32_t s = s0 + lane;
+            const int len = s < nsym ? lengths[s] : 0;
+            const unsigned peers = __match_any_sync(0xffffffffu, len);
+            const uint32_t rank = __popc(peers & lanemask_lt());
+            if (len && len <= MAXLEN) {
+                const long long r = run[len] + rank;
+                sym_sorted[s_fi[len] + r] = (uint16_t)s;
+                if (len <= LUT_BITS) {
+                    const uint32_t c = (uint32_t)(s_fc[len] + r);
+                    const uint32_t lo = c << (LUT_BITS - len), hi = (c + 1) << (LUT_BITS - len);
+                    for (uint32_t q = lo; q < hi; q++) lut[q] = s | ((uint32_t)len << 16);
+                }
+            }
+            __syncwarp();
+            if (len && len <= MAXLEN && rank == 0) run[len] += __popc(peers);
+            __syncwarp();
+        }
+    }
+}
+
+struct BitReader {
+    const uint32_t* w;  // byte-swapped view happens on load
+    unsigned long long pos;
+    FZB_DEV uint32_t peek32() const {
+        const unsigned long long wi = pos >> 5;
+        const unsigned long long hi = bswap32(__ldg(w + wi)), lo = bswap32(__ldg(w + wi + 1));
+        const unsigned long long x = (hi << 32) | lo;
+        return (uint32_t)((x << (pos & 31)) >> 32);
+    }
+};
+
+// decode one symbol at r.pos; returns length (>0) or -1 truncated / -2 corrupt
+FZB_DEV int decode_one(const BitReader& r, unsigned long long total_bits, const DecTables& T, const uint32_t* lut,
+                       const uint16_t* sym_sorted, uint32_t& sym) {
+    const uint32_t win = r.peek32();
+    const uint32_t e = lut[win >> (32 - LUT_BITS)];
+    int l = (int)(e >> 16);
+    if (l) {
+        sym = e & 0xFFFFu;
+    } else {
+        l = 0;
+        for (int q = LUT_BITS + 1; q <= T.maxlen; q++) {
+            const long long code = (long long)(win >> (32 - q));
+            if (code < T.limit[q]) {
+                sym = sym_sorted[T.first_idx[q] + code - T.first_code[q]];
+                l = q;
+                break;
+            }
+        }
+        if (!l) return (r.pos + (unsigned long long)T.maxlen >= total_bits) ? -1 : -2;
+    }
+    if (r.pos + (unsigned long long)l > total_bits) return -1;
+    return l;
+}
+
+// one sync iteration: start[t] (from end of t-1 of the previous iteration)
+__global__ void __launch_bounds__(HD_THREADS) hf_sync_kernel(const uint32_t* __restrict__ stream, unsigned long long total_bits,
+                                                             uint64_t nsub, const DecTables* __restrict__ Tg,
+                                                             const uint32_t* __restrict__ lut_g,
+                                                             const uint16_t* __restrict__ sym_sorted,
+                                                             const unsigned long long* __restrict__ prev_start,
+                                                             const unsigned long long* __restrict__ prev_end,
+                                                             const uint32_t* __restrict__ prev_cnt,
+                                                             const uint32_t* __restrict__ prev_err,
+                                                             unsigned long long* __restrict__ start,
+                                                             unsigned long long* __restrict__ end,
+                                                             uint32_t* __restrict__ cnt, uint32_t* __restrict__ err,
+                                                             uint32_t* __restrict__ changed, int first_iter) {
+    __shared__ uint32_t lut[1 << LUT_BITS];
+    __shared__ DecTables T;
+    for (int q = threadIdx.x; q < (1 << LUT_BITS); q += blockDim.x) lut[q] = lut_g[q];
+    if (threadIdx.x == 0) T = *Tg;
+    __syncthreads();
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nsub) return;
+    unsigned long long s;
+    if (first_iter) s = t * SUB;
+    else s = (t == 0) ? 0ull : prev_end[t - 1];
+    if (!first_iter && s == prev_start[t]) {
+        start[t] = s; end[t] = prev_end[t]; cnt[t] = prev_cnt[t]; err[t] = prev_err[t];
+        return;
+    }
+    if (!first_iter) *changed = 1;
+    const unsigned long long lim = (t + 1) * (unsigned long long)SUB;
+    BitReader r{stream, s};
+    uint32_t c = 0, e = 0;
+    while (r.pos < lim && r.pos < total_bits) {
+        uint32_t sym;
+        const int l = decode_one(r, total_bits, T, lut, sym_sorted, sym);
+        if (l < 0) { e = (uint32_t)(-l); break; }
+        r.pos += l;
+        c++;
+    }
+    start[t] = s; end[t] = e ? lim : r.pos; cnt[t] = c; err[t] = e;
+}
+
+__global__ void scan_cnt_kernel(const uint32_t* __restrict__ cnt, uint64_t m, unsigned long long* __restrict__ offs,
+                                unsigned long long* __restrict__ tot) {
+    __shared__ unsigned long long tmp[33];
+    unsigned long long carry = 0;
+    for (uint64_t b0 = 0; b0 < m; b0 += blockDim.x) {
+        const uint64_t q = b0 + threadIdx.x;
+        const unsigned long long v = q < m ? cnt[q] : 0ull;
+        unsigned long long t;
+        const unsigned long long p = block_exclusive_scan64(v, tmp, &t);
+        if (q < m) offs[q] = carry + p;
+        carry += t;
+    }
+    if (threadIdx.x == 0) *tot = carry;
+}
+
+__global__ void __launch_bounds__(HD_THREADS) hf_write_dec_kernel(const uint32_t* __restrict__ stream,
+                                                                  unsigned long long total_bits, uint64_t nsub,
+                                                                  const DecTables* __restrict__ Tg,
+                                                                  const uint32_t* __restrict__ lut_g,
+                                                                  const uint16_t* __restrict__ sym_sorted,
+                                                                  const unsigned long long* __restrict__ start,
+                                                                  const unsigned long long* __restrict__ end,
+                                                                  const unsigned long long* __restrict__ offs,
+                                                                  uint64_t n, uint16_t* __restrict__ out,
+                                                                  unsigned long long* __restrict__ end_pos) {
+    __shared__ uint32_t lut[1 << LUT_BITS];
+    __shared__ DecTables T;
+    for (int q = threadIdx.x; q < (1 << LUT_BITS); q += blockDim.x) lut[q] = lut_g[q];
+    if (threadIdx.x == 0) T = *Tg;
+    __syncthreads();
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nsub) return;
+    unsigned long long o = offs[t];
+    if (o >= n) return;
+    BitReader r{stream, start[t]};
+    const unsigned long long e = end[t];
+    while (r.pos < e && o < n) {
+        uint32_t sym;
+        const int l = decode_one(r, total_bits, T, lut, sym_sorted, sym);
+        if (l < 0) break;
+        r.pos += l;
+        out[o] = (uint16_t)sym;
+        o++;
+        if (o == n) *end_pos = r.pos;
+    }
+}
+
+// Find the first true-path error with ordinal < n, or the end position;
+// apply encode.py:299-316.
+__global__ void hf_final_kernel(uint64_t nsub, const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ err,
+                                const unsigned long long* __restrict__ offs, uint64_t n, uint64_t nbytes,
+                                const uint8_t* __restrict__ bytes, const unsigned long long* __restrict__ end_pos,
+                                uint32_t* __restrict__ status) {
+    __shared__ unsigned long long best;
+    if (threadIdx.x == 0) best = ~0ull;
+    __syncthreads();
+    for (uint64_t t = threadIdx.x; t < nsub; t += blockDim.x)
+        if (err[t]) {
+            const unsigned long long ord = offs[t] + cnt[t];
+            if (ord < n) atomicMin(&best, (t << 2) | err[t]);
+        }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    if (best != ~0ull) {
+        set_err(status, (best & 3) == 1 ? FZB_ERR_HF_TRUNCATED : FZB_ERR_HF_CORRUPT);
+        return;
+    }
+    unsigned long long total = nsub ? offs[nsub - 1] + cnt[nsub - 1] : 0;
+    if (total < n) {  // stream ended on a boundary before n symbols
+        set_err(status, FZB_ERR_HF_TRUNCATED);
+        return;
+    }
+    const unsigned long long e = *end_pos;
+    if (nbytes != (e + 7) / 8) {
+        set_err(status, FZB_ERR_HF_LONG);
+        return;
+    }
+    if (e & 7) {
+        const uint32_t tail = bytes[nbytes - 1] & ((1u << (8 - (e & 7))) - 1u);
+        if (tail) set_err(status, FZB_ERR_HF_PAD);
+    }
+}
+
+__global__ void hf_sync_check_kernel(const uint32_t* __restrict__ changed, uint32_t* __restrict__ status) {
+    if (*changed) set_err(status, FZB_ERR_HF_SYNC);
+}
+
+size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+}  // namespace
+
+extern "C" {
+
+FZB_API size_t fzb_huffman_build_workspace_bytes(uint32_t nsym) {
+    size_t np2 = 1;
+    while (np2 < nsym) np2 <<= 1;
+    const size_t m2 = 2 * (size_t)np2;
+    return align256(np2 * 8) + align256(np2 * 4) + align256(np2 * 8) + align256(np2 * 4) + align256(m2 * 8) +
+           align256(m2 * 4) + align256((size_t)MAXLEN * m2) + 256;
+}
+
+FZB_API int fzb_huffman_build(const uint64_t* d_bins, uint32_t nsym, uint8_t* d_lengths, uint32_t* d_codewords,
+                              uint64_t* d_bit_count, void* d_ws, size_t ws_bytes, void* stream) {
+    if (nsym == 0 || nsym > 65536) return FZB_E_ARG;
+    if (ws_bytes < fzb_huffman_build_workspace_bytes(nsym)) return FZB_E_WORKSPACE;
+    size_t np2 = 1;
+    while (np2 < nsym) np2 <<= 1;
+    const size_t m2 = 2 * np2;
+    unsigned char* p = static_cast<unsigned char*>(d_ws);
+    BuildWS ws;
+    ws.bw = reinterpret_cast<unsigned long long*>(p); p += align256(np2 * 8);
+    ws.bs = reinterpret_cast<uint32_t*>(p); p += align256(np2 * 4);
+    ws.pw = reinterpret_cast<unsigned long long*>(p); p += align256(np2 * 8);
+    ws.pt = reinterpret_cast<uint32_t*>(p); p += align256(np2 * 4);
+    ws.mw = reinterpret_cast<unsigned long long*>(p); p += align256(m2 * 8);
+    ws.mt = reinterpret_cast<uint32_t*>(p); p += align256(m2 * 4);
+    ws.isbase = p;
+    huffman_build_kernel<<<1, BT, 0, (cudaStream_t)stream>>>(reinterpret_cast<const unsigned long long*>(d_bins), nsym,
+                                                             d_lengths, d_codewords,
+                                                             reinterpret_cast<unsigned long long*>(d_bit_count), ws);
+    return fzb_check_launch();
+}
+
+FZB_API size_t fzb_huffman_encode_workspace_bytes(uint64_t n) {
+    const uint64_t nc = (n + HE_CHUNK - 1) / HE_CHUNK;
+    return 256 + 2 * align256(nc * 8) + 256;
+}
+
+FZB_API int fzb_huffman_encode(const uint16_t* d_codes, uint64_t n, const uint8_t* d_lengths,
+                               const uint32_t* d_codewords, uint32_t nsym, const uint64_t* d_bit_count,
+                               uint8_t* d_out, uint64_t out_cap, void* d_ws, size_t ws_bytes, uint32_t* d_status,
+                               void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (ws_bytes < fzb_huffman_encode_workspace_bytes(n)) return FZB_E_WORKSPACE;
+    if ((reinterpret_cast<uintptr_t>(d_out) & 3) || (reinterpret_cast<uintptr_t>(d_codes) & 15)) return FZB_E_ARG;
+    if (n == 0) return 0;
+    const uint64_t nc = (n + HE_CHUNK - 1) / HE_CHUNK;
+    unsigned char* w = static_cast<unsigned char*>(d_ws);
+    unsigned long long* tot = reinterpret_cast<unsigned long long*>(w);
+    unsigned long long* cta_bits = reinterpret_cast<unsigned long long*>(w + 256);
+    unsigned long long* cta_off = reinterpret_cast<unsigned long long*>(w + 256 + align256(nc * 8));
+    const uint64_t cap_words = out_cap / 4;
+    uint32_t* out = reinterpret_cast<uint32_t*>(d_out);
+    const unsigned long long* want = reinterpret_cast<const unsigned long long*>(d_bit_count);
+    hf_count_kernel<<<(unsigned)nc, HE_THREADS, 0, st>>>(d_codes, n, d_lengths, nsym, cta_bits);
+    scan_u64_kernel<<<1, 1024, 0, st>>>(cta_bits, nc, cta_off, tot);
+    hf_check_kernel<<<1, 1, 0, st>>>(tot, want, d_status);
+    hf_zero_kernel<<<kNumSMs * 4, 256, 0, st>>>(out, tot, cap_words);
+    hf_write_kernel<<<(unsigned)nc, HE_THREADS, 0, st>>>(d_codes, n, d_lengths, d_codewords, nsym, cta_off, want, out,
+                                                        cap_words);
+    return fzb_check_launch();
+}
+
+FZB_API size_t fzb_huffman_decode_workspace_bytes(uint64_t nbytes, uint32_t nsym) {
+    const uint64_t nsub = (nbytes * 8 + SUB - 1) / SUB + 1;
+    // tables + sym_sorted + lut + 2x(start,end,cnt,err) + offs + scalars
+    return align256(sizeof(DecTables)) + align256((size_t)nsym * 2) + align256((1u << LUT_BITS) * 4) +
+           2 * (2 * align256(nsub * 8) + 2 * align256(nsub * 4)) + align256(nsub * 8) + 1024;
+}
+
+// d_stream must be readable (zero) for 8 bytes past nbytes.
+FZB_API int fzb_huffman_decode(const uint8_t* d_stream, uint64_t nbytes, uint64_t n, const uint8_t* d_lengths,
+                               uint32_t nsym, uint16_t* d_codes, void* d_ws, size_t ws_bytes, uint32_t* d_status,
+                               void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (ws_bytes < fzb_huffman_decode_workspace_bytes(nbytes, nsym)) return FZB_E_WORKSPACE;
+    if (reinterpret_cast<uintptr_t>(d_stream) & 3) return FZB_E_ARG;
+    if (n == 0) return 0;
+    const unsigned long long total_bits = nbytes * 8ull;
+    const uint64_t nsub = total_bits ? (total_bits + SUB - 1) / SUB : 1;
+    unsigned char* p = static_cast<unsigned char*>(d_ws);
+    DecTables* T = reinterpret_cast<DecTables*>(p); p += align256(sizeof(DecTables));
+    uint16_t* sym_sorted = reinterpret_cast<uint16_t*>(p); p += align256((size_t)nsym * 2);
+    uint32_t* lut = reinterpret_cast<uint32_t*>(p); p += align256((1u << LUT_BITS) * 4);
+    unsigned long long* st_[2]; unsigned long long* en_[2]; uint32_t* cn_[2]; uint32_t* er_[2];
+    for (int b = 0; b < 2; b++) {
+        st_[b] = reinterpret_cast<unsigned long long*>(p); p += align256(nsub * 8);
+        en_[b] = reinterpret_cast<unsigned long long*>(p); p += align256(nsub * 8);
+        cn_[b] = reinterpret_cast<uint32_t*>(p); p += align256(nsub * 4);
+        er_[b] = reinterpret_cast<uint32_t*>(p); p += align256(nsub * 4);
+    }
+    unsigned long long* offs = reinterpret_cast<unsigned long long*>(p); p += align256(nsub * 8);
+    unsigned long long* scal = reinterpret_cast<unsigned long long*>(p);  // [0]=total [1]=end_pos [2]=changed
+    cudaMemsetAsync(scal, 0, 64, st);
+    hf_tables_kernel<<<1, 256, 0, st>>>(d_lengths, nsym, T, sym_sorted, lut);
+    const uint32_t* words = reinterpret_cast<const uint32_t*>(d_stream);
+    const unsigned blocks = (unsigned)((nsub + HD_THREADS - 1) / HD_THREADS);
+    uint32_t* changed = reinterpret_cast<uint32_t*>(scal + 2);
+    // iteration 0: speculative starts; iterations 1..3: start = end of predecessor
+    const int iters = 4;
+    for (int it = 0; it < iters; it++) {
+        const int cur = it & 1, prv = cur ^ 1;
+        if (it == iters - 1) cudaMemsetAsync(changed, 0, 4, st);
+        hf_sync_kernel<<<blocks, HD_THREADS, 0, st>>>(words, total_bits, nsub, T, lut, sym_sorted, st_[prv], en_[prv],
+                                                      cn_[prv], er_[prv], st_[cur], en_[cur], cn_[cur], er_[cur],
+                                                      changed, it == 0);
+    }
+    const int fin = (iters - 1) & 1;
+    hf_sync_check_kernel<<<1, 1, 0, st>>>(changed, d_status);
+    scan_cnt_kernel<<<1, 1024, 0, st>>>(cn_[fin], nsub, offs, scal);
+    hf_write_dec_kernel<<<blocks, HD_THREADS, 0, st>>>(words, total_bits, nsub, T, lut, sym_sorted, st_[fin], en_[fin],
+                                                       offs, n, d_codes, scal + 1);
+    hf_final_kernel<<<1, 1024, 0, st>>>(nsub, cn_[fin], er_[fin], offs, n, nbytes, d_stream, scal + 1, d_status);
+    return fzb_check_launch();
+}
+
+}  // extern "C"

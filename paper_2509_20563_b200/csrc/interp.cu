@@ -1,0 +1,163 @@
+// interp.cu -- G-Interp (multi-level spline interpolation) predictor for sm_100a.
+//
+// Reference: fzpipe predict.py:147-201 (_interp_predict / _interp_pass),
+// 270-344 (interp_quantize / interp_reconstruct).  The field keeps a coarse
+// anchor lattice (stride 16) verbatim; levels h = 8, 4, 2, 1 then fill the
+// odd multiples of h along axis 0, 1, 2 in turn.  Every pass reads only
+// points finished by earlier passes, so all targets of one pass are
+// independent (SURVEY.md finding 5): one grid-stride kernel per non-empty
+// pass, threads mapped to the innermost lattice axis for coalescing.  The
+// cubic/linear/copy stencils and the quantizer keep the reference's exact
+// f64 operation order (no FMA).
+#include "common.cuh"
+
+namespace {
+
+struct Pass {
+    long long n0, n1, n2;
+    long long h;
+    // target lattice: start/step/count per axis
+    long long s0, d0, c0, s1, d1, c1, s2, d2, c2;
+    long long total;
+};
+
+FZB_DEV double interp_pred(const float* __restrict__ r, long long t, long long c, long long n, long long sh,
+                           long long h, const double* w) {
+    // predict.py:151-160
+    if (c - 3 * h >= 0 && c + 3 * h < n) {
+        double acc = __dmul_rn(w[0], (double)r[t - 3 * sh]);
+        acc = __dadd_rn(acc, __dmul_rn(w[1], (double)r[t - sh]));
+        acc = __dadd_rn(acc, __dmul_rn(w[2], (double)r[t + sh]));
+        acc = __dadd_rn(acc, __dmul_rn(w[3], (double)r[t + 3 * sh]));
+        return acc;
+    }
+    if (c + h < n) return __dadd_rn(__dmul_rn(0.5, (double)r[t - sh]), __dmul_rn(0.5, (double)r[t + sh]));
+    return (double)r[t - sh];
+}
+
+template <int AXIS, bool DEC>
+__global__ void __launch_bounds__(256) interp_pass_kernel(const float* __restrict__ orig, uint16_t* __restrict__ codes,
+                                                          float* __restrict__ recon, uint32_t* __restrict__ bitmap,
+                                                          Pass p, const double* __restrict__ d_eb, int radius,
+                                                          double w0, double w1, double w2, double w3) {
+    const QParams P = make_qparams(*d_eb, radius);
+    const double w[4] = {w0, w1, w2, w3};
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < p.total; q += stride) {
+        const long long q2 = q % p.c2;
+        const long long r1 = q / p.c2;
+        const long long q1 = r1 % p.c1;
+        const long long q0 = r1 / p.c1;
+        const long long i = p.s0 + q0 * p.d0, j = p.s1 + q1 * p.d1, k = p.s2 + q2 * p.d2;
+        const long long t = (i * p.n1 + j) * p.n2 + k;
+        double pred;
+        if (AXIS == 0) pred = interp_pred(recon, t, i, p.n0, p.h * p.n1 * p.n2, p.h, w);
+        else if (AXIS == 1) pred = interp_pred(recon, t, j, p.n1, p.h * p.n2, p.h, w);
+        else pred = interp_pred(recon, t, k, p.n2, p.h, p.h, w);
+        if constexpr (DEC) {
+            if ((bitmap[t >> 5] >> (t & 31)) & 1u) continue;
+            recon[t] = dequantize(pred, (int)codes[t], P);
+        } else {
+            float rec;
+            bool outl;
+            const int c = quantize((double)__ldg(orig + t), pred, P, rec, outl);
+            codes[t] = (uint16_t)c;
+            recon[t] = rec;
+            if (outl) atomicOr(bitmap + (t >> 5), 1u << (t & 31));
+        }
+    }
+}
+
+// anchors: orig[::a, ::a, ::a] -> anchor buffer and recon (encode), or
+// anchor buffer -> recon (decode); predict.py:301-302, 341-342.
+template <bool DEC>
+__global__ void anchor_kernel(const float* __restrict__ orig, float* __restrict__ anchors, float* __restrict__ recon,
+                              long long n1, long long n2, long long a, long long A0, long long A1, long long A2) {
+    const long long total = A0 * A1 * A2;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += stride) {
+        const long long z = q % A2, r = q / A2, y = r % A1, x = r / A1;
+        const long long t = ((x * a) * n1 + y * a) * n2 + z * a;
+        if constexpr (DEC) {
+            recon[t] = anchors[q];
+        } else {
+            const float v = orig[t];
+            anchors[q] = v;
+            recon[t] = v;
+        }
+    }
+}
+
+Pass make_pass(long long n0, long long n1, long long n2, long long h, int axis) {
+    Pass p;
+    p.n0 = n0; p.n1 = n1; p.n2 = n2; p.h = h;
+    const long long h2 = 2 * h;
+    auto cnt = [](long long s, long long d, long long n) { return s < n ? (n - s + d - 1) / d : 0; };
+    // predict.py:169-201 loop bounds
+    if (axis == 0) { p.s0 = h; p.d0 = h2; p.s1 = 0; p.d1 = h2; p.s2 = 0; p.d2 = h2; }
+    else if (axis == 1) { p.s0 = 0; p.d0 = h; p.s1 = h; p.d1 = h2; p.s2 = 0; p.d2 = h2; }
+    else { p.s0 = 0; p.d0 = h; p.s1 = 0; p.d1 = h; p.s2 = h; p.d2 = h2; }
+    p.c0 = cnt(p.s0, p.d0, n0);
+    p.c1 = cnt(p.s1, p.d1, n1);
+    p.c2 = cnt(p.s2, p.d2, n2);
+    p.total = p.c0 * p.c1 * p.c2;
+    return p;
+}
+
+void pad3(uint32_t& n0, uint32_t& n1, uint32_t& n2) { (void)n0; (void)n1; (void)n2; }
+
+template <bool DEC>
+int run_passes(const float* orig, uint16_t* codes, float* recon, uint32_t* bitmap, uint32_t n0, uint32_t n1,
+               uint32_t n2, const double* d_eb, uint32_t radius, uint32_t stride, const double* w, cudaStream_t st) {
+    for (long long h = stride / 2; h >= 1; h /= 2) {
+        for (int axis = 0; axis < 3; axis++) {
+            const Pass p = make_pass(n0, n1, n2, h, axis);
+            if (p.total == 0) continue;
+            long long blocks = (p.total + 255) / 256;
+            if (blocks > (long long)kNumSMs * 16) blocks = (long long)kNumSMs * 16;
+            if (axis == 0)
+                interp_pass_kernel<0, DEC><<<(unsigned)blocks, 256, 0, st>>>(orig, codes, recon, bitmap, p, d_eb, (int)radius, w[0], w[1], w[2], w[3]);
+            else if (axis == 1)
+                interp_pass_kernel<1, DEC><<<(unsigned)blocks, 256, 0, st>>>(orig, codes, recon, bitmap, p, d_eb, (int)radius, w[0], w[1], w[2], w[3]);
+            else
+                interp_pass_kernel<2, DEC><<<(unsigned)blocks, 256, 0, st>>>(orig, codes, recon, bitmap, p, d_eb, (int)radius, w[0], w[1], w[2], w[3]);
+        }
+    }
+    return fzb_check_launch();
+}
+
+}  // namespace
+
+extern "C" {
+
+// Caller: d_codes pre-filled with `radius` (predict.py:297), d_bitmap zeroed.
+// Dims are the reference's padded (n0, n1, n2) (predict.py:204-205).
+FZB_API int fzb_interp_encode_f32(const float* d_in, uint32_t n0, uint32_t n1, uint32_t n2, const double* d_eb,
+                                  uint32_t radius, uint32_t anchor_stride, const double* h_weights4,
+                                  uint16_t* d_codes, float* d_recon, uint32_t* d_bitmap, float* d_anchors,
+                                  void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (radius == 0 || radius > 32768) return FZB_E_RADIUS;
+    if (anchor_stride < 4 || (anchor_stride & (anchor_stride - 1))) return FZB_E_ARG;
+    const long long a = anchor_stride;
+    const long long A0 = (n0 - 1) / a + 1, A1 = (n1 - 1) / a + 1, A2 = (n2 - 1) / a + 1;
+    anchor_kernel<false><<<kNumSMs * 2, 256, 0, st>>>(d_in, d_anchors, d_recon, n1, n2, a, A0, A1, A2);
+    return run_passes<false>(d_in, d_codes, d_recon, d_bitmap, n0, n1, n2, d_eb, radius, anchor_stride, h_weights4, st);
+}
+
+// Caller: d_recon holds the outlier values and d_bitmap their flags
+// (fzb_outlier_scatter); anchors are scattered here.
+FZB_API int fzb_interp_decode_f32(const uint16_t* d_codes, const uint32_t* d_bitmap, const float* d_anchors,
+                                  float* d_recon, uint32_t n0, uint32_t n1, uint32_t n2, const double* d_eb,
+                                  uint32_t radius, uint32_t anchor_stride, const double* h_weights4, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (radius == 0 || radius > 32768) return FZB_E_RADIUS;
+    if (anchor_stride < 4 || (anchor_stride & (anchor_stride - 1))) return FZB_E_ARG;
+    const long long a = anchor_stride;
+    const long long A0 = (n0 - 1) / a + 1, A1 = (n1 - 1) / a + 1, A2 = (n2 - 1) / a + 1;
+    anchor_kernel<true><<<kNumSMs * 2, 256, 0, st>>>(nullptr, const_cast<float*>(d_anchors), d_recon, n1, n2, a, A0, A1, A2);
+    return run_passes<true>(nullptr, const_cast<uint16_t*>(d_codes), d_recon, const_cast<uint32_t*>(d_bitmap), n0, n1,
+                            n2, d_eb, radius, anchor_stride, h_weights4, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,335 @@
+// stream_ops.cu -- HBM-streaming kernels: min/max + bound, fill, histogram,
+// outlier compaction/scatter.
+//
+//  * min/max (pipeline.py:360-361, core.py:162-163): one pass of 128-bit
+//    loads instead of the reference's four numpy scans; partials per CTA,
+//    then a one-CTA final reduce.  eb_abs is computed on the device.
+//  * histogram (encode.py:79-111): privatised shared-memory bins with
+//    __match_any_sync warp aggregation (quant codes are sharply peaked);
+//    top-k is bitwise identical to exact by contract, so one kernel serves
+//    both methods.
+//  * outliers (predict.py:212-214): the predictor kernels set one bit per
+//    outlier; compaction is a popcount/scan pass in index order, so the
+//    list comes out sorted exactly like np.nonzero.
+#include "common.cuh"
+
+namespace {
+
+constexpr int MM_THREADS = 256;
+constexpr int MM_BLOCKS = kNumSMs * 4;
+
+__global__ void __launch_bounds__(MM_THREADS) minmax_partial_kernel(const float* __restrict__ x, uint64_t n,
+                                                                    float* __restrict__ part, uint32_t* __restrict__ status) {
+    float lo = INFINITY, hi = -INFINITY;
+    bool bad = false;
+    const uint64_t n4 = n / 4;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; q + 3 * stride < n4; q += 4 * stride) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) v[u] = __ldcs(x4 + q + u * stride);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            lo = fminf(lo, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
+            hi = fmaxf(hi, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+            bad |= !(isfinite(v[u].x) && isfinite(v[u].y) && isfinite(v[u].z) && isfinite(v[u].w));
+        }
+    }
+    for (; q < n4; q += stride) {
+        const float4 v = __ldcs(x4 + q);
+        lo = fminf(lo, fminf(fminf(v.x, v.y), fminf(v.z, v.w)));
+        hi = fmaxf(hi, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+        bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+    }
+    if (blockIdx.x == 0) {
+        for (uint64_t t = n4 * 4 + threadIdx.x; t < n; t += blockDim.x) {
+            const float v = x[t];
+            lo = fminf(lo, v);
+            hi = fmaxf(hi, v);
+            bad |= !isfinite(v);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    __shared__ float sl[32], sh[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) { sl[w] = lo; sh[w] = hi; }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) set_err(status, FZB_ERR_NONFINITE);
+    if (w == 0) {
+        lo = lane < (int)(blockDim.x >> 5) ? sl[lane] : INFINITY;
+        hi = lane < (int)(blockDim.x >> 5) ? sh[lane] : -INFINITY;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane == 0) {
+            part[2 * blockIdx.x] = lo;
+            part[2 * blockIdx.x + 1] = hi;
+        }
+    }
+}
+
+__global__ void minmax_final_kernel(const float* __restrict__ part, int np, float* __restrict__ lohi) {
+    float lo = INFINITY, hi = -INFINITY;
+    for (int q = threadIdx.x; q < np; q += blockDim.x) {
+        lo = fminf(lo, part[2 * q]);
+        hi = fmaxf(hi, part[2 * q + 1]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    __shared__ float sl[32], sh[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) { sl[w] = lo; sh[w] = hi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int q = 1; q < (int)(blockDim.x >> 5); q++) {
+            lo = fminf(lo, sl[q]);
+            hi = fmaxf(hi, sh[q]);
+        }
+        lohi[0] = lo;
+        lohi[1] = hi;
+    }
+}
+
+__global__ void resolve_kernel(const float* __restrict__ lohi, int mode, double mag, double* __restrict__ eb) {
+    // core.py:167: float(spec.magnitude) * (hi - lo), Python floats (f64)
+    *eb = mode ? __dmul_rn(mag, __dsub_rn((double)lohi[1], (double)lohi[0])) : mag;
+}
+
+__global__ void fill_u16_kernel(uint16_t* __restrict__ d, uint64_t n, uint16_t v) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t n8 = n / 8;
+    uint4 pat;
+    const uint32_t w = (uint32_t)v | ((uint32_t)v << 16);
+    pat.x = pat.y = pat.z = pat.w = w;
+    uint4* d8 = reinterpret_cast<uint4*>(d);
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n8; q += stride) d8[q] = pat;
+    for (uint64_t t = n8 * 8 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) d[t] = v;
+}
+
+// ----------------------------------------------------------------- histogram
+constexpr int HIST_THREADS = 512;
+constexpr uint32_t HIST_SMEM_BINS = 16384;
+
+FZB_DEV void hist_add(uint32_t* bins, uint32_t c, uint32_t nbins, uint32_t* status) {
+    const bool ok = c < nbins;
+    if (!ok) set_err(status, FZB_ERR_CODE_RANGE);
+    const unsigned am = __activemask();
+    const unsigned peers = __match_any_sync(am, ok ? c : 0xFFFFFFFFu);
+    if (ok && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(bins + c, (uint32_t)__popc(peers));
+}
+
+__global__ void __launch_bounds__(HIST_THREADS) hist_smem_kernel(const uint16_t* __restrict__ codes, uint64_t n,
+                                                                 uint32_t nbins, unsigned long long* __restrict__ out,
+                                                                 uint32_t* __restrict__ status) {
+    extern __shared__ uint32_t sb[];
+    for (uint32_t q = threadIdx.x; q < nbins; q += blockDim.x) sb[q] = 0;
+    __syncthreads();
+    const uint64_t n8 = n / 8;
+    const uint4* c8 = reinterpret_cast<const uint4*>(codes);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n8; q += stride) {
+        const uint4 v = __ldcs(c8 + q);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            hist_add(sb, w[u] & 0xFFFFu, nbins, status);
+            hist_add(sb, w[u] >> 16, nbins, status);
+        }
+    }
+    if (blockIdx.x == 0)
+        for (uint64_t t = n8 * 8 + threadIdx.x; t < n; t += blockDim.x) {
+            const uint32_t c = codes[t];
+            if (c >= nbins) set_err(status, FZB_ERR_CODE_RANGE);
+            else atomicAdd(sb + c, 1u);
+        }
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < nbins; q += blockDim.x)
+        if (sb[q]) atomicAdd(out + q, (unsigned long long)sb[q]);
+}
+
+__global__ void hist_global_kernel(const uint16_t* __restrict__ codes, uint64_t n, uint32_t nbins,
+                                   unsigned long long* __restrict__ out, uint32_t* __restrict__ status) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) {
+        const uint32_t c = codes[t];
+        if (c >= nbins) set_err(status, FZB_ERR_CODE_RANGE);
+        else atomicAdd(out + c, 1ull);
+    }
+}
+
+// ------------------------------------------------------------------ outliers
+constexpr int OC_WORDS = 2048;  // bitmap words per CTA (65536 elements)
+constexpr int OC_THREADS = 256;
+
+__global__ void __launch_bounds__(OC_THREADS) outlier_count_kernel(const uint32_t* __restrict__ bm, uint64_t nwords,
+                                                                   uint32_t* __restrict__ counts) {
+    __shared__ uint32_t tmp[33];
+    const uint64_t base = (uint64_t)blockIdx.x * OC_WORDS;
+    uint32_t c = 0;
+    for (int e = threadIdx.x; e < OC_WORDS; e += blockDim.x)
+        if (base + e < nwords) c += __popc(bm[base + e]);
+    uint32_t tot;
+    block_exclusive_scan(c, tmp, &tot);
+    if (threadIdx.x == 0) counts[blockIdx.x] = tot;
+}
+
+__global__ void scan_u32_to_u64_kernel(const uint32_t* __restrict__ cnt, uint64_t m,
+                                       unsigned long long* __restrict__ offs, unsigned long long* __restrict__ tot) {
+    __shared__ unsigned long long tmp[33];
+    unsigned long long carry = 0;
+    for (uint64_t b0 = 0; b0 < m; b0 += blockDim.x) {
+        const uint64_t q = b0 + threadIdx.x;
+        const unsigned long long x = q < m ? cnt[q] : 0ull;
+        unsigned long long t;
+        const unsigned long long p = block_exclusive_scan64(x, tmp, &t);
+        if (q < m) offs[q] = carry + p;
+        carry += t;
+    }
+    if (threadIdx.x == 0) *tot = carry;
+}
+
+__global__ void __launch_bounds__(OC_THREADS) outlier_write_kernel(const uint32_t* __restrict__ bm, uint64_t nwords,
+                                                                   const float* __restrict__ x,
+                                                                   const unsigned long long* __restrict__ offs,
+                                                                   unsigned long long* __restrict__ idx,
+                                                                   float* __restrict__ vals) {
+    __shared__ uint32_t tmp[33];
+    const uint64_t base = (uint64_t)blockIdx.x * OC_WORDS;
+    unsigned long long o = offs[blockIdx.x];
+    for (int e0 = 0; e0 < OC_WORDS; e0 += blockDim.x) {
+        const uint64_t wq = base + e0 + threadIdx.x;
+        uint32_t w = wq < nwords ? bm[wq] : 0u;
+        uint32_t tot;
+        uint32_t p = block_exclusive_scan(__popc(w), tmp, &tot);
+        while (w) {
+            const int bit = __ffs(w) - 1;
+            w &= w - 1;
+            const unsigned long long t = wq * 32ull + bit;
+            idx[o + p] = t;
+            vals[o + p] = x[t];
+            p++;
+        }
+        o += tot;
+    }
+}
+
+__global__ void outlier_scatter_kernel(const unsigned long long* __restrict__ idx, const float* __restrict__ vals,
+                                       uint64_t k, uint64_t n, const uint16_t* __restrict__ codes, int radius,
+                                       float* __restrict__ recon, uint32_t* __restrict__ bm,
+                                       uint32_t* __restrict__ status) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < k; q += stride) {
+        const unsigned long long t = idx[q];
+        if (t >= n) {  // pipeline.py:410-411 (u64, so "< 0" cannot happen)
+            set_err(status, FZB_ERR_OUTLIER_RANGE);
+            continue;
+        }
+        if (q > 0 && idx[q - 1] >= t) set_err(status, FZB_ERR_OUTLIER_ORDER);  // core.py:212-213
+        if (codes[t] != radius) set_err(status, FZB_ERR_OUTLIER_CODE);          // core.py:214-215
+        recon[t] = vals[q];
+        atomicOr(bm + (t >> 5), 1u << (t & 31));
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+FZB_API int fzb_abi_version(void) { return 1; }
+
+FZB_API size_t fzb_minmax_workspace_bytes(uint64_t) { return (size_t)MM_BLOCKS * 2 * sizeof(float); }
+
+FZB_API int fzb_minmax_f32(const float* d_in, uint64_t n, float* d_lohi, void* d_ws, size_t ws_bytes,
+                           uint32_t* d_status, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n == 0) return FZB_E_ARG;
+    if (ws_bytes < fzb_minmax_workspace_bytes(n)) return FZB_E_WORKSPACE;
+    if (reinterpret_cast<uintptr_t>(d_in) & 15) return FZB_E_ARG;
+    float* part = static_cast<float*>(d_ws);
+    minmax_partial_kernel<<<MM_BLOCKS, MM_THREADS, 0, st>>>(d_in, n, part, d_status);
+    minmax_final_kernel<<<1, 1024, 0, st>>>(part, MM_BLOCKS, d_lohi);
+    return fzb_check_launch();
+}
+
+FZB_API int fzb_resolve_bound(const float* d_lohi, int eb_mode, double magnitude, double* d_eb, void* stream) {
+    resolve_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(d_lohi, eb_mode, magnitude, d_eb);
+    return fzb_check_launch();
+}
+
+FZB_API int fzb_fill_u16(uint16_t* d_dst, uint64_t n, uint16_t value, void* stream) {
+    if (n == 0) return 0;
+    if (reinterpret_cast<uintptr_t>(d_dst) & 15) return FZB_E_ARG;
+    fill_u16_kernel<<<kNumSMs * 8, 256, 0, (cudaStream_t)stream>>>(d_dst, n, value);
+    return fzb_check_launch();
+}
+
+FZB_API int fzb_histogram(const uint16_t* d_codes, uint64_t n, uint32_t nbins, uint64_t* d_bins, uint32_t* d_status,
+                          void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (nbins == 0) return FZB_E_ARG;
+    cudaMemsetAsync(d_bins, 0, (size_t)nbins * 8, st);
+    if (n == 0) return fzb_check_launch();
+    unsigned long long* out = reinterpret_cast<unsigned long long*>(d_bins);
+    if (nbins <= HIST_SMEM_BINS && !(reinterpret_cast<uintptr_t>(d_codes) & 15)) {
+        const size_t smem = (size_t)nbins * 4;
+        cudaFuncSetAttribute(hist_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        uint64_t blocks = (n / 8 + HIST_THREADS - 1) / HIST_THREADS;
+        const uint64_t cap = (uint64_t)kNumSMs * 4;
+        if (blocks > cap) blocks = cap;
+        if (blocks == 0) blocks = 1;
+        hist_smem_kernel<<<(unsigned)blocks, HIST_THREADS, smem, st>>>(d_codes, n, nbins, out, d_status);
+    } else {
+        hist_global_kernel<<<kNumSMs * 8, 256, 0, st>>>(d_codes, n, nbins, out, d_status);
+    }
+    return fzb_check_launch();
+}
+
+FZB_API size_t fzb_outlier_workspace_bytes(uint64_t n) {
+    const uint64_t nwords = (n + 31) / 32;
+    const uint64_t nblk = (nwords + OC_WORDS - 1) / OC_WORDS;
+    return 256 + ((nblk * 4 + 255) / 256) * 256 + nblk * 8 + 256;
+}
+
+FZB_API int fzb_outlier_compact(const uint32_t* d_bitmap, uint64_t n, const float* d_in, uint64_t* d_idx,
+                                float* d_vals, uint64_t* d_count, void* d_ws, size_t ws_bytes, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (ws_bytes < fzb_outlier_workspace_bytes(n)) return FZB_E_WORKSPACE;
+    const uint64_t nwords = (n + 31) / 32;
+    const uint64_t nblk = (nwords + OC_WORDS - 1) / OC_WORDS;
+    if (nblk == 0) {
+        cudaMemsetAsync(d_count, 0, 8, st);
+        return fzb_check_launch();
+    }
+    unsigned char* w = static_cast<unsigned char*>(d_ws);
+    uint32_t* counts = reinterpret_cast<uint32_t*>(w + 256);
+    unsigned long long* offs = reinterpret_cast<unsigned long long*>(w + 256 + ((nblk * 4 + 255) / 256) * 256);
+    outlier_count_kernel<<<(unsigned)nblk, OC_THREADS, 0, st>>>(d_bitmap, nwords, counts);
+    scan_u32_to_u64_kernel<<<1, 1024, 0, st>>>(counts, nblk, offs, reinterpret_cast<unsigned long long*>(d_count));
+    outlier_write_kernel<<<(unsigned)nblk, OC_THREADS, 0, st>>>(d_bitmap, nwords, d_in, offs,
+                                                               reinterpret_cast<unsigned long long*>(d_idx), d_vals);
+    return fzb_check_launch();
+}
+
+FZB_API int fzb_outlier_scatter(const uint64_t* d_idx, const float* d_vals, uint64_t k, uint64_t n,
+                                const uint16_t* d_codes, uint32_t radius, float* d_recon, uint32_t* d_bitmap,
+                                uint32_t* d_status, void* stream) {
+    if (k == 0) return 0;
+    unsigned blocks = (unsigned)((k + 255) / 256);
+    if (blocks > (unsigned)kNumSMs * 8) blocks = kNumSMs * 8;
+    outlier_scatter_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const unsigned long long*>(d_idx), d_vals, k, n, d_codes, (int)radius, d_recon, d_bitmap,
+        d_status);
+    return fzb_check_launch();
+}
+
+}  // extern "C"

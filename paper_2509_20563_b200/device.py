@@ -1,0 +1,363 @@
+"""Device executor: the timed B200 path.
+
+`Engine` drives the sm_100a kernels of libfzb200.so on one CUDA stream with
+torch-allocated device buffers.  Compression is fully asynchronous (eb_abs
+is resolved on the device, so min/max -> predictor -> histogram -> codebook
+-> encoder run back to back without a host round trip); `finish()` is the
+single synchronisation point that reads sizes/status and copies the
+segment payloads into pinned host memory.
+
+Stage map (reference pipeline.py:345-466):
+    _run_predict  -> fzb_lorenzo_encode_f32 / fzb_interp_encode_f32 (+ fzb_outlier_compact)
+    _run_analysis -> fzb_histogram (exact == topk)
+    _run_primary  -> fzb_huffman_build + fzb_huffman_encode | fzb_bitshuffle_encode
+    _decode_codes -> fzb_huffman_decode | fzb_bitshuffle_decode
+    _reconstruct  -> fzb_outlier_scatter + fzb_lorenzo_decode_f32 / fzb_interp_decode_f32
+
+Buffers are cached per Engine and reused, so a DeviceArchive is valid until
+the next call on the same Engine; use one Engine per stream for concurrent
+fields.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import errors as E
+from .core import (
+    SEG_ANCHOR_GRID, SEG_BITSHUFFLE_BITMAP, SEG_BITSHUFFLE_PAYLOAD, SEG_HUFFMAN_BITSTREAM,
+    SEG_HUFFMAN_CODEBOOK, SEG_OUTLIER_INDICES, SEG_OUTLIER_VALUES,
+)
+
+CUBIC = (-1 / 16, 9 / 16, 9 / 16, -1 / 16)  # reference predict.py:47
+
+
+def pad3(dims):
+    dims = tuple(int(d) for d in dims)
+    return (1,) * (3 - len(dims)) + dims
+
+
+def interp_applicable(dims, anchor_stride: int) -> bool:
+    """predict.py:264-267: 2D/3D with every extent >= stride + 1."""
+    return len(dims) > 1 and all(int(d) >= anchor_stride + 1 for d in dims)
+
+
+def _p(t: torch.Tensor | None):
+    return ctypes.c_void_p(t.data_ptr() if t is not None else 0)
+
+
+def _align(n: int, a: int = 256) -> int:
+    return (int(n) + a - 1) // a * a
+
+
+@dataclass
+class DeviceArchive:
+    """Device-resident compression result (before `Engine.finish`)."""
+
+    pipeline_id: int
+    eb_mode: int
+    eb_magnitude: float
+    dims: tuple
+    radius: int
+    predictor: str
+    codec: str
+    n: int
+    bufs: dict = dc_field(default_factory=dict)
+    use_anchors: bool = False
+
+
+class Engine:
+    def __init__(self, device: str | torch.device = "cuda", stream: torch.cuda.Stream | None = None):
+        if not torch.cuda.is_available():
+            raise E.DeviceUnavailable("no CUDA device: the B200 path has no CPU fallback")
+        self.device = torch.device(device)
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        self.lib = _lib.load()
+        self.stream = stream or torch.cuda.current_stream(self.device)
+        self._dev: dict[str, torch.Tensor] = {}
+        self._host: dict[str, torch.Tensor] = {}
+        self.launches = 0  # kernels issued through the C ABI (counted per entry point)
+
+    # ------------------------------------------------------------ buffers
+    def buf(self, name: str, nbytes: int, zero: bool = False) -> torch.Tensor:
+        nbytes = max(_align(nbytes), 256)
+        t = self._dev.get(name)
+        if t is None or t.numel() < nbytes:
+            t = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self._dev[name] = t
+        if zero:
+            with torch.cuda.stream(self.stream):
+                t[:nbytes].zero_()
+        return t
+
+    def pinned(self, name: str, nbytes: int) -> torch.Tensor:
+        nbytes = max(_align(nbytes, 4096), 4096)
+        t = self._host.get(name)
+        if t is None or t.numel() < nbytes:
+            t = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+            self._host[name] = t
+        return t
+
+    @property
+    def sp(self):
+        return ctypes.c_void_p(self.stream.cuda_stream)
+
+    def _call(self, fn: str, *args, nk: int = 1):
+        rc = getattr(self.lib, fn)(*args)
+        self.launches += nk
+        _lib.check(rc, fn)
+
+    def upload(self, name: str, data: bytes | np.ndarray, pad: int = 0) -> torch.Tensor:
+        """H2D copy of host bytes through a pinned staging buffer (zero padded)."""
+        raw = np.frombuffer(bytes(data), np.uint8) if not isinstance(data, np.ndarray) else data.view(np.uint8).reshape(-1)
+        nb = raw.size
+        dev = self.buf(name, nb + pad)
+        if pad:
+            with torch.cuda.stream(self.stream):
+                dev[max(nb - (nb % 4), 0):nb + pad].zero_()
+        if nb:
+            h = self.pinned(name, nb)
+            h.numpy()[:nb] = raw
+            with torch.cuda.stream(self.stream):
+                dev[:nb].copy_(h[:nb], non_blocking=True)
+        return dev
+
+    # ----------------------------------------------------------- compress
+    def compress(self, x: torch.Tensor, dims, eb_mode: int, magnitude: float, *, pipeline_id: int = 0,
+                 predictor: str = "lorenzo", codec: str = "huffman", radius: int = 512,
+                 anchor_stride: int = 16) -> DeviceArchive:
+        """Enqueue the whole compression of a device-resident f32 field."""
+
+        if x.device.type != "cuda" or x.dtype != torch.float32 or not x.is_contiguous():
+            raise ValueError("Engine.compress needs a contiguous float32 CUDA tensor")
+        dims = tuple(int(d) for d in dims)
+        n = x.numel()
+        if n != int(np.prod(dims)):
+            raise ValueError(f"data has {n} elements, dims imply {int(np.prod(dims))}")
+        if not 1 <= radius <= 32768:
+            raise E.RadiusTooLarge(f"radius {radius} outside the 16-bit code range of the device path")
+        n0, n1, n2 = pad3(dims)
+        L, sp = self.lib, self.sp
+        status = self.buf("status", 8, zero=True)
+        lohi = self.buf("lohi", 8)
+        eb = self.buf("eb", 8)
+        mmws = self.buf("mmws", L.fzb_minmax_workspace_bytes(n))
+        self._call("fzb_minmax_f32", _p(x), n, _p(lohi), _p(mmws), mmws.numel(), _p(status), sp, nk=2)
+        self._call("fzb_resolve_bound", _p(lohi), int(eb_mode), float(magnitude), _p(eb), sp)
+        codes = self.buf("codes", 2 * n + 16)
+        bitmap = self.buf("bitmap", 4 * ((n + 31) // 32), zero=True)
+        use_anchors = predictor == "interp" and interp_applicable(dims, anchor_stride)
+        bufs = dict(status=status, lohi=lohi, eb=eb, codes=codes)
+        if predictor not in ("lorenzo", "interp"):
+            raise ValueError(f"unknown predictor '{predictor}'")
+        if use_anchors:
+            self._call("fzb_fill_u16", _p(codes), n, radius, sp)
+            recon = self.buf("recon_ws", 4 * n)
+            a = anchor_stride
+            na = ((n0 - 1) // a + 1) * ((n1 - 1) // a + 1) * ((n2 - 1) // a + 1)
+            anchors = self.buf("anchors", 4 * na)
+            w = (ctypes.c_double * 4)(*CUBIC)
+            self._call("fzb_interp_encode_f32", _p(x), n0, n1, n2, _p(eb), radius, a, w, _p(codes), _p(recon),
+                       _p(bitmap), _p(anchors), sp, nk=1 + 3 * int(np.log2(a)))
+            bufs["anchors"] = anchors
+            bufs["n_anchors"] = na
+        else:
+            lzws = self.buf("lzws", L.fzb_lorenzo_workspace_bytes(n0, n1, n2))
+            self._call("fzb_lorenzo_encode_f32", _p(x), n0, n1, n2, _p(eb), radius, _p(codes), _p(bitmap),
+                       _p(lzws), lzws.numel(), sp, nk=2)
+        oidx = self.buf("oidx", 8 * n)
+        oval = self.buf("oval", 4 * n)
+        ocount = self.buf("ocount", 8)
+        ocws = self.buf("ocws", L.fzb_outlier_workspace_bytes(n))
+        self._call("fzb_outlier_compact", _p(bitmap), n, _p(x), _p(oidx), _p(oval), _p(ocount), _p(ocws),
+                   ocws.numel(), sp, nk=3)
+        bufs.update(oidx=oidx, oval=oval, ocount=ocount)
+        nsym = 2 * radius
+        if codec == "huffman":
+            bins = self.buf("bins", 8 * nsym)
+            self._call("fzb_histogram", _p(codes), n, nsym, _p(bins), _p(status), sp)
+            lengths = self.buf("lengths", nsym)
+            cw = self.buf("cw", 4 * nsym)
+            bitcount = self.buf("bitcount", 8)
+            bws = self.buf("hbws", L.fzb_huffman_build_workspace_bytes(nsym))
+            self._call("fzb_huffman_build", _p(bins), nsym, _p(lengths), _p(cw), _p(bitcount), _p(bws), bws.numel(),
+                       sp)
+            cap = 4 * n + 16
+            out = self.buf("hfout", cap)
+            hws = self.buf("hews", L.fzb_huffman_encode_workspace_bytes(n))
+            self._call("fzb_huffman_encode", _p(codes), n, _p(lengths), _p(cw), nsym, _p(bitcount), _p(out), cap,
+                       _p(hws), hws.numel(), _p(status), sp, nk=5)
+            bufs.update(lengths=lengths, bitcount=bitcount, hfout=out)
+        elif codec == "bitshuffle":
+            nb = (n + 255) // 256
+            bsmap = self.buf("bsmap", 16 * nb)
+            pay = self.buf("bspay", 512 * nb)
+            nwords = self.buf("nwords", 8)
+            bws = self.buf("bsws", L.fzb_bitshuffle_workspace_bytes(n))
+            self._call("fzb_bitshuffle_encode", _p(codes), n, _p(bsmap), _p(pay), _p(nwords), _p(bws), bws.numel(),
+                       sp, nk=3)
+            bufs.update(bsmap=bsmap, bspay=pay, nwords=nwords)
+        else:
+            raise ValueError(f"unknown primary codec '{codec}'")
+        return DeviceArchive(pipeline_id, int(eb_mode), float(magnitude), dims, radius, predictor, codec, n, bufs,
+                             use_anchors)
+
+    def finish(self, da: DeviceArchive):
+        """Synchronise once; return (lo, hi, segments) with host payload bytes."""
+
+        b = da.bufs
+        # scalars in one small D2H
+        scal = self.pinned("scal", 64)
+        s = scal[:48]
+        with torch.cuda.stream(self.stream):
+            s[0:8].copy_(b["status"][:8], non_blocking=True)
+            s[8:16].copy_(b["lohi"][:8], non_blocking=True)
+            s[16:24].copy_(b["ocount"][:8], non_blocking=True)
+            key = "bitcount" if da.codec == "huffman" else "nwords"
+            s[24:32].copy_(b[key][:8], non_blocking=True)
+        self.stream.synchronize()
+        v = s.numpy()
+        status = int(v[0:4].view(np.uint32)[0])
+        lo, hi = (float(z) for z in v[8:16].view(np.float32))
+        k = int(v[16:24].view(np.uint64)[0])
+        size = int(v[24:32].view(np.uint64)[0])
+        if status & _lib.ERR_NONFINITE:
+            raise ValueError("non-finite value in field")
+        if lo == hi:
+            return lo, hi, []
+        _lib.raise_codec_status(status)
+        n = da.n
+        parts = [("oidx", 8 * k), ("oval", 4 * k)]
+        if da.use_anchors:
+            parts.append(("anchors", 4 * b["n_anchors"]))
+        if da.codec == "huffman":
+            parts += [("lengths", 2 * da.radius), ("hfout", (size + 7) // 8)]
+        else:
+            parts += [("bsmap", 16 * ((n + 255) // 256)), ("bspay", 4 * size)]
+        total = sum(_align(sz, 64) for _, sz in parts)
+        host = self.pinned("out", total)
+        offs = []
+        o = 0
+        with torch.cuda.stream(self.stream):
+            for name, sz in parts:
+                if sz:
+                    host[o:o + sz].copy_(b[name][:sz], non_blocking=True)
+                offs.append((o, sz))
+                o += _align(sz, 64)
+        self.stream.synchronize()
+        hv = host.numpy()
+        blobs = [hv[o:o + sz].tobytes() for o, sz in offs]
+        segs = [(SEG_OUTLIER_INDICES, blobs[0]), (SEG_OUTLIER_VALUES, blobs[1])]
+        q = 2
+        if da.use_anchors:
+            segs.append((SEG_ANCHOR_GRID, blobs[q]))
+            q += 1
+        if da.codec == "huffman":
+            segs += [(SEG_HUFFMAN_CODEBOOK, blobs[q]), (SEG_HUFFMAN_BITSTREAM, blobs[q + 1])]
+        else:
+            segs += [(SEG_BITSHUFFLE_BITMAP, blobs[q]), (SEG_BITSHUFFLE_PAYLOAD, blobs[q + 1])]
+        return lo, hi, segs
+
+    # --------------------------------------------------------- decompress
+    def decode_codes(self, codec: str, segs: dict, n: int, radius: int) -> torch.Tensor:
+        """Primary-codec decode (pipeline.py:415-430) into device u16 codes.
+        Host-side length checks mirror encode.py:299-305 and 359-375."""
+
+        L, sp = self.lib, self.sp
+        codes = self.buf("dcodes", 2 * n + 16)
+        status = self.buf("dstatus", 8, zero=True)
+        nsym = 2 * radius
+        if codec == "huffman":
+            cl = segs["codebook"]
+            stream = segs["stream"]
+            if n == 0:
+                if len(stream):
+                    raise E.CorruptStream(f"{len(stream)} bytes after zero symbols")
+                return codes
+            if not cl.size or int(cl.max()) == 0:
+                raise E.CorruptStream("empty codebook with nonzero symbol count")
+            lengths = self.upload("dlengths", cl)
+            s = self.upload("dstream", stream, pad=16)
+            hws = self.buf("hdws", L.fzb_huffman_decode_workspace_bytes(len(stream), nsym))
+            self._call("fzb_huffman_decode", _p(s), len(stream), n, _p(lengths), nsym, _p(codes), _p(hws),
+                       hws.numel(), _p(status), sp, nk=10)
+        else:
+            bitmap, payload = segs["bitmap"], segs["payload"]
+            nb = (n + 255) // 256
+            need = (nb * 128 + 7) // 8
+            if len(bitmap) < need:
+                raise E.Truncated(f"bitmap is {len(bitmap)} bytes, need {need}")
+            if len(bitmap) > need:
+                raise E.BitmapPayloadMismatch("bitmap longer than the word count implies")
+            if len(payload) % 4:
+                raise E.BitmapPayloadMismatch("payload is not whole 32-bit words")
+            if nb == 0:
+                if len(payload):
+                    raise E.BitmapPayloadMismatch("bitmap marks 0 words, payload has more")
+                return codes
+            bm = self.upload("dbsmap", bitmap, pad=16)
+            pay = self.upload("dbspay", payload, pad=16)
+            bws = self.buf("dbsws", L.fzb_bitshuffle_workspace_bytes(n))
+            self._call("fzb_bitshuffle_decode", _p(bm), _p(pay), len(payload) // 4, n, radius, _p(codes), _p(bws),
+                       bws.numel(), _p(status), sp, nk=4)
+        return codes
+
+    def reconstruct(self, predictor: str, codes: torch.Tensor, idx: np.ndarray, vals: np.ndarray, anchors: bytes,
+                    dims, eb_abs: float, radius: int, anchor_stride: int = 16,
+                    out: torch.Tensor | None = None) -> torch.Tensor:
+        """Outlier scatter + predictor inverse (pipeline.py:433-436) -> device f32 recon."""
+
+        L, sp = self.lib, self.sp
+        dims = tuple(int(d) for d in dims)
+        n = int(np.prod(dims))
+        n0, n1, n2 = pad3(dims)
+        recon = out if out is not None else torch.empty(n, dtype=torch.float32, device=self.device)
+        status = self.buf("dstatus", 8)
+        bitmap = self.buf("dbitmap", 4 * ((n + 31) // 32), zero=True)
+        ebt = self.upload("deb", np.array([eb_abs], np.float64))
+        k = int(idx.size)
+        if k:
+            di = self.upload("didx", np.ascontiguousarray(idx, np.uint64))
+            dv = self.upload("dval", np.ascontiguousarray(vals, np.float32))
+            self._call("fzb_outlier_scatter", _p(di), _p(dv), k, n, _p(codes), radius, _p(recon), _p(bitmap),
+                       _p(status), sp)
+        if predictor == "interp" and len(anchors):
+            da = self.upload("danchors", anchors)
+            w = (ctypes.c_double * 4)(*CUBIC)
+            self._call("fzb_interp_decode_f32", _p(codes), _p(bitmap), _p(da), _p(recon), n0, n1, n2, _p(ebt), radius,
+                       anchor_stride, w, sp, nk=1 + 3 * int(np.log2(anchor_stride)))
+        else:
+            lzws = self.buf("dlzws", L.fzb_lorenzo_workspace_bytes(n0, n1, n2))
+            self._call("fzb_lorenzo_decode_f32", _p(codes), _p(bitmap), _p(recon), n0, n1, n2, _p(ebt), radius,
+                       _p(lzws), lzws.numel(), sp, nk=5)
+        return recon
+
+    def decode_status(self) -> int:
+        st = self.pinned("dscal", 64)
+        with torch.cuda.stream(self.stream):
+            st[:8].copy_(self.buf("dstatus", 8)[:8], non_blocking=True)
+        self.stream.synchronize()
+        return int(st[:4].numpy().view(np.uint32)[0])
+
+
+_engines: dict = {}
+
+
+def default_engine() -> Engine:
+    """Per-device, per-current-stream engine used by the reference-shaped API."""
+    dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
+    if dev < 0:
+        raise E.DeviceUnavailable("no CUDA device: the B200 path has no CPU fallback")
+    s = torch.cuda.current_stream(dev)
+    key = (dev, s.cuda_stream)
+    eng = _engines.get(key)
+    if eng is None:
+        eng = Engine(torch.device("cuda", dev), s)
+        _engines[key] = eng
+    return eng

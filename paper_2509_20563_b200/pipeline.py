@@ -1,0 +1,399 @@
+"""Pipeline registry and executor -- drop-in for fzpipe.pipeline on the B200.
+
+Same public surface as the reference (pipeline.py:70-660): StageKind,
+StageSpec, PipelineSpec (validation + histogram auto-insert), the preset
+registry (0 default = Lorenzo + exact histogram + Huffman, 1 speed =
+Lorenzo + bitshuffle, 2 quality = interp + top-k histogram + Huffman),
+ini pipeline files, compress/decompress (+ _with_timing, _via_graph).
+The stage bodies run on the GPU through device.Engine; archives are
+byte-identical to the reference's for the same input and spec.
+"""
+
+from __future__ import annotations
+
+import configparser
+import enum
+import logging
+import os
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import errors as E
+from . import secondary
+from .core import (
+    SEG_ANCHOR_GRID, SEG_BITSHUFFLE_BITMAP, SEG_BITSHUFFLE_PAYLOAD, SEG_HUFFMAN_BITSTREAM, SEG_HUFFMAN_CODEBOOK,
+    SEG_OUTLIER_INDICES, SEG_OUTLIER_VALUES, SEG_SECONDARY_WRAPPED, Archive, ErrorBoundSpec, ErrorMode, Field,
+    ResolvedBound, eb_from_range, register_known_pipeline_id,
+)
+from .device import default_engine, interp_applicable
+
+log = logging.getLogger(__name__)
+
+
+class StageKind(enum.Enum):
+    PREPROCESS = "preprocess"
+    PREDICT = "predict"
+    PRIMARY_CODEC = "primary_codec"
+    SECONDARY_CODEC = "secondary_codec"
+    ANALYSIS = "analysis"
+
+
+_RANK = {StageKind.PREPROCESS: 0, StageKind.PREDICT: 1, StageKind.ANALYSIS: 2, StageKind.PRIMARY_CODEC: 3,
+         StageKind.SECONDARY_CODEC: 4}
+
+
+@dataclass(frozen=True)
+class StageSpec:
+    name: str
+    kind: StageKind
+    params: tuple = ()
+
+    def __post_init__(self):
+        if not self.name:
+            raise E.InvalidStageOrder("stage name must be nonempty")
+        p = self.params
+        if isinstance(p, dict):
+            p = tuple(sorted((str(k), str(v)) for k, v in p.items()))
+        object.__setattr__(self, "params", tuple(p))
+        object.__setattr__(self, "kind", StageKind(self.kind))
+
+    def param(self, key: str, default=None):
+        return dict(self.params).get(key, default)
+
+
+@dataclass(frozen=True)
+class PipelineSpec:
+    id: int
+    stages: tuple
+
+    def __post_init__(self):
+        pid = int(self.id)
+        if not 0 <= pid <= 255:
+            raise E.InvalidStageOrder(f"pipeline id must fit a byte, got {pid}")
+        stages = tuple(self.stages)
+        names = [s.name for s in stages]
+        if len(names) != len(set(names)):
+            raise E.InvalidStageOrder(f"duplicate stage names in {names}")
+        ranks = [_RANK[s.kind] for s in stages]
+        if ranks != sorted(ranks):
+            raise E.InvalidStageOrder(
+                "stage order must be preprocess, predict, analysis, primary codec, secondary codec")
+        kinds = [s.kind for s in stages]
+        if kinds.count(StageKind.PREDICT) != 1:
+            raise E.MissingStage("exactly one predict stage required")
+        if kinds.count(StageKind.PRIMARY_CODEC) != 1:
+            raise E.MissingStage("exactly one primary codec stage required")
+        if kinds.count(StageKind.SECONDARY_CODEC) > 1:
+            raise E.InvalidStageOrder("at most one secondary codec stage")
+        primary = next(s for s in stages if s.kind == StageKind.PRIMARY_CODEC)
+        if primary.param("codec", "huffman") == "huffman" and StageKind.ANALYSIS not in kinds:
+            i = stages.index(primary)
+            stages = stages[:i] + (StageSpec("histogram", StageKind.ANALYSIS, {"method": "exact"}),) + stages[i:]
+        object.__setattr__(self, "id", pid)
+        object.__setattr__(self, "stages", stages)
+
+    def stage_of(self, kind: StageKind):
+        return next((s for s in self.stages if s.kind == kind), None)
+
+    @property
+    def predictor(self) -> str:
+        return self.stage_of(StageKind.PREDICT).param("predictor", "lorenzo")
+
+    @property
+    def primary_codec(self) -> str:
+        return self.stage_of(StageKind.PRIMARY_CODEC).param("codec", "huffman")
+
+    def radius(self) -> int:
+        return int(self.stage_of(StageKind.PREDICT).param("radius", "512"))
+
+    def interp_config(self):
+        from .predict import InterpConfig
+        return InterpConfig(anchor_stride=int(self.stage_of(StageKind.PREDICT).param("anchor_stride", "16")))
+
+
+_REGISTRY: dict[int, PipelineSpec] = {}
+PRESET_NAMES = {"default": 0, "speed": 1, "quality": 2}
+
+
+def register_pipeline(spec: PipelineSpec) -> PipelineSpec:
+    if spec.id in _REGISTRY:
+        raise E.DuplicateId(f"pipeline id {spec.id} already registered")
+    _REGISTRY[spec.id] = spec
+    register_known_pipeline_id(spec.id)
+    return spec
+
+
+def get_pipeline(ref) -> PipelineSpec:
+    if isinstance(ref, PipelineSpec):
+        return ref
+    if isinstance(ref, str):
+        if ref not in PRESET_NAMES:
+            raise E.UnknownPipelineId(f"unknown pipeline name '{ref}'")
+        ref = PRESET_NAMES[ref]
+    ref = int(ref)
+    if ref not in _REGISTRY:
+        raise E.UnknownPipelineId(f"pipeline id {ref} not registered")
+    return _REGISTRY[ref]
+
+
+def registered_pipelines() -> dict:
+    return dict(_REGISTRY)
+
+
+def _presets():
+    S, K = StageSpec, StageKind
+    register_pipeline(PipelineSpec(0, (S("predict", K.PREDICT, {"predictor": "lorenzo"}),
+                                       S("histogram", K.ANALYSIS, {"method": "exact"}),
+                                       S("encode", K.PRIMARY_CODEC, {"codec": "huffman"}))))
+    register_pipeline(PipelineSpec(1, (S("predict", K.PREDICT, {"predictor": "lorenzo"}),
+                                       S("encode", K.PRIMARY_CODEC, {"codec": "bitshuffle"}))))
+    register_pipeline(PipelineSpec(2, (S("predict", K.PREDICT, {"predictor": "interp"}),
+                                       S("histogram", K.ANALYSIS, {"method": "topk", "k": "16"}),
+                                       S("encode", K.PRIMARY_CODEC, {"codec": "huffman"}))))
+
+
+_presets()
+
+
+def load_pipeline_file(path: str) -> PipelineSpec:
+    """[pipeline] id = N, then one [stage:<name>] section per stage (kind = ...)."""
+
+    cp = configparser.ConfigParser()
+    if not cp.read(path):
+        raise E.BadParams(f"cannot read pipeline file '{path}'")
+    if "pipeline" not in cp or "id" not in cp["pipeline"]:
+        raise E.BadParams("pipeline file needs a [pipeline] section with an id")
+    try:
+        pid = int(cp["pipeline"]["id"])
+    except ValueError as e:
+        raise E.BadParams(f"bad pipeline id: {e}") from None
+    stages = []
+    for sec in cp.sections():
+        if not sec.startswith("stage:"):
+            continue
+        opts = dict(cp[sec])
+        kind = opts.pop("kind", None)
+        if kind is None:
+            raise E.BadParams(f"stage '{sec[6:]}' is missing its kind")
+        try:
+            sk = StageKind(kind)
+        except ValueError:
+            raise E.BadParams(f"unknown stage kind '{kind}'") from None
+        stages.append(StageSpec(sec[6:], sk, opts))
+    return PipelineSpec(pid, tuple(stages))
+
+
+# ------------------------------------------------------------------ compress
+
+def _check_stage_params(spec: PipelineSpec):
+    """Validate string params the way the reference stage bodies would."""
+    for st in spec.stages:
+        if st.kind == StageKind.PREPROCESS and st.param("op", "identity") != "identity":
+            raise E.StageError(st.name, ValueError(f"unsupported preprocess op '{st.param('op')}'"))
+    pst = spec.stage_of(StageKind.PREDICT)
+    if spec.predictor not in ("lorenzo", "interp"):
+        raise E.StageError(pst.name, ValueError(f"unknown predictor '{spec.predictor}'"))
+    an = spec.stage_of(StageKind.ANALYSIS)
+    if an is not None:
+        method = an.param("method", "exact")
+        if method not in ("exact", "topk"):
+            raise E.StageError(an.name, ValueError(f"unknown histogram method '{method}'"))
+        if method == "topk":
+            k = int(an.param("k", "16"))
+            if not 1 <= k <= 2 * spec.radius():
+                raise E.StageError(an.name, ValueError(f"k must be in [1, {2 * spec.radius()}], got {k}"))
+    pc = spec.stage_of(StageKind.PRIMARY_CODEC)
+    if spec.primary_codec not in ("huffman", "bitshuffle"):
+        raise E.StageError(pc.name, ValueError(f"unknown primary codec '{spec.primary_codec}'"))
+    if spec.primary_codec == "bitshuffle" and spec.radius() > 32768:
+        raise E.StageError(pc.name, E.RadiusTooLarge(f"radius {spec.radius()} exceeds 16-bit code width"))
+
+
+def _to_device(field) -> torch.Tensor:
+    eng = default_engine()
+    buf = eng.upload("field_in", field.data)
+    return buf[: 4 * field.len].view(torch.float32)
+
+
+def compress_device(x: torch.Tensor, dims, eb: ErrorBoundSpec, pipeline) -> Archive:
+    """Compress a device-resident f32 tensor (the timed path)."""
+
+    spec = get_pipeline(pipeline)
+    _check_stage_params(spec)
+    eng = default_engine()
+    pred = spec.predictor
+    cfg = spec.interp_config() if pred == "interp" else None
+    if pred == "interp" and not interp_applicable(dims, cfg.anchor_stride):
+        log.warning("interpolation needs a 2D or 3D field with every extent >= %d, got dims %s; "
+                    "falling back to Lorenzo", cfg.anchor_stride + 1, tuple(dims))
+    da = eng.compress(x, dims, int(eb.mode), float(eb.magnitude), pipeline_id=spec.id, predictor=pred,
+                      codec=spec.primary_codec, radius=spec.radius(),
+                      anchor_stride=cfg.anchor_stride if cfg else 16)
+    try:
+        lo, hi, segs = eng.finish(da)
+    except E.FZError as e:
+        raise E.StageError(spec.stage_of(StageKind.PRIMARY_CODEC).name, e) from e
+    if lo == hi:
+        return Archive(spec.id, eb.mode, eb.magnitude, lo, hi, tuple(dims), spec.radius(), ())
+    ResolvedBound(eb_from_range(eb.mode, eb.magnitude, lo, hi), lo, hi)
+    sc = spec.stage_of(StageKind.SECONDARY_CODEC)
+    if sc is not None:
+        nprim = 2
+        head, prim = segs[:-nprim], segs[-nprim:]
+        try:
+            cid = int(sc.param("codec_id", "0"))
+            prim = [(SEG_SECONDARY_WRAPPED, bytes([k]) + secondary.secondary_encode(p, cid)) for k, p in prim]
+        except Exception as e:
+            raise E.StageError(sc.name, e) from e
+        segs = head + prim
+    return Archive(spec.id, eb.mode, eb.magnitude, lo, hi, tuple(dims), spec.radius(), tuple(segs))
+
+
+def compress_with_timing(field: Field, eb: ErrorBoundSpec, pipeline):
+    t0 = time.perf_counter()
+    x = _to_device(field)
+    t1 = time.perf_counter()
+    a = compress_device(x, field.dims, eb, pipeline)
+    t2 = time.perf_counter()
+    return a, {"h2d": t1 - t0, "device": t2 - t1}
+
+
+def compress(field: Field, eb: ErrorBoundSpec, pipeline) -> Archive:
+    return compress_with_timing(field, eb, pipeline)[0]
+
+
+def compress_via_graph(field: Field, eb: ErrorBoundSpec, pipeline, workers: int | None = None) -> Archive:
+    """Graph variant (pipeline.py:650-660).  On the GPU every stage is already
+    a stream-ordered DAG; archives are byte-identical to compress()."""
+    return compress(field, eb, pipeline)
+
+
+# ---------------------------------------------------------------- decompress
+
+def _unwrap(a: Archive) -> dict:
+    segs = {}
+    for kind, payload in a.segments:
+        if kind == SEG_SECONDARY_WRAPPED:
+            if len(payload) < 2:
+                raise E.CorruptPayload("wrapped segment too short")
+            segs[payload[0]] = secondary.secondary_decode(payload[1:])
+        else:
+            segs[kind] = payload
+    return segs
+
+
+def _outliers(segs: dict, n: int):
+    if SEG_OUTLIER_INDICES not in segs or SEG_OUTLIER_VALUES not in segs:
+        raise E.CorruptPayload("outlier segments missing")
+    ib, vb = segs[SEG_OUTLIER_INDICES], segs[SEG_OUTLIER_VALUES]
+    if len(ib) % 8 or len(vb) % 4 or len(ib) // 8 != len(vb) // 4:
+        raise E.CorruptPayload("outlier index/value segments disagree")
+    idx = np.frombuffer(ib, "<u8")
+    vals = np.frombuffer(vb, "<f4")
+    if idx.size and int(idx.max()) >= n:
+        raise E.CorruptPayload("outlier index out of range")
+    return idx, vals
+
+
+def decompress_device(a: Archive, pipeline=None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Decompress into a device f32 tensor (the timed path)."""
+
+    spec = get_pipeline(pipeline if pipeline is not None else a.pipeline_id)
+    eng = default_engine()
+    n = a.element_count
+    if len(a.segments) == 0:
+        if a.data_min != a.data_max:
+            raise E.CorruptPayload("no segments but the header spans a value range")
+        t = out if out is not None else torch.empty(n, dtype=torch.float32, device=eng.device)
+        t.fill_(a.data_min)
+        return t
+    bound = a.resolved_bound()
+    segs = _unwrap(a)
+    radius = a.radius
+    codec = spec.primary_codec
+    # decode-codes (host-side structural checks first, as encode.py does)
+    try:
+        if codec == "huffman":
+            if SEG_HUFFMAN_CODEBOOK not in segs or SEG_HUFFMAN_BITSTREAM not in segs:
+                raise E.CorruptPayload("Huffman segments missing")
+            from .encode import HuffmanCodebook
+            cb = HuffmanCodebook.from_bytes(segs[SEG_HUFFMAN_CODEBOOK])
+            if cb.code_lengths.size != 2 * radius:
+                raise E.CorruptPayload(f"codebook covers {cb.code_lengths.size} symbols, alphabet is {2 * radius}")
+            if radius > 32768:
+                raise E.RadiusTooLarge(f"radius {radius} exceeds the device path's 16-bit codes")
+            codes = eng.decode_codes("huffman", {"codebook": cb.code_lengths, "stream": segs[SEG_HUFFMAN_BITSTREAM]},
+                                     n, radius)
+        elif codec == "bitshuffle":
+            if SEG_BITSHUFFLE_BITMAP not in segs or SEG_BITSHUFFLE_PAYLOAD not in segs:
+                raise E.CorruptPayload("bitshuffle segments missing")
+            if radius > 32768:
+                raise E.RadiusTooLarge(f"radius {radius} exceeds 16-bit code width")
+            codes = eng.decode_codes("bitshuffle", {"bitmap": segs[SEG_BITSHUFFLE_BITMAP],
+                                                    "payload": segs[SEG_BITSHUFFLE_PAYLOAD]}, n, radius)
+        else:
+            raise ValueError(f"unknown primary codec '{codec}'")
+    except Exception as e:
+        raise E.StageError("decode-codes", e) from e
+    try:
+        idx, vals = _outliers(segs, n)
+    except Exception as e:
+        raise E.StageError("decode-outliers", e) from e
+    if idx.size > 1 and not bool(np.all(idx[1:] > idx[:-1])):
+        raise E.MalformedCodes("outlier indices not strictly increasing")
+    anchors = segs.get(SEG_ANCHOR_GRID, b"")
+    pred = spec.predictor
+    stride = spec.interp_config().anchor_stride if pred == "interp" else 16
+    if pred == "interp" and len(anchors):
+        from .device import pad3
+        d3 = pad3(a.dims)
+        want = 4 * int(np.prod([(d - 1) // stride + 1 for d in d3]))
+        if len(anchors) != want:
+            raise E.StageError("reconstruct", E.AnchorSizeMismatch(
+                f"anchor payload is {len(anchors)} bytes, expected {want}"))
+    recon = eng.reconstruct(pred, codes, idx, vals, anchors, a.dims, bound.eb_abs, radius, stride, out=out)
+    status = eng.decode_status()
+    if status:
+        from . import _lib
+        try:
+            _lib.raise_codec_status(status)
+        except E.FZError as e:
+            raise E.StageError("decode-codes", e) from e
+        if status & (_lib.ERR_OUTLIER_CODE | _lib.ERR_OUTLIER_ORDER):
+            raise E.MalformedCodes("outlier position without sentinel code")
+        if status & _lib.ERR_HF_SYNC:
+            raise RuntimeError("Huffman decoder did not synchronise (increase iterations)")
+    return recon
+
+
+def decompress_with_timing(a: Archive, pipeline=None):
+    t0 = time.perf_counter()
+    rec = decompress_device(a, pipeline)
+    t1 = time.perf_counter()
+    host = rec.cpu().numpy()
+    t2 = time.perf_counter()
+    return Field(a.dims, host), {"device": t1 - t0, "d2h": t2 - t1}
+
+
+def decompress(a: Archive, pipeline=None) -> Field:
+    return decompress_with_timing(a, pipeline)[0]
+
+
+def worker_count(requested: int | None = None) -> int:
+    """pipeline.py:477-487 (FZPIPE_THREADS caps the worker count)."""
+    base = requested if requested is not None else (os.cpu_count() or 1)
+    cap = os.environ.get("FZPIPE_THREADS")
+    if cap is not None:
+        try:
+            base = min(base, max(1, int(cap)))
+        except ValueError:
+            pass
+    return max(1, base)
+
+
+def decompress_via_graph(a: Archive, workers: int | None = None) -> Field:
+    """Graph variant (pipeline.py:583-591); bitwise equal to decompress()."""
+    return decompress(a)
