@@ -206,6 +206,10 @@ lz_wave_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ code
     __syncthreads();
     load_group(0);
     store_group(0);
+    // The corner value r[i0-1, j0-1, 0] lives at step -1 of halo row jj = -1
+    // (slot 31); no group covers negative steps, so load it here.
+    if (tid == 0 && A > 0 && B > 0 && j0 - 1 < n1)
+        HU[RING - 1] = __ldcg(faceI + ((long long)(A - 1) * n1 + (j0 - 1)) * n2);
 
     float up_prev = 0.f, left_prev = 0.f, diag_prev = 0.f, self_prev = 0.f;
 
