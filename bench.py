@@ -1,0 +1,371 @@
+"""Benchmark: FZModules hot path on B200 vs the CPU reference.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2|c1|c3|c4]
+
+Workload (default) = BASELINE.json configs[1]: FZMod-Speed (Lorenzo +
+bitshuffle) on a synthetic smooth_trig 512^3 f32 Nyx-shaped field at rel eb
+1e-3.  A "step" = one compress + decompress round trip of one field per GPU.
+
+* value   : device-resident GB/s (input f32 bytes / step time), input in HBM
+            when the timed region starts; compress kernels -> one 32-byte size
+            read -> decompress kernels on the resident segments.
+* e2e     : the public API (compress(Field) -> Archive -> decompress(Archive)
+            -> Field) from pinned host memory, H2D/D2H inside the timed region.
+* roofline: dominant kernel, algorithmic bytes / CUDA-event duration vs the
+            measured HBM copy peak (MEASURED_PEAKS.json).
+* cpu_baseline: the C oracle (restated fzpipe; test infrastructure) on this
+            box's host cores over a bounded slab sample of the same field.
+Multi-GPU (torchrun): one field per rank (weak scaling); per step the ranks
+all-gather their compressed sizes (the container-offset collective);
+time = max over ranks.  L2 hygiene: every input/working set (537 MB + 268 MB
+codes) exceeds the 126 MB L2.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "c2": dict(name="FZMod-Speed smooth_trig 512x512x512 (Nyx-shaped) rel 1e-3", pipeline="speed",
+               dims=(512, 512, 512), kind="trig", rel=1e-3),
+    "c1": dict(name="FZMod-Default smooth_trig 100x500x500 (Hurricane-shaped) rel 1e-4", pipeline="default",
+               dims=(100, 500, 500), kind="trig", rel=1e-4),
+    "c3": dict(name="FZMod-Quality smooth_trig 1800x3600 (CESM-shaped) rel 1e-4", pipeline="quality",
+               dims=(1800, 3600), kind="trig", rel=1e-4),
+    "c4": dict(name="FZMod-Default particle1d 280953867 (HACC-shaped) rel 1e-4", pipeline="default",
+               dims=(280953867,), kind="particle", rel=1e-4),
+}
+METRIC = "compress/decompress GB/s per GPU & per box at fixed rel eb; CR+PSNR vs CPU ref"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """SM clocks + throttle reasons sampled (NVML, 10 ms) during the timed region."""
+
+    def __init__(self, index: int):
+        self.index, self.rows, self._stop = index, [], threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+
+    def _run(self):
+        nv = self.nv
+        bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                "sw_power_cap": 0x4}
+        while True:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((sm, [k for k, b in bits.items() if r & b]))
+            except Exception:
+                pass
+            if self._stop.wait(0.01):
+                break
+
+    def __enter__(self):
+        if self.ok:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({x for r in self.rows for x in r[1]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.max, "reasons": reasons,
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU side
+
+def cpu_roundtrip(x: np.ndarray, dims, pipeline: str, rel: float, threads: int, slab: int):
+    """Oracle (fzpipe restated in C) compress+decompress on `threads` slabs of
+    `slab` leading planes each; ctypes releases the GIL, so threads run in
+    parallel.  Returns (GB/s, cores, seconds, sample description)."""
+    from oracle import fzoracle as O
+    O.build()
+    nd = x.reshape(dims)
+    lead = dims[0]
+    starts = [(t * slab) % max(lead - slab + 1, 1) for t in range(threads)] if len(dims) > 1 else \
+        [(t * slab) % max(lead - slab + 1, 1) for t in range(threads)]
+    jobs = [np.ascontiguousarray(nd[s:s + slab]) for s in starts]
+    sub_dims = (slab,) + tuple(dims[1:])
+
+    def work(a):
+        blob = O.compress(a.reshape(-1), sub_dims, 1, rel, pipeline)
+        O.decompress(blob)
+
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=work, args=(a,)) for a in jobs]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    dt = time.perf_counter() - t0
+    nbytes = sum(a.nbytes for a in jobs)
+    desc = (f"{threads} thread(s) x {sub_dims} slab of the same field, oracle C port "
+            f"(-O2, no FMA) compress+decompress, {dt:.2f} s wall")
+    return nbytes / dt / 1e9, threads, dt, desc
+
+
+def run_reference(args, wl):
+    """--impl reference: the reference algorithm (C oracle port) on host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2509_20563_b200 import data
+    dims = wl["dims"]
+    x = _host_field(wl)
+    threads = min(os.cpu_count() or 1, 64)
+    slab = _slab(dims)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, cores, dt, desc = cpu_roundtrip(x, dims, wl["pipeline"], wl["rel"], threads, slab)
+        if i >= args.warmup:
+            vals.append(v)
+    v = float(np.median(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 data, f64 predictor arithmetic", "data": "synthetic",
+            "config": {"workload": wl["name"], "pipeline": wl["pipeline"], "dims": list(dims), "rel_eb": wl["rel"]},
+            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "port", "sample": desc},
+            "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _slab(dims):
+    if len(dims) == 3:
+        return max(1, min(dims[0], 32))
+    if len(dims) == 2:
+        return max(17, min(dims[0], 256))
+    return min(dims[0], 1 << 23)
+
+
+_HOST_CACHE = {}
+
+
+def _host_field(wl):
+    key = (wl["dims"], wl["kind"])
+    if key not in _HOST_CACHE:
+        import torch
+        from paper_2509_20563_b200 import data
+        if torch.cuda.is_available():
+            x = _device_field(wl, 0).cpu().numpy()
+        else:
+            x = data.smooth_trig_host(wl["dims"], 0) if wl["kind"] == "trig" else data.particle1d_host(wl["dims"][0])
+        _HOST_CACHE[key] = x
+    return _HOST_CACHE[key]
+
+
+def _device_field(wl, seed):
+    from paper_2509_20563_b200 import data
+    if wl["kind"] == "trig":
+        return data.smooth_trig_device(wl["dims"], seed)
+    return data.particle1d_device(wl["dims"][0], seed)
+
+
+# ------------------------------------------------------------------ GPU side
+
+def run_ours(args, wl):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2509_20563_b200 as fz
+    from paper_2509_20563_b200.core import ErrorBoundSpec, ErrorMode, Field
+    from paper_2509_20563_b200.device import default_engine
+    from paper_2509_20563_b200.metrics import quality_arrays
+    from paper_2509_20563_b200.pipeline import get_pipeline
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    dims = wl["dims"]
+    n = int(np.prod(dims))
+    spec = get_pipeline(wl["pipeline"])
+    x = _device_field(wl, seed=rank).contiguous()
+    eng = default_engine()
+    out = torch.empty(n, dtype=torch.float32, device=dev)
+    ebs = ErrorBoundSpec(ErrorMode.VALUE_RANGE_RELATIVE, wl["rel"])
+
+    def device_step():
+        da = eng.compress(x, dims, 1, wl["rel"], pipeline_id=spec.id, predictor=spec.predictor,
+                          codec=spec.primary_codec, radius=spec.radius())
+        sz = eng.sizes(da)
+        eb_abs = wl["rel"] * (sz["hi"] - sz["lo"])
+        eng.decompress_resident(da, sz, eb_abs, out)
+        if world > 1:
+            t = torch.tensor([eng.compressed_bytes(da, sz)], dtype=torch.int64, device=dev)
+            g = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(g, t)
+        return da, sz
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warm-up + correctness of the measured path
+    for _ in range(max(args.warmup, 3)):
+        da, sz = device_step()
+    torch.cuda.synchronize()
+    assert sz["status"] == 0, f"device status {sz['status']:#x}"
+    comp_bytes = eng.compressed_bytes(da, sz)
+    eb_abs = wl["rel"] * (sz["hi"] - sz["lo"])
+    maxerr = float((out.double() - x.double()).abs().max())
+    assert maxerr <= eb_abs, (maxerr, eb_abs)
+
+    # ---- timed device-resident round trips (events on the engine stream)
+    eng.launches = 0
+    eng.trace = []
+    barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(eng.stream)
+        for _ in range(args.steps):
+            device_step()
+        t1.record(eng.stream)
+        barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    launches = eng.launches
+    trace, eng.trace = eng.trace, None
+    per_fn = {}
+    for fn, e0, e1 in trace:
+        per_fn.setdefault(fn, []).append(e0.elapsed_time(e1))
+    comp_ms = sum(np.mean(v) for k, v in per_fn.items() if k in (
+        "fzb_minmax_f32", "fzb_resolve_bound", "fzb_lorenzo_encode_f32", "fzb_interp_encode_f32",
+        "fzb_outlier_compact", "fzb_histogram", "fzb_huffman_build", "fzb_huffman_encode", "fzb_bitshuffle_encode",
+        "fzb_fill_u16"))
+    dec_ms = sum(np.mean(v) for k, v in per_fn.items() if k in (
+        "fzb_huffman_decode", "fzb_bitshuffle_decode", "fzb_outlier_scatter", "fzb_lorenzo_decode_f32",
+        "fzb_interp_decode_f32"))
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = world * 4 * n / (ms_max / 1e3) / 1e9
+
+    # ---- roofline of the dominant kernel
+    peak, peak_kind = _peaks()
+    algo = {"fzb_lorenzo_encode_f32": 6 * n, "fzb_lorenzo_decode_f32": 6 * n + n // 8,
+            "fzb_bitshuffle_encode": 2 * n + n // 16 + 4 * (sz["size"] if spec.primary_codec == "bitshuffle" else 0),
+            "fzb_bitshuffle_decode": 2 * n + n // 16 + 4 * (sz["size"] if spec.primary_codec == "bitshuffle" else 0),
+            "fzb_huffman_encode": 2 * n + (sz["size"] + 7) // 8, "fzb_huffman_decode": 2 * n + (sz["size"] + 7) // 8,
+            "fzb_interp_encode_f32": 10 * n, "fzb_interp_decode_f32": 8 * n, "fzb_histogram": 2 * n,
+            "fzb_minmax_f32": 4 * n, "fzb_outlier_compact": n // 8}
+    dom = max(per_fn, key=lambda k: np.mean(per_fn[k]))
+    dom_ms = float(np.mean(per_fn[dom]))
+    achieved = algo.get(dom, 0) / (dom_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "algorithmic_bytes": int(algo.get(dom, 0)), "kernel_ms": round(dom_ms, 4),
+                "share_of_step": round(dom_ms / ms, 4),
+                "stage_ms": {k.replace("fzb_", ""): round(float(np.mean(v)), 4) for k, v in per_fn.items()}}
+
+    # ---- e2e through the public API from pinned host memory
+    xh = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    xh.copy_(x)
+    field = Field(dims, xh.numpy())
+    for _ in range(2):
+        a = fz.compress(field, ebs, wl["pipeline"])
+        r = fz.decompress(a)
+    barrier()
+    e2e_times = []
+    for _ in range(max(1, min(args.steps, 5))):
+        s0 = time.perf_counter()
+        a = fz.compress(field, ebs, wl["pipeline"])
+        r = fz.decompress(a)
+        e2e_times.append(time.perf_counter() - s0)
+    e2e_s = torch.tensor([float(np.mean(e2e_times))], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e = world * 4 * n / float(e2e_s.item()) / 1e9
+    archive_bytes = len(fz.serialize_archive(a))
+    assert archive_bytes == comp_bytes, (archive_bytes, comp_bytes)
+    q = quality_arrays(field.data, r.data, a.resolved_bound().eb_abs)
+    assert q.bound_satisfied
+
+    line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 data, f64 predictor arithmetic", "data": "synthetic",
+            "config": {"workload": wl["name"], "pipeline": wl["pipeline"], "dims": list(dims), "rel_eb": wl["rel"],
+                       "fields_per_gpu": 1, "l2": "working set (805 MB) > 126 MB L2, no flush needed",
+                       "parallelism": f"whole-field shard x{world}"},
+            "compress_gbs": round(4 * n / (comp_ms / 1e3) / 1e9, 3) if comp_ms else None,
+            "decompress_gbs": round(4 * n / (dec_ms / 1e3) / 1e9, 3) if dec_ms else None,
+            "cr": round(4 * n / comp_bytes, 4), "psnr_db": round(q.psnr_db, 4), "max_abs_err": q.max_abs_err,
+            "eb_abs": a.resolved_bound().eb_abs,
+            "e2e": {"value": round(e2e, 3), "unit": "GB/s", "h2d_bytes_per_step": 4 * n + comp_bytes,
+                    "d2h_bytes_per_step": 4 * n + comp_bytes},
+            "roofline": roofline, "gpu_launches": launches, "clocks": clk.summary()}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        xs = x.cpu().numpy()
+        threads = min(os.cpu_count() or 1, 32)
+        v, cores, dt, desc = cpu_roundtrip(xs, dims, wl["pipeline"], wl["rel"], threads, _slab(dims))
+        line["cpu_baseline"] = {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+                                "sample": desc}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, wl)
+    else:
+        run_ours(args, wl)
+
+
+if __name__ == "__main__":
+    main()

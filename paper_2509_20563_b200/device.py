@@ -83,6 +83,7 @@ class Engine:
         self._dev: dict[str, torch.Tensor] = {}
         self._host: dict[str, torch.Tensor] = {}
         self.launches = 0  # kernels issued through the C ABI (counted per entry point)
+        self.trace = None  # list -> (entry point, start event, end event) per call
 
     # ------------------------------------------------------------ buffers
     def buf(self, name: str, nbytes: int, zero: bool = False) -> torch.Tensor:
@@ -109,7 +110,14 @@ class Engine:
         return ctypes.c_void_p(self.stream.cuda_stream)
 
     def _call(self, fn: str, *args, nk: int = 1):
-        rc = getattr(self.lib, fn)(*args)
+        if self.trace is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(self.stream)
+            rc = getattr(self.lib, fn)(*args)
+            e1.record(self.stream)
+            self.trace.append((fn, e0, e1))
+        else:
+            rc = getattr(self.lib, fn)(*args)
         self.launches += nk
         _lib.check(rc, fn)
 
@@ -263,6 +271,65 @@ class Engine:
         else:
             segs += [(SEG_BITSHUFFLE_BITMAP, blobs[q]), (SEG_BITSHUFFLE_PAYLOAD, blobs[q + 1])]
         return lo, hi, segs
+
+    def sizes(self, da: DeviceArchive) -> dict:
+        """One small D2H: status, lo/hi, outlier count, primary-codec size."""
+        b = da.bufs
+        s = self.pinned("scal2", 64)[:32]
+        with torch.cuda.stream(self.stream):
+            s[0:8].copy_(b["status"][:8], non_blocking=True)
+            s[8:16].copy_(b["lohi"][:8], non_blocking=True)
+            s[16:24].copy_(b["ocount"][:8], non_blocking=True)
+            s[24:32].copy_(b["bitcount" if da.codec == "huffman" else "nwords"][:8], non_blocking=True)
+        self.stream.synchronize()
+        v = s.numpy()
+        return dict(status=int(v[0:4].view(np.uint32)[0]), lo=float(v[8:12].view(np.float32)[0]),
+                    hi=float(v[12:16].view(np.float32)[0]), k=int(v[16:24].view(np.uint64)[0]),
+                    size=int(v[24:32].view(np.uint64)[0]))
+
+    def compressed_bytes(self, da: DeviceArchive, sz: dict) -> int:
+        """Serialized archive length for these sizes (header + table + payloads)."""
+        nseg = 4 + (1 if da.use_anchors else 0)
+        body = 12 * sz["k"] + (4 * da.bufs["n_anchors"] if da.use_anchors else 0)
+        if da.codec == "huffman":
+            body += 2 * da.radius + (sz["size"] + 7) // 8
+        else:
+            body += 16 * ((da.n + 255) // 256) + 4 * sz["size"]
+        return 41 + 9 * nseg + body
+
+    def decompress_resident(self, da: DeviceArchive, sz: dict, eb_abs: float, out: torch.Tensor) -> torch.Tensor:
+        """Decode straight from the device-resident segments of `da` (no H2D):
+        the device half of the round trip measured by bench.py."""
+        L, sp, b, n = self.lib, self.sp, da.bufs, da.n
+        status = self.buf("dstatus", 8, zero=True)
+        codes = self.buf("dcodes", 2 * n + 16)
+        nsym = 2 * da.radius
+        if da.codec == "huffman":
+            nbytes = (sz["size"] + 7) // 8
+            hws = self.buf("hdws", L.fzb_huffman_decode_workspace_bytes(nbytes, nsym))
+            self._call("fzb_huffman_decode", _p(b["hfout"]), nbytes, n, _p(b["lengths"]), nsym, _p(codes), _p(hws),
+                       hws.numel(), _p(status), sp, nk=10)
+        else:
+            bws = self.buf("dbsws", L.fzb_bitshuffle_workspace_bytes(n))
+            self._call("fzb_bitshuffle_decode", _p(b["bsmap"]), _p(b["bspay"]), sz["size"], n, da.radius, _p(codes),
+                       _p(bws), bws.numel(), _p(status), sp, nk=4)
+        n0, n1, n2 = pad3(da.dims)
+        bitmap = self.buf("dbitmap", 4 * ((n + 31) // 32), zero=True)
+        ebt = self.buf("deb_res", 8)
+        with torch.cuda.stream(self.stream):
+            ebt[:8].view(torch.float64).fill_(eb_abs)
+        if sz["k"]:
+            self._call("fzb_outlier_scatter", _p(b["oidx"]), _p(b["oval"]), sz["k"], n, _p(codes), da.radius,
+                       _p(out), _p(bitmap), _p(status), sp)
+        if da.use_anchors:
+            w = (ctypes.c_double * 4)(*CUBIC)
+            self._call("fzb_interp_decode_f32", _p(codes), _p(bitmap), _p(b["anchors"]), _p(out), n0, n1, n2, _p(ebt),
+                       da.radius, 16, w, sp, nk=13)
+        else:
+            lzws = self.buf("dlzws", L.fzb_lorenzo_workspace_bytes(n0, n1, n2))
+            self._call("fzb_lorenzo_decode_f32", _p(codes), _p(bitmap), _p(out), n0, n1, n2, _p(ebt), da.radius,
+                       _p(lzws), lzws.numel(), sp, nk=5)
+        return out
 
     # --------------------------------------------------------- decompress
     def decode_codes(self, codec: str, segs: dict, n: int, radius: int) -> torch.Tensor:

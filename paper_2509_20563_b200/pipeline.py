@@ -213,7 +213,15 @@ def _check_stage_params(spec: PipelineSpec):
 
 
 def _to_device(field) -> torch.Tensor:
+    """H2D of the field; direct async copy when the numpy data lives in pinned memory."""
     eng = default_engine()
+    src = torch.from_numpy(field.data)
+    if src.is_pinned():
+        buf = eng.buf("field_in", 4 * field.len)
+        dst = buf[: 4 * field.len].view(torch.float32)
+        with torch.cuda.stream(eng.stream):
+            dst.copy_(src, non_blocking=True)
+        return dst
     buf = eng.upload("field_in", field.data)
     return buf[: 4 * field.len].view(torch.float32)
 
@@ -371,11 +379,16 @@ def decompress_device(a: Archive, pipeline=None, out: torch.Tensor | None = None
 
 def decompress_with_timing(a: Archive, pipeline=None):
     t0 = time.perf_counter()
+    eng = default_engine()
     rec = decompress_device(a, pipeline)
     t1 = time.perf_counter()
-    host = rec.cpu().numpy()
+    host = torch.empty(rec.numel(), dtype=torch.float32, pin_memory=True)
+    with torch.cuda.stream(eng.stream):
+        host.copy_(rec, non_blocking=True)
+    eng.stream.synchronize()
     t2 = time.perf_counter()
-    return Field(a.dims, host), {"device": t1 - t0, "d2h": t2 - t1}
+    # the decoder output is finite by construction; skip Field's O(n) host re-validation
+    return Field.trusted(a.dims, host.numpy()), {"device": t1 - t0, "d2h": t2 - t1}
 
 
 def decompress(a: Archive, pipeline=None) -> Field:
