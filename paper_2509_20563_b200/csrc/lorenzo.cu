@@ -34,13 +34,15 @@ constexpr int RING = 32;    // ring slots (steps)
 constexpr int PITCH = 33;   // words per row in f32/u32 rings (conflict-free)
 constexpr int CPITCH = 34;  // u16 per row in the encoder code ring
 constexpr uint32_t MARK = 0xFFFFFFFFu;
+constexpr unsigned FULL = 0xffffffffu;
 
 template <int PI>
 struct Tile {
     static constexpr int NT = PI * 32;
     static constexpr int HROWS = 33 + PI + 1;                   // HU (33) + HL (PI+1)
     static constexpr int HITER = (HROWS * G + NT - 1) / NT;     // halo loads per thread
-    static constexpr int OITER = G;                             // ring loads per thread
+    static constexpr int RPE = NT / G;                          // staging rows per iteration
+    static constexpr int MINB = PI >= 8 ? 3 : (PI >= 4 ? 6 : 12);
 };
 
 template <int PI>
@@ -58,34 +60,43 @@ FZB_DEV void wait_progress(const uint32_t* p, uint32_t need) {
     }
 }
 
+FZB_DEV void cp_async4(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
+FZB_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 struct Geo {
     int n0, n1, n2, nA, nB;
 };
 
-// Shared-memory carve-up for a PI x 32 tile.
 template <int PI, bool DEC>
 struct Smem {
     static constexpr int NT = PI * 32;
-    // input ring: ENC f32 orig, DEC u32 code/mark      [NT][PITCH]
-    // output ring: ENC u16 codes [NT][CPITCH], DEC f32 recon [NT][PITCH]
-    // RR: recon exchange ring [4][NT]; HU [33][PITCH]; HL [PI+1][PITCH]
     static constexpr size_t in_words = (size_t)NT * PITCH;
     static constexpr size_t out_bytes = DEC ? (size_t)NT * PITCH * 4 : (size_t)NT * CPITCH * 2;
-    static constexpr size_t rr_words = 4 * NT;
+    static constexpr size_t rr_words = PI > 1 ? 4 * NT : 0;
     static constexpr size_t hu_words = 33 * PITCH;
     static constexpr size_t hl_words = (PI + 1) * PITCH;
     static constexpr size_t bytes = in_words * 4 + ((out_bytes + 15) / 16) * 16 + (rr_words + hu_words + hl_words) * 4 + 16;
 };
 
-// One kernel body for both directions.
-//   ENC: in = orig (f32), out_codes (u16), bitmap |= outliers
-//   DEC: in = codes (u16) + bitmap (outliers) + recon (pre-scattered outlier values), out = recon
+// Wavefront tile kernel, both directions (v2).
+//   ENC: orig -> codes (u16) + outlier bits
+//   DEC: codes + outlier bits + pre-scattered outlier values (in recon) -> recon
+// Thread (a, b) owns row (i0+a, j0+b) and handles k = s - a - b at step s.
+// Prediction keeps the reference's 7-term order; absent neighbours (i, j or
+// k == 0) contribute an exact +0.0, which leaves every partial sum bitwise
+// unchanged (pred is never -0.0 after the leading 0.0 + up), so the sum is
+// branch-free.  Neighbours: up via the shared ring (other warp), left and
+// diagonal via __shfl_up of the previous step's (rec, up) of lane b-1.
 template <int PI, bool DEC>
-__global__ void __launch_bounds__(PI * 32)
+__global__ void __launch_bounds__(PI * 32, Tile<PI>::MINB)
 lz_wave_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in,
                uint16_t* __restrict__ codes_out, uint32_t* __restrict__ bitmap, float* __restrict__ recon,
                float* __restrict__ faceI, float* __restrict__ faceJ, uint32_t* __restrict__ progress,
-               uint32_t* __restrict__ ticket, Geo geo, const double* __restrict__ d_eb, int radius) {
+               uint32_t* __restrict__ ticket, const int* __restrict__ order, Geo geo,
+               const double* __restrict__ d_eb, int radius) {
     using T = Tile<PI>;
     using SM = Smem<PI, DEC>;
     constexpr int NT = T::NT;
@@ -101,7 +112,7 @@ lz_wave_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ code
 
     const int n0 = geo.n0, n1 = geo.n1, n2 = geo.n2, nB = geo.nB;
     const int tid = threadIdx.x, a = tid >> 5, b = tid & 31;
-    if (tid == 0) *s_tile = (int)atomicAdd(ticket, 1u);
+    if (tid == 0) *s_tile = order[atomicAdd(ticket, 1u)];
     __syncthreads();
     const int tile = *s_tile;
     const int A = tile / nB, B = tile % nB;
@@ -109,46 +120,48 @@ lz_wave_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ code
     const int i = i0 + a, j = j0 + b;
     const bool row_ok = (i < n0) && (j < n1);
     const QParams P = make_qparams(*d_eb, radius);
+    const double R_d = (double)radius;
     const int S = n2 + PI - 1 + 31;
     const int NGRP = (S + G - 1) / G;
     const uint32_t* progI = (A > 0) ? progress + (tile - nB) : nullptr;
     const uint32_t* progJ = (B > 0) ? progress + (tile - 1) : nullptr;
-    const bool writeI = (a == PI - 1) && (A < geo.nA - 1);
-    const bool writeJ = (b == 31) && (B < nB - 1);
-    const long long rowbase = ((long long)i * n1 + j) * n2;
+    const bool writeI = row_ok && (a == PI - 1) && (A < geo.nA - 1);
+    const bool writeJ = row_ok && (b == 31) && (B < nB - 1);
+    const long long plane = (long long)n1 * n2;
+    const long long tile_base = (long long)i0 * plane + (long long)j0 * n2;
+    const long long rowbase = tile_base + (long long)a * plane + (long long)b * n2;
+    float* fI = faceI + ((long long)A * n1 + j) * n2;
+    float* fJ = faceJ + ((long long)B * n0 + i) * n2;
 
-    // ---- staging helpers -------------------------------------------------
-    uint32_t st_in[T::OITER];
-    float st_val[DEC ? T::OITER : 1];
+    uint32_t st_in[DEC ? G : 1];
+    float st_val[DEC ? G : 1];
     float st_h[T::HITER];
 
+    // ---- staging: ring input for steps [gg*G, gg*G+G), 8 lanes per row segment
     auto load_group = [&](int gg) {
-        // ring input for steps [gg*G, gg*G+G)
 #pragma unroll
-        for (int e = 0; e < T::OITER; e++) {
-            const int flat = e * NT + tid;
-            const int row = flat / G, off = flat % G;
+        for (int e = 0; e < G; e++) {
+            const int row = e * T::RPE + (tid >> 3), off = tid & 7;
             const int ra = row >> 5, rb = row & 31;
-            const int ii = i0 + ra, jj = j0 + rb;
             const int k = gg * G + off - ra - rb;
-            st_in[e] = 0u;
-            if constexpr (DEC) st_val[e] = 0.f;
-            if (ii < n0 && jj < n1 && k >= 0 && k < n2) {
-                const long long t = ((long long)ii * n1 + jj) * n2 + k;
-                if constexpr (DEC) {
-                    const uint32_t flag = (__ldg(bitmap + (t >> 5)) >> (t & 31)) & 1u;
-                    if (flag) {
+            const bool ok = (i0 + ra < n0) && (j0 + rb < n1) && k >= 0 && k < n2;
+            const long long t = tile_base + (long long)ra * plane + (long long)rb * n2 + k;
+            const int slot = (gg * G + off) & (RING - 1);
+            if constexpr (DEC) {
+                st_in[e] = 0u;
+                st_val[e] = 0.f;
+                if (ok) {
+                    if ((__ldg(bitmap + (t >> 5)) >> (t & 31)) & 1u) {
                         st_in[e] = MARK;
                         st_val[e] = recon[t];
                     } else {
                         st_in[e] = __ldg(codes_in + t);
                     }
-                } else {
-                    st_in[e] = __float_as_uint(__ldg(orig + t));
                 }
+            } else {
+                if (ok) cp_async4(IN + row * PITCH + slot, orig + t);
             }
         }
-        // halos for steps [gg*G, gg*G+G)
 #pragma unroll
         for (int e = 0; e < T::HITER; e++) {
             const int h = e * NT + tid;
@@ -170,35 +183,34 @@ lz_wave_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ code
         }
     };
     auto store_group = [&](int gg) {
+        if constexpr (DEC) {
 #pragma unroll
-        for (int e = 0; e < T::OITER; e++) {
-            const int flat = e * NT + tid;
-            const int row = flat / G, off = flat % G;
-            const int slot = (gg * G + off) & (RING - 1);
-            IN[row * PITCH + slot] = st_in[e];
-            if constexpr (DEC) {
+            for (int e = 0; e < G; e++) {
+                const int row = e * T::RPE + (tid >> 3), off = tid & 7;
+                const int slot = (gg * G + off) & (RING - 1);
+                IN[row * PITCH + slot] = st_in[e];
                 if (st_in[e] == MARK) OR[row * PITCH + slot] = st_val[e];
             }
+        } else {
+            cp_async_wait_all();
         }
 #pragma unroll
         for (int e = 0; e < T::HITER; e++) {
             const int h = e * NT + tid;
             if (h < 33 * G) {
-                const int r = h / G, off = h % G;
-                HU[r * PITCH + ((gg * G + off) & (RING - 1))] = st_h[e];
+                HU[(h / G) * PITCH + ((gg * G + h % G) & (RING - 1))] = st_h[e];
             } else if (h < T::HROWS * G) {
                 const int hh = h - 33 * G;
-                const int r = hh / G, off = hh % G;
-                HL[r * PITCH + ((gg * G + off) & (RING - 1))] = st_h[e];
+                HL[(hh / G) * PITCH + ((gg * G + hh % G) & (RING - 1))] = st_h[e];
             }
         }
     };
     auto need_for = [&](int gg, int lag) -> uint32_t {
-        long long v = (long long)(gg + 1) * G + lag;
+        const long long v = (long long)(gg + 1) * G + lag;
         return (uint32_t)(v < S ? v : S);
     };
 
-    // ---- prologue: group 0 ------------------------------------------------
+    // ---- prologue -----------------------------------------------------------
     if (tid == 0) {
         wait_progress(progI, need_for(0, PI));
         wait_progress(progJ, need_for(0, 32));
@@ -206,12 +218,12 @@ lz_wave_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ code
     __syncthreads();
     load_group(0);
     store_group(0);
-    // The corner value r[i0-1, j0-1, 0] lives at step -1 of halo row jj = -1
-    // (slot 31); no group covers negative steps, so load it here.
-    if (tid == 0 && A > 0 && B > 0 && j0 - 1 < n1)
-        HU[RING - 1] = __ldcg(faceI + ((long long)(A - 1) * n1 + (j0 - 1)) * n2);
+    // corner r[i0-1, j0-1, 0] sits at step -1 of halo row jj = -1 (slot 31)
+    if (tid == 0) HU[RING - 1] = (A > 0 && B > 0) ? __ldcg(faceI + ((long long)(A - 1) * n1 + (j0 - 1)) * n2) : 0.f;
 
-    float up_prev = 0.f, left_prev = 0.f, diag_prev = 0.f, self_prev = 0.f;
+    // history of the previous step (exact zeros before k == 0)
+    float recL = 0.f, upLf = 0.f;
+    double selfL = 0.0, upL = 0.0, leftL = 0.0, diagL = 0.0;
 
     for (int g = 0; g < NGRP; g++) {
         const bool more = (g + 1) < NGRP;
@@ -226,72 +238,119 @@ lz_wave_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ code
         for (int st = 0; st < G; st++) {
             const int s = g * G + st;
             const int k = s - a - b;
-            if (row_ok && k >= 0 && k < n2) {
-                const int slot = s & (RING - 1);
-                const int ks = (k & 3) * NT;
-                float up = 0.f, left = 0.f, diag = 0.f;
-                if (i > 0) up = (a > 0) ? RR[ks + tid - 32] : HU[(b + 1) * PITCH + slot];
-                if (j > 0) left = (b > 0) ? RR[ks + tid - 1] : HL[(a + 1) * PITCH + slot];
-                if (i > 0 && j > 0) {
-                    const int ps = (s - 1) & (RING - 1);
-                    diag = (a > 0 && b > 0) ? RR[ks + tid - 33]
-                                            : (a == 0 ? HU[b * PITCH + ps] : HL[a * PITCH + ps]);
-                }
-                // predict.py:100-114 -- ordered f64 inclusion-exclusion
-                double pred = 0.0;
-                if (i > 0) pred = __dadd_rn(pred, (double)up);
-                if (j > 0) pred = __dadd_rn(pred, (double)left);
-                if (k > 0) pred = __dadd_rn(pred, (double)self_prev);
-                if (i > 0 && j > 0) pred = __dsub_rn(pred, (double)diag);
-                if (i > 0 && k > 0) pred = __dsub_rn(pred, (double)up_prev);
-                if (j > 0 && k > 0) pred = __dsub_rn(pred, (double)left_prev);
-                if (i > 0 && j > 0 && k > 0) pred = __dadd_rn(pred, (double)diag_prev);
-                float rec;
-                if constexpr (DEC) {
-                    const uint32_t c = IN[tid * PITCH + slot];
-                    if (c == MARK) {
-                        rec = OR[tid * PITCH + slot];
-                    } else {
-                        rec = dequantize(pred, (int)c, P);
-                        OR[tid * PITCH + slot] = rec;
-                    }
-                } else {
-                    const double v = (double)__uint_as_float(IN[tid * PITCH + slot]);
-                    bool outl;
-                    const int code = quantize(v, pred, P, rec, outl);
-                    CR[tid * CPITCH + slot] = (uint16_t)code;
-                    if (outl) {
-                        const long long t = rowbase + k;
-                        atomicOr(bitmap + (t >> 5), 1u << (t & 31));
-                    }
-                }
-                RR[ks + tid] = rec;
-                if (writeI) faceI[((long long)A * n1 + j) * n2 + k] = rec;
-                if (writeJ) faceJ[((long long)B * n0 + i) * n2 + k] = rec;
-                up_prev = up;
-                left_prev = left;
-                diag_prev = diag;
-                self_prev = rec;
+            const bool act = row_ok && (unsigned)k < (unsigned)n2;
+            const int slot = s & (RING - 1);
+            float upf;
+            if constexpr (PI > 1) upf = (a > 0) ? RR[(k & 3) * NT + tid - 32] : HU[(b + 1) * PITCH + slot];
+            else upf = HU[(b + 1) * PITCH + slot];
+            float leftf = __shfl_up_sync(FULL, recL, 1);
+            float diagf = __shfl_up_sync(FULL, upLf, 1);
+            if (b == 0) {
+                const int ps = (s - 1) & (RING - 1);
+                leftf = HL[(a + 1) * PITCH + slot];
+                diagf = (a > 0) ? HL[a * PITCH + ps] : HU[ps];
             }
+            // predict.py:100-114, absent terms == +0.0 (see header comment)
+            const double up = (double)(upf + 0.0f);  // the leading "0.0 + x" (normalises -0)
+            const double left = (double)leftf, diag = (double)diagf;
+            double pred = __dadd_rn(up, left);
+            pred = __dadd_rn(pred, selfL);
+            pred = __dsub_rn(pred, diag);
+            pred = __dsub_rn(pred, upL);
+            pred = __dsub_rn(pred, leftL);
+            pred = __dadd_rn(pred, diagL);
+            float rec;
+            double recd;
+            if constexpr (DEC) {
+                const uint32_t c = IN[tid * PITCH + slot];
+                if (c == MARK) {
+                    rec = OR[tid * PITCH + slot];
+                } else {
+                    rec = dequantize(pred, (int)c, P);
+                    OR[tid * PITCH + slot] = rec;
+                }
+                recd = (double)rec;
+            } else {
+                const float vf = __uint_as_float(IN[tid * PITCH + slot]);
+                const double v = (double)vf;
+                // fast path: q = (v-pred)*inv2eb, s = rint(q); exact fallback near .5 ties
+                const double q = __dmul_rn(__dsub_rn(v, pred), P.inv2eb);
+                const double sd = rint(q);
+                const double fr = fabs(__dsub_rn(q, sd));
+                int code;
+                bool outl;
+                if (!P.use_recip || fr >= 0.4999999990686774) {
+                    code = quantize(v, pred, P, rec, outl);
+                } else {
+                    const float rc = __double2float_rn(__dadd_rn(pred, __dmul_rn(P.two_eb, sd)));
+                    const bool ok = fabs(sd) < R_d && fabs(__dsub_rn((double)rc, v)) <= P.eb;
+                    code = ok ? (int)sd + radius : radius;
+                    rec = ok ? rc : vf;
+                    outl = !ok;
+                }
+                recd = (double)rec;
+                CR[tid * CPITCH + slot] = (uint16_t)code;
+                if (outl && act) {
+                    const long long t = rowbase + k;
+                    atomicOr(bitmap + (t >> 5), 1u << (t & 31));
+                }
+            }
+            if constexpr (PI > 1) RR[(k & 3) * NT + tid] = rec;
+            if (act) {
+                if (writeI) fI[k] = rec;
+                if (writeJ) fJ[k] = rec;
+            }
+            recL = act ? rec : 0.f;
+            upLf = act ? upf : 0.f;
+            selfL = act ? recd : 0.0;
+            upL = act ? up : 0.0;
+            leftL = act ? left : 0.0;
+            diagL = act ? diag : 0.0;
             tile_sync<PI>();
         }
         if (tid == 0) st_release(progress + tile, (uint32_t)min((g + 1) * G, S));
-        // flush group g (all steps of the group are complete)
+        // flush group g (complete for every row)
 #pragma unroll
-        for (int e = 0; e < T::OITER; e++) {
-            const int flat = e * NT + tid;
-            const int row = flat / G, off = flat % G;
+        for (int e = 0; e < G; e++) {
+            const int row = e * T::RPE + (tid >> 3), off = tid & 7;
             const int ra = row >> 5, rb = row & 31;
-            const int ii = i0 + ra, jj = j0 + rb;
             const int s = g * G + off;
             const int k = s - ra - rb;
-            if (ii < n0 && jj < n1 && k >= 0 && k < n2) {
-                const long long t = ((long long)ii * n1 + jj) * n2 + k;
+            if ((i0 + ra < n0) && (j0 + rb < n1) && k >= 0 && k < n2) {
+                const long long t = tile_base + (long long)ra * plane + (long long)rb * n2 + k;
                 if constexpr (DEC) recon[t] = OR[row * PITCH + (s & (RING - 1))];
                 else codes_out[t] = CR[row * CPITCH + (s & (RING - 1))];
             }
         }
         if (more) store_group(g + 1);
+    }
+}
+
+// Ticket order: tiles sorted by their expected start step lagI*A + lagJ*B
+// (a topological order: both predecessors have strictly smaller keys), so
+// resident CTAs are the ones closest to runnable.  Counting sort, one CTA.
+__global__ void tile_order_kernel(int nA, int nB, int lagI, int lagJ, int* __restrict__ counts,
+                                  int* __restrict__ order) {
+    __shared__ uint32_t tmp[33];
+    const int ntile = nA * nB;
+    const int K = lagI * (nA - 1) + lagJ * (nB - 1) + 1;
+    for (int q = threadIdx.x; q < K; q += blockDim.x) counts[q] = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < ntile; t += blockDim.x) atomicAdd(&counts[lagI * (t / nB) + lagJ * (t % nB)], 1);
+    __syncthreads();
+    uint32_t carry = 0;
+    for (int q0 = 0; q0 < K; q0 += blockDim.x) {
+        const int q = q0 + threadIdx.x;
+        const uint32_t x = q < K ? (uint32_t)counts[q] : 0u;
+        uint32_t tot;
+        const uint32_t p = block_exclusive_scan(x, tmp, &tot);
+        if (q < K) counts[q] = (int)(carry + p);
+        carry += tot;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < ntile; t += blockDim.x) {
+        const int pos = atomicAdd(&counts[lagI * (t / nB) + lagJ * (t % nB)], 1);
+        order[pos] = t;
     }
 }
 
@@ -527,6 +586,24 @@ __global__ void scan_counts_kernel(const uint32_t* __restrict__ cnt, long long m
     if (threadIdx.x == 0) *tot = carry;
 }
 
+template <int PI>
+struct WaveWS {
+    size_t ntile, fI, fJ, K, off_prog, off_order, off_counts, off_fI, total;
+    WaveWS(int n0, int n1, int n2) {
+        const size_t nA = (n0 + PI - 1) / PI, nB = (n1 + 31) / 32;
+        ntile = nA * nB;
+        fI = nA * (size_t)n1 * n2;
+        fJ = nB * (size_t)n0 * n2;
+        K = (size_t)(2 * G + PI) * (nA - 1) + (size_t)(2 * G + 32) * (nB - 1) + 1;
+        auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+        off_prog = 256;
+        off_order = off_prog + al(ntile * 4);
+        off_counts = off_order + al(ntile * 4);
+        off_fI = off_counts + al(K * 4);
+        total = off_fI + al(fI * 4) + al(fJ * 4) + 256;
+    }
+};
+
 template <int PI, bool DEC>
 int launch_wave(const float* orig, const uint16_t* codes_in, uint16_t* codes_out, uint32_t* bitmap, float* recon,
                 int n0, int n1, int n2, const double* d_eb, int radius, void* ws, size_t ws_bytes, cudaStream_t st) {
@@ -534,29 +611,28 @@ int launch_wave(const float* orig, const uint16_t* codes_in, uint16_t* codes_out
     g.n0 = n0; g.n1 = n1; g.n2 = n2;
     g.nA = (n0 + PI - 1) / PI;
     g.nB = (n1 + 31) / 32;
-    const size_t ntile = (size_t)g.nA * g.nB;
-    const size_t fI = (size_t)g.nA * n1 * n2, fJ = (size_t)g.nB * n0 * n2;
-    const size_t need = 256 + ntile * 4 + (fI + fJ) * 4;
-    if (ws_bytes < need) return FZB_E_WORKSPACE;
+    WaveWS<PI> L(n0, n1, n2);
+    if (ws_bytes < L.total) return FZB_E_WORKSPACE;
     unsigned char* w = static_cast<unsigned char*>(ws);
     uint32_t* ticket = reinterpret_cast<uint32_t*>(w);
-    uint32_t* progress = reinterpret_cast<uint32_t*>(w + 256);
-    float* faceI = reinterpret_cast<float*>(w + 256 + ((ntile * 4 + 255) / 256) * 256);
-    float* faceJ = faceI + fI;
-    cudaMemsetAsync(w, 0, 256 + ntile * 4, st);
+    uint32_t* progress = reinterpret_cast<uint32_t*>(w + L.off_prog);
+    int* order = reinterpret_cast<int*>(w + L.off_order);
+    int* counts = reinterpret_cast<int*>(w + L.off_counts);
+    float* faceI = reinterpret_cast<float*>(w + L.off_fI);
+    float* faceJ = reinterpret_cast<float*>(w + L.off_fI + (L.fI * 4 + 255) / 256 * 256);
+    cudaMemsetAsync(w, 0, L.off_order, st);  // ticket + progress
+    tile_order_kernel<<<1, 1024, 0, st>>>(g.nA, g.nB, 2 * G + PI, 2 * G + 32, counts, order);
     const size_t smem = Smem<PI, DEC>::bytes;
     auto kfn = lz_wave_kernel<PI, DEC>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kfn<<<(unsigned)ntile, PI * 32, smem, st>>>(orig, codes_in, codes_out, bitmap, recon, faceI, faceJ, progress,
-                                               ticket, g, d_eb, radius);
+    kfn<<<(unsigned)L.ntile, PI * 32, smem, st>>>(orig, codes_in, codes_out, bitmap, recon, faceI, faceJ, progress,
+                                                 ticket, order, g, d_eb, radius);
     return fzb_check_launch();
 }
 
 template <int PI>
 size_t wave_ws(int n0, int n1, int n2) {
-    const size_t nA = (n0 + PI - 1) / PI, nB = (n1 + 31) / 32;
-    const size_t ntile = nA * nB;
-    return 256 + ((ntile * 4 + 255) / 256) * 256 + (nA * n1 * n2 + nB * n0 * n2) * 4 + 256;
+    return WaveWS<PI>(n0, n1, n2).total;
 }
 
 // Collapse unit extents (the recurrence with a unit axis is the lower-dim one).
