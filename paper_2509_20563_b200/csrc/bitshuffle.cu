@@ -102,6 +102,174 @@ __global__ void __launch_bounds__(BS_THREADS) bs_enc_write_kernel(const uint16_t
     }
 }
 
+// Single-pass encoder: ballots once, per-CTA nonzero-word count published
+// through decoupled look-back (CTA order from an atomic ticket, so every
+// predecessor is resident or done), then compacted payload writes.
+// State word per CTA: bits 62-63 = flag (1 aggregate, 2 inclusive prefix),
+// bits 0-61 = value.
+constexpr unsigned long long LB_AGG = 1ull << 62, LB_PRE = 2ull << 62, LB_VAL = (1ull << 62) - 1;
+
+FZB_DEV unsigned long long ld_volatile64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(BS_THREADS) bs_enc_fused_kernel(const uint16_t* __restrict__ codes, uint64_t n,
+                                                                  uint64_t nblocks, uint32_t* __restrict__ bitmap,
+                                                                  uint32_t* __restrict__ payload,
+                                                                  unsigned long long* __restrict__ state,
+                                                                  uint32_t* __restrict__ ticket,
+                                                                  unsigned long long* __restrict__ nwords) {
+    __shared__ uint32_t wc[BS_WARPS];
+    __shared__ unsigned long long s_excl;
+    __shared__ uint32_t s_cta;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_cta = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t cta = s_cta;
+    uint32_t mine[BS_BPW][4];
+    uint32_t bms[BS_BPW][4];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int q = 0; q < BS_BPW; q++) {
+        const uint64_t blk = (uint64_t)cta * BS_BPC + warp * BS_BPW + q;
+        if (blk < nblocks) {
+            block_words(codes, n, blk, mine[q]);
+        } else {
+#pragma unroll
+            for (int s = 0; s < 4; s++) mine[q][s] = 0;
+        }
+#pragma unroll
+        for (int s = 0; s < 4; s++) {
+            bms[q][s] = __ballot_sync(0xffffffffu, mine[q][s] != 0u);
+            cnt += __popc(bms[q][s]);
+        }
+        if (blk < nblocks && lane < 4) bitmap[blk * 4 + lane] = bms[q][0] * (lane == 0) + bms[q][1] * (lane == 1) +
+                                                                 bms[q][2] * (lane == 2) + bms[q][3] * (lane == 3);
+    }
+    if (lane == 0) wc[warp] = cnt;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t agg = 0;
+        for (int w = 0; w < BS_WARPS; w++) agg += wc[w];
+        unsigned long long excl = 0;
+        if (cta == 0) {
+            if (lane == 0) {
+                __threadfence();
+                atomicExch(state, LB_PRE | agg);
+            }
+        } else {
+            if (lane == 0) {
+                __threadfence();
+                atomicExch(state + cta, LB_AGG | agg);
+            }
+            // parallel look-back over 32 predecessors at a time
+            long long base = (long long)cta - 1;
+            while (true) {
+                const long long p = base - lane;
+                unsigned long long v = LB_PRE;  // lanes before CTA 0 act as prefix 0
+                if (p >= 0) {
+                    do { v = ld_volatile64(state + p); } while ((v >> 62) == 0);
+                }
+                const unsigned pre = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+                const int stop = pre ? __ffs(pre) - 1 : 32;
+                unsigned long long add = (lane <= stop && p >= 0) ? (v & LB_VAL) : 0ull;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
+                excl += add;
+                if (pre) break;
+                base -= 32;
+            }
+            if (lane == 0) {
+                __threadfence();
+                atomicExch(state + cta, LB_PRE | (excl + agg));
+            }
+        }
+        if (lane == 0) {
+            s_excl = excl;
+            if ((uint64_t)(cta + 1) * BS_BPC >= nblocks) *nwords = excl + agg;
+        }
+    }
+    __syncthreads();
+    unsigned long long o = s_excl;
+    for (int w = 0; w < warp; w++) o += wc[w];
+#pragma unroll
+    for (int q = 0; q < BS_BPW; q++) {
+#pragma unroll
+        for (int s = 0; s < 4; s++) {
+            if (mine[q][s]) payload[o + __popc(bms[q][s] & lanemask_lt())] = mine[q][s];
+            o += __popc(bms[q][s]);
+        }
+    }
+}
+
+// Decoder: each warp stages its block's 128 words in shared memory, every
+// lane then extracts its own bit from each word (broadcast reads).
+__global__ void __launch_bounds__(BS_THREADS) bs_dec2_kernel(const uint32_t* __restrict__ bitmap,
+                                                             const uint32_t* __restrict__ payload, uint64_t payload_words,
+                                                             uint64_t n, uint64_t nblocks, uint32_t radius,
+                                                             const unsigned long long* __restrict__ offs,
+                                                             uint16_t* __restrict__ codes, uint32_t* __restrict__ status) {
+    __shared__ uint32_t wc[BS_WARPS];
+    __shared__ __align__(16) uint32_t sw[BS_WARPS][128];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t cnt = 0;
+    for (int q = 0; q < BS_BPW; q++) {
+        const uint64_t blk = (uint64_t)blockIdx.x * BS_BPC + warp * BS_BPW + q;
+        if (blk >= nblocks) break;
+        if (lane < 4) cnt += __popc(bitmap[blk * 4 + lane]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) wc[warp] = cnt;
+    __syncthreads();
+    unsigned long long o = offs[blockIdx.x];
+    for (int w = 0; w < warp; w++) o += wc[w];
+    bool pad_bad = false, range_bad = false;
+    uint32_t* W = sw[warp];
+    for (int q = 0; q < BS_BPW; q++) {
+        const uint64_t blk = (uint64_t)blockIdx.x * BS_BPC + warp * BS_BPW + q;
+        if (blk >= nblocks) break;
+#pragma unroll
+        for (int s = 0; s < 4; s++) {
+            const uint32_t bm = bitmap[blk * 4 + s];
+            uint32_t x = 0u;
+            if ((bm >> lane) & 1u) {
+                const unsigned long long pos = o + __popc(bm & lanemask_lt());
+                if (pos < payload_words) x = payload[pos];
+            }
+            W[s * 32 + lane] = x;
+            o += __popc(bm);
+        }
+        __syncwarp();
+        uint32_t c[8];
+#pragma unroll
+        for (int w = 0; w < 8; w++) c[w] = 0;
+#pragma unroll
+        for (int p = 0; p < 16; p++) {
+            const uint4 lo = *reinterpret_cast<const uint4*>(W + p * 8);
+            const uint4 hi = *reinterpret_cast<const uint4*>(W + p * 8 + 4);
+            const uint32_t x[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+            for (int w = 0; w < 8; w++) c[w] |= ((x[w] >> lane) & 1u) << p;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int w = 0; w < 8; w++) {
+            const uint64_t t = blk * 256 + 32 * w + lane;
+            if (t < n) {
+                codes[t] = (uint16_t)c[w];
+                range_bad |= c[w] >= 2 * radius;
+            } else {
+                pad_bad |= c[w] != 0;
+            }
+        }
+    }
+    if (pad_bad) set_err(status, FZB_ERR_BS_PAD);
+    if (range_bad) set_err(status, FZB_ERR_BS_RANGE);
+}
+
 __global__ void scan_counts_u64_kernel(const uint32_t* __restrict__ cnt, uint64_t m,
                                        unsigned long long* __restrict__ offs, unsigned long long* __restrict__ tot) {
     __shared__ unsigned long long tmp[33];
@@ -203,7 +371,7 @@ extern "C" {
 
 FZB_API size_t fzb_bitshuffle_workspace_bytes(uint64_t n) {
     const uint64_t c = ncta_of(n);
-    return 256 + ((c * 4 + 255) / 256) * 256 + c * 8 + 256;
+    return 512 + ((c * 4 + 255) / 256) * 256 + c * 8 + 256;
 }
 
 FZB_API int fzb_bitshuffle_encode(const uint16_t* d_codes, uint64_t n, uint8_t* d_bitmap, uint32_t* d_payload,
@@ -216,12 +384,12 @@ FZB_API int fzb_bitshuffle_encode(const uint16_t* d_codes, uint64_t n, uint8_t* 
         return fzb_check_launch();
     }
     unsigned char* w = static_cast<unsigned char*>(d_ws);
-    uint32_t* counts = reinterpret_cast<uint32_t*>(w + 256);
-    unsigned long long* offs = reinterpret_cast<unsigned long long*>(w + 256 + ((nc * 4 + 255) / 256) * 256);
-    uint32_t* bm = reinterpret_cast<uint32_t*>(d_bitmap);
-    bs_enc_count_kernel<<<(unsigned)nc, BS_THREADS, 0, st>>>(d_codes, n, nb, bm, counts);
-    scan_counts_u64_kernel<<<1, 1024, 0, st>>>(counts, nc, offs, reinterpret_cast<unsigned long long*>(d_nwords));
-    bs_enc_write_kernel<<<(unsigned)nc, BS_THREADS, 0, st>>>(d_codes, n, nb, bm, offs, d_payload);
+    uint32_t* ticket = reinterpret_cast<uint32_t*>(w);
+    unsigned long long* state = reinterpret_cast<unsigned long long*>(w + 256);
+    cudaMemsetAsync(w, 0, 256 + nc * 8, st);
+    bs_enc_fused_kernel<<<(unsigned)nc, BS_THREADS, 0, st>>>(d_codes, n, nb, reinterpret_cast<uint32_t*>(d_bitmap),
+                                                            d_payload, state, ticket,
+                                                            reinterpret_cast<unsigned long long*>(d_nwords));
     return fzb_check_launch();
 }
 
@@ -242,8 +410,8 @@ FZB_API int fzb_bitshuffle_decode(const uint8_t* d_bitmap, const uint32_t* d_pay
     bs_dec_count_kernel<<<(unsigned)nc, BS_THREADS, 0, st>>>(bm, nb, counts);
     scan_counts_u64_kernel<<<1, 1024, 0, st>>>(counts, nc, offs, tot);
     bs_check_total_kernel<<<1, 1, 0, st>>>(tot, payload_words, d_status);
-    bs_dec_kernel<<<(unsigned)nc, BS_THREADS, 0, st>>>(bm, d_payload, payload_words, n, nb, radius, offs, d_codes,
-                                                       d_status);
+    bs_dec2_kernel<<<(unsigned)nc, BS_THREADS, 0, st>>>(bm, d_payload, payload_words, n, nb, radius, offs, d_codes,
+                                                        d_status);
     return fzb_check_launch();
 }
 

@@ -29,6 +29,7 @@
 
 namespace {
 
+constexpr bool kUseWave3 = false;  // R=2 rows/thread variant (slower on B200; kept for experiments)
 constexpr int G = 8;        // steps per group (staging / progress granularity)
 constexpr int RING = 32;    // ring slots (steps)
 constexpr int PITCH = 33;   // words per row in f32/u32 rings (conflict-free)
@@ -127,6 +128,7 @@ lz_wave_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ code
     const uint32_t* progJ = (B > 0) ? progress + (tile - 1) : nullptr;
     const bool writeI = row_ok && (a == PI - 1) && (A < geo.nA - 1);
     const bool writeJ = row_ok && (b == 31) && (B < nB - 1);
+    const bool has_dep = (A < geo.nA - 1) || (B < nB - 1);
     const long long plane = (long long)n1 * n2;
     const long long tile_base = (long long)i0 * plane + (long long)j0 * n2;
     const long long rowbase = tile_base + (long long)a * plane + (long long)b * n2;
@@ -308,7 +310,7 @@ lz_wave_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ code
             diagL = act ? diag : 0.0;
             tile_sync<PI>();
         }
-        if (tid == 0) st_release(progress + tile, (uint32_t)min((g + 1) * G, S));
+        if (tid == 0 && has_dep) st_release(progress + tile, (uint32_t)min((g + 1) * G, S));
         // flush group g (complete for every row)
 #pragma unroll
         for (int e = 0; e < G; e++) {
@@ -323,6 +325,583 @@ lz_wave_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ code
             }
         }
         if (more) store_group(g + 1);
+    }
+}
+
+// ---------------------------------------------------------------- v3 (3D)
+// Same wavefront as above, but each thread owns R rows a = w + W*r (ILP R:
+// R independent dependency chains per step, one barrier per R elements) and
+// all staging offsets are 32-bit relative to the tile origin.  Requires
+// PI * n1 * n2 < 2^31 (checked on the host).
+template <int W, int R, bool DEC>
+struct Smem3 {
+    static constexpr int PI = W * R, NROW = PI * 32;
+    static constexpr size_t in_words = (size_t)NROW * PITCH;
+    static constexpr size_t out_bytes = DEC ? (size_t)NROW * PITCH * 4 : (size_t)NROW * CPITCH * 2;
+    static constexpr size_t rr_words = 4 * NROW;
+    static constexpr size_t hu_words = 33 * PITCH;
+    static constexpr size_t hl_words = (PI + 1) * PITCH;
+    static constexpr size_t bytes = in_words * 4 + ((out_bytes + 15) / 16) * 16 + (rr_words + hu_words + hl_words) * 4 + 16;
+};
+
+template <int W, int R, bool DEC>
+__global__ void __launch_bounds__(W * 32, (W >= 4 ? 4 : 8))
+lz_wave3_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in,
+                uint16_t* __restrict__ codes_out, uint32_t* __restrict__ bitmap, float* __restrict__ recon,
+                float* __restrict__ faceI, float* __restrict__ faceJ, uint32_t* __restrict__ progress,
+                uint32_t* __restrict__ ticket, const int* __restrict__ order, Geo geo,
+                const double* __restrict__ d_eb, int radius) {
+    constexpr int PI = W * R, NT = W * 32, NROW = PI * 32;
+    constexpr int SE = R * G;                      // staging elements per thread per group
+    constexpr int HROWS = 33 + PI + 1;
+    constexpr int HITER = (HROWS * G + NT - 1) / NT;
+    using SM = Smem3<W, R, DEC>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint32_t* IN = reinterpret_cast<uint32_t*>(smem_raw);
+    unsigned char* OUTB = smem_raw + SM::in_words * 4;
+    float* RR = reinterpret_cast<float*>(OUTB + ((SM::out_bytes + 15) / 16) * 16);
+    float* HU = RR + SM::rr_words;
+    float* HL = HU + SM::hu_words;
+    int* s_tile = reinterpret_cast<int*>(HL + SM::hl_words);
+    uint16_t* CR = reinterpret_cast<uint16_t*>(OUTB);
+    float* OR = reinterpret_cast<float*>(OUTB);
+
+    const int n0 = geo.n0, n1 = geo.n1, n2 = geo.n2, nB = geo.nB;
+    const int tid = threadIdx.x, w = tid >> 5, b = tid & 31;
+    if (tid == 0) *s_tile = order[atomicAdd(ticket, 1u)];
+    __syncthreads();
+    const int tile = *s_tile;
+    const int A = tile / nB, B = tile % nB;
+    const int i0 = A * PI, j0 = B * 32;
+    const int j = j0 + b;
+    const QParams P = make_qparams(*d_eb, radius);
+    const double R_d = (double)radius;
+    const int S = n2 + PI - 1 + 31;
+    const int NGRP = (S + G - 1) / G;
+    const uint32_t* progI = (A > 0) ? progress + (tile - nB) : nullptr;
+    const uint32_t* progJ = (B > 0) ? progress + (tile - 1) : nullptr;
+    const int plane = n1 * n2;  // fits: PI * plane < 2^31
+    const long long tile_base = (long long)i0 * plane + (long long)j0 * n2;
+    const float* tin = DEC ? nullptr : orig + tile_base;
+    const uint16_t* tcin = DEC ? codes_in + tile_base : nullptr;
+    float* trec = DEC ? recon + tile_base : nullptr;
+    uint16_t* tcout = DEC ? nullptr : codes_out + tile_base;
+
+    bool row_ok[R], wI[R], wJ[R];
+    int roff[R];
+    float* fI[R];
+    float* fJ[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        const int a = w + W * r, i = i0 + a;
+        row_ok[r] = (i < n0) && (j < n1);
+        wI[r] = row_ok[r] && (a == PI - 1) && (A < geo.nA - 1);
+        wJ[r] = row_ok[r] && (b == 31) && (B < nB - 1);
+        roff[r] = a * plane + b * n2;
+        fI[r] = faceI + ((long long)A * n1 + j) * n2;
+        fJ[r] = faceJ + ((long long)B * n0 + i) * n2;
+    }
+    const int soff = tid & 7;  // staging: 8 lanes per row segment
+
+    uint32_t st_in[DEC ? SE : 1];
+    float st_val[DEC ? SE : 1];
+    float st_h[HITER];
+
+    auto srow = [&](int e) { return e * (NT / G) + (tid >> 3); };
+    auto load_group = [&](int gg) {
+#pragma unroll
+        for (int e = 0; e < SE; e++) {
+            const int row = srow(e), ra = row >> 5, rb = row & 31;
+            const int k = gg * G + soff - ra - rb;
+            const bool ok = (i0 + ra < n0) && (j0 + rb < n1) && (unsigned)k < (unsigned)n2;
+            const int t = ra * plane + rb * n2 + k;
+            if constexpr (DEC) {
+                st_in[e] = 0u;
+                st_val[e] = 0.f;
+                if (ok) {
+                    const long long gt = tile_base + t;
+                    if ((__ldg(bitmap + (gt >> 5)) >> (gt & 31)) & 1u) {
+                        st_in[e] = MARK;
+                        st_val[e] = trec[t];
+                    } else {
+                        st_in[e] = __ldg(tcin + t);
+                    }
+                }
+            } else {
+                if (ok) cp_async4(IN + row * PITCH + ((gg * G + soff) & (RING - 1)), tin + t);
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < HITER; e++) {
+            const int h = e * NT + tid;
+            st_h[e] = 0.f;
+            if (h < 33 * G) {
+                const int jj = h / G - 1, off = h % G;
+                const int k = gg * G + off - jj;
+                const int jg = j0 + jj;
+                if (A > 0 && jg >= 0 && jg < n1 && k >= 0 && k < n2)
+                    st_h[e] = __ldcg(faceI + ((long long)(A - 1) * n1 + jg) * n2 + k);
+            } else if (h < HROWS * G) {
+                const int hh = h - 33 * G;
+                const int aa = hh / G - 1, off = hh % G;
+                const int k = gg * G + off - aa;
+                const int ig = i0 + aa;
+                if (B > 0 && ig >= 0 && ig < n0 && k >= 0 && k < n2)
+                    st_h[e] = __ldcg(faceJ + ((long long)(B - 1) * n0 + ig) * n2 + k);
+            }
+        }
+    };
+    auto store_group = [&](int gg) {
+        if constexpr (DEC) {
+#pragma unroll
+            for (int e = 0; e < SE; e++) {
+                const int row = srow(e);
+                const int slot = (gg * G + soff) & (RING - 1);
+                IN[row * PITCH + slot] = st_in[e];
+                if (st_in[e] == MARK) OR[row * PITCH + slot] = st_val[e];
+            }
+        } else {
+            cp_async_wait_all();
+        }
+#pragma unroll
+        for (int e = 0; e < HITER; e++) {
+            const int h = e * NT + tid;
+            if (h < 33 * G) {
+                HU[(h / G) * PITCH + ((gg * G + h % G) & (RING - 1))] = st_h[e];
+            } else if (h < HROWS * G) {
+                const int hh = h - 33 * G;
+                HL[(hh / G) * PITCH + ((gg * G + hh % G) & (RING - 1))] = st_h[e];
+            }
+        }
+    };
+    auto need_for = [&](int gg, int lag) -> uint32_t {
+        const long long v = (long long)(gg + 1) * G + lag;
+        return (uint32_t)(v < S ? v : S);
+    };
+
+    if (tid == 0) {
+        wait_progress(progI, need_for(0, PI));
+        wait_progress(progJ, need_for(0, 32));
+    }
+    __syncthreads();
+    load_group(0);
+    store_group(0);
+    if (tid == 0) HU[RING - 1] = (A > 0 && B > 0) ? __ldcg(faceI + ((long long)(A - 1) * n1 + (j0 - 1)) * n2) : 0.f;
+
+    float recL[R], upLf[R];
+    double selfL[R], upL[R], leftL[R], diagL[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        recL[r] = 0.f; upLf[r] = 0.f;
+        selfL[r] = 0.0; upL[r] = 0.0; leftL[r] = 0.0; diagL[r] = 0.0;
+    }
+
+    for (int g = 0; g < NGRP; g++) {
+        const bool more = (g + 1) < NGRP;
+        if (tid == 0 && more) {
+            wait_progress(progI, need_for(g + 1, PI));
+            wait_progress(progJ, need_for(g + 1, 32));
+        }
+        __syncthreads();
+        if (more) load_group(g + 1);
+
+#pragma unroll 2
+        for (int st = 0; st < G; st++) {
+            const int s = g * G + st;
+            const int slot = s & (RING - 1);
+            const int ps = (s - 1) & (RING - 1);
+#pragma unroll
+            for (int r = 0; r < R; r++) {
+                const int a = w + W * r;
+                const int row = a * 32 + b;
+                const int k = s - a - b;
+                const bool act = row_ok[r] && (unsigned)k < (unsigned)n2;
+                const float upf = (a > 0) ? RR[(k & 3) * NROW + row - 32] : HU[(b + 1) * PITCH + slot];
+                float leftf = __shfl_up_sync(FULL, recL[r], 1);
+                float diagf = __shfl_up_sync(FULL, upLf[r], 1);
+                if (b == 0) {
+                    leftf = HL[(a + 1) * PITCH + slot];
+                    diagf = (a > 0) ? HL[a * PITCH + ps] : HU[ps];
+                }
+                const double up = (double)(upf + 0.0f);
+                const double left = (double)leftf, diag = (double)diagf;
+                double pred = __dadd_rn(up, left);
+                pred = __dadd_rn(pred, selfL[r]);
+                pred = __dsub_rn(pred, diag);
+                pred = __dsub_rn(pred, upL[r]);
+                pred = __dsub_rn(pred, leftL[r]);
+                pred = __dadd_rn(pred, diagL[r]);
+                float rec;
+                double recd;
+                if constexpr (DEC) {
+                    const uint32_t c = IN[row * PITCH + slot];
+                    if (c == MARK) {
+                        rec = OR[row * PITCH + slot];
+                    } else {
+                        rec = dequantize(pred, (int)c, P);
+                        OR[row * PITCH + slot] = rec;
+                    }
+                    recd = (double)rec;
+                } else {
+                    const float vf = __uint_as_float(IN[row * PITCH + slot]);
+                    const double v = (double)vf;
+                    const double q = __dmul_rn(__dsub_rn(v, pred), P.inv2eb);
+                    const double sd = rint(q);
+                    const double fr = fabs(__dsub_rn(q, sd));
+                    int code;
+                    bool outl;
+                    if (!P.use_recip || fr >= 0.4999999990686774) {
+                        code = quantize(v, pred, P, rec, outl);
+                        recd = (double)rec;
+                    } else {
+                        const float rc = __double2float_rn(__dadd_rn(pred, __dmul_rn(P.two_eb, sd)));
+                        const double rcd = (double)rc;
+                        const bool ok = fabs(sd) < R_d && fabs(__dsub_rn(rcd, v)) <= P.eb;
+                        code = ok ? (int)sd + radius : radius;
+                        rec = ok ? rc : vf;
+                        recd = ok ? rcd : v;
+                        outl = !ok;
+                    }
+                    CR[row * CPITCH + slot] = (uint16_t)code;
+                    if (outl && act) {
+                        const long long t = tile_base + roff[r] + k;
+                        atomicOr(bitmap + (t >> 5), 1u << (t & 31));
+                    }
+                }
+                RR[(k & 3) * NROW + row] = rec;
+                recL[r] = rec;
+                upLf[r] = upf;
+                if (act) {
+                    if (wI[r]) fI[r][k] = rec;
+                    if (wJ[r]) fJ[r][k] = rec;
+                    selfL[r] = recd;
+                    upL[r] = up;
+                    leftL[r] = left;
+                    diagL[r] = diag;
+                }
+            }
+            __syncthreads();
+        }
+        if (tid == 0) st_release(progress + tile, (uint32_t)min((g + 1) * G, S));
+#pragma unroll
+        for (int e = 0; e < SE; e++) {
+            const int row = srow(e), ra = row >> 5, rb = row & 31;
+            const int s = g * G + soff;
+            const int k = s - ra - rb;
+            if ((i0 + ra < n0) && (j0 + rb < n1) && (unsigned)k < (unsigned)n2) {
+                const int t = ra * plane + rb * n2 + k;
+                if constexpr (DEC) trec[t] = OR[row * PITCH + (s & (RING - 1))];
+                else tcout[t] = CR[row * CPITCH + (s & (RING - 1))];
+            }
+        }
+        if (more) store_group(g + 1);
+    }
+}
+
+// ---------------------------------------------------------------- v4
+// Warp-specialised wavefront.  Warps 0..PI-1 compute (thread (a, b) owns row
+// (i0+a, j0+b), element k = s-a-b at step s); warp PI is the producer: it
+// waits on upstream progress, stages the input ring (cp.async, zero-filled
+// outside the field) and the halos one group ahead, flushes finished
+// groups and publishes progress (the gpu-scope fences stay off the compute
+// warps).  Inputs of steps before a row's k == 0 are exact zeros, so those
+// steps compute exact zeros and the 7-term history needs no masking.
+// Lane 0's left/diagonal halo values ride the same rotated shuffle as the
+// in-warp neighbours (lane 31 forwards them), so there is no divergence.
+// Barriers: 1 = per-step among compute warps, 2 = FULL (producer ->
+// compute, group staged), 3 = DONE (compute -> producer, group finished).
+FZB_DEV void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+FZB_DEV void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+FZB_DEV void cp_async4_zfill(void* smem, const void* gmem, bool ok) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int n = ok ? 4 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+
+template <int PI, bool DEC>
+struct Smem4 {
+    static constexpr int NT = PI * 32;
+    static constexpr size_t in_words = (size_t)NT * PITCH;
+    static constexpr size_t out_bytes = DEC ? (size_t)NT * PITCH * 4 : (size_t)NT * CPITCH * 2;
+    static constexpr size_t rr_words = PI > 1 ? 8 * NT : 0;
+    static constexpr size_t hu_words = 33 * PITCH;
+    static constexpr size_t hl_words = (PI + 1) * PITCH;
+    static constexpr size_t bytes = in_words * 4 + ((out_bytes + 15) / 16) * 16 + (rr_words + hu_words + hl_words) * 4 + 16;
+};
+
+template <int PI>
+struct Blocks4 {
+    static constexpr int MINB = PI >= 8 ? 3 : (PI >= 4 ? 5 : (PI >= 2 ? 8 : 12));
+};
+
+template <int PI, bool DEC>
+__global__ void __launch_bounds__((PI + 1) * 32, Blocks4<PI>::MINB)
+lz_wave4_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in,
+                uint16_t* __restrict__ codes_out, uint32_t* __restrict__ bitmap, float* __restrict__ recon,
+                float* __restrict__ faceI, float* __restrict__ faceJ, uint32_t* __restrict__ progress,
+                uint32_t* __restrict__ ticket, const int* __restrict__ order, Geo geo,
+                const double* __restrict__ d_eb, int radius) {
+    constexpr int NT = PI * 32;           // compute threads
+    constexpr int HROWS = 33 + PI + 1;
+    using SM = Smem4<PI, DEC>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint32_t* IN = reinterpret_cast<uint32_t*>(smem_raw);
+    unsigned char* OUTB = smem_raw + SM::in_words * 4;
+    float* RR = reinterpret_cast<float*>(OUTB + ((SM::out_bytes + 15) / 16) * 16);
+    float* HU = RR + SM::rr_words;
+    float* HL = HU + SM::hu_words;
+    int* s_tile = reinterpret_cast<int*>(HL + SM::hl_words);
+    uint16_t* CR = reinterpret_cast<uint16_t*>(OUTB);
+    float* OR = reinterpret_cast<float*>(OUTB);
+
+    const int n0 = geo.n0, n1 = geo.n1, n2 = geo.n2, nB = geo.nB;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // exact zeros everywhere a step before k == 0 can look (RR, HU, HL rings)
+    for (int q = tid; q < (int)(SM::rr_words + SM::hu_words + SM::hl_words); q += blockDim.x) RR[q] = 0.f;
+    if (tid == 0) *s_tile = order[atomicAdd(ticket, 1u)];
+    __syncthreads();
+    const int tile = *s_tile;
+    const int A = tile / nB, B = tile % nB;
+    const int i0 = A * PI, j0 = B * 32;
+    const int S = n2 + PI - 1 + 31;
+    const int NGRP = (S + G - 1) / G;
+    const long long plane = (long long)n1 * n2;
+    const long long tile_base = (long long)i0 * plane + (long long)j0 * n2;
+
+    if (warp == PI) {
+        // ============ producer: upstream waits, halos, progress fences ============
+        const uint32_t* progI = (A > 0) ? progress + (tile - nB) : nullptr;
+        const uint32_t* progJ = (B > 0) ? progress + (tile - 1) : nullptr;
+        const bool has_dep = (A < geo.nA - 1) || (B < nB - 1);
+        constexpr int HE = (HROWS * G + 31) / 32;
+        float hreg[HE];
+        auto need = [&](int gg, int lag) -> uint32_t {
+            const long long v = (long long)(gg + 1) * G + lag;
+            return (uint32_t)(v < S ? v : S);
+        };
+        auto stage = [&](int gg) {
+            if (progI) wait_progress(progI, need(gg, PI));
+            if (progJ) wait_progress(progJ, need(gg, 32));
+#pragma unroll
+            for (int e = 0; e < HE; e++) {
+                const int h = e * 32 + lane;
+                hreg[e] = 0.f;
+                if (h < 33 * G) {
+                    const int jj = h / G - 1, off = h % G;
+                    const int k = gg * G + off - jj;
+                    const int jg = j0 + jj;
+                    if (A > 0 && jg >= 0 && jg < n1 && k >= 0 && k < n2)
+                        hreg[e] = __ldcg(faceI + ((long long)(A - 1) * n1 + jg) * n2 + k);
+                } else if (h < HROWS * G) {
+                    const int hh = h - 33 * G;
+                    const int aa = hh / G - 1, off = hh % G;
+                    const int k = gg * G + off - aa;
+                    const int ig = i0 + aa;
+                    if (B > 0 && ig >= 0 && ig < n0 && k >= 0 && k < n2)
+                        hreg[e] = __ldcg(faceJ + ((long long)(B - 1) * n0 + ig) * n2 + k);
+                }
+            }
+        };
+        auto commit = [&](int gg) {
+#pragma unroll
+            for (int e = 0; e < HE; e++) {
+                const int h = e * 32 + lane;
+                if (h < 33 * G) HU[(h / G) * PITCH + ((gg * G + h % G) & (RING - 1))] = hreg[e];
+                else if (h < HROWS * G) {
+                    const int hh = h - 33 * G;
+                    HL[(hh / G) * PITCH + ((gg * G + hh % G) & (RING - 1))] = hreg[e];
+                }
+            }
+        };
+        stage(0);
+        commit(0);
+        if (lane == 0)  // corner r[i0-1, j0-1, 0] lives at step -1 of halo row jj = -1
+            HU[RING - 1] = (A > 0 && B > 0) ? __ldcg(faceI + ((long long)(A - 1) * n1 + (j0 - 1)) * n2) : 0.f;
+        __syncwarp();
+        bar_arrive(2, NT + 32);                    // FULL(0)
+        if (NGRP > 1) stage(1);
+        for (int g = 0; g < NGRP; g++) {
+            bar_sync(3, NT + 32);                  // DONE(g): faces of group g written
+            if (lane == 0 && has_dep) st_release(progress + tile, (uint32_t)min((g + 1) * G, S));
+            if (g + 1 < NGRP) {
+                commit(g + 1);
+                __syncwarp();
+                bar_arrive(2, NT + 32);            // FULL(g+1)
+            }
+            if (g + 2 < NGRP) stage(g + 2);
+        }
+        return;
+    }
+
+    // ================================ compute ================================
+    const int a = warp, b = lane;
+    const int i = i0 + a, j = j0 + b;
+    const bool row_ok = (i < n0) && (j < n1);
+    const QParams P = make_qparams(*d_eb, radius);
+    const double R_d = (double)radius;
+    const bool wI = row_ok && (a == PI - 1) && (A < geo.nA - 1);
+    const bool wJ = row_ok && (b == 31) && (B < nB - 1);
+    float* fI = faceI + ((long long)A * n1 + j) * n2 - a - b;   // index by step s
+    float* fJ = faceJ + ((long long)B * n0 + i) * n2 - a - b;
+    const long long rowbase = tile_base + a * plane + (long long)b * n2 - a - b;  // + s
+    const int src = (b + 31) & 31;
+    uint32_t* INr = IN + tid * PITCH;
+    float* ORr = OR + tid * PITCH;
+    uint16_t* CRr = CR + tid * CPITCH;
+    // warp-local staging / flush of this warp's 32 rows: lane -> (row q*4 + lane/8, offset lane%8)
+    const int soff = lane & 7, sr = lane >> 3;
+    const bool irow = (i < n0);
+    const long long wbase = tile_base + a * plane - a;   // + rb*n2 - rb + s
+
+    uint32_t creg[DEC ? 8 : 1];
+    float vreg[DEC ? 8 : 1];
+    auto stage_own = [&](int gg) {
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const int rb = q * 4 + sr;
+            const int k = gg * G + soff - a - rb;
+            const bool ok = irow && (j0 + rb < n1) && (unsigned)k < (unsigned)n2;
+            const long long t = wbase + (long long)rb * n2 - rb + gg * G + soff;
+            const int slot = (gg * G + soff) & (RING - 1);
+            if constexpr (DEC) {
+                creg[q] = (uint32_t)radius;
+                vreg[q] = 0.f;
+                if (ok) {
+                    if ((__ldg(bitmap + (t >> 5)) >> (t & 31)) & 1u) {
+                        creg[q] = MARK;
+                        vreg[q] = recon[t];
+                    } else {
+                        creg[q] = __ldg(codes_in + t);
+                    }
+                }
+            } else {
+                cp_async4_zfill(IN + (a * 32 + rb) * PITCH + slot, orig + (ok ? t : tile_base), ok);
+            }
+        }
+    };
+    auto commit_own = [&](int gg) {
+        if constexpr (DEC) {
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const int rb = q * 4 + sr;
+                const int slot = (gg * G + soff) & (RING - 1);
+                IN[(a * 32 + rb) * PITCH + slot] = creg[q];
+                if (creg[q] == MARK) OR[(a * 32 + rb) * PITCH + slot] = vreg[q];
+            }
+        } else {
+            cp_async_wait_all();
+        }
+        __syncwarp();
+    };
+    auto flush_own = [&](int gg) {
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const int rb = q * 4 + sr;
+            const int s = gg * G + soff;
+            const int k = s - a - rb;
+            if (irow && (j0 + rb < n1) && (unsigned)k < (unsigned)n2) {
+                const long long t = wbase + (long long)rb * n2 - rb + s;
+                if constexpr (DEC) recon[t] = OR[(a * 32 + rb) * PITCH + (s & (RING - 1))];
+                else codes_out[t] = CR[(a * 32 + rb) * CPITCH + (s & (RING - 1))];
+            }
+        }
+    };
+
+    stage_own(0);
+    commit_own(0);
+    float recL = 0.f, upLf = 0.f;
+    double selfL = 0.0, upL = 0.0, leftL = 0.0, diagL = 0.0;
+    float fwdL = 0.f, fwdD = 0.f;   // lane 31: lane 0's left / diagonal for the next step
+
+    for (int g = 0; g < NGRP; g++) {
+        bar_sync(2, NT + 32);        // FULL(g): halos of group g in shared memory
+        if (g + 1 < NGRP) stage_own(g + 1);
+        const int s0 = g * G;
+        const int sl0 = s0 & (RING - 1);
+        if (b == 31) {
+            fwdL = HL[(a + 1) * PITCH + sl0];
+            fwdD = (a > 0) ? HL[a * PITCH + ((s0 - 1) & (RING - 1))] : HU[(s0 - 1) & (RING - 1)];
+        }
+#pragma unroll
+        for (int st = 0; st < G; st++) {
+            const int s = s0 + st;
+            const int slot = sl0 + st;   // G divides RING: no wrap inside a group
+            float upf;
+            if constexpr (PI > 1) upf = (a > 0) ? RR[((s - 1) & 7) * NT + tid - 32] : HU[(b + 1) * PITCH + slot];
+            else upf = HU[(b + 1) * PITCH + slot];
+            const float leftf = __shfl_sync(FULL, b == 31 ? fwdL : recL, src);
+            const float diagf = __shfl_sync(FULL, b == 31 ? fwdD : upLf, src);
+            const double up = (double)(upf + 0.0f);   // the leading "0.0 + x" (normalises -0)
+            const double left = (double)leftf, diag = (double)diagf;
+            double pred = __dadd_rn(up, left);
+            pred = __dadd_rn(pred, selfL);
+            pred = __dsub_rn(pred, diag);
+            pred = __dsub_rn(pred, upL);
+            pred = __dsub_rn(pred, leftL);
+            pred = __dadd_rn(pred, diagL);
+            float rec;
+            double recd;
+            if constexpr (DEC) {
+                const uint32_t c = INr[slot];
+                if (c == MARK) {
+                    rec = ORr[slot];
+                } else {
+                    rec = dequantize(pred, (int)c, P);
+                    ORr[slot] = rec;
+                }
+                recd = (double)rec;
+            } else {
+                const float vf = __uint_as_float(INr[slot]);
+                const double v = (double)vf;
+                const double q = __dmul_rn(__dsub_rn(v, pred), P.inv2eb);
+                const double sd = rint(q);
+                const double fr = fabs(__dsub_rn(q, sd));
+                int code;
+                bool outl;
+                if (!P.use_recip || fr >= 0.4999999990686774) {
+                    code = quantize(v, pred, P, rec, outl);
+                    recd = (double)rec;
+                } else {
+                    const float rc = __double2float_rn(__dadd_rn(pred, __dmul_rn(P.two_eb, sd)));
+                    const double rcd = (double)rc;
+                    const bool ok = fabs(sd) < R_d && fabs(__dsub_rn(rcd, v)) <= P.eb;
+                    code = ok ? (int)sd + radius : radius;
+                    rec = ok ? rc : vf;
+                    recd = ok ? rcd : v;
+                    outl = !ok;
+                }
+                CRr[slot] = (uint16_t)code;
+                if (outl) {
+                    const int k = s - a - b;
+                    if (row_ok && (unsigned)k < (unsigned)n2) {
+                        const long long t = rowbase + s;
+                        atomicOr(bitmap + (t >> 5), 1u << (t & 31));
+                    }
+                }
+            }
+            {
+                const int k = s - a - b;
+                const bool act = (unsigned)k < (unsigned)n2;
+                if (wI && act) fI[s] = rec;
+                if (wJ && act) fJ[s] = rec;
+            }
+            if constexpr (PI > 1) RR[(s & 7) * NT + tid] = rec;
+            recL = rec;
+            upLf = upf;
+            selfL = recd;
+            upL = up;
+            leftL = left;
+            diagL = diag;
+            if (st + 1 < G && b == 31) {
+                fwdL = HL[(a + 1) * PITCH + slot + 1];
+                fwdD = (a > 0) ? HL[a * PITCH + slot] : HU[slot];
+            }
+            if constexpr (PI > 1) bar_sync(1, NT);
+            else __syncwarp();
+        }
+        bar_arrive(3, NT + 32);      // DONE(g)
+        flush_own(g);
+        if (g + 1 < NGRP) commit_own(g + 1);
     }
 }
 
@@ -630,6 +1209,59 @@ int launch_wave(const float* orig, const uint16_t* codes_in, uint16_t* codes_out
     return fzb_check_launch();
 }
 
+template <int W, int R, bool DEC>
+int launch_wave3(const float* orig, const uint16_t* codes_in, uint16_t* codes_out, uint32_t* bitmap, float* recon,
+                 int n0, int n1, int n2, const double* d_eb, int radius, void* ws, size_t ws_bytes, cudaStream_t st) {
+    constexpr int PI = W * R;
+    Geo g;
+    g.n0 = n0; g.n1 = n1; g.n2 = n2;
+    g.nA = (n0 + PI - 1) / PI;
+    g.nB = (n1 + 31) / 32;
+    WaveWS<PI> L(n0, n1, n2);
+    if (ws_bytes < L.total) return FZB_E_WORKSPACE;
+    unsigned char* w = static_cast<unsigned char*>(ws);
+    uint32_t* ticket = reinterpret_cast<uint32_t*>(w);
+    uint32_t* progress = reinterpret_cast<uint32_t*>(w + L.off_prog);
+    int* order = reinterpret_cast<int*>(w + L.off_order);
+    int* counts = reinterpret_cast<int*>(w + L.off_counts);
+    float* faceI = reinterpret_cast<float*>(w + L.off_fI);
+    float* faceJ = reinterpret_cast<float*>(w + L.off_fI + (L.fI * 4 + 255) / 256 * 256);
+    cudaMemsetAsync(w, 0, L.off_order, st);
+    tile_order_kernel<<<1, 1024, 0, st>>>(g.nA, g.nB, 2 * G + PI, 2 * G + 32, counts, order);
+    const size_t smem = Smem3<W, R, DEC>::bytes;
+    auto kfn = lz_wave3_kernel<W, R, DEC>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kfn<<<(unsigned)L.ntile, W * 32, smem, st>>>(orig, codes_in, codes_out, bitmap, recon, faceI, faceJ, progress,
+                                                ticket, order, g, d_eb, radius);
+    return fzb_check_launch();
+}
+
+template <int PI, bool DEC>
+int launch_wave4(const float* orig, const uint16_t* codes_in, uint16_t* codes_out, uint32_t* bitmap, float* recon,
+                 int n0, int n1, int n2, const double* d_eb, int radius, void* ws, size_t ws_bytes, cudaStream_t st) {
+    Geo g;
+    g.n0 = n0; g.n1 = n1; g.n2 = n2;
+    g.nA = (n0 + PI - 1) / PI;
+    g.nB = (n1 + 31) / 32;
+    WaveWS<PI> L(n0, n1, n2);
+    if (ws_bytes < L.total) return FZB_E_WORKSPACE;
+    unsigned char* w = static_cast<unsigned char*>(ws);
+    uint32_t* ticket = reinterpret_cast<uint32_t*>(w);
+    uint32_t* progress = reinterpret_cast<uint32_t*>(w + L.off_prog);
+    int* order = reinterpret_cast<int*>(w + L.off_order);
+    int* counts = reinterpret_cast<int*>(w + L.off_counts);
+    float* faceI = reinterpret_cast<float*>(w + L.off_fI);
+    float* faceJ = reinterpret_cast<float*>(w + L.off_fI + (L.fI * 4 + 255) / 256 * 256);
+    cudaMemsetAsync(w, 0, L.off_order, st);
+    tile_order_kernel<<<1, 1024, 0, st>>>(g.nA, g.nB, 2 * G + PI, 2 * G + 32, counts, order);
+    const size_t smem = Smem4<PI, DEC>::bytes;
+    auto kfn = lz_wave4_kernel<PI, DEC>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kfn<<<(unsigned)L.ntile, (PI + 1) * 32, smem, st>>>(orig, codes_in, codes_out, bitmap, recon, faceI, faceJ,
+                                                       progress, ticket, order, g, d_eb, radius);
+    return fzb_check_launch();
+}
+
 template <int PI>
 size_t wave_ws(int n0, int n1, int n2) {
     return WaveWS<PI>(n0, n1, n2).total;
@@ -688,11 +1320,13 @@ FZB_API int fzb_lorenzo_encode_f32(const float* d_in, uint32_t n0, uint32_t n1, 
         lz1d_walk_kernel<<<1, 32, 0, st>>>(d_in, n, d_codes, d_bitmap, bmin, bmax, nblk, d_eb, (int)radius);
         return fzb_check_launch();
     }
+    if (kUseWave3 && n0 >= 8 && 8ll * n1 * n2 < (1ll << 31))
+        return launch_wave3<4, 2, false>(d_in, nullptr, d_codes, d_bitmap, nullptr, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
     switch (pick_pi(n0)) {
-        case 8: return launch_wave<8, false>(d_in, nullptr, d_codes, d_bitmap, nullptr, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
-        case 4: return launch_wave<4, false>(d_in, nullptr, d_codes, d_bitmap, nullptr, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
-        case 2: return launch_wave<2, false>(d_in, nullptr, d_codes, d_bitmap, nullptr, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
-        default: return launch_wave<1, false>(d_in, nullptr, d_codes, d_bitmap, nullptr, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
+        case 8: return launch_wave4<8, false>(d_in, nullptr, d_codes, d_bitmap, nullptr, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
+        case 4: return launch_wave4<4, false>(d_in, nullptr, d_codes, d_bitmap, nullptr, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
+        case 2: return launch_wave4<2, false>(d_in, nullptr, d_codes, d_bitmap, nullptr, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
+        default: return launch_wave4<1, false>(d_in, nullptr, d_codes, d_bitmap, nullptr, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
     }
 }
 
@@ -722,11 +1356,13 @@ FZB_API int fzb_lorenzo_decode_f32(const uint16_t* d_codes, const uint32_t* d_bi
         lz1d_fill_kernel<<<(unsigned)nch, 256, 0, st>>>(d_codes, d_bitmap, n, (int)radius, offs, evpos, d_recon);
         return fzb_check_launch();
     }
+    if (kUseWave3 && n0 >= 8 && 8ll * n1 * n2 < (1ll << 31))
+        return launch_wave3<4, 2, true>(nullptr, d_codes, nullptr, const_cast<uint32_t*>(d_bitmap), d_recon, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
     switch (pick_pi(n0)) {
-        case 8: return launch_wave<8, true>(nullptr, d_codes, nullptr, const_cast<uint32_t*>(d_bitmap), d_recon, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
-        case 4: return launch_wave<4, true>(nullptr, d_codes, nullptr, const_cast<uint32_t*>(d_bitmap), d_recon, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
-        case 2: return launch_wave<2, true>(nullptr, d_codes, nullptr, const_cast<uint32_t*>(d_bitmap), d_recon, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
-        default: return launch_wave<1, true>(nullptr, d_codes, nullptr, const_cast<uint32_t*>(d_bitmap), d_recon, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
+        case 8: return launch_wave4<8, true>(nullptr, d_codes, nullptr, const_cast<uint32_t*>(d_bitmap), d_recon, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
+        case 4: return launch_wave4<4, true>(nullptr, d_codes, nullptr, const_cast<uint32_t*>(d_bitmap), d_recon, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
+        case 2: return launch_wave4<2, true>(nullptr, d_codes, nullptr, const_cast<uint32_t*>(d_bitmap), d_recon, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
+        default: return launch_wave4<1, true>(nullptr, d_codes, nullptr, const_cast<uint32_t*>(d_bitmap), d_recon, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
     }
 }
 
