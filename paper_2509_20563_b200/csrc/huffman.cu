@@ -23,6 +23,9 @@
 //    encode.py:299-316 exactly.
 #include "common.cuh"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace {
 
 constexpr int MAXLEN = 32;
@@ -315,7 +318,7 @@ __global__ void __launch_bounds__(HE_THREADS) hf_write_kernel(const uint16_t* __
 
 // ------------------------------------------------------------------ decode
 constexpr int LUT_BITS = 12;
-constexpr int SUB = 1024;  // bits per decode subsequence
+constexpr int SUB = 256;   // bits per decode subsequence
 constexpr int HD_THREADS = 128;
 
 struct DecTables {
@@ -365,32 +368,62 @@ __global__ void hf_tables_kernel(const uint8_t* __restrict__ lengths, uint32_t n
             if (len && len <= MAXLEN) {
                 const long long r = run[len] + rank;
                 sym_sorted[s_fi[len] + r] = (uint16_t)s;
-                if (len <= LUT_BITS) {
-                    const uint32_t c = (uint32_t)(s_fc[len] + r);
-                    const uint32_t lo = c << (LUT_BITS - len), hi = (c + 1) << (LUT_BITS - len);
-                    for (uint32_t q = lo; q < hi; q++) lut[q] = s | ((uint32_t)len << 16);
-                }
             }
             __syncwarp();
             if (len && len <= MAXLEN && rank == 0) run[len] += __popc(peers);
             __syncwarp();
         }
     }
+    __syncthreads();
+    // LUT: canonical decode of every 12-bit window (encode.py:248-253), in parallel
+    const int maxlen = T->maxlen;
+    for (uint32_t q = tid; q < (1u << LUT_BITS); q += blockDim.x) {
+        uint32_t e = 0;
+        for (int l = 1; l <= LUT_BITS && l <= maxlen; l++) {
+            const long long code = (long long)(q >> (LUT_BITS - l));
+            if (code < T->limit[l]) {
+                e = (uint32_t)sym_sorted[T->first_idx[l] + code - T->first_code[l]] | ((uint32_t)l << 16);
+                break;
+            }
+        }
+        lut[q] = e;
+    }
 }
 
+// MSB-first bit reader with a 64-bit register buffer: one 32-bit (byte
+// swapped) load per 32 consumed bits instead of two loads per symbol.
 struct BitReader {
-    const uint32_t* w;  // byte-swapped view happens on load
-    unsigned long long pos;
-    FZB_DEV uint32_t peek32() const {
-        const unsigned long long wi = pos >> 5;
+    const uint32_t* w;
+    unsigned long long pos;   // absolute bit position of the buffer head
+    unsigned long long buf;   // next bits, MSB-aligned
+    int nb;                   // valid bits in buf
+    unsigned long long nextw; // next word index to load
+    FZB_DEV void init(const uint32_t* words, unsigned long long p) {
+        w = words;
+        pos = p;
+        const unsigned long long wi = p >> 5;
         const unsigned long long hi = bswap32(__ldg(w + wi)), lo = bswap32(__ldg(w + wi + 1));
-        const unsigned long long x = (hi << 32) | lo;
-        return (uint32_t)((x << (pos & 31)) >> 32);
+        buf = ((hi << 32) | lo) << (p & 31);
+        nb = 64 - (int)(p & 31);
+        nextw = wi + 2;
+    }
+    FZB_DEV uint32_t peek32() {
+        if (nb < 32) {
+            buf |= (unsigned long long)bswap32(__ldg(w + nextw)) << (32 - nb);
+            nb += 32;
+            nextw++;
+        }
+        return (uint32_t)(buf >> 32);
+    }
+    FZB_DEV void skip(int l) {
+        buf <<= l;
+        nb -= l;
+        pos += l;
     }
 };
 
 // decode one symbol at r.pos; returns length (>0) or -1 truncated / -2 corrupt
-FZB_DEV int decode_one(const BitReader& r, unsigned long long total_bits, const DecTables& T, const uint32_t* lut,
+FZB_DEV int decode_one(BitReader& r, unsigned long long total_bits, const DecTables& T, const uint32_t* lut,
                        const uint16_t* sym_sorted, uint32_t& sym) {
     const uint32_t win = r.peek32();
     const uint32_t e = lut[win >> (32 - LUT_BITS)];
@@ -442,16 +475,73 @@ __global__ void __launch_bounds__(HD_THREADS) hf_sync_kernel(const uint32_t* __r
     }
     if (!first_iter) *changed = 1;
     const unsigned long long lim = (t + 1) * (unsigned long long)SUB;
-    BitReader r{stream, s};
+    BitReader r;
+    r.init(stream, s);
     uint32_t c = 0, e = 0;
     while (r.pos < lim && r.pos < total_bits) {
         uint32_t sym;
         const int l = decode_one(r, total_bits, T, lut, sym_sorted, sym);
         if (l < 0) { e = (uint32_t)(-l); break; }
-        r.pos += l;
+        r.skip(l);
         c++;
     }
     start[t] = s; end[t] = e ? lim : r.pos; cnt[t] = c; err[t] = e;
+}
+
+// Persistent, cooperative fixed-point iteration of the subsequence starts:
+// sweep 0 starts every subsequence at its nominal bit offset (speculative);
+// later sweeps restart subsequence t at end[t-1] whenever that differs from
+// its recorded start (in-place, Gauss-Seidel).  A sweep that changes nothing
+// proves start[t] == end[t-1] for every t, i.e. the true codeword path.
+__global__ void __launch_bounds__(HD_THREADS) hf_sync_coop_kernel(const uint32_t* __restrict__ stream,
+                                                                  unsigned long long total_bits, uint64_t nsub,
+                                                                  const DecTables* __restrict__ Tg,
+                                                                  const uint32_t* __restrict__ lut_g,
+                                                                  const uint16_t* __restrict__ sym_sorted,
+                                                                  unsigned long long* start, unsigned long long* end,
+                                                                  uint32_t* __restrict__ cnt, uint32_t* __restrict__ err,
+                                                                  uint32_t* changed, uint32_t* __restrict__ status,
+                                                                  int max_iter) {
+    __shared__ uint32_t lut[1 << LUT_BITS];
+    __shared__ DecTables T;
+    for (int q = threadIdx.x; q < (1 << LUT_BITS); q += blockDim.x) lut[q] = lut_g[q];
+    if (threadIdx.x == 0) T = *Tg;
+    __syncthreads();
+    cg::grid_group grid = cg::this_grid();
+    const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
+    int it = 0;
+    for (; it < max_iter; it++) {
+        if (gt == 0) changed[(it + 1) % 3] = 0;  // last read two sweeps ago
+        for (uint64_t t = gt; t < nsub; t += gs) {
+            unsigned long long s;
+            if (it == 0) {
+                s = t * SUB;
+            } else {
+                s = (t == 0) ? 0ull : *(volatile unsigned long long*)(end + t - 1);
+                if (s == start[t]) continue;
+                changed[it % 3] = 1;
+            }
+            const unsigned long long lim = (t + 1) * (unsigned long long)SUB;
+            BitReader r;
+            r.init(stream, s);
+            uint32_t c = 0, e = 0;
+            while (r.pos < lim && r.pos < total_bits) {
+                uint32_t sym;
+                const int l = decode_one(r, total_bits, T, lut, sym_sorted, sym);
+                if (l < 0) { e = (uint32_t)(-l); break; }
+                r.skip(l);
+                c++;
+            }
+            start[t] = s;
+            cnt[t] = c;
+            err[t] = e;
+            *(volatile unsigned long long*)(end + t) = e ? lim : r.pos;
+        }
+        grid.sync();
+        if (it > 0 && *(volatile uint32_t*)(changed + (it % 3)) == 0) break;
+    }
+    if (gt == 0 && it >= max_iter) set_err(status, FZB_ERR_HF_SYNC);
 }
 
 __global__ void scan_cnt_kernel(const uint32_t* __restrict__ cnt, uint64_t m, unsigned long long* __restrict__ offs,
@@ -488,13 +578,14 @@ __global__ void __launch_bounds__(HD_THREADS) hf_write_dec_kernel(const uint32_t
     if (t >= nsub) return;
     unsigned long long o = offs[t];
     if (o >= n) return;
-    BitReader r{stream, start[t]};
+    BitReader r;
+    r.init(stream, start[t]);
     const unsigned long long e = end[t];
     while (r.pos < e && o < n) {
         uint32_t sym;
         const int l = decode_one(r, total_bits, T, lut, sym_sorted, sym);
         if (l < 0) break;
-        r.pos += l;
+        r.skip(l);
         out[o] = (uint16_t)sym;
         o++;
         if (o == n) *end_pos = r.pos;
@@ -642,17 +733,27 @@ FZB_API int fzb_huffman_decode(const uint8_t* d_stream, uint64_t nbytes, uint64_
     const uint32_t* words = reinterpret_cast<const uint32_t*>(d_stream);
     const unsigned blocks = (unsigned)((nsub + HD_THREADS - 1) / HD_THREADS);
     uint32_t* changed = reinterpret_cast<uint32_t*>(scal + 2);
-    // iteration 0: speculative starts; iterations 1..3: start = end of predecessor
-    const int iters = 4;
-    for (int it = 0; it < iters; it++) {
-        const int cur = it & 1, prv = cur ^ 1;
-        if (it == iters - 1) cudaMemsetAsync(changed, 0, 4, st);
-        hf_sync_kernel<<<blocks, HD_THREADS, 0, st>>>(words, total_bits, nsub, T, lut, sym_sorted, st_[prv], en_[prv],
-                                                      cn_[prv], er_[prv], st_[cur], en_[cur], cn_[cur], er_[cur],
-                                                      changed, it == 0);
+    static int coop_blocks = 0;
+    if (coop_blocks == 0) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hf_sync_coop_kernel, HD_THREADS, 0);
+        int dev = 0, nsm = kNumSMs;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        coop_blocks = (per_sm > 0 ? per_sm : 1) * nsm;
     }
-    const int fin = (iters - 1) & 1;
-    hf_sync_check_kernel<<<1, 1, 0, st>>>(changed, d_status);
+    unsigned gridc = (unsigned)coop_blocks;
+    if ((uint64_t)gridc > blocks) gridc = blocks;
+    int max_iter = 256;
+    unsigned long long* sp = st_[0];
+    unsigned long long* ep = en_[0];
+    uint32_t* cp = cn_[0];
+    uint32_t* erp = er_[0];
+    void* kargs[] = {(void*)&words, (void*)&total_bits, (void*)&nsub, (void*)&T, (void*)&lut, (void*)&sym_sorted,
+                     (void*)&sp, (void*)&ep, (void*)&cp, (void*)&erp, (void*)&changed, (void*)&d_status,
+                     (void*)&max_iter};
+    cudaLaunchCooperativeKernel((const void*)hf_sync_coop_kernel, dim3(gridc), dim3(HD_THREADS), kargs, 0, st);
+    const int fin = 0;
     scan_cnt_kernel<<<1, 1024, 0, st>>>(cn_[fin], nsub, offs, scal);
     hf_write_dec_kernel<<<blocks, HD_THREADS, 0, st>>>(words, total_bits, nsub, T, lut, sym_sorted, st_[fin], en_[fin],
                                                        offs, n, d_codes, scal + 1);

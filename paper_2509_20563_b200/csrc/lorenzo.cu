@@ -26,6 +26,7 @@
 //    The decoder compacts events, replays the chain per outlier-delimited
 //    segment, and broadcast-fills recon in parallel.
 #include "common.cuh"
+#include "scan.cuh"
 
 namespace {
 
@@ -934,10 +935,15 @@ __global__ void tile_order_kernel(int nA, int nB, int lagI, int lagJ, int* __res
 }
 
 // ------------------------------------------------------------------- 1D ---
+// Encoder: one warp walks the chain.  At an event the exact quantizer runs;
+// then the exact f32 interval [zlo, zhi] of inputs that keep a zero code
+// (convex: the predicate is monotone in v on each side of the state) is
+// pinned with 32-key windows around r -/+ eb, and the walk continues with
+// plain float compares over 32K / 1K min-max summaries and coalesced
+// element scans.
+constexpr int BS1 = 1024;        // elements per summary block
+constexpr int BS2 = 32 * BS1;    // elements per superblock
 
-constexpr int BS1 = 1024;  // elements per summary block
-
-// codes := R everywhere (zero-code default) and per-block [min, max].
 __global__ void lz1d_summary_kernel(const float* __restrict__ x, long long n, uint16_t* __restrict__ codes,
                                     int radius, float* __restrict__ bmin, float* __restrict__ bmax,
                                     long long nblk) {
@@ -947,7 +953,7 @@ __global__ void lz1d_summary_kernel(const float* __restrict__ x, long long n, ui
     for (long long blk = warp; blk < nblk; blk += nw) {
         const long long base = blk * BS1;
         float lo = INFINITY, hi = -INFINITY;
-#pragma unroll 4
+#pragma unroll 8
         for (int e = 0; e < BS1 / 32; e++) {
             const long long t = base + e * 32 + lane;
             if (t < n) {
@@ -969,26 +975,77 @@ __global__ void lz1d_summary_kernel(const float* __restrict__ x, long long n, ui
     }
 }
 
-// Zero-code predicate for fixed predictor value pred: code R, not an outlier.
+__global__ void lz1d_super_kernel(const float* __restrict__ bmin, const float* __restrict__ bmax, long long nblk,
+                                  float* __restrict__ smin, float* __restrict__ smax, long long nsb) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long sb = warp; sb < nsb; sb += nw) {
+        const long long b = sb * 32 + lane;
+        float lo = b < nblk ? bmin[b] : INFINITY, hi = b < nblk ? bmax[b] : -INFINITY;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane == 0) { smin[sb] = lo; smax[sb] = hi; }
+    }
+}
+
 FZB_DEV bool zero_code(double v, double pred, const QParams& P) {
     float rec;
     bool outl;
     const int c = quantize(v, pred, P, rec, outl);
     return c == P.radius && !outl;
 }
+FZB_DEV uint32_t fkey(float f) {
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+FZB_DEV float kfloat(uint32_t k) { return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k); }
 
-// One warp walks the whole chain.
+// Exact bounds of the zero-code key interval that contains k0 = key(state).
+// The predicate is monotone on each side of k0 (true up to the bound, false
+// beyond), so 32-key windows started at the estimate c (key of r -/+ eb)
+// pin the transition, sliding until it lies inside the window.
+FZB_DEV bool zkey(long long k, double pred, const QParams& P) {
+    if (k < 0 || k > 0xFFFFFFFFll) return false;
+    const float f = kfloat((uint32_t)k);
+    return isfinite(f) && zero_code((double)f, pred, P);
+}
+FZB_DEV uint32_t zupper(long long k0, long long c, double pred, const QParams& P) {
+    const int lane = threadIdx.x & 31;
+    long long w = max(c - 16, k0);
+    for (;;) {
+        const unsigned m = __ballot_sync(0xffffffffu, zkey(w + lane, pred, P));
+        if (m == 0xffffffffu) { w += 32; continue; }
+        if (m == 0) { w = max(w - 32, k0); continue; }
+        return (uint32_t)(w + __ffs(~m) - 2);  // trues occupy the low lanes
+    }
+}
+FZB_DEV uint32_t zlower(long long k0, long long c, double pred, const QParams& P) {
+    const int lane = threadIdx.x & 31;
+    long long e = min(c + 15, k0);
+    for (;;) {
+        const unsigned m = __ballot_sync(0xffffffffu, zkey(e - 31 + lane, pred, P));
+        if (m == 0xffffffffu) { e -= 32; continue; }
+        if (m == 0) { e = min(e + 32, k0); continue; }
+        return (uint32_t)(e - 31 + __ffs(m) - 1);  // trues occupy the high lanes
+    }
+}
+
 __global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__ x, long long n,
                                                         uint16_t* __restrict__ codes, uint32_t* __restrict__ bitmap,
                                                         const float* __restrict__ bmin, const float* __restrict__ bmax,
-                                                        long long nblk, const double* __restrict__ d_eb, int radius) {
+                                                        long long nblk, const float* __restrict__ smin,
+                                                        const float* __restrict__ smax, long long nsb,
+                                                        const double* __restrict__ d_eb, int radius) {
     const int lane = threadIdx.x;
     const QParams P = make_qparams(*d_eb, radius);
     long long t = 0;
     float r = 0.f;
     while (t < n) {
-        // process event t (every lane computes the same thing)
-        {
+        {   // event at t
             const double v = (double)__ldg(x + t);
             const double pred = (t == 0) ? 0.0 : __dadd_rn(0.0, (double)r);
             float rec;
@@ -1001,96 +1058,125 @@ __global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__
             r = rec;
             t++;
         }
+        if (t >= n) break;
         const double pred = __dadd_rn(0.0, (double)r);
-        // find next t' >= t with !zero_code(x[t'])
-        for (;;) {
-            if (t >= n) break;
-            long long blk = t / BS1;
-            if (t % BS1 != 0) {
-                // finish the current block: each lane takes 32 contiguous elements
-                const long long bend = min((blk + 1) * BS1, n);
-                long long found = -1;
-                for (long long c0 = t; c0 < bend && found < 0; c0 += 32 * 32) {
-                    long long mine = -1;
-                    const long long lb = c0 + (long long)lane * 32;
-                    for (int e = 0; e < 32; e++) {
-                        const long long tt = lb + e;
-                        if (tt >= bend) break;
-                        if (!zero_code((double)__ldg(x + tt), pred, P)) { mine = tt; break; }
-                    }
-                    const unsigned m = __ballot_sync(0xffffffffu, mine >= 0);
-                    if (m) found = __shfl_sync(0xffffffffu, mine, __ffs(m) - 1);
-                }
-                if (found >= 0) { t = found; break; }
-                t = bend;
-                continue;
-            }
-            // block-aligned: probe 32 block summaries at once
-            const long long bb = blk + lane;
-            bool skip = false;
-            if (bb < nblk) {
-                skip = zero_code((double)__ldg(bmin + bb), pred, P) && zero_code((double)__ldg(bmax + bb), pred, P);
-            }
-            const unsigned nonskip = __ballot_sync(0xffffffffu, !skip);  // lanes past nblk count as non-skip
-            if (nonskip == 0) { t = (blk + 32) * BS1; continue; }
-            const int first = __ffs(nonskip) - 1;
-            const long long fb = blk + first;
-            if (fb >= nblk) { t = n; break; }
-            // scan block fb entirely (32 lanes x 32 elements)
-            const long long lb = fb * BS1 + (long long)lane * 32;
-            long long mine = -1;
+        const long long k0 = fkey(__double2float_rn(pred));
+        const uint32_t khi = zupper(k0, fkey(__double2float_rn(__dadd_rn(pred, P.eb))), pred, P);
+        const uint32_t klo = zlower(k0, fkey(__double2float_rn(__dsub_rn(pred, P.eb))), pred, P);
+        const float zlo = kfloat(klo), zhi = kfloat(khi);
+        auto inside = [&](float v) { return v >= zlo && v <= zhi; };
+        // scan [a, b) (b - a <= 1024) with coalesced loads; returns first outside index or -1
+        auto scan = [&](long long a, long long b) -> long long {
+            float v[32];
+#pragma unroll
             for (int e = 0; e < 32; e++) {
-                const long long tt = lb + e;
-                if (tt >= n) break;
-                if (!zero_code((double)__ldg(x + tt), pred, P)) { mine = tt; break; }
+                const long long i = a + e * 32 + lane;
+                v[e] = i < b ? __ldg(x + i) : zlo;
             }
-            const unsigned m = __ballot_sync(0xffffffffu, mine >= 0);
-            if (m) { t = __shfl_sync(0xffffffffu, mine, __ffs(m) - 1); break; }
-            t = min((fb + 1) * BS1, n);
+#pragma unroll
+            for (int e = 0; e < 32; e++) {
+                const unsigned m = __ballot_sync(0xffffffffu, !inside(v[e]));
+                if (m) return a + e * 32 + (__ffs(m) - 1);
+            }
+            return -1;
+        };
+        long long found = -1;
+        if (t % BS1) {
+            const long long be = min(n, (t / BS1 + 1) * BS1);
+            found = scan(t, be);
+            t = be;
         }
+        while (found < 0 && t < n) {
+            if (t % BS2 == 0) {  // probe 32 superblocks
+                const long long sb = t / BS2 + lane;
+                const bool skip = sb < nsb && smin[sb] >= zlo && smax[sb] <= zhi;
+                const unsigned ns = __ballot_sync(0xffffffffu, !skip);
+                if (!ns) { t = (t / BS2 + 32) * BS2; continue; }
+                t = (t / BS2 + (__ffs(ns) - 1)) * BS2;
+                if (t >= n) break;
+            }
+            const long long b0 = t / BS1;
+            const long long bb = b0 + lane;
+            const bool in_sb = (bb / 32) == (b0 / 32);
+            const bool skip = bb < nblk && in_sb && bmin[bb] >= zlo && bmax[bb] <= zhi;
+            const unsigned nsk = __ballot_sync(0xffffffffu, !skip);
+            const int first = __ffs(nsk) - 1;
+            const long long fb = b0 + first;
+            if (fb >= nblk) { t = n; break; }
+            if ((fb / 32) != (b0 / 32)) { t = fb * BS1; continue; }  // rest of the superblock is skippable
+            t = fb * BS1;
+            const long long be = min(n, t + BS1);
+            found = scan(t, be);
+            t = be;
+        }
+        if (found < 0) break;
+        t = found;
     }
 }
 
 // ---- 1D decode: events = nonzero code or outlier --------------------------
-// Between events the recon value is bitwise constant, so the decoder
-// (1) compacts event positions, (2) replays the chain per segment that
-// starts at event 0 or at an outlier (outliers reset the state), writing
-// each event's value into recon[pos], and (3) fills every other element
-// with the value of the last event at or before it.
-constexpr int EV_CHUNK = 4096;  // elements per counting CTA
+// Between events the recon value is bitwise constant: (1) per-1024-element
+// warp chunks count events (code mask | outlier bitmap word), (2) scan,
+// (3) compact event positions, (4) replay the chain per segment that starts
+// at event 0 or at an outlier (outliers reset the state), writing each
+// event's value into recon[pos], (5) fill the rest with the last event's
+// value.
+constexpr int EVC = 1024;  // elements per warp chunk (32 lanes x 32)
 
-FZB_DEV bool is_event(const uint16_t* codes, const uint32_t* bitmap, long long t, int radius) {
-    return codes[t] != radius || ((bitmap[t >> 5] >> (t & 31)) & 1u);
+FZB_DEV uint32_t event_mask(const uint16_t* __restrict__ codes, const uint32_t* __restrict__ bitmap, long long n,
+                            long long base, int radius) {
+    // base = first element of this lane's 32-element group (multiple of 32)
+    uint32_t m = 0;
+    if (base + 32 <= n) {
+        const uint4* p = reinterpret_cast<const uint4*>(codes + base);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const uint4 q = __ldg(p + u);
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int h = 0; h < 4; h++) {
+                m |= (uint32_t)((w[h] & 0xFFFFu) != (uint32_t)radius) << (u * 8 + h * 2);
+                m |= (uint32_t)((w[h] >> 16) != (uint32_t)radius) << (u * 8 + h * 2 + 1);
+            }
+        }
+        m |= __ldg(bitmap + (base >> 5));
+    } else if (base < n) {
+        for (int e = 0; e < 32 && base + e < n; e++) m |= (uint32_t)(codes[base + e] != radius) << e;
+        m |= __ldg(bitmap + (base >> 5)) & (0xFFFFFFFFu >> (32 - (int)(n - base)));
+    }
+    return m;
 }
-FZB_DEV bool is_outlier(const uint32_t* bitmap, long long t) { return (bitmap[t >> 5] >> (t & 31)) & 1u; }
 
 __global__ void lz1d_event_count_kernel(const uint16_t* __restrict__ codes, const uint32_t* __restrict__ bitmap,
-                                        long long n, int radius, uint32_t* __restrict__ counts) {
-    __shared__ uint32_t tmp[33];
-    const long long base = (long long)blockIdx.x * EV_CHUNK;
-    uint32_t c = 0;
-    for (int e = threadIdx.x; e < EV_CHUNK; e += blockDim.x) {
-        const long long t = base + e;
-        if (t < n && is_event(codes, bitmap, t, radius)) c++;
-    }
-    uint32_t tot;
-    block_exclusive_scan(c, tmp, &tot);
-    if (threadIdx.x == 0) counts[blockIdx.x] = tot;
+                                        long long n, int radius, uint32_t* __restrict__ counts, long long nch) {
+    const int lane = threadIdx.x & 31;
+    const long long ch = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (ch >= nch) return;
+    uint32_t c = __popc(event_mask(codes, bitmap, n, ch * EVC + lane * 32, radius));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) counts[ch] = c;
 }
 
 __global__ void lz1d_event_compact_kernel(const uint16_t* __restrict__ codes, const uint32_t* __restrict__ bitmap,
                                           long long n, int radius, const unsigned long long* __restrict__ offs,
-                                          long long* __restrict__ evpos) {
-    __shared__ uint32_t tmp[33];
-    const long long base = (long long)blockIdx.x * EV_CHUNK;
-    unsigned long long o = offs[blockIdx.x];
-    for (int e0 = 0; e0 < EV_CHUNK; e0 += blockDim.x) {
-        const long long t = base + e0 + threadIdx.x;
-        const bool evt = (t < n) && is_event(codes, bitmap, t, radius);
-        uint32_t tot;
-        const uint32_t p = block_exclusive_scan(evt ? 1u : 0u, tmp, &tot);
-        if (evt) evpos[o + p] = t;
-        o += tot;
+                                          long long* __restrict__ evpos, long long nch) {
+    const int lane = threadIdx.x & 31;
+    const long long ch = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (ch >= nch) return;
+    const long long base = ch * EVC + lane * 32;
+    uint32_t m = event_mask(codes, bitmap, n, base, radius);
+    uint32_t c = __popc(m), inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    unsigned long long o = offs[ch] + inc - c;
+    while (m) {
+        const int e = __ffs(m) - 1;
+        m &= m - 1;
+        evpos[o++] = base + e;
     }
 }
 
@@ -1102,11 +1188,12 @@ __global__ void lz1d_event_chain_kernel(const long long* __restrict__ evpos, con
     for (unsigned long long e = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; e < nev;
          e += (unsigned long long)gridDim.x * blockDim.x) {
         const long long p0 = evpos[e];
-        if (!(e == 0 || is_outlier(bitmap, p0))) continue;
+        const bool o0 = (bitmap[p0 >> 5] >> (p0 & 31)) & 1u;
+        if (!(e == 0 || o0)) continue;
         float r = 0.f;
         for (unsigned long long q = e; q < nev; q++) {
             const long long p = evpos[q];
-            const bool outl = is_outlier(bitmap, p);
+            const bool outl = (bitmap[p >> 5] >> (p & 31)) & 1u;
             if (q != e && outl) break;
             if (outl) {
                 r = recon[p];  // pre-scattered outlier value
@@ -1121,31 +1208,31 @@ __global__ void lz1d_event_chain_kernel(const long long* __restrict__ evpos, con
 
 __global__ void lz1d_fill_kernel(const uint16_t* __restrict__ codes, const uint32_t* __restrict__ bitmap, long long n,
                                  int radius, const unsigned long long* __restrict__ offs,
-                                 const long long* __restrict__ evpos, float* __restrict__ recon) {
-    __shared__ long long wmax[32];
-    const long long base = (long long)blockIdx.x * EV_CHUNK;
-    const unsigned long long o = offs[blockIdx.x];
-    long long carry = o > 0 ? evpos[o - 1] : -1;  // last event before this chunk
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int e0 = 0; e0 < EV_CHUNK; e0 += blockDim.x) {
-        const long long t = base + e0 + threadIdx.x;
-        const bool evt = (t < n) && is_event(codes, bitmap, t, radius);
-        long long m = evt ? t : -1;
+                                 const long long* __restrict__ evpos, float* __restrict__ recon, long long nch) {
+    const int lane = threadIdx.x & 31;
+    const long long ch = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (ch >= nch) return;
+    const long long base = ch * EVC + lane * 32;
+    const uint32_t m = event_mask(codes, bitmap, n, base, radius);
+    // last event position at or before the end of each lane's group
+    long long last = m ? base + 31 - __clz(m) : -1;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const long long y = __shfl_up_sync(0xffffffffu, m, d);
-            if (lane >= d) m = max(m, y);
-        }
-        if (lane == 31) wmax[warp] = m;
-        __syncthreads();
-        long long pre = carry;
-        for (int w = 0; w < warp; w++) pre = max(pre, wmax[w]);
-        m = max(m, pre);
-        long long blockmax = carry;
-        for (int w = 0; w < nw; w++) blockmax = max(blockmax, wmax[w]);
-        __syncthreads();
-        if (t < n && !evt) recon[t] = m >= 0 ? recon[m] : 0.f;
-        carry = blockmax;
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, last, o);
+        if (lane >= o) last = max(last, y);
+    }
+    long long carry = __shfl_up_sync(0xffffffffu, last, 1);
+    if (lane == 0) carry = -1;
+    if (carry < 0) {
+        const unsigned long long o = offs[ch];
+        carry = o > 0 ? evpos[o - 1] : -1;
+    }
+    if (base >= n) return;
+    // a zero-code element reconstructs to f32(0.0 + r): same value, -0 -> +0
+    float cur = carry >= 0 ? recon[carry] + 0.0f : 0.f;
+    for (int e = 0; e < 32 && base + e < n; e++) {
+        if ((m >> e) & 1u) cur = recon[base + e] + 0.0f;
+        else recon[base + e] = cur;
     }
 }
 
@@ -1286,10 +1373,9 @@ FZB_API size_t fzb_lorenzo_workspace_bytes(uint32_t n0, uint32_t n1, uint32_t n2
     canon(n0, n1, n2);
     const long long n = (long long)n0 * n1 * n2;
     if (n0 == 1 && n1 == 1) {
-        // encode: block summaries; decode: counts + offsets + event records + event recon
-        const long long nblk = (n + BS1 - 1) / BS1, nch = (n + EV_CHUNK - 1) / EV_CHUNK;
-        const size_t enc = (size_t)nblk * 8 + 512;
-        const size_t dec = 1024 + (size_t)nch * 4 + (size_t)nch * 8 + (size_t)n * 8;
+        const long long nblk = (n + BS1 - 1) / BS1, nsb = (nblk + 31) / 32, nch = (n + EVC - 1) / EVC;
+        const size_t enc = (size_t)(nblk + nsb) * 8 + 1024;
+        const size_t dec = 1024 + (size_t)nch * 4 + (size_t)nch * 8 + fzscan::ws_bytes(nch) + 256 + (size_t)n * 8;
         return enc > dec ? enc : dec;
     }
     switch (pick_pi(n0)) {
@@ -1312,12 +1398,16 @@ FZB_API int fzb_lorenzo_encode_f32(const float* d_in, uint32_t n0, uint32_t n1, 
     const long long n = (long long)n0 * n1 * n2;
     if (n == 0) return 0;
     if (n0 == 1 && n1 == 1) {
-        const long long nblk = (n + BS1 - 1) / BS1;
-        if (ws_bytes < (size_t)nblk * 8) return FZB_E_WORKSPACE;
+        const long long nblk = (n + BS1 - 1) / BS1, nsb = (nblk + 31) / 32;
+        if (ws_bytes < (size_t)(nblk + nsb) * 8) return FZB_E_WORKSPACE;
         float* bmin = static_cast<float*>(d_ws);
         float* bmax = bmin + nblk;
+        float* smin = bmax + nblk;
+        float* smax = smin + nsb;
         lz1d_summary_kernel<<<kNumSMs * 8, 256, 0, st>>>(d_in, n, d_codes, (int)radius, bmin, bmax, nblk);
-        lz1d_walk_kernel<<<1, 32, 0, st>>>(d_in, n, d_codes, d_bitmap, bmin, bmax, nblk, d_eb, (int)radius);
+        lz1d_super_kernel<<<kNumSMs * 2, 256, 0, st>>>(bmin, bmax, nblk, smin, smax, nsb);
+        lz1d_walk_kernel<<<1, 32, 0, st>>>(d_in, n, d_codes, d_bitmap, bmin, bmax, nblk, smin, smax, nsb, d_eb,
+                                           (int)radius);
         return fzb_check_launch();
     }
     if (kUseWave3 && n0 >= 8 && 8ll * n1 * n2 < (1ll << 31))
@@ -1342,18 +1432,21 @@ FZB_API int fzb_lorenzo_decode_f32(const uint16_t* d_codes, const uint32_t* d_bi
     const long long n = (long long)n0 * n1 * n2;
     if (n == 0) return 0;
     if (n0 == 1 && n1 == 1) {
-        const long long nch = (n + EV_CHUNK - 1) / EV_CHUNK;
+        const long long nch = (n + EVC - 1) / EVC;
         if (ws_bytes < fzb_lorenzo_workspace_bytes(1, 1, (uint32_t)n)) return FZB_E_WORKSPACE;
         unsigned char* w = static_cast<unsigned char*>(d_ws);
+        auto al = [](size_t x) { return (x + 255) / 256 * 256; };
         unsigned long long* nev = reinterpret_cast<unsigned long long*>(w);
         uint32_t* counts = reinterpret_cast<uint32_t*>(w + 256);
-        unsigned long long* offs = reinterpret_cast<unsigned long long*>(w + 256 + ((nch * 4 + 255) / 256) * 256);
-        long long* evpos = reinterpret_cast<long long*>(reinterpret_cast<unsigned char*>(offs) + ((nch * 8 + 255) / 256) * 256);
-        lz1d_event_count_kernel<<<(unsigned)nch, 256, 0, st>>>(d_codes, d_bitmap, n, (int)radius, counts);
-        scan_counts_kernel<<<1, 1024, 0, st>>>(counts, nch, offs, nev);
-        lz1d_event_compact_kernel<<<(unsigned)nch, 256, 0, st>>>(d_codes, d_bitmap, n, (int)radius, offs, evpos);
+        unsigned long long* offs = reinterpret_cast<unsigned long long*>(w + 256 + al(nch * 4));
+        void* sws = w + 256 + al(nch * 4) + al(nch * 8);
+        long long* evpos = reinterpret_cast<long long*>(w + 256 + al(nch * 4) + al(nch * 8) + al(fzscan::ws_bytes(nch)));
+        const unsigned blocks = (unsigned)((nch * 32 + 255) / 256);
+        lz1d_event_count_kernel<<<blocks, 256, 0, st>>>(d_codes, d_bitmap, n, (int)radius, counts, nch);
+        fzscan::exclusive(counts, nch, offs, nev, sws, st);
+        lz1d_event_compact_kernel<<<blocks, 256, 0, st>>>(d_codes, d_bitmap, n, (int)radius, offs, evpos, nch);
         lz1d_event_chain_kernel<<<kNumSMs * 4, 128, 0, st>>>(evpos, nev, d_codes, d_bitmap, d_recon, d_eb, (int)radius);
-        lz1d_fill_kernel<<<(unsigned)nch, 256, 0, st>>>(d_codes, d_bitmap, n, (int)radius, offs, evpos, d_recon);
+        lz1d_fill_kernel<<<blocks, 256, 0, st>>>(d_codes, d_bitmap, n, (int)radius, offs, evpos, d_recon, nch);
         return fzb_check_launch();
     }
     if (kUseWave3 && n0 >= 8 && 8ll * n1 * n2 < (1ll << 31))

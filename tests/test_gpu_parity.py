@@ -224,3 +224,32 @@ def test_full_size_c1_archive_matches_oracle(oracle, preset):
     _, orec = oracle.decompress(want)
     assert rec.data.tobytes() == orec.tobytes()
     assert float(np.max(np.abs(rec.data.astype(np.float64) - x))) <= a.resolved_bound().eb_abs
+
+
+def test_lorenzo_1d_negative_zero_and_outliers(oracle):
+    # -0.0 outliers followed by zero-code runs: recon must normalise to +0.0 exactly like the reference
+    x = np.zeros(5000, np.float32)
+    x[::7] = -0.0
+    x[100] = 1e6
+    x[101:400] = -0.0
+    x[1000:1100] = np.linspace(-1, 1, 100, dtype=np.float32)
+    e = 1e-3
+    codes, idx, vals, recon = oracle.lorenzo_quantize(x, (x.size,), e, 4)
+    lo, hi = float(x.min()), float(x.max())
+    q = pr.lorenzo_quantize(Field((x.size,), x), ResolvedBound(e, lo, hi), 4)
+    assert np.array_equal(q.codes, codes) and np.array_equal(q.outlier_indices, idx)
+    assert pr.lorenzo_reconstruct(q, ResolvedBound(e, lo, hi)).data.tobytes() == recon.tobytes()
+
+
+@pytest.mark.parametrize("preset", ["default", "speed"])
+def test_full_size_c4_archive_matches_oracle(oracle, preset):
+    """BASELINE config C4: HACC-shaped 1D particle field, 280,953,867 values, rel 1e-4."""
+    from paper_2509_20563_b200 import data
+    n = 280_953_867
+    x = data.particle1d_device(n, 0).cpu().numpy()
+    want = oracle.compress(x, (n,), 1, 1e-4, preset)
+    a = fz.compress(Field((n,), x), ErrorBoundSpec(REL, 1e-4), preset)
+    assert fz.serialize_archive(a) == want
+    rec = fz.decompress(a)
+    _, orec = oracle.decompress(want)
+    assert rec.data.tobytes() == orec.tobytes()
