@@ -46,6 +46,9 @@ FZB_API int fzb_minmax_f32(const float *d_in, uint64_t n, float *d_lohi, void *d
 FZB_API int fzb_resolve_bound(const float *d_lohi, int eb_mode, double magnitude, double *d_eb, void *stream);
 
 /* ---- a2-a4: Lorenzo (predict.py:93-144, 221-253) ------------------------ */
+/* The workspace carries a launch epoch and tagged halo slots across calls:
+ * zero-fill it once when it is allocated, then pass it unchanged (any later
+ * geometry that fits may reuse it; never share one between two streams). */
 FZB_API size_t fzb_lorenzo_workspace_bytes(uint32_t n0, uint32_t n1, uint32_t n2);
 /* codes u16[n]; d_bitmap u32[ceil(n/32)] zeroed by caller; outliers set bits. */
 FZB_API int fzb_lorenzo_encode_f32(const float *d_in, uint32_t n0, uint32_t n1, uint32_t n2, const double *d_eb,

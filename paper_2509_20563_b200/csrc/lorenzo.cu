@@ -25,6 +25,9 @@
 //    lies inside the zero-code interval (the predicate is convex in v).
 //    The decoder compacts events, replays the chain per outlier-delimited
 //    segment, and broadcast-fills recon in parallel.
+#include <stdio.h>
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "scan.cuh"
 
@@ -934,6 +937,8 @@ __global__ void tile_order_kernel(int nA, int nB, int lagI, int lagJ, int* __res
     }
 }
 
+#include "lorenzo6.cuh"
+
 // ------------------------------------------------------------------- 1D ---
 // Encoder: one warp walks the chain.  At an event the exact quantizer runs;
 // then the exact f32 interval [zlo, zhi] of inputs that keep a zero code
@@ -1365,6 +1370,62 @@ void canon(uint32_t& n0, uint32_t& n1, uint32_t& n2) {
 
 int pick_pi(uint32_t n0) { return n0 >= 8 ? 8 : (n0 >= 4 ? 4 : (n0 >= 2 ? 2 : 1)); }
 
+// FZB_LORENZO=4 selects the previous (barrier-per-step) wavefront for A/B runs.
+bool use_v4(uint32_t n2) {
+    // v7 stages 16-byte row quads; rows that are not a multiple of 4 long use v4
+    const char* e = getenv("FZB_LORENZO");
+    return (e && e[0] == '4') || (n2 % 4 != 0);
+}
+
+// v7 wavefront configurations (W compute warps x R rows per thread); the
+// tile height W*R must not exceed n0.  FZB_LZ_CFG=WxR overrides (tuning).
+struct Cfg7 { int W, R; };
+Cfg7 pick7(uint32_t n0) {
+    const char* e = getenv("FZB_LZ_CFG");
+    if (e) {
+        int W = 0, R = 0;
+        if (sscanf(e, "%dx%d", &W, &R) == 2 && (uint32_t)(W * R) <= n0) return {W, R};
+    }
+    if (n0 >= 8) return {4, 2};
+    if (n0 >= 4) return {2, 2};
+    if (n0 >= 2) return {1, 2};
+    return {1, 1};
+}
+
+#define FZB_LZ7_CFGS(X) X(8, 2) X(4, 4) X(4, 2) X(8, 1) X(2, 4) X(2, 2) X(1, 2) X(1, 1) X(16, 1) X(4, 1) X(2, 1)
+
+template <bool DEC>
+int launch_v7(const float* orig, const uint16_t* codes_in, uint16_t* codes_out, uint32_t* bitmap, float* recon,
+              uint32_t n0, uint32_t n1, uint32_t n2, const double* d_eb, int radius, void* ws, size_t ws_bytes,
+              cudaStream_t st) {
+    const Cfg7 c = pick7(n0);
+#define FZB_LZ7_CASE(W_, R_)                                                                                   \
+    if (c.W == W_ && c.R == R_)                                                                                 \
+        return v6::launch7<W_, R_, DEC>(orig, codes_in, codes_out, bitmap, recon, n0, n1, n2, d_eb, radius, ws, \
+                                        ws_bytes, st);
+    FZB_LZ7_CFGS(FZB_LZ7_CASE)
+#undef FZB_LZ7_CASE
+    return FZB_E_ARG;
+}
+
+size_t v7_ws(uint32_t n0, uint32_t n1, uint32_t n2) {
+    // enough for every configuration pick7 may return (tuning overrides included)
+    size_t m = 0;
+    for (int pi : {1, 2, 4, 8, 16}) {
+        if ((uint32_t)pi > n0 && pi > 1) continue;
+        size_t t = 0;
+        switch (pi) {
+            case 1: t = v6::WS7<1>(n0, n1, n2).total; break;
+            case 2: t = v6::WS7<2>(n0, n1, n2).total; break;
+            case 4: t = v6::WS7<4>(n0, n1, n2).total; break;
+            case 8: t = v6::WS7<8>(n0, n1, n2).total; break;
+            default: t = v6::WS7<16>(n0, n1, n2).total; break;
+        }
+        m = t > m ? t : m;
+    }
+    return m;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1378,12 +1439,15 @@ FZB_API size_t fzb_lorenzo_workspace_bytes(uint32_t n0, uint32_t n1, uint32_t n2
         const size_t dec = 1024 + (size_t)nch * 4 + (size_t)nch * 8 + fzscan::ws_bytes(nch) + 256 + (size_t)n * 8;
         return enc > dec ? enc : dec;
     }
+    size_t w4;
     switch (pick_pi(n0)) {
-        case 8: return wave_ws<8>(n0, n1, n2);
-        case 4: return wave_ws<4>(n0, n1, n2);
-        case 2: return wave_ws<2>(n0, n1, n2);
-        default: return wave_ws<1>(n0, n1, n2);
+        case 8: w4 = wave_ws<8>(n0, n1, n2); break;
+        case 4: w4 = wave_ws<4>(n0, n1, n2); break;
+        case 2: w4 = wave_ws<2>(n0, n1, n2); break;
+        default: w4 = wave_ws<1>(n0, n1, n2); break;
     }
+    const size_t w6 = v7_ws(n0, n1, n2);
+    return w4 > w6 ? w4 : w6;
 }
 
 // Reference: predict.py:93-115 (_lorenzo_encode) + the outlier flags of
@@ -1410,6 +1474,8 @@ FZB_API int fzb_lorenzo_encode_f32(const float* d_in, uint32_t n0, uint32_t n1, 
                                            (int)radius);
         return fzb_check_launch();
     }
+    if (!use_v4(n2))
+        return launch_v7<false>(d_in, nullptr, d_codes, d_bitmap, nullptr, n0, n1, n2, d_eb, (int)radius, d_ws, ws_bytes, st);
     if (kUseWave3 && n0 >= 8 && 8ll * n1 * n2 < (1ll << 31))
         return launch_wave3<4, 2, false>(d_in, nullptr, d_codes, d_bitmap, nullptr, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
     switch (pick_pi(n0)) {
@@ -1449,6 +1515,8 @@ FZB_API int fzb_lorenzo_decode_f32(const uint16_t* d_codes, const uint32_t* d_bi
         lz1d_fill_kernel<<<blocks, 256, 0, st>>>(d_codes, d_bitmap, n, (int)radius, offs, evpos, d_recon, nch);
         return fzb_check_launch();
     }
+    if (!use_v4(n2))
+        return launch_v7<true>(nullptr, d_codes, nullptr, const_cast<uint32_t*>(d_bitmap), d_recon, n0, n1, n2, d_eb, (int)radius, d_ws, ws_bytes, st);
     if (kUseWave3 && n0 >= 8 && 8ll * n1 * n2 < (1ll << 31))
         return launch_wave3<4, 2, true>(nullptr, d_codes, nullptr, const_cast<uint32_t*>(d_bitmap), d_recon, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
     switch (pick_pi(n0)) {

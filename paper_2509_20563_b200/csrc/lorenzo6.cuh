@@ -1,0 +1,623 @@
+// lorenzo6.cuh -- register-resident exact Lorenzo wavefront (v6), 2D/3D.
+//
+// Reference: fzpipe predict.py:93-144 (_lorenzo_encode / _lorenzo_decode).
+// Same recurrence, same 7-term f64 order and quantizer as lz_wave4 (see the
+// arithmetic notes in lorenzo.cu / common.cuh); what changes is how the
+// dependency DAG is mapped onto the SM:
+//
+//  * Tile = R i-rows x 32 j-lanes, marching along k; ONE compute warp owns a
+//    tile.  Lane b holds all R rows of column j0+b in registers and at step
+//    s computes the R elements (i0+r, j0+b, k = s-r-b): they are independent
+//    of each other within a step (ILP R), every intra-thread neighbour (up,
+//    self, up-left, ...) is a register from the previous one or two steps,
+//    and the only cross-lane value per row and step is `left`, one 64-bit
+//    shuffle (lane 0's left halo rides the same shuffle from lane 31).  No
+//    barrier, no shared-memory ring on the dependency chain.
+//  * Halos move as LL pairs: a 64-bit word {f32 value, u32 tag} written with
+//    one 64-bit store, so value and tag become visible together and the
+//    consumer needs no fence -- it polls until the tag matches.  Producer
+//    tiles publish their last row (faceI) and lane 31 (faceJ) to global
+//    memory every step (tag = launch epoch); the consumer CTA's helper warp
+//    polls L2 and re-tags them into shared-memory rings (tag = step + 1)
+//    which the compute warp checks one step before it needs them.
+//  * The helper warp also stages the inputs (16-byte cp.async into a
+//    k-indexed ring, zero-filled outside the field so steps before a row's
+//    k == 0 compute exact zeros) and flushes the outputs, which the compute
+//    warp writes in place into the same ring; helper <-> compute group
+//    handshakes are release/acquire counters in shared memory.
+//  * Tiles are claimed by an atomic ticket in topological (expected start)
+//    order, so every CTA only waits on tiles that are resident or finished.
+//
+// Signed zeros: the recon values kept for prediction are normalised (x+0.0f)
+// so `up` is never -0.0; then `up + left` equals the reference's
+// `(0.0 + up) + left` and no partial sum is ever -0.0 (x + y == -0.0 needs
+// both -0.0), which also makes absent neighbours (+0.0) exact.  The f32
+// values written to the recon output keep their sign.
+#pragma once
+
+namespace v6 {
+
+constexpr int G = 8;        // steps per group (staging / flush / handshake granularity)
+constexpr int KR = 32;      // k-indexed ring slots per row (4 chunks of 8)
+constexpr int IP = 36;      // ring pitch in words: multiple of 4 (16 B cp.async) and
+                            // IP-1 odd, so lane b's row at k = c-b hits bank (3b + c) % 32
+constexpr int HR = 32;      // halo ring slots (steps)
+constexpr int HUW = 33;     // ghost-row entries per step: corner + 32 lanes
+constexpr uint32_t CODE_TAG = 0x7FC00000u;  // decode ring: NaN-tagged code; finite outliers stay raw f32 bits
+constexpr int OFF = 2;      // element k = s - OFF - r - b at step s: every halo a step needs is from step >= 0
+
+struct Geo6 {
+    int n0, n1, n2, nA, nB, S;
+    int vec;  // n2 % 4 == 0: 16-byte staging / flush
+};
+
+
+FZB_DEV uint64_t ll_pack(float v, uint32_t tag) {
+    return ((uint64_t)tag << 32) | (uint64_t)__float_as_uint(v);
+}
+FZB_DEV uint64_t ld_ll_gpu(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+FZB_DEV void st_ll_gpu(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+FZB_DEV void st_ll_gpu_if(bool pred, uint64_t* p, uint64_t v) {
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q st.relaxed.gpu.global.u64 [%0], %1; }" ::"l"(p), "l"(v),
+                 "r"((int)pred)
+                 : "memory");
+}
+FZB_DEV uint64_t ld_ll_cta(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+    return v;
+}
+FZB_DEV void st_ll_cta(uint64_t* p, uint64_t v) {
+    asm volatile("st.volatile.shared.u64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "l"(v) : "memory");
+}
+FZB_DEV uint32_t ld_acq_cta(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+    return v;
+}
+FZB_DEV void st_rel_cta(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+FZB_DEV void cp_async16_zfill(void* smem, const void* gmem, int nbytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+                 "l"(gmem), "r"(nbytes)
+                 : "memory");
+}
+FZB_DEV void cp_async4_z(void* smem, const void* gmem, int nbytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+                 "l"(gmem), "r"(nbytes)
+                 : "memory");
+}
+
+// Spin until every one of the n per-warp counters reaches `target`.
+FZB_DEV void wait_min(const uint32_t* cnt, int n, uint32_t target) {
+    while (true) {
+        uint32_t m = 0xFFFFFFFFu;
+        for (int q = 0; q < n; q++) {
+            const uint32_t v = ld_acq_cta(cnt + q);
+            m = v < m ? v : m;
+        }
+        if (m >= target) return;
+        __nanosleep(32);
+    }
+}
+
+// Chunk (8 consecutive k) of row (r, b), d = r + b, that group j first needs:
+// the one holding its last k of the group (floor division).
+FZB_DEV int chunk_of(int j, int d) { return (j * G + G - 1 - OFF - d) >> 3; }
+
+// ------------------------------------------------------------------ helper
+// Staging is asynchronous and one group ahead: stage_issue(j) puts group j's
+// new chunk of every row in flight (encode: 16-byte cp.async straight into
+// the ring; decode: 8-byte code quads + their bitmap word into a raw double
+// buffer), stage_finish(j) runs once those copies landed (decode: NaN-tag the
+// codes, splice in outlier values).  Rows are spread as
+// (row = q*16 + lane/2, half = lane&1); n2 % 4 != 0 uses a scalar path.
+template <int PI>
+struct Raw {
+    static constexpr size_t bytes = 2ull * PI * 32 * 2 * 12;   // 2 slots x rows x halves x (8 B codes + 4 B bitmap)
+};
+
+FZB_DEV void cp_async8_z(void* smem, const void* gmem, int nbytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+                 "l"(gmem), "r"(nbytes)
+                 : "memory");
+}
+FZB_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+FZB_DEV void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <int PI, bool DEC>
+FZB_DEV void stage_issue(int j, uint32_t* ring, unsigned char* raw, const float* __restrict__ orig,
+                         const uint16_t* __restrict__ codes, const uint32_t* __restrict__ bitmap, const float* recon,
+                         const Geo6& geo, int i0, int j0, int lane, uint32_t pad_code) {
+    const int n0 = geo.n0, n1 = geo.n1, n2 = geo.n2;
+    if (geo.vec) {
+        uint2* rc = reinterpret_cast<uint2*>(raw) + (size_t)(j & 1) * PI * 64;
+        uint32_t* rb = reinterpret_cast<uint32_t*>(raw + 2ull * PI * 64 * 8) + (size_t)(j & 1) * PI * 64;
+#pragma unroll 8
+        for (int q = 0; q < 2 * PI; q++) {
+            const int row = q * 16 + (lane >> 1), half = lane & 1;
+            const int r = row >> 5, b = row & 31;
+            const int k = chunk_of(j, r + b) * 8 + half * 4;
+            const int i = i0 + r, jj = j0 + b;
+            const bool ok = (i < n0) && (jj < n1) && k >= 0 && k < n2;   // n2 % 4 == 0: a half is all-in or all-out
+            const long long t = ok ? ((long long)i * n1 + jj) * n2 + k : 0;
+            if constexpr (!DEC) {
+                cp_async16_zfill(ring + row * IP + (k & (KR - 1)), orig + t, ok ? 16 : 0);
+            } else {
+                cp_async8_z(rc + row * 2 + half, codes + t, ok ? 8 : 0);
+                cp_async4_z(rb + row * 2 + half, bitmap + (t >> 5), ok ? 4 : 0);
+            }
+        }
+    } else {
+#pragma unroll 4
+        for (int q = 0; q < PI * 8; q++) {
+            const int e = q * 32 + lane;
+            const int row = e >> 3, off = e & 7;
+            const int r = row >> 5, b = row & 31;
+            const int k = chunk_of(j, r + b) * 8 + off;
+            const int i = i0 + r, jj = j0 + b;
+            const bool ok = (i < n0) && (jj < n1) && k >= 0 && k < n2;
+            uint32_t* dst = ring + row * IP + (k & (KR - 1));
+            const long long t = ok ? ((long long)i * n1 + jj) * n2 + k : 0;
+            if constexpr (!DEC) {
+                cp_async4_z(dst, orig + t, ok ? 4 : 0);
+            } else {
+                uint32_t w = pad_code;
+                if (ok) {
+                    w = CODE_TAG | (uint32_t)__ldg(codes + t);
+                    if ((__ldg(bitmap + (t >> 5)) >> (t & 31)) & 1u) w = __float_as_uint(recon[t]);
+                }
+                *dst = w;
+            }
+        }
+    }
+}
+
+template <int PI, bool DEC>
+FZB_DEV void stage_finish(int j, uint32_t* ring, const unsigned char* raw, const float* recon, const Geo6& geo, int i0,
+                          int j0, int lane, uint32_t pad_code) {
+    if constexpr (DEC) {
+        if (geo.vec) {
+            const int n0 = geo.n0, n1 = geo.n1, n2 = geo.n2;
+            const uint2* rc = reinterpret_cast<const uint2*>(raw) + (size_t)(j & 1) * PI * 64;
+            const uint32_t* rb = reinterpret_cast<const uint32_t*>(raw + 2ull * PI * 64 * 8) + (size_t)(j & 1) * PI * 64;
+#pragma unroll 4
+            for (int q = 0; q < 2 * PI; q++) {
+                const int row = q * 16 + (lane >> 1), half = lane & 1;
+                const int r = row >> 5, b = row & 31;
+                const int k = chunk_of(j, r + b) * 8 + half * 4;
+                const int i = i0 + r, jj = j0 + b;
+                const bool ok = (i < n0) && (jj < n1) && k >= 0 && k < n2;
+                uint4 w = make_uint4(pad_code, pad_code, pad_code, pad_code);   // code R: exact zeros before k == 0
+                if (ok) {
+                    const uint2 c = rc[row * 2 + half];
+                    w.x = CODE_TAG | (c.x & 0xFFFFu);
+                    w.y = CODE_TAG | (c.x >> 16);
+                    w.z = CODE_TAG | (c.y & 0xFFFFu);
+                    w.w = CODE_TAG | (c.y >> 16);
+                    const long long t = ((long long)i * n1 + jj) * n2 + k;
+                    const uint32_t bits = (rb[row * 2 + half] >> (t & 31)) & 0xFu;   // t % 4 == 0: one word
+                    if (bits) {  // rare: outlier values verbatim (pre-scattered into recon)
+                        if (bits & 1u) w.x = __float_as_uint(recon[t]);
+                        if (bits & 2u) w.y = __float_as_uint(recon[t + 1]);
+                        if (bits & 4u) w.z = __float_as_uint(recon[t + 2]);
+                        if (bits & 8u) w.w = __float_as_uint(recon[t + 3]);
+                    }
+                }
+                *reinterpret_cast<uint4*>(ring + row * IP + (k & (KR - 1))) = w;
+            }
+        }
+    }
+    __threadfence_block();
+}
+
+template <int PI, bool DEC>
+FZB_DEV void helper_flush(int m_of_j, uint32_t* ring, uint16_t* __restrict__ codes_out, uint32_t* __restrict__ bitmap,
+                          float* recon, const Geo6& geo, int i0, int j0, int lane) {
+    // flush chunk (chunk_of(m_of_j, d) - 1) of every row: complete once group m_of_j is done
+    const int n0 = geo.n0, n1 = geo.n1, n2 = geo.n2;
+    if (geo.vec) {
+#pragma unroll 4
+        for (int q = 0; q < 2 * PI; q++) {
+            const int row = q * 16 + (lane >> 1), half = lane & 1;
+            const int r = row >> 5, b = row & 31;
+            const int m = chunk_of(m_of_j, r + b) - 1;
+            const int k = m * 8 + half * 4;
+            const int i = i0 + r, jj = j0 + b;
+            if ((i < n0) && (jj < n1) && k >= 0 && k < n2) {
+                const long long t = ((long long)i * n1 + jj) * n2 + k;
+                const uint4 w = *reinterpret_cast<const uint4*>(ring + row * IP + (k & (KR - 1)));
+                if constexpr (DEC) {
+                    *reinterpret_cast<uint4*>(recon + t) = w;
+                } else {
+                    uint2 c;
+                    c.x = (w.x & 0xFFFFu) | (w.y << 16);
+                    c.y = (w.z & 0xFFFFu) | (w.w << 16);
+                    *reinterpret_cast<uint2*>(codes_out + t) = c;
+                    // bit 16 = outlier; t % 4 == 0, so the 4 flags share one bitmap word
+                    const uint32_t ob = ((w.x >> 16) & 1u) | ((w.y >> 15) & 2u) | ((w.z >> 14) & 4u) | ((w.w >> 13) & 8u);
+                    if (ob) atomicOr(bitmap + (t >> 5), ob << (t & 31));
+                }
+            }
+        }
+    } else {
+#pragma unroll 4
+        for (int q = 0; q < PI * 8; q++) {
+            const int e = q * 32 + lane;
+            const int row = e >> 3, off = e & 7;
+            const int r = row >> 5, b = row & 31;
+            const int k = (chunk_of(m_of_j, r + b) - 1) * 8 + off;
+            const int i = i0 + r, jj = j0 + b;
+            if ((i < n0) && (jj < n1) && k >= 0 && k < n2) {
+                const long long t = ((long long)i * n1 + jj) * n2 + k;
+                const uint32_t w = ring[row * IP + (k & (KR - 1))];
+                if constexpr (DEC) {
+                    recon[t] = __uint_as_float(w);
+                } else {
+                    codes_out[t] = (uint16_t)w;
+                    if (w & 0x10000u) atomicOr(bitmap + (t >> 5), 1u << (t & 31));
+                }
+            }
+        }
+    }
+}
+
+// Poll the faces this tile needs for the steps of group j and re-tag them
+// into the shared halo rings (tag = step + 1):
+//   HU[t][b]     ghost row i0-1, lane b     <- faceI(A-1, B)  at producer step t + PI
+//   HL[t][0]     corner (i0-1, j0-1)        <- faceJ(A-1, B-1) row PI-1, step t + PI + 32
+//   HL[t][1 + a] left halo of tile row a    <- faceJ(A, B-1)  row a,     step t + 32
+template <int PI>
+FZB_DEV void helper_halo(int j, uint64_t* HU, uint64_t* HL, const uint64_t* faceI, const uint64_t* faceJ, int tile,
+                         int A, int B, int nB, int S, uint32_t epoch, int lane) {
+    constexpr int NE = 32 + PI + 1;
+    constexpr int E = NE * G;
+    constexpr int EPL = (E + 31) / 32;
+    const uint64_t* srcI = A > 0 ? faceI + (size_t)(tile - nB) * S * 32 : nullptr;
+    const uint64_t* srcJ = B > 0 ? faceJ + (size_t)(tile - 1) * S * PI : nullptr;
+    const uint64_t* srcC = (A > 0 && B > 0) ? faceJ + (size_t)(tile - nB - 1) * S * PI : nullptr;
+    uint64_t val[EPL];
+    const uint64_t* src[EPL];
+    uint64_t* dst[EPL];
+    uint32_t pend = 0;
+#pragma unroll
+    for (int q = 0; q < EPL; q++) {
+        const int e = q * 32 + lane;
+        const int tt = j * G + e / NE, c = e % NE;
+        src[q] = nullptr;
+        dst[q] = nullptr;
+        val[q] = 0;
+        if (e < E && tt < S) {
+            if (c < 32) {
+                dst[q] = HU + (tt & (HR - 1)) * 32 + c;
+                if (srcI && tt + PI < S) src[q] = srcI + (size_t)(tt + PI) * 32 + c;
+            } else if (c == 32) {
+                dst[q] = HL + (tt & (HR - 1)) * (PI + 1);
+                if (srcC && tt + PI + 32 < S) src[q] = srcC + (size_t)(tt + PI + 32) * PI + (PI - 1);
+            } else {
+                dst[q] = HL + (tt & (HR - 1)) * (PI + 1) + (c - 32);
+                if (srcJ && tt + 32 < S) src[q] = srcJ + (size_t)(tt + 32) * PI + (c - 33);
+            }
+            if (src[q]) {
+                val[q] = ld_ll_gpu(src[q]);
+                pend |= 1u << q;
+            } else {
+                st_ll_cta(dst[q], ll_pack(0.f, (uint32_t)(tt + 1)));
+            }
+        }
+    }
+    while (true) {
+#pragma unroll
+        for (int q = 0; q < EPL; q++) {
+            if ((pend >> q) & 1u) {
+                if ((uint32_t)(val[q] >> 32) == epoch) {
+                    const int tt = j * G + (q * 32 + lane) / NE;
+                    st_ll_cta(dst[q], (val[q] & 0xFFFFFFFFull) | ((uint64_t)(tt + 1) << 32));
+                    pend &= ~(1u << q);
+                }
+            }
+        }
+        if (!__any_sync(FULL, pend)) break;
+#pragma unroll
+        for (int q = 0; q < EPL; q++)
+            if ((pend >> q) & 1u) val[q] = ld_ll_gpu(src[q]);
+    }
+}
+
+constexpr double RINT_MAGIC = 6755399441055744.0;   // 1.5 * 2^52: x + M - M == rint(x) for |x| < 2^51
+
+template <int W, int R, bool DEC>
+struct Smem7 {
+    static constexpr int PI = W * R;
+    static constexpr size_t ring = (size_t)PI * 32 * IP * 4;
+    static constexpr size_t hu = (size_t)HR * 32 * 8;
+    static constexpr size_t hl = (size_t)HR * (PI + 1) * 8;
+    static constexpr size_t gr = (size_t)(W > 1 ? W - 1 : 1) * HR * 32 * 8;
+    static constexpr size_t raw = DEC ? Raw<PI>::bytes : 0;
+    static constexpr size_t bytes = ring + hu + hl + gr + raw + 128;
+};
+
+// ------------------------------------------------------------------ kernel
+// CTA = W compute warps (warp w owns tile rows a = w*R + r) + 1 helper warp.
+// Warp w's ghost row (a = w*R - 1) arrives as LL pairs every step: from the
+// helper (w = 0, row i0-1 of the tile above) or from warp w-1 (GR ring).
+template <int W, int R, bool DEC>
+__global__ void __launch_bounds__((W + 2) * 32, 1)
+lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in, uint16_t* __restrict__ codes_out,
+           uint32_t* __restrict__ bitmap, float* recon, uint64_t* __restrict__ faceI, uint64_t* __restrict__ faceJ,
+           const uint32_t* __restrict__ hdr, uint32_t* __restrict__ ticket, const int* __restrict__ order, Geo6 geo,
+           const double* __restrict__ d_eb, int radius) {
+    using SM = Smem7<W, R, DEC>;
+    constexpr int PI = W * R;
+    constexpr int NT = (W + 2) * 32;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint32_t* ring = reinterpret_cast<uint32_t*>(smem_raw);
+    uint64_t* HU = reinterpret_cast<uint64_t*>(smem_raw + SM::ring);
+    uint64_t* HL = HU + HR * 32;
+    uint64_t* GR = HL + HR * (PI + 1);
+    unsigned char* raw = smem_raw + SM::ring + SM::hu + SM::hl + SM::gr;
+    uint32_t* flags = reinterpret_cast<uint32_t*>(raw + SM::raw);   // [0] tile, [1] staged groups
+    uint32_t* done = flags + 2;                                      // [w] groups finished by warp w
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    {   // ring: exact zeros (decode: code R) wherever a step before k == 0 looks;
+        // halo rings: tag 0 / value 0 == "step -1" (all k < 0)
+        const uint32_t pad = DEC ? (CODE_TAG | (uint32_t)radius) : 0u;
+        for (int q = tid; q < PI * 32 * IP; q += NT) ring[q] = pad;
+        const int nh = (int)((SM::hu + SM::hl + SM::gr) / 8);
+        for (int q = tid; q < nh; q += NT) HU[q] = 0;
+    }
+    if (tid == 0) flags[0] = (uint32_t)order[atomicAdd(ticket, 1u)];
+    if (tid < W + 2) flags[1 + tid] = 0;
+    __syncthreads();
+    const int tile = (int)flags[0];
+    const int nB = geo.nB, S = geo.S;
+    const int A = tile / nB, B = tile % nB;
+    const int i0 = A * PI, j0 = B * 32;
+    const int NGRP = S / G;
+    const uint32_t epoch = hdr[0];
+
+    if (warp == W) {
+        // ================= stager: inputs one group ahead, outputs =================
+        const uint32_t pad = CODE_TAG | (uint32_t)radius;
+        stage_issue<PI, DEC>(0, ring, raw, orig, codes_in, bitmap, recon, geo, i0, j0, lane, pad);
+        cp_async_commit();
+        for (int jg = 0; jg < NGRP; jg++) {
+            if (jg >= 2) {
+                // every warp done with group jg-2: its completed chunks flush, and
+                // chunk m(jg+1) - 4 = m(jg-3) frees its ring slots for group jg+1
+                wait_min(done, W, (uint32_t)(jg - 1));
+                helper_flush<PI, DEC>(jg - 2, ring, codes_out, bitmap, recon, geo, i0, j0, lane);
+            }
+            if (jg + 1 < NGRP)
+                stage_issue<PI, DEC>(jg + 1, ring, raw, orig, codes_in, bitmap, recon, geo, i0, j0, lane, pad);
+            cp_async_commit();
+            cp_async_wait1();   // group jg's copies have landed
+            stage_finish<PI, DEC>(jg, ring, raw, recon, geo, i0, j0, lane, pad);
+            __syncwarp();
+            if (lane == 0) st_rel_cta(flags + 1, (uint32_t)(jg + 1));
+        }
+        if (NGRP >= 2) {
+            wait_min(done, W, (uint32_t)(NGRP - 1));
+            helper_flush<PI, DEC>(NGRP - 2, ring, codes_out, bitmap, recon, geo, i0, j0, lane);
+        }
+        wait_min(done, W, (uint32_t)NGRP);
+        helper_flush<PI, DEC>(NGRP - 1, ring, codes_out, bitmap, recon, geo, i0, j0, lane);
+        helper_flush<PI, DEC>(NGRP, ring, codes_out, bitmap, recon, geo, i0, j0, lane);
+        return;
+    }
+    if (warp == W + 1) {
+        // ================= halo warp: polls faces up to 3 groups ahead =================
+        for (int jg = 0; jg < NGRP; jg++) {
+            // ring slots of steps 8jg-32.. are free once every warp finished group jg-3
+            if (jg >= 3) wait_min(done, W, (uint32_t)(jg - 2));
+            helper_halo<PI>(jg, HU, HL, faceI, faceJ, tile, A, B, nB, S, epoch, lane);
+        }
+        return;
+    }
+
+    // ============================ compute warps ============================
+    // One basic block per step: the R rows interleave; the rare exact-division
+    // quantizer runs under a warp-uniform branch afterwards; outlier flags
+    // ride in bit 16 of the ring word (the helper sets the bitmap on flush).
+    const int w = warp, b = lane;
+    const QParams P = make_qparams(*d_eb, radius);
+    const double R_d = (double)radius;
+    // state per row x: 0 = ghost row (w*R - 1), 1..R = rows w*R .. w*R+R-1
+    double C1[R + 1], C2[R + 1], L1[R + 1], L2[R + 1];
+    float F1[R + 1];   // f32 copy of C1 (what moves through the shuffles)
+#pragma unroll
+    for (int x = 0; x <= R; x++) {
+        C1[x] = C2[x] = L1[x] = L2[x] = 0.0;
+        F1[x] = 0.f;
+    }
+    const uint64_t* ghost_src = (w == 0) ? HU + b : GR + (size_t)(w - 1) * HR * 32 + b;   // + slot*32
+    uint64_t* ghost_dst = (w < W - 1) ? GR + (size_t)w * HR * 32 + b : nullptr;
+    uint64_t* fI = (w == W - 1 && A < geo.nA - 1) ? faceI + (size_t)tile * S * 32 + b : nullptr;
+    uint64_t* fJ = (B < nB - 1) ? faceJ + (size_t)tile * S * PI + w * R : nullptr;
+    const bool l31 = (b == 31), l0 = (b == 0);
+    const uint64_t* hlw = HL + w * R;   // + slot*(PI+1): entries x = 0..R (row w*R-1+x)
+    uint32_t* ringl = ring + (w * R * 32 + b) * IP;
+
+    for (int g = 0; g < NGRP; g++) {
+        if (ld_acq_cta(flags + 1) < (uint32_t)(g + 1))
+            while (ld_acq_cta(flags + 1) < (uint32_t)(g + 1)) {
+            }
+#pragma unroll
+        for (int st = 0; st < G; st++) {
+            const int s = g * G + st;
+            // ---- step s-1 values of the ghost row and of lane -1 (LL, tag s)
+            const int ps = (s - 1) & (HR - 1);
+            uint64_t gh, hh[R + 1];
+            while (true) {
+                gh = ld_ll_cta(ghost_src + ps * 32);
+                bool ok = (uint32_t)(gh >> 32) == (uint32_t)s;
+#pragma unroll
+                for (int x = 0; x <= R; x++) {
+                    hh[x] = ld_ll_cta(hlw + ps * (PI + 1) + x);
+                    ok &= (uint32_t)(hh[x] >> 32) == (uint32_t)s;
+                }
+                if (__all_sync(FULL, ok)) break;
+            }
+            F1[0] = __uint_as_float((uint32_t)gh);
+            C1[0] = (double)F1[0];
+            // ---- left neighbours: lane b-1's previous values; lane 0 <- lane -1 halo
+            double Ln[R + 1];
+#pragma unroll
+            for (int x = 0; x <= R; x++) {
+                const float up1 = __shfl_up_sync(FULL, F1[x], 1);
+                Ln[x] = (double)(l0 ? __uint_as_float((uint32_t)hh[x]) : up1);
+            }
+            const int u = s - OFF - w * R - b;
+            double pred[R + 1];
+            uint32_t* cell[R + 1];
+#pragma unroll
+            for (int x = 1; x <= R; x++) {
+                cell[x] = ringl + (x - 1) * 32 * IP + ((u - (x - 1)) & (KR - 1));
+                double p = __dadd_rn(C1[x - 1], Ln[x]);   // up + left (up never -0.0)
+                p = __dadd_rn(p, C1[x]);                   // + self
+                p = __dsub_rn(p, L1[x - 1]);               // - diag
+                p = __dsub_rn(p, C2[x - 1]);               // - up(k-1)
+                p = __dsub_rn(p, L1[x]);                   // - left(k-1)
+                pred[x] = __dadd_rn(p, L2[x - 1]);         // + diag(k-1)
+            }
+            double Cn[R + 1];
+            float Fn[R + 1];
+            if constexpr (!DEC) {
+                uint32_t slow = 0;
+                uint32_t word[R + 1];
+#pragma unroll
+                for (int x = 1; x <= R; x++) {
+                    const float vf = __uint_as_float(*cell[x]) + 0.0f;   // normalised -0 (same quantisation)
+                    const double v = (double)vf;
+                    const double q = __dmul_rn(__dsub_rn(v, pred[x]), P.inv2eb);
+                    const double t = __dadd_rn(q, RINT_MAGIC);
+                    const double sd = __dsub_rn(t, RINT_MAGIC);   // rint(q) (|q| >= 2^51 -> outlier anyway)
+                    const double fr = fabs(__dsub_rn(q, sd));
+                    slow |= (uint32_t)(fr >= 0.4999999990686774) << x;
+                    const float rc = __double2float_rn(__dadd_rn(pred[x], __dmul_rn(P.two_eb, sd)));
+                    const double rcd = (double)rc;
+                    const bool okq = (fabs(sd) < R_d) & (fabs(__dsub_rn(rcd, v)) <= P.eb);
+                    const int si = (int)(uint32_t)__double_as_longlong(t);
+                    word[x] = okq ? (uint32_t)(si + radius) : ((uint32_t)radius | 0x10000u);
+                    Fn[x] = okq ? rc : vf;
+                    Cn[x] = okq ? rcd : v;
+                }
+                if (!P.use_recip) slow = ~1u;
+                if (__any_sync(FULL, slow)) {
+                    // frac(|q|) within ~1e-9 of .5: the exact IEEE-division quantizer decides
+#pragma unroll
+                    for (int x = 1; x <= R; x++) {
+                        if ((slow >> x) & 1u) {
+                            const float vf = __uint_as_float(*cell[x]) + 0.0f;
+                            float rec;
+                            bool outl;
+                            const int code = quantize((double)vf, pred[x], P, rec, outl);
+                            word[x] = (uint32_t)code | (outl ? 0x10000u : 0u);
+                            Fn[x] = rec;
+                            Cn[x] = (double)rec;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int x = 1; x <= R; x++) *cell[x] = word[x];
+            } else {
+#pragma unroll
+                for (int x = 1; x <= R; x++) {
+                    const uint32_t wv = *cell[x];
+                    const bool is_code = (wv & 0x7F800000u) == 0x7F800000u;
+                    // (code - R) exactly via the 2^52 mantissa trick, no int->double convert
+                    const double cm = __dsub_rn(__longlong_as_double(0x4330000000000000ll | (long long)(wv & 0xFFFFu)),
+                                                4503599627370496.0 + R_d);
+                    const float rc = __double2float_rn(__dadd_rn(pred[x], __dmul_rn(P.two_eb, cm)));   // never -0.0
+                    const float ov = __uint_as_float(wv) + 0.0f;   // outlier (verbatim in the output)
+                    *cell[x] = is_code ? __float_as_uint(rc) : wv;
+                    Fn[x] = is_code ? rc : ov;
+                    Cn[x] = (double)Fn[x];
+                }
+            }
+            // ---- publish: ghost for warp w+1 / faceI, and lane 31's faceJ rows
+            const uint64_t myrow = ll_pack(Fn[R], (uint32_t)(s + 1));
+            if (ghost_dst) st_ll_cta(ghost_dst + (s & (HR - 1)) * 32, myrow);
+            if (fI) st_ll_gpu(fI + (size_t)s * 32, ll_pack(Fn[R], epoch));
+            if (fJ) {
+#pragma unroll
+                for (int x = 1; x <= R; x++) st_ll_gpu_if(l31, fJ + (size_t)s * PI + (x - 1), ll_pack(Fn[x], epoch));
+            }
+            // ---- shift the history
+#pragma unroll
+            for (int x = 0; x <= R; x++) {
+                C2[x] = C1[x];
+                L2[x] = L1[x];
+                L1[x] = Ln[x];
+            }
+#pragma unroll
+            for (int x = 1; x <= R; x++) {
+                C1[x] = Cn[x];
+                F1[x] = Fn[x];
+            }
+        }
+        __syncwarp();
+        if (b == 0) st_rel_cta(done + w, (uint32_t)(g + 1));
+    }
+}
+
+__global__ void lz7_prep_kernel(uint32_t* hdr) {
+    hdr[0] += 1u;   // launch epoch: face tags of earlier launches never match
+    hdr[1] = 0u;    // ticket
+}
+
+template <int PI>
+struct WS7 {
+    size_t ntile, S, K, off_order, off_counts, off_fI, off_fJ, total;
+    WS7(int n0, int n1, int n2) {
+        const size_t nA = (n0 + PI - 1) / PI, nB = (n1 + 31) / 32;
+        ntile = nA * nB;
+        // last element: k = n2-1 at a + b = PI + 30; whole groups (the compute warps run them)
+        S = ((size_t)n2 + PI + 30 + OFF + G - 1) / G * G;
+        K = (size_t)(PI + 8) * (nA - 1) + (size_t)(32 + 8) * (nB - 1) + 1;
+        auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+        off_order = 256;
+        off_counts = off_order + al(ntile * 4);
+        off_fI = off_counts + al(K * 4);
+        off_fJ = off_fI + al(ntile * S * 32 * 8);
+        total = off_fJ + al(ntile * S * PI * 8);
+    }
+};
+
+template <int W, int R, bool DEC>
+int launch7(const float* orig, const uint16_t* codes_in, uint16_t* codes_out, uint32_t* bitmap, float* recon, int n0,
+            int n1, int n2, const double* d_eb, int radius, void* ws, size_t ws_bytes, cudaStream_t st) {
+    constexpr int PI = W * R;
+    WS7<PI> L(n0, n1, n2);
+    if (ws_bytes < L.total) return FZB_E_WORKSPACE;
+    Geo6 g;
+    g.n0 = n0; g.n1 = n1; g.n2 = n2;
+    g.nA = (n0 + PI - 1) / PI;
+    g.nB = (n1 + 31) / 32;
+    g.S = (int)L.S;
+    g.vec = (n2 % 4 == 0) ? 1 : 0;
+    unsigned char* w = static_cast<unsigned char*>(ws);
+    uint32_t* hdr = reinterpret_cast<uint32_t*>(w);
+    int* order = reinterpret_cast<int*>(w + L.off_order);
+    int* counts = reinterpret_cast<int*>(w + L.off_counts);
+    uint64_t* faceI = reinterpret_cast<uint64_t*>(w + L.off_fI);
+    uint64_t* faceJ = reinterpret_cast<uint64_t*>(w + L.off_fJ);
+    lz7_prep_kernel<<<1, 1, 0, st>>>(hdr);
+    tile_order_kernel<<<1, 1024, 0, st>>>(g.nA, g.nB, PI + 8, 32 + 8, counts, order);
+    const size_t smem = Smem7<W, R, DEC>::bytes;
+    auto kfn = lz7_kernel<W, R, DEC>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kfn<<<(unsigned)L.ntile, (W + 2) * 32, smem, st>>>(orig, codes_in, codes_out, bitmap, recon, faceI, faceJ, hdr,
+                                                      hdr + 1, order, g, d_eb, radius);
+    return fzb_check_launch();
+}
+
+}  // namespace v6

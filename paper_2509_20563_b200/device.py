@@ -47,6 +47,17 @@ def interp_applicable(dims, anchor_stride: int) -> bool:
     return len(dims) > 1 and all(int(d) >= anchor_stride + 1 for d in dims)
 
 
+def _pinned_view(raw: np.ndarray):
+    """A uint8 tensor aliasing `raw` when it lives in page-locked memory, else None."""
+    if not raw.size:
+        return None
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")  # read-only buffers: we only ever read from them
+        t = torch.frombuffer(raw, dtype=torch.uint8)
+    return t if t.is_pinned() else None
+
+
 def _p(t: torch.Tensor | None):
     return ctypes.c_void_p(t.data_ptr() if t is not None else 0)
 
@@ -82,16 +93,22 @@ class Engine:
         self.stream = stream or torch.cuda.current_stream(self.device)
         self._dev: dict[str, torch.Tensor] = {}
         self._host: dict[str, torch.Tensor] = {}
+        self._inflight: list = []  # pinned sources of queued H2D copies (dropped at the next sync)
         self.launches = 0  # kernels issued through the C ABI (counted per entry point)
         self.trace = None  # list -> (entry point, start event, end event) per call
 
     # ------------------------------------------------------------ buffers
-    def buf(self, name: str, nbytes: int, zero: bool = False) -> torch.Tensor:
+    def buf(self, name: str, nbytes: int, zero: bool = False, zero_new: bool = False) -> torch.Tensor:
+        """Cached device buffer; `zero` clears it every call, `zero_new` only
+        when it is (re)allocated (workspaces that carry state across calls)."""
         nbytes = max(_align(nbytes), 256)
         t = self._dev.get(name)
         if t is None or t.numel() < nbytes:
             t = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
             self._dev[name] = t
+            if zero_new:
+                with torch.cuda.stream(self.stream):
+                    t.zero_()
         if zero:
             with torch.cuda.stream(self.stream):
                 t[:nbytes].zero_()
@@ -104,6 +121,10 @@ class Engine:
             t = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
             self._host[name] = t
         return t
+
+    def _sync(self):
+        self.stream.synchronize()
+        self._inflight.clear()
 
     @property
     def sp(self):
@@ -121,19 +142,28 @@ class Engine:
         self.launches += nk
         _lib.check(rc, fn)
 
-    def upload(self, name: str, data: bytes | np.ndarray, pad: int = 0) -> torch.Tensor:
-        """H2D copy of host bytes through a pinned staging buffer (zero padded)."""
-        raw = np.frombuffer(bytes(data), np.uint8) if not isinstance(data, np.ndarray) else data.view(np.uint8).reshape(-1)
+    def upload(self, name: str, data, pad: int = 0) -> torch.Tensor:
+        """H2D copy of host bytes (zero padded).  Payloads that already live in
+        pinned memory (archives produced by `finish`) are DMA-ed directly;
+        anything else goes through a cached pinned staging buffer."""
+        if isinstance(data, np.ndarray):
+            raw = np.ascontiguousarray(data).view(np.uint8).reshape(-1)
+        else:
+            raw = np.frombuffer(data, np.uint8) if len(data) else np.zeros(0, np.uint8)
         nb = raw.size
         dev = self.buf(name, nb + pad)
         if pad:
             with torch.cuda.stream(self.stream):
                 dev[max(nb - (nb % 4), 0):nb + pad].zero_()
         if nb:
-            h = self.pinned(name, nb)
-            h.numpy()[:nb] = raw
+            src = _pinned_view(raw)
+            if src is None:
+                h = self.pinned(name, nb)
+                h.numpy()[:nb] = raw
+                src = h[:nb]
             with torch.cuda.stream(self.stream):
-                dev[:nb].copy_(h[:nb], non_blocking=True)
+                dev[:nb].copy_(src, non_blocking=True)
+            self._inflight.append(src)  # keep the source alive until the next sync
         return dev
 
     # ----------------------------------------------------------- compress
@@ -176,7 +206,7 @@ class Engine:
             bufs["anchors"] = anchors
             bufs["n_anchors"] = na
         else:
-            lzws = self.buf("lzws", L.fzb_lorenzo_workspace_bytes(n0, n1, n2))
+            lzws = self.buf("lzws", L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
             self._call("fzb_lorenzo_encode_f32", _p(x), n0, n1, n2, _p(eb), radius, _p(codes), _p(bitmap),
                        _p(lzws), lzws.numel(), sp, nk=2)
         oidx = self.buf("oidx", 8 * n)
@@ -229,7 +259,7 @@ class Engine:
             s[16:24].copy_(b["ocount"][:8], non_blocking=True)
             key = "bitcount" if da.codec == "huffman" else "nwords"
             s[24:32].copy_(b[key][:8], non_blocking=True)
-        self.stream.synchronize()
+        self._sync()
         v = s.numpy()
         status = int(v[0:4].view(np.uint32)[0])
         lo, hi = (float(z) for z in v[8:16].view(np.float32))
@@ -249,7 +279,10 @@ class Engine:
         else:
             parts += [("bsmap", 16 * ((n + 255) // 256)), ("bspay", 4 * size)]
         total = sum(_align(sz, 64) for _, sz in parts)
-        host = self.pinned("out", total)
+        # a fresh block from torch's pinned caching allocator: the archive's
+        # payloads are read-only views into it (no host-side copy); the block
+        # returns to the cache when the archive is dropped
+        host = torch.empty(max(total, 64), dtype=torch.uint8, pin_memory=True)
         offs = []
         o = 0
         with torch.cuda.stream(self.stream):
@@ -258,9 +291,9 @@ class Engine:
                     host[o:o + sz].copy_(b[name][:sz], non_blocking=True)
                 offs.append((o, sz))
                 o += _align(sz, 64)
-        self.stream.synchronize()
-        hv = host.numpy()
-        blobs = [hv[o:o + sz].tobytes() for o, sz in offs]
+        self._sync()
+        mv = memoryview(host.numpy()).toreadonly()
+        blobs = [mv[o:o + sz] for o, sz in offs]
         segs = [(SEG_OUTLIER_INDICES, blobs[0]), (SEG_OUTLIER_VALUES, blobs[1])]
         q = 2
         if da.use_anchors:
@@ -281,7 +314,7 @@ class Engine:
             s[8:16].copy_(b["lohi"][:8], non_blocking=True)
             s[16:24].copy_(b["ocount"][:8], non_blocking=True)
             s[24:32].copy_(b["bitcount" if da.codec == "huffman" else "nwords"][:8], non_blocking=True)
-        self.stream.synchronize()
+        self._sync()
         v = s.numpy()
         return dict(status=int(v[0:4].view(np.uint32)[0]), lo=float(v[8:12].view(np.float32)[0]),
                     hi=float(v[12:16].view(np.float32)[0]), k=int(v[16:24].view(np.uint64)[0]),
@@ -326,7 +359,7 @@ class Engine:
             self._call("fzb_interp_decode_f32", _p(codes), _p(bitmap), _p(b["anchors"]), _p(out), n0, n1, n2, _p(ebt),
                        da.radius, 16, w, sp, nk=13)
         else:
-            lzws = self.buf("dlzws", L.fzb_lorenzo_workspace_bytes(n0, n1, n2))
+            lzws = self.buf("dlzws", L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
             self._call("fzb_lorenzo_decode_f32", _p(codes), _p(bitmap), _p(out), n0, n1, n2, _p(ebt), da.radius,
                        _p(lzws), lzws.numel(), sp, nk=5)
         return out
@@ -400,7 +433,7 @@ class Engine:
             self._call("fzb_interp_decode_f32", _p(codes), _p(bitmap), _p(da), _p(recon), n0, n1, n2, _p(ebt), radius,
                        anchor_stride, w, sp, nk=1 + 3 * int(np.log2(anchor_stride)))
         else:
-            lzws = self.buf("dlzws", L.fzb_lorenzo_workspace_bytes(n0, n1, n2))
+            lzws = self.buf("dlzws", L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
             self._call("fzb_lorenzo_decode_f32", _p(codes), _p(bitmap), _p(recon), n0, n1, n2, _p(ebt), radius,
                        _p(lzws), lzws.numel(), sp, nk=5)
         return recon
@@ -409,7 +442,7 @@ class Engine:
         st = self.pinned("dscal", 64)
         with torch.cuda.stream(self.stream):
             st[:8].copy_(self.buf("dstatus", 8)[:8], non_blocking=True)
-        self.stream.synchronize()
+        self._sync()
         return int(st[:4].numpy().view(np.uint32)[0])
 
 

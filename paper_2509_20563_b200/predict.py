@@ -74,7 +74,7 @@ def lorenzo_quantize(field: Field, bound: ResolvedBound, radius: int = 512) -> Q
     eb = eng.upload("p_eb", np.array([bound.eb_abs], np.float64))
     codes = eng.buf("p_codes", 2 * n + 16)
     bitmap = eng.buf("p_bitmap", 4 * ((n + 31) // 32), zero=True)
-    ws = eng.buf("p_lzws", eng.lib.fzb_lorenzo_workspace_bytes(n0, n1, n2))
+    ws = eng.buf("p_lzws", eng.lib.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
     eng._call("fzb_lorenzo_encode_f32", _p(x), n0, n1, n2, _p(eb), int(radius), _p(codes), _p(bitmap), _p(ws),
               ws.numel(), eng.sp)
     idx, vals = _compact(eng, x, bitmap, n)
