@@ -12,7 +12,7 @@ import os
 from . import errors as E
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "libfzb200.so")
+SO_PATH = os.environ.get("FZB_SO") or os.path.join(HERE, "libfzb200.so")  # FZB_SO: tuning builds only
 
 # device status bits (csrc/common.cuh)
 ERR_CODE_RANGE = 1 << 0

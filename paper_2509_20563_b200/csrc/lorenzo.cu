@@ -1527,4 +1527,10 @@ FZB_API int fzb_lorenzo_decode_f32(const uint16_t* d_codes, const uint32_t* d_bi
     }
 }
 
+#ifdef LZ7_TIMING
+FZB_API int fzb_debug_lz_timing(long long* host_out) {
+    return (int)cudaMemcpyFromSymbol(host_out, v6::g_lz_stamp, sizeof(v6::g_lz_stamp));
+}
+#endif
+
 }  // extern "C"

@@ -38,9 +38,12 @@
 namespace v6 {
 
 constexpr int G = 8;        // steps per group (staging / flush / handshake granularity)
-constexpr int KR = 32;      // k-indexed ring slots per row (4 chunks of 8)
-constexpr int IP = 36;      // ring pitch in words: multiple of 4 (16 B cp.async) and
+constexpr int KR = 64;      // k-indexed ring slots per row (8 chunks of 8)
+constexpr int IP = 68;      // ring pitch in words: multiple of 4 (16 B cp.async) and
                             // IP-1 odd, so lane b's row at k = c-b hits bank (3b + c) % 32
+constexpr int SD = 4;       // staging distance: group j+SD is put in flight while group j is published
+                            // (needs KR/8 >= SD + 4 chunks: two in use, SD in flight, one draining)
+constexpr int RAWS = SD + 1;   // decode raw-copy slots
 constexpr int HR = 32;      // halo ring slots (steps)
 constexpr int HUW = 33;     // ghost-row entries per step: corner + 32 lanes
 constexpr uint32_t CODE_TAG = 0x7FC00000u;  // decode ring: NaN-tagged code; finite outliers stay raw f32 bits
@@ -121,7 +124,7 @@ FZB_DEV int chunk_of(int j, int d) { return (j * G + G - 1 - OFF - d) >> 3; }
 // (row = q*16 + lane/2, half = lane&1); n2 % 4 != 0 uses a scalar path.
 template <int PI>
 struct Raw {
-    static constexpr size_t bytes = 2ull * PI * 32 * 2 * 12;   // 2 slots x rows x halves x (8 B codes + 4 B bitmap)
+    static constexpr size_t bytes = (size_t)RAWS * PI * 32 * 2 * 12;   // slots x rows x halves x (8 B codes + 4 B bitmap)
 };
 
 FZB_DEV void cp_async8_z(void* smem, const void* gmem, int nbytes) {
@@ -130,7 +133,8 @@ FZB_DEV void cp_async8_z(void* smem, const void* gmem, int nbytes) {
                  : "memory");
 }
 FZB_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-FZB_DEV void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+template <int N>
+FZB_DEV void cp_async_wait_n() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int PI, bool DEC>
 FZB_DEV void stage_issue(int j, uint32_t* ring, unsigned char* raw, const float* __restrict__ orig,
@@ -138,8 +142,8 @@ FZB_DEV void stage_issue(int j, uint32_t* ring, unsigned char* raw, const float*
                          const Geo6& geo, int i0, int j0, int lane, uint32_t pad_code) {
     const int n0 = geo.n0, n1 = geo.n1, n2 = geo.n2;
     if (geo.vec) {
-        uint2* rc = reinterpret_cast<uint2*>(raw) + (size_t)(j & 1) * PI * 64;
-        uint32_t* rb = reinterpret_cast<uint32_t*>(raw + 2ull * PI * 64 * 8) + (size_t)(j & 1) * PI * 64;
+        uint2* rc = reinterpret_cast<uint2*>(raw) + (size_t)(j % RAWS) * PI * 64;
+        uint32_t* rb = reinterpret_cast<uint32_t*>(raw + (size_t)RAWS * PI * 64 * 8) + (size_t)(j % RAWS) * PI * 64;
 #pragma unroll 8
         for (int q = 0; q < 2 * PI; q++) {
             const int row = q * 16 + (lane >> 1), half = lane & 1;
@@ -186,8 +190,8 @@ FZB_DEV void stage_finish(int j, uint32_t* ring, const unsigned char* raw, const
     if constexpr (DEC) {
         if (geo.vec) {
             const int n0 = geo.n0, n1 = geo.n1, n2 = geo.n2;
-            const uint2* rc = reinterpret_cast<const uint2*>(raw) + (size_t)(j & 1) * PI * 64;
-            const uint32_t* rb = reinterpret_cast<const uint32_t*>(raw + 2ull * PI * 64 * 8) + (size_t)(j & 1) * PI * 64;
+            const uint2* rc = reinterpret_cast<const uint2*>(raw) + (size_t)(j % RAWS) * PI * 64;
+            const uint32_t* rb = reinterpret_cast<const uint32_t*>(raw + (size_t)RAWS * PI * 64 * 8) + (size_t)(j % RAWS) * PI * 64;
 #pragma unroll 4
             for (int q = 0; q < 2 * PI; q++) {
                 const int row = q * 16 + (lane >> 1), half = lane & 1;
@@ -331,7 +335,37 @@ FZB_DEV void helper_halo(int j, uint64_t* HU, uint64_t* HL, const uint64_t* face
     }
 }
 
-constexpr double RINT_MAGIC = 6755399441055744.0;   // 1.5 * 2^52: x + M - M == rint(x) for |x| < 2^51
+constexpr double RINT_MAGIC = 6755399441055744.0;
+
+// Debug timing (build with -DLZ7_TIMING): clock64 stamps of tile 0's compute
+// warps at 4 points of every step; read back with fzb_debug_lz_timing.
+#ifdef LZ7_TIMING
+__device__ long long g_lz_stamp[8][1024][4];
+#define LZ_STAMP(i)                                                                                    \
+    do {                                                                                               \
+        const long long c_ = clock64();                                                                \
+        if (tile == 0 && b == 0 && s < 1024 && w < 8) g_lz_stamp[w][s][i] = c_;                        \
+    } while (0)
+#else
+#define LZ_STAMP(i) \
+    do {            \
+    } while (0)
+#endif
+
+#ifndef LZ7_UNROLL
+#define LZ7_UNROLL 2   // steps unrolled per iteration: the 8-step unroll thrashed the i-cache
+#endif
+constexpr int kStepUnroll = LZ7_UNROLL;
+
+// Out of line (rare, and keeps the unrolled step body small): the exact
+// IEEE-division quantizer; returns the ring word (code | outlier << 16).
+__device__ __noinline__ uint32_t quantize_word_slow(float vf, double pred, QParams P, float* rec) {
+    bool outl;
+    float r;
+    const int code = quantize((double)vf, pred, P, r, outl);
+    *rec = r;
+    return (uint32_t)code | (outl ? 0x10000u : 0u);
+}   // 1.5 * 2^52: x + M - M == rint(x) for |x| < 2^51
 
 template <int W, int R, bool DEC>
 struct Smem7 {
@@ -339,7 +373,7 @@ struct Smem7 {
     static constexpr size_t ring = (size_t)PI * 32 * IP * 4;
     static constexpr size_t hu = (size_t)HR * 32 * 8;
     static constexpr size_t hl = (size_t)HR * (PI + 1) * 8;
-    static constexpr size_t gr = (size_t)(W > 1 ? W - 1 : 1) * HR * 32 * 8;
+    static constexpr size_t gr = (size_t)W * HR * 32 * 8;   // W-1 ghost rings + warp W-1's scratch
     static constexpr size_t raw = DEC ? Raw<PI>::bytes : 0;
     static constexpr size_t bytes = ring + hu + hl + gr + raw + 128;
 };
@@ -365,6 +399,7 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
     unsigned char* raw = smem_raw + SM::ring + SM::hu + SM::hl + SM::gr;
     uint32_t* flags = reinterpret_cast<uint32_t*>(raw + SM::raw);   // [0] tile, [1] staged groups
     uint32_t* done = flags + 2;                                      // [w] groups finished by warp w
+    uint32_t* hready = done + W;                                     // halo groups published
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     {   // ring: exact zeros (decode: code R) wherever a step before k == 0 looks;
@@ -375,7 +410,7 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
         for (int q = tid; q < nh; q += NT) HU[q] = 0;
     }
     if (tid == 0) flags[0] = (uint32_t)order[atomicAdd(ticket, 1u)];
-    if (tid < W + 2) flags[1 + tid] = 0;
+    if (tid < W + 3) flags[1 + tid] = 0;
     __syncthreads();
     const int tile = (int)flags[0];
     const int nB = geo.nB, S = geo.S;
@@ -385,31 +420,35 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
     const uint32_t epoch = hdr[0];
 
     if (warp == W) {
-        // ================= stager: inputs one group ahead, outputs =================
+        // ================= stager: inputs SD groups ahead, outputs =================
+        // iteration jg: group jg's copies (issued SD iterations earlier) land ->
+        // publish.  Group jg+SD's chunk m(jg+SD) reuses the slots of
+        // m(jg+SD-8), last read by group jg+SD-7: once every warp finished
+        // that group, flush it and put group jg+SD in flight.  One commit per
+        // iteration (empty ones included) keeps wait_group's count fixed.
         const uint32_t pad = CODE_TAG | (uint32_t)radius;
-        stage_issue<PI, DEC>(0, ring, raw, orig, codes_in, bitmap, recon, geo, i0, j0, lane, pad);
-        cp_async_commit();
-        for (int jg = 0; jg < NGRP; jg++) {
-            if (jg >= 2) {
-                // every warp done with group jg-2: its completed chunks flush, and
-                // chunk m(jg+1) - 4 = m(jg-3) frees its ring slots for group jg+1
-                wait_min(done, W, (uint32_t)(jg - 1));
-                helper_flush<PI, DEC>(jg - 2, ring, codes_out, bitmap, recon, geo, i0, j0, lane);
-            }
-            if (jg + 1 < NGRP)
-                stage_issue<PI, DEC>(jg + 1, ring, raw, orig, codes_in, bitmap, recon, geo, i0, j0, lane, pad);
+        for (int d = 0; d < SD; d++) {
+            if (d < NGRP) stage_issue<PI, DEC>(d, ring, raw, orig, codes_in, bitmap, recon, geo, i0, j0, lane, pad);
             cp_async_commit();
-            cp_async_wait1();   // group jg's copies have landed
+        }
+        for (int jg = 0; jg < NGRP; jg++) {
+            cp_async_wait_n<SD - 1>();
             stage_finish<PI, DEC>(jg, ring, raw, recon, geo, i0, j0, lane, pad);
             __syncwarp();
             if (lane == 0) st_rel_cta(flags + 1, (uint32_t)(jg + 1));
+            const int jf = jg + SD - 7;
+            if (jf >= 0) {
+                wait_min(done, W, (uint32_t)(jf + 1));
+                helper_flush<PI, DEC>(jf, ring, codes_out, bitmap, recon, geo, i0, j0, lane);
+            }
+            if (jg + SD < NGRP)
+                stage_issue<PI, DEC>(jg + SD, ring, raw, orig, codes_in, bitmap, recon, geo, i0, j0, lane, pad);
+            cp_async_commit();
         }
-        if (NGRP >= 2) {
-            wait_min(done, W, (uint32_t)(NGRP - 1));
-            helper_flush<PI, DEC>(NGRP - 2, ring, codes_out, bitmap, recon, geo, i0, j0, lane);
+        for (int jf = (NGRP + SD - 7 > 0 ? NGRP + SD - 7 : 0); jf < NGRP; jf++) {
+            wait_min(done, W, (uint32_t)(jf + 1));
+            helper_flush<PI, DEC>(jf, ring, codes_out, bitmap, recon, geo, i0, j0, lane);
         }
-        wait_min(done, W, (uint32_t)NGRP);
-        helper_flush<PI, DEC>(NGRP - 1, ring, codes_out, bitmap, recon, geo, i0, j0, lane);
         helper_flush<PI, DEC>(NGRP, ring, codes_out, bitmap, recon, geo, i0, j0, lane);
         return;
     }
@@ -419,14 +458,19 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
             // ring slots of steps 8jg-32.. are free once every warp finished group jg-3
             if (jg >= 3) wait_min(done, W, (uint32_t)(jg - 2));
             helper_halo<PI>(jg, HU, HL, faceI, faceJ, tile, A, B, nB, S, epoch, lane);
+            __syncwarp();
+            if (lane == 0) st_rel_cta(hready, (uint32_t)(jg + 1));
         }
         return;
     }
 
     // ============================ compute warps ============================
-    // One basic block per step: the R rows interleave; the rare exact-division
-    // quantizer runs under a warp-uniform branch afterwards; outlier flags
-    // ride in bit 16 of the ring word (the helper sets the bitmap on flush).
+    // One basic block per step and ONE warp-uniform branch: the ghost row of
+    // warps w > 0 (written by warp w-1 every step) is loaded at the start of
+    // the step that precedes its use and its LL tag is checked at the end,
+    // together with the rare near-tie flag of the reciprocal quantizer; halo
+    // rings (helper-written) are guaranteed per group by `hready`.  Outlier
+    // flags ride in bit 16 of the ring word (the stager sets the bitmap).
     const int w = warp, b = lane;
     const QParams P = make_qparams(*d_eb, radius);
     const double R_d = (double)radius;
@@ -438,34 +482,42 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
         C1[x] = C2[x] = L1[x] = L2[x] = 0.0;
         F1[x] = 0.f;
     }
-    const uint64_t* ghost_src = (w == 0) ? HU + b : GR + (size_t)(w - 1) * HR * 32 + b;   // + slot*32
-    uint64_t* ghost_dst = (w < W - 1) ? GR + (size_t)w * HR * 32 + b : nullptr;
-    uint64_t* fI = (w == W - 1 && A < geo.nA - 1) ? faceI + (size_t)tile * S * 32 + b : nullptr;
-    uint64_t* fJ = (B < nB - 1) ? faceJ + (size_t)tile * S * PI + w * R : nullptr;
-    const bool l31 = (b == 31), l0 = (b == 0);
+    const bool polled = (w > 0);
+    const uint64_t* ghost_src = polled ? GR + (size_t)(w - 1) * HR * 32 + b : HU + b;   // + slot*32
+    // warp W-1 has no consumer in the CTA: its ghost stores go to a scratch ring
+    uint64_t* ghost_dst = GR + (size_t)(w < W - 1 ? w : W - 1) * HR * 32 + b;
+    const bool pubI = (w == W - 1) && (A < geo.nA - 1);
+    uint64_t* fI = faceI + (size_t)tile * S * 32 + b;
+    const bool pubJ = (B < nB - 1) && (b == 31);
+    uint64_t* fJ = faceJ + (size_t)tile * S * PI + w * R;
+    const bool l0 = (b == 0);
     const uint64_t* hlw = HL + w * R;   // + slot*(PI+1): entries x = 0..R (row w*R-1+x)
     uint32_t* ringl = ring + (w * R * 32 + b) * IP;
+    // step s consumes step s-1's ghost value and lane -1 halos (step -1: zeros)
+    uint64_t gh = 0;
+    float hf[R + 1];
+#pragma unroll
+    for (int x = 0; x <= R; x++) hf[x] = 0.f;
 
     for (int g = 0; g < NGRP; g++) {
         if (ld_acq_cta(flags + 1) < (uint32_t)(g + 1))
-            while (ld_acq_cta(flags + 1) < (uint32_t)(g + 1)) {
-            }
-#pragma unroll
+            while (ld_acq_cta(flags + 1) < (uint32_t)(g + 1)) __nanosleep(64);
+        if (ld_acq_cta(hready) < (uint32_t)(g + 1))
+            while (ld_acq_cta(hready) < (uint32_t)(g + 1)) __nanosleep(32);
+        // stay within 3 groups of warp w+1: the ghost ring holds HR = 32 steps
+        if (w + 1 < W && ld_acq_cta(done + w + 1) + 2 < (uint32_t)g)
+            while (ld_acq_cta(done + w + 1) + 2 < (uint32_t)g) __nanosleep(32);
+#pragma unroll kStepUnroll
         for (int st = 0; st < G; st++) {
             const int s = g * G + st;
-            // ---- step s-1 values of the ghost row and of lane -1 (LL, tag s)
-            const int ps = (s - 1) & (HR - 1);
-            uint64_t gh, hh[R + 1];
-            while (true) {
-                gh = ld_ll_cta(ghost_src + ps * 32);
-                bool ok = (uint32_t)(gh >> 32) == (uint32_t)s;
+            const int cs = s & (HR - 1);
+            LZ_STAMP(0);
+            // ---- next step's inputs: ghost (tag checked at the end) and halos
+            uint64_t ghn = ld_ll_cta(ghost_src + cs * 32);
+            float hfn[R + 1];
 #pragma unroll
-                for (int x = 0; x <= R; x++) {
-                    hh[x] = ld_ll_cta(hlw + ps * (PI + 1) + x);
-                    ok &= (uint32_t)(hh[x] >> 32) == (uint32_t)s;
-                }
-                if (__all_sync(FULL, ok)) break;
-            }
+            for (int x = 0; x <= R; x++) hfn[x] = __uint_as_float((uint32_t)ld_ll_cta(hlw + cs * (PI + 1) + x));
+            LZ_STAMP(1);
             F1[0] = __uint_as_float((uint32_t)gh);
             C1[0] = (double)F1[0];
             // ---- left neighbours: lane b-1's previous values; lane 0 <- lane -1 halo
@@ -473,7 +525,7 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
 #pragma unroll
             for (int x = 0; x <= R; x++) {
                 const float up1 = __shfl_up_sync(FULL, F1[x], 1);
-                Ln[x] = (double)(l0 ? __uint_as_float((uint32_t)hh[x]) : up1);
+                Ln[x] = (double)(l0 ? hf[x] : up1);
             }
             const int u = s - OFF - w * R - b;
             double pred[R + 1];
@@ -488,10 +540,11 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
                 p = __dsub_rn(p, L1[x]);                   // - left(k-1)
                 pred[x] = __dadd_rn(p, L2[x - 1]);         // + diag(k-1)
             }
+            LZ_STAMP(2);
             double Cn[R + 1];
             float Fn[R + 1];
+            uint32_t slow = 0;
             if constexpr (!DEC) {
-                uint32_t slow = 0;
                 uint32_t word[R + 1];
 #pragma unroll
                 for (int x = 1; x <= R; x++) {
@@ -511,20 +564,21 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
                     Cn[x] = okq ? rcd : v;
                 }
                 if (!P.use_recip) slow = ~1u;
-                if (__any_sync(FULL, slow)) {
-                    // frac(|q|) within ~1e-9 of .5: the exact IEEE-division quantizer decides
+                // ---- the step's one branch: ghost not yet published, or a near-tie
+                if (!__all_sync(FULL, (slow == 0) & (!polled || (uint32_t)(ghn >> 32) == (uint32_t)(s + 1)))) {
 #pragma unroll
                     for (int x = 1; x <= R; x++) {
                         if ((slow >> x) & 1u) {
-                            const float vf = __uint_as_float(*cell[x]) + 0.0f;
+                            // frac(|q|) within ~1e-9 of .5: the exact IEEE-division quantizer decides
                             float rec;
-                            bool outl;
-                            const int code = quantize((double)vf, pred[x], P, rec, outl);
-                            word[x] = (uint32_t)code | (outl ? 0x10000u : 0u);
+                            word[x] = quantize_word_slow(__uint_as_float(*cell[x]) + 0.0f, pred[x], P, &rec);
                             Fn[x] = rec;
                             Cn[x] = (double)rec;
                         }
                     }
+                    if (polled)
+                        while (!__all_sync(FULL, (uint32_t)(ghn >> 32) == (uint32_t)(s + 1)))
+                            ghn = ld_ll_cta(ghost_src + cs * 32);
                 }
 #pragma unroll
                 for (int x = 1; x <= R; x++) *cell[x] = word[x];
@@ -542,27 +596,30 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
                     Fn[x] = is_code ? rc : ov;
                     Cn[x] = (double)Fn[x];
                 }
+                if (polled && !__all_sync(FULL, (uint32_t)(ghn >> 32) == (uint32_t)(s + 1)))
+                    while (!__all_sync(FULL, (uint32_t)(ghn >> 32) == (uint32_t)(s + 1)))
+                        ghn = ld_ll_cta(ghost_src + cs * 32);
             }
-            // ---- publish: ghost for warp w+1 / faceI, and lane 31's faceJ rows
-            const uint64_t myrow = ll_pack(Fn[R], (uint32_t)(s + 1));
-            if (ghost_dst) st_ll_cta(ghost_dst + (s & (HR - 1)) * 32, myrow);
-            if (fI) st_ll_gpu(fI + (size_t)s * 32, ll_pack(Fn[R], epoch));
-            if (fJ) {
+            LZ_STAMP(3);
+            // ---- publish (predicated, no branches): ghost for warp w+1, faces
+            st_ll_cta(ghost_dst + cs * 32, ll_pack(Fn[R], (uint32_t)(s + 1)));
+            st_ll_gpu_if(pubI, fI + (size_t)s * 32, ll_pack(Fn[R], epoch));
 #pragma unroll
-                for (int x = 1; x <= R; x++) st_ll_gpu_if(l31, fJ + (size_t)s * PI + (x - 1), ll_pack(Fn[x], epoch));
-            }
+            for (int x = 1; x <= R; x++) st_ll_gpu_if(pubJ, fJ + (size_t)s * PI + (x - 1), ll_pack(Fn[x], epoch));
             // ---- shift the history
 #pragma unroll
             for (int x = 0; x <= R; x++) {
                 C2[x] = C1[x];
                 L2[x] = L1[x];
                 L1[x] = Ln[x];
+                hf[x] = hfn[x];
             }
 #pragma unroll
             for (int x = 1; x <= R; x++) {
                 C1[x] = Cn[x];
                 F1[x] = Fn[x];
             }
+            gh = ghn;
         }
         __syncwarp();
         if (b == 0) st_rel_cta(done + w, (uint32_t)(g + 1));
