@@ -2,111 +2,33 @@
 //
 // Reference: fzpipe encode.py:324-391.  Codes are u16, zero-padded to
 // 256-code blocks; each block is 16 bit planes of 8 LE u32 words, word
-// blk*128 + p*8 + w holding bit p of codes[blk*256 + 32w + j] at bit j --
-// which is exactly __ballot_sync over a warp holding those 32 codes.  The
+// blk*128 + p*8 + w holding bit p of codes[blk*256 + 32w + j] at bit j.  The
 // bitmap has one bit per word (LSB-first == LE u32 word blk*4 + i/32, bit
 // i%32), the payload keeps the nonzero words in index order.
 //
-// Encode: pass 1 = one warp per block, 128 ballots, bitmap words via 4 more
-// ballots, per-CTA nonzero counts; scan; pass 2 = recompute the ballots and
-// scatter the nonzero words at compacted offsets (coalesced).
-// Decode: per-CTA popcounts, scan, then one warp per block gathers its
-// nonzero words and inverts the transpose with 128 shuffles.
+// One warp owns a block at a time; lane l = 4w + i holds codes 8l..8l+7
+// (one 16-byte load) and ends up owning the four words with index
+// 32i + 8c + w (c = 0..3), i.e. planes p = 4i + c of the 32-code group w.
+// The bit matrix is moved with register arithmetic instead of 128 ballots:
+//   (1) two 8x8 bit transposes (64-bit masked-XOR network) turn the lane's
+//       8 codes into 16 plane bytes e_p;
+//   (2) word (p, w) is byte e_p of the four lanes of group w: a 4-lane
+//       exchange (3 xor-shuffles) plus a 4x4 byte transpose (PRMT).
+// A word is nonzero iff bit p of the OR of its 32 codes is set, so block
+// word counts, the bitmap and every word's payload rank come from 16-bit
+// OR reductions -- cheap enough to publish a CTA's aggregate for the
+// decoupled look-back *before* the transposes, which then hide the
+// look-back latency.  The decoder runs the same network backwards.
 #include "common.cuh"
 
 namespace {
 
 constexpr int BS_THREADS = 256;
 constexpr int BS_WARPS = BS_THREADS / 32;
-constexpr int BS_BPW = 8;                         // blocks per warp
-constexpr int BS_BPC = BS_WARPS * BS_BPW;         // blocks per CTA (64 -> 16384 codes)
+constexpr int BS_BPW = 4;                         // blocks per warp
+constexpr int BS_BPC = BS_WARPS * BS_BPW;         // blocks per CTA (32 -> 8192 codes)
 
-// all 128 words of block `blk`; lane l keeps words l, l+32, l+64, l+96
-FZB_DEV void block_words(const uint16_t* __restrict__ codes, uint64_t n, uint64_t blk, uint32_t mine[4]) {
-    const int lane = threadIdx.x & 31;
-    uint32_t c[8];
-#pragma unroll
-    for (int w = 0; w < 8; w++) {
-        const uint64_t t = blk * 256 + 32 * w + lane;
-        c[w] = t < n ? (uint32_t)__ldg(codes + t) : 0u;
-    }
-#pragma unroll
-    for (int s = 0; s < 4; s++) mine[s] = 0;
-#pragma unroll
-    for (int p = 0; p < 16; p++)
-#pragma unroll
-        for (int w = 0; w < 8; w++) {
-            const int i = p * 8 + w;
-            const uint32_t x = __ballot_sync(0xffffffffu, (c[w] >> p) & 1u);
-            if (lane == (i & 31)) mine[i >> 5] = x;
-        }
-}
-
-__global__ void __launch_bounds__(BS_THREADS) bs_enc_count_kernel(const uint16_t* __restrict__ codes, uint64_t n,
-                                                                  uint64_t nblocks, uint32_t* __restrict__ bitmap,
-                                                                  uint32_t* __restrict__ counts) {
-    __shared__ uint32_t wc[BS_WARPS];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t cnt = 0;
-    for (int q = 0; q < BS_BPW; q++) {
-        const uint64_t blk = (uint64_t)blockIdx.x * BS_BPC + warp * BS_BPW + q;
-        if (blk >= nblocks) break;
-        uint32_t mine[4];
-        block_words(codes, n, blk, mine);
-#pragma unroll
-        for (int s = 0; s < 4; s++) {
-            const uint32_t bm = __ballot_sync(0xffffffffu, mine[s] != 0u);
-            if (lane == s) bitmap[blk * 4 + s] = bm;
-            cnt += __popc(bm);
-        }
-    }
-    if (lane == 0) wc[warp] = cnt;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t t = 0;
-        for (int w = 0; w < BS_WARPS; w++) t += wc[w];
-        counts[blockIdx.x] = t;
-    }
-}
-
-__global__ void __launch_bounds__(BS_THREADS) bs_enc_write_kernel(const uint16_t* __restrict__ codes, uint64_t n,
-                                                                  uint64_t nblocks, const uint32_t* __restrict__ bitmap,
-                                                                  const unsigned long long* __restrict__ offs,
-                                                                  uint32_t* __restrict__ payload) {
-    __shared__ uint32_t wc[BS_WARPS];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // per-warp counts from the stored bitmap
-    uint32_t cnt = 0;
-    for (int q = 0; q < BS_BPW; q++) {
-        const uint64_t blk = (uint64_t)blockIdx.x * BS_BPC + warp * BS_BPW + q;
-        if (blk >= nblocks) break;
-        if (lane < 4) cnt += __popc(bitmap[blk * 4 + lane]);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (lane == 0) wc[warp] = cnt;
-    __syncthreads();
-    unsigned long long o = offs[blockIdx.x];
-    for (int w = 0; w < warp; w++) o += wc[w];
-    for (int q = 0; q < BS_BPW; q++) {
-        const uint64_t blk = (uint64_t)blockIdx.x * BS_BPC + warp * BS_BPW + q;
-        if (blk >= nblocks) break;
-        uint32_t mine[4];
-        block_words(codes, n, blk, mine);
-#pragma unroll
-        for (int s = 0; s < 4; s++) {
-            const uint32_t bm = __ballot_sync(0xffffffffu, mine[s] != 0u);
-            if (mine[s]) payload[o + __popc(bm & lanemask_lt())] = mine[s];
-            o += __popc(bm);
-        }
-    }
-}
-
-// Single-pass encoder: ballots once, per-CTA nonzero-word count published
-// through decoupled look-back (CTA order from an atomic ticket, so every
-// predecessor is resident or done), then compacted payload writes.
-// State word per CTA: bits 62-63 = flag (1 aggregate, 2 inclusive prefix),
-// bits 0-61 = value.
+// decoupled look-back state per CTA: bits 62-63 flag (1 aggregate, 2 inclusive prefix), 0-61 value
 constexpr unsigned long long LB_AGG = 1ull << 62, LB_PRE = 2ull << 62, LB_VAL = (1ull << 62) - 1;
 
 FZB_DEV unsigned long long ld_volatile64(const unsigned long long* p) {
@@ -115,176 +37,239 @@ FZB_DEV unsigned long long ld_volatile64(const unsigned long long* p) {
     return v;
 }
 
-__global__ void __launch_bounds__(BS_THREADS) bs_enc_fused_kernel(const uint16_t* __restrict__ codes, uint64_t n,
-                                                                  uint64_t nblocks, uint32_t* __restrict__ bitmap,
-                                                                  uint32_t* __restrict__ payload,
-                                                                  unsigned long long* __restrict__ state,
-                                                                  uint32_t* __restrict__ ticket,
-                                                                  unsigned long long* __restrict__ nwords) {
-    __shared__ uint32_t wc[BS_WARPS];
-    __shared__ unsigned long long s_excl;
+FZB_DEV uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+    return r;
+}
+
+// 8x8 bit transpose of the 64-bit word (hi:lo): bit 8j+k <-> bit 8k+j.
+FZB_DEV void t8x8(uint32_t& lo, uint32_t& hi) {
+    uint32_t t;
+    t = (lo ^ (lo >> 7)) & 0x00AA00AAu; lo ^= t ^ (t << 7);
+    t = (hi ^ (hi >> 7)) & 0x00AA00AAu; hi ^= t ^ (t << 7);
+    t = (lo ^ (lo >> 14)) & 0x0000CCCCu; lo ^= t ^ (t << 14);
+    t = (hi ^ (hi >> 14)) & 0x0000CCCCu; hi ^= t ^ (t << 14);
+    t = (lo ^ (hi << 4)) & 0xF0F0F0F0u; lo ^= t; hi ^= t >> 4;
+}
+
+// 8 codes (LE u16 pairs in r.x..r.w) -> plane bytes: E[k] holds e_{4k..4k+3},
+// e_p bit j = bit p of code j.  Self-inverse up to the packing (see below).
+FZB_DEV void codes_to_planes(const uint4 r, uint32_t E[4]) {
+    uint32_t lo0 = prmt(r.x, r.y, 0x6420), lo1 = prmt(r.z, r.w, 0x6420);   // low bytes of codes 0..7
+    uint32_t hi0 = prmt(r.x, r.y, 0x7531), hi1 = prmt(r.z, r.w, 0x7531);   // high bytes
+    t8x8(lo0, lo1);
+    t8x8(hi0, hi1);
+    E[0] = lo0; E[1] = lo1; E[2] = hi0; E[3] = hi1;
+}
+FZB_DEV uint4 planes_to_codes(const uint32_t E[4]) {
+    uint32_t lo0 = E[0], lo1 = E[1], hi0 = E[2], hi1 = E[3];
+    t8x8(lo0, lo1);
+    t8x8(hi0, hi1);
+    uint4 r;
+    r.x = prmt(lo0, hi0, 0x5140);
+    r.y = prmt(lo0, hi0, 0x7362);
+    r.z = prmt(lo1, hi1, 0x5140);
+    r.w = prmt(lo1, hi1, 0x7362);
+    return r;
+}
+
+FZB_DEV uint32_t sel4(const uint32_t E[4], int k) {
+    const uint32_t a = (k & 1) ? E[1] : E[0], b = (k & 1) ? E[3] : E[2];
+    return (k & 2) ? b : a;
+}
+
+// Lane (w, i): plane bytes E (own codes) -> its 4 words W[c] = word (4i+c, w).
+// A[x] = E_i of lane i^x; V_c = byte c of A[0..3]; word_c = V_c with byte
+// position x moved to x^i.
+FZB_DEV void planes_to_words(const uint32_t E[4], int i, uint32_t xsel, uint32_t W[4]) {
+    uint32_t A[4];
+    A[0] = sel4(E, i);
+#pragma unroll
+    for (int x = 1; x < 4; x++) A[x] = __shfl_xor_sync(0xffffffffu, sel4(E, i ^ x), x);
+    const uint32_t t0 = prmt(A[0], A[1], 0x5140), t1 = prmt(A[2], A[3], 0x5140);   // bytes 0,1 interleaved
+    const uint32_t t2 = prmt(A[0], A[1], 0x7362), t3 = prmt(A[2], A[3], 0x7362);   // bytes 2,3
+    W[0] = prmt(prmt(t0, t1, 0x5410), 0, xsel);
+    W[1] = prmt(prmt(t0, t1, 0x7632), 0, xsel);
+    W[2] = prmt(prmt(t2, t3, 0x5410), 0, xsel);
+    W[3] = prmt(prmt(t2, t3, 0x7632), 0, xsel);
+}
+FZB_DEV void words_to_planes(const uint32_t W[4], int i, uint32_t xsel, uint32_t E[4]) {
+    // undo the x^i byte move, then the 4x4 byte transpose gives A[x]
+    const uint32_t v0 = prmt(W[0], 0, xsel), v1 = prmt(W[1], 0, xsel);
+    const uint32_t v2 = prmt(W[2], 0, xsel), v3 = prmt(W[3], 0, xsel);
+    const uint32_t u0 = prmt(v0, v1, 0x5140), u1 = prmt(v2, v3, 0x5140);
+    const uint32_t u2 = prmt(v0, v1, 0x7362), u3 = prmt(v2, v3, 0x7362);
+    uint32_t A[4];
+    A[0] = prmt(u0, u1, 0x5410);
+    A[1] = prmt(u0, u1, 0x7632);
+    A[2] = prmt(u2, u3, 0x5410);
+    A[3] = prmt(u2, u3, 0x7632);
+    // A[x] = E_i of lane i^x  ->  E_k of this lane comes back from lane i^k's A[i^k]
+    uint32_t R[4];
+    R[0] = A[0];
+#pragma unroll
+    for (int x = 1; x < 4; x++) R[x] = __shfl_xor_sync(0xffffffffu, A[x], x);   // R[x] = E_{i^x} (own)
+#pragma unroll
+    for (int k = 0; k < 4; k++) E[k] = sel4(R, k ^ i);
+}
+
+// 16-bit OR of the 32 codes of this lane's group w (bit p set <=> word (p, w) nonzero)
+FZB_DEV uint32_t group_or(const uint4 r) {
+    uint32_t o = r.x | r.y | r.z | r.w;
+    o = (o | (o >> 16)) & 0xFFFFu;
+    o |= __shfl_xor_sync(0xffffffffu, o, 1);
+    o |= __shfl_xor_sync(0xffffffffu, o, 2);
+    return o;
+}
+
+// Bitmap word i of the block (bits 8c + w <-> plane 4i + c of group w), for the
+// calling lane's i; every lane of the warp gets all four in BM[0..3].
+FZB_DEV void block_bitmap(uint32_t gor, int w, int i, uint32_t BM[4]) {
+    uint32_t mine = 0;
+#pragma unroll
+    for (int c = 0; c < 4; c++) mine |= ((gor >> (4 * i + c)) & 1u) << (8 * c + w);
+    mine |= __shfl_xor_sync(0xffffffffu, mine, 4);
+    mine |= __shfl_xor_sync(0xffffffffu, mine, 8);
+    mine |= __shfl_xor_sync(0xffffffffu, mine, 16);
+#pragma unroll
+    for (int k = 0; k < 4; k++) BM[k] = __shfl_sync(0xffffffffu, mine, k);
+}
+
+FZB_DEV uint4 load_codes(const uint16_t* __restrict__ codes, uint64_t n, uint64_t blk, int lane) {
+    const uint64_t t0 = blk * 256 + 8 * lane;
+    if (t0 + 8 <= n) return __ldg(reinterpret_cast<const uint4*>(codes + t0));
+    uint32_t c[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) c[j] = (t0 + j < n) ? (uint32_t)__ldg(codes + t0 + j) : 0u;
+    return make_uint4(c[0] | (c[1] << 16), c[2] | (c[3] << 16), c[4] | (c[5] << 16), c[6] | (c[7] << 16));
+}
+
+// CTA-wide exclusive prefix of `agg` by decoupled look-back (CTA ids from a
+// ticket, so every predecessor is resident or done).  Called by warp 0.
+FZB_DEV unsigned long long lookback(uint32_t cta, unsigned long long agg, unsigned long long* state) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long excl = 0;
+    if (cta == 0) {
+        if (lane == 0) {
+            __threadfence();
+            atomicExch(state, LB_PRE | agg);
+        }
+        return 0;
+    }
+    long long base = (long long)cta - 1;
+    while (true) {
+        const long long p = base - lane;
+        unsigned long long v = LB_PRE;   // lanes before CTA 0 act as prefix 0
+        if (p >= 0) {
+            do { v = ld_volatile64(state + p); } while ((v >> 62) == 0);
+        }
+        const unsigned pre = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+        const int stop = pre ? __ffs(pre) - 1 : 32;
+        unsigned long long add = (lane <= stop && p >= 0) ? (v & LB_VAL) : 0ull;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
+        excl += add;
+        if (pre) break;
+        base -= 32;
+    }
+    if (lane == 0) {
+        __threadfence();
+        atomicExch(state + cta, LB_PRE | (excl + agg));
+    }
+    return excl;
+}
+
+__global__ void __launch_bounds__(BS_THREADS) bs_enc3_kernel(const uint16_t* __restrict__ codes, uint64_t n,
+                                                             uint64_t nblocks, uint32_t* __restrict__ bitmap,
+                                                             uint32_t* __restrict__ payload,
+                                                             unsigned long long* __restrict__ state,
+                                                             uint32_t* __restrict__ ticket,
+                                                             unsigned long long* __restrict__ nwords) {
+    __shared__ uint32_t s_off[BS_BPC];
+    __shared__ unsigned long long s_agg, s_excl;
     __shared__ uint32_t s_cta;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gw = lane >> 2, gi = lane & 3;
+    const uint32_t xsel = (uint32_t)(gi | ((1 ^ gi) << 4) | ((2 ^ gi) << 8) | ((3 ^ gi) << 12));
     if (threadIdx.x == 0) s_cta = atomicAdd(ticket, 1u);
     __syncthreads();
     const uint32_t cta = s_cta;
-    uint32_t mine[BS_BPW][4];
-    uint32_t bms[BS_BPW][4];
-    uint32_t cnt = 0;
+    const uint64_t blk0 = (uint64_t)cta * BS_BPC + warp * BS_BPW;
+
+    // ---- loads + word counts (from 16-bit ORs); the CTA aggregate is
+    //      published before the transposes so they hide the look-back
+    uint4 r[BS_BPW];
+    uint32_t gor[BS_BPW];
 #pragma unroll
     for (int q = 0; q < BS_BPW; q++) {
-        const uint64_t blk = (uint64_t)cta * BS_BPC + warp * BS_BPW + q;
-        if (blk < nblocks) {
-            block_words(codes, n, blk, mine[q]);
-        } else {
+        r[q] = (blk0 + q < nblocks) ? load_codes(codes, n, blk0 + q, lane) : make_uint4(0, 0, 0, 0);
+        gor[q] = group_or(r[q]);
+        uint32_t c = __popc(gor[q]);   // counted by each of the group's 4 lanes
 #pragma unroll
-            for (int s = 0; s < 4; s++) mine[q][s] = 0;
-        }
-#pragma unroll
-        for (int s = 0; s < 4; s++) {
-            bms[q][s] = __ballot_sync(0xffffffffu, mine[q][s] != 0u);
-            cnt += __popc(bms[q][s]);
-        }
-        if (blk < nblocks && lane < 4) bitmap[blk * 4 + lane] = bms[q][0] * (lane == 0) + bms[q][1] * (lane == 1) +
-                                                                 bms[q][2] * (lane == 2) + bms[q][3] * (lane == 3);
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) s_off[warp * BS_BPW + q] = c >> 2;
     }
-    if (lane == 0) wc[warp] = cnt;
     __syncthreads();
     if (warp == 0) {
-        uint32_t agg = 0;
-        for (int w = 0; w < BS_WARPS; w++) agg += wc[w];
-        unsigned long long excl = 0;
-        if (cta == 0) {
-            if (lane == 0) {
-                __threadfence();
-                atomicExch(state, LB_PRE | agg);
-            }
-        } else {
-            if (lane == 0) {
-                __threadfence();
-                atomicExch(state + cta, LB_AGG | agg);
-            }
-            // parallel look-back over 32 predecessors at a time
-            long long base = (long long)cta - 1;
-            while (true) {
-                const long long p = base - lane;
-                unsigned long long v = LB_PRE;  // lanes before CTA 0 act as prefix 0
-                if (p >= 0) {
-                    do { v = ld_volatile64(state + p); } while ((v >> 62) == 0);
-                }
-                const unsigned pre = __ballot_sync(0xffffffffu, (v >> 62) == 2);
-                const int stop = pre ? __ffs(pre) - 1 : 32;
-                unsigned long long add = (lane <= stop && p >= 0) ? (v & LB_VAL) : 0ull;
+        const uint32_t a = s_off[lane];   // BS_BPC == 32
+        uint32_t incl = a;
 #pragma unroll
-                for (int o = 16; o; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
-                excl += add;
-                if (pre) break;
-                base -= 32;
-            }
-            if (lane == 0) {
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        s_off[lane] = incl - a;
+        if (lane == 31) {
+            s_agg = incl;
+            if (cta != 0) {
                 __threadfence();
-                atomicExch(state + cta, LB_PRE | (excl + agg));
+                atomicExch(state + cta, LB_AGG | (unsigned long long)incl);
             }
         }
+    }
+    // ---- bit-matrix transposes (independent of the offsets)
+    uint32_t Wd[BS_BPW][4];
+#pragma unroll
+    for (int q = 0; q < BS_BPW; q++) {
+        uint32_t E[4];
+        codes_to_planes(r[q], E);
+        planes_to_words(E, gi, xsel, Wd[q]);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const unsigned long long agg = s_agg;
+        const unsigned long long excl = lookback(cta, agg, state);
         if (lane == 0) {
             s_excl = excl;
             if ((uint64_t)(cta + 1) * BS_BPC >= nblocks) *nwords = excl + agg;
         }
     }
     __syncthreads();
-    unsigned long long o = s_excl;
-    for (int w = 0; w < warp; w++) o += wc[w];
+    // ---- bitmap + compacted payload
 #pragma unroll
     for (int q = 0; q < BS_BPW; q++) {
-#pragma unroll
-        for (int s = 0; s < 4; s++) {
-            if (mine[q][s]) payload[o + __popc(bms[q][s] & lanemask_lt())] = mine[q][s];
-            o += __popc(bms[q][s]);
-        }
-    }
-}
-
-// Decoder: each warp stages its block's 128 words in shared memory, every
-// lane then extracts its own bit from each word (broadcast reads).
-__global__ void __launch_bounds__(BS_THREADS) bs_dec2_kernel(const uint32_t* __restrict__ bitmap,
-                                                             const uint32_t* __restrict__ payload, uint64_t payload_words,
-                                                             uint64_t n, uint64_t nblocks, uint32_t radius,
-                                                             const unsigned long long* __restrict__ offs,
-                                                             uint16_t* __restrict__ codes, uint32_t* __restrict__ status) {
-    __shared__ uint32_t wc[BS_WARPS];
-    __shared__ __align__(16) uint32_t sw[BS_WARPS][128];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t cnt = 0;
-    for (int q = 0; q < BS_BPW; q++) {
-        const uint64_t blk = (uint64_t)blockIdx.x * BS_BPC + warp * BS_BPW + q;
+        const uint64_t blk = blk0 + q;
         if (blk >= nblocks) break;
-        if (lane < 4) cnt += __popc(bitmap[blk * 4 + lane]);
-    }
+        uint32_t BM[4];
+        block_bitmap(gor[q], gw, gi, BM);
+        if (lane < 4) bitmap[blk * 4 + lane] = sel4(BM, lane);
+        const unsigned long long base = s_excl + s_off[warp * BS_BPW + q];
+        uint32_t before = 0;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (lane == 0) wc[warp] = cnt;
-    __syncthreads();
-    unsigned long long o = offs[blockIdx.x];
-    for (int w = 0; w < warp; w++) o += wc[w];
-    bool pad_bad = false, range_bad = false;
-    uint32_t* W = sw[warp];
-    for (int q = 0; q < BS_BPW; q++) {
-        const uint64_t blk = (uint64_t)blockIdx.x * BS_BPC + warp * BS_BPW + q;
-        if (blk >= nblocks) break;
+        for (int k = 0; k < 4; k++) before += (k < gi) ? __popc(BM[k]) : 0u;
+        const uint32_t bmi = sel4(BM, gi);
 #pragma unroll
-        for (int s = 0; s < 4; s++) {
-            const uint32_t bm = bitmap[blk * 4 + s];
-            uint32_t x = 0u;
-            if ((bm >> lane) & 1u) {
-                const unsigned long long pos = o + __popc(bm & lanemask_lt());
-                if (pos < payload_words) x = payload[pos];
-            }
-            W[s * 32 + lane] = x;
-            o += __popc(bm);
-        }
-        __syncwarp();
-        uint32_t c[8];
-#pragma unroll
-        for (int w = 0; w < 8; w++) c[w] = 0;
-#pragma unroll
-        for (int p = 0; p < 16; p++) {
-            const uint4 lo = *reinterpret_cast<const uint4*>(W + p * 8);
-            const uint4 hi = *reinterpret_cast<const uint4*>(W + p * 8 + 4);
-            const uint32_t x[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-#pragma unroll
-            for (int w = 0; w < 8; w++) c[w] |= ((x[w] >> lane) & 1u) << p;
-        }
-        __syncwarp();
-#pragma unroll
-        for (int w = 0; w < 8; w++) {
-            const uint64_t t = blk * 256 + 32 * w + lane;
-            if (t < n) {
-                codes[t] = (uint16_t)c[w];
-                range_bad |= c[w] >= 2 * radius;
-            } else {
-                pad_bad |= c[w] != 0;
+        for (int c = 0; c < 4; c++) {
+            if ((gor[q] >> (4 * gi + c)) & 1u) {
+                const uint32_t rank = before + __popc(bmi & ((1u << (8 * c + gw)) - 1u));
+                payload[base + rank] = Wd[q][c];
             }
         }
     }
-    if (pad_bad) set_err(status, FZB_ERR_BS_PAD);
-    if (range_bad) set_err(status, FZB_ERR_BS_RANGE);
 }
 
-__global__ void scan_counts_u64_kernel(const uint32_t* __restrict__ cnt, uint64_t m,
-                                       unsigned long long* __restrict__ offs, unsigned long long* __restrict__ tot) {
-    __shared__ unsigned long long tmp[33];
-    unsigned long long carry = 0;
-    for (uint64_t b0 = 0; b0 < m; b0 += blockDim.x) {
-        const uint64_t q = b0 + threadIdx.x;
-        const unsigned long long x = q < m ? cnt[q] : 0ull;
-        unsigned long long t;
-        const unsigned long long p = block_exclusive_scan64(x, tmp, &t);
-        if (q < m) offs[q] = carry + p;
-        carry += t;
-    }
-    if (threadIdx.x == 0) *tot = carry;
-}
-
+// Per-CTA word counts of the decoder (bitmap popcounts), then one scan.
 __global__ void __launch_bounds__(BS_THREADS) bs_dec_count_kernel(const uint32_t* __restrict__ bitmap, uint64_t nblocks,
                                                                   uint32_t* __restrict__ counts) {
     __shared__ uint32_t tmp[33];
@@ -297,69 +282,98 @@ __global__ void __launch_bounds__(BS_THREADS) bs_dec_count_kernel(const uint32_t
     if (threadIdx.x == 0) counts[blockIdx.x] = tot;
 }
 
-__global__ void bs_check_total_kernel(const unsigned long long* __restrict__ tot, uint64_t payload_words,
-                                      uint32_t* __restrict__ status) {
-    if (*tot != payload_words) set_err(status, FZB_ERR_BS_MISMATCH);
+__global__ void scan_counts_u64_kernel(const uint32_t* __restrict__ cnt, uint64_t m,
+                                       unsigned long long* __restrict__ offs, unsigned long long* __restrict__ tot,
+                                       uint64_t payload_words, uint32_t* __restrict__ status) {
+    __shared__ unsigned long long tmp[33];
+    unsigned long long carry = 0;
+    for (uint64_t b0 = 0; b0 < m; b0 += blockDim.x) {
+        const uint64_t q = b0 + threadIdx.x;
+        const unsigned long long x = q < m ? cnt[q] : 0ull;
+        unsigned long long t;
+        const unsigned long long p = block_exclusive_scan64(x, tmp, &t);
+        if (q < m) offs[q] = carry + p;
+        carry += t;
+    }
+    if (threadIdx.x == 0) {
+        *tot = carry;
+        if (carry != payload_words) set_err(status, FZB_ERR_BS_MISMATCH);   // encode.py:372-375
+    }
 }
 
-__global__ void __launch_bounds__(BS_THREADS) bs_dec_kernel(const uint32_t* __restrict__ bitmap,
-                                                            const uint32_t* __restrict__ payload, uint64_t payload_words,
-                                                            uint64_t n, uint64_t nblocks, uint32_t radius,
-                                                            const unsigned long long* __restrict__ offs,
-                                                            uint16_t* __restrict__ codes, uint32_t* __restrict__ status) {
-    __shared__ uint32_t wc[BS_WARPS];
+__global__ void __launch_bounds__(BS_THREADS) bs_dec3_kernel(const uint32_t* __restrict__ bitmap,
+                                                             const uint32_t* __restrict__ payload,
+                                                             uint64_t payload_words, uint64_t n, uint64_t nblocks,
+                                                             uint32_t radius, const unsigned long long* __restrict__ offs,
+                                                             uint16_t* __restrict__ codes, uint32_t* __restrict__ status) {
+    __shared__ uint32_t s_off[BS_BPC];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t cnt = 0;
-    for (int q = 0; q < BS_BPW; q++) {
-        const uint64_t blk = (uint64_t)blockIdx.x * BS_BPC + warp * BS_BPW + q;
-        if (blk >= nblocks) break;
-        if (lane < 4) cnt += __popc(bitmap[blk * 4 + lane]);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (lane == 0) wc[warp] = cnt;
-    __syncthreads();
-    unsigned long long o = offs[blockIdx.x];
-    for (int w = 0; w < warp; w++) o += wc[w];
-    bool pad_bad = false, range_bad = false;
-    for (int q = 0; q < BS_BPW; q++) {
-        const uint64_t blk = (uint64_t)blockIdx.x * BS_BPC + warp * BS_BPW + q;
-        if (blk >= nblocks) break;
-        uint32_t mine[4];
-#pragma unroll
-        for (int s = 0; s < 4; s++) {
-            const uint32_t bm = bitmap[blk * 4 + s];
-            mine[s] = 0u;
-            if ((bm >> lane) & 1u) {
-                const unsigned long long pos = o + __popc(bm & lanemask_lt());
-                if (pos < payload_words) mine[s] = payload[pos];
-            }
-            o += __popc(bm);
+    const int gw = lane >> 2, gi = lane & 3;
+    const uint32_t xsel = (uint32_t)(gi | ((1 ^ gi) << 4) | ((2 ^ gi) << 8) | ((3 ^ gi) << 12));
+    const uint64_t cblk = (uint64_t)blockIdx.x * BS_BPC;
+    if (warp == 0) {
+        uint32_t a = 0;
+        if (cblk + lane < nblocks) {
+            const uint4 bm = __ldg(reinterpret_cast<const uint4*>(bitmap) + cblk + lane);
+            a = __popc(bm.x) + __popc(bm.y) + __popc(bm.z) + __popc(bm.w);
         }
-        uint32_t c[8];
+        uint32_t incl = a;
 #pragma unroll
-        for (int w = 0; w < 8; w++) c[w] = 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        s_off[lane] = incl - a;
+    }
+    __syncthreads();
+    const unsigned long long cbase = offs[blockIdx.x];
+    const uint32_t two_r = 2u * radius;
+    bool pad_bad = false, range_bad = false;
 #pragma unroll
-        for (int p = 0; p < 16; p++)
+    for (int q = 0; q < BS_BPW; q++) {
+        const uint64_t blk = cblk + warp * BS_BPW + q;
+        if (blk >= nblocks) break;
+        const uint4 bmv = __ldg(reinterpret_cast<const uint4*>(bitmap) + blk);
+        const uint32_t BM[4] = {bmv.x, bmv.y, bmv.z, bmv.w};
+        const unsigned long long base = cbase + s_off[warp * BS_BPW + q];
+        uint32_t before = 0;
 #pragma unroll
-            for (int w = 0; w < 8; w++) {
-                const int i = p * 8 + w;
-                const uint32_t x = __shfl_sync(0xffffffffu, mine[i >> 5], i & 31);
-                c[w] |= ((x >> lane) & 1u) << p;
+        for (int k = 0; k < 4; k++) before += (k < gi) ? __popc(BM[k]) : 0u;
+        const uint32_t bmi = sel4(BM, gi);
+        uint32_t W[4];
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            W[c] = 0u;
+            const uint32_t bit = 8 * c + gw;
+            if ((bmi >> bit) & 1u) {
+                const unsigned long long pos = base + before + __popc(bmi & ((1u << bit) - 1u));
+                if (pos < payload_words) W[c] = __ldg(payload + pos);
             }
+        }
+        uint32_t E[4];
+        words_to_planes(W, gi, xsel, E);
+        const uint4 rc = planes_to_codes(E);
+        const uint64_t t0 = blk * 256 + 8 * lane;
+        const uint32_t c8[8] = {rc.x & 0xFFFFu, rc.x >> 16, rc.y & 0xFFFFu, rc.y >> 16,
+                                rc.z & 0xFFFFu, rc.z >> 16, rc.w & 0xFFFFu, rc.w >> 16};
+        if (t0 + 8 <= n) {
+            *reinterpret_cast<uint4*>(codes + t0) = rc;
 #pragma unroll
-        for (int w = 0; w < 8; w++) {
-            const uint64_t t = blk * 256 + 32 * w + lane;
-            if (t < n) {
-                codes[t] = (uint16_t)c[w];
-                range_bad |= c[w] >= 2 * radius;
-            } else {
-                pad_bad |= c[w] != 0;
+            for (int j = 0; j < 8; j++) range_bad |= c8[j] >= two_r;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                if (t0 + j < n) {
+                    codes[t0 + j] = (uint16_t)c8[j];
+                    range_bad |= c8[j] >= two_r;
+                } else {
+                    pad_bad |= c8[j] != 0;   // encode.py:386-387
+                }
             }
         }
     }
     if (pad_bad) set_err(status, FZB_ERR_BS_PAD);
-    if (range_bad) set_err(status, FZB_ERR_BS_RANGE);
+    if (range_bad) set_err(status, FZB_ERR_BS_RANGE);   // encode.py:389-390
 }
 
 uint64_t nblk_of(uint64_t n) { return (n + 255) / 256; }
@@ -374,10 +388,12 @@ FZB_API size_t fzb_bitshuffle_workspace_bytes(uint64_t n) {
     return 512 + ((c * 4 + 255) / 256) * 256 + c * 8 + 256;
 }
 
+// Reference: encode.py:324-353.  d_codes needs 16-byte alignment.
 FZB_API int fzb_bitshuffle_encode(const uint16_t* d_codes, uint64_t n, uint8_t* d_bitmap, uint32_t* d_payload,
                                   uint64_t* d_nwords, void* d_ws, size_t ws_bytes, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (ws_bytes < fzb_bitshuffle_workspace_bytes(n)) return FZB_E_WORKSPACE;
+    if (reinterpret_cast<uintptr_t>(d_codes) % 16 || reinterpret_cast<uintptr_t>(d_bitmap) % 16) return FZB_E_ARG;
     const uint64_t nb = nblk_of(n), nc = ncta_of(n);
     if (nb == 0) {
         cudaMemsetAsync(d_nwords, 0, 8, st);
@@ -387,19 +403,21 @@ FZB_API int fzb_bitshuffle_encode(const uint16_t* d_codes, uint64_t n, uint8_t* 
     uint32_t* ticket = reinterpret_cast<uint32_t*>(w);
     unsigned long long* state = reinterpret_cast<unsigned long long*>(w + 256);
     cudaMemsetAsync(w, 0, 256 + nc * 8, st);
-    bs_enc_fused_kernel<<<(unsigned)nc, BS_THREADS, 0, st>>>(d_codes, n, nb, reinterpret_cast<uint32_t*>(d_bitmap),
-                                                            d_payload, state, ticket,
-                                                            reinterpret_cast<unsigned long long*>(d_nwords));
+    bs_enc3_kernel<<<(unsigned)nc, BS_THREADS, 0, st>>>(d_codes, n, nb, reinterpret_cast<uint32_t*>(d_bitmap),
+                                                       d_payload, state, ticket,
+                                                       reinterpret_cast<unsigned long long*>(d_nwords));
     return fzb_check_launch();
 }
 
-// Host side has already checked bitmap length and payload % 4 (encode.py:362-371).
+// Reference: encode.py:356-391.  The host side has already checked bitmap
+// length and payload % 4 (encode.py:362-371).
 FZB_API int fzb_bitshuffle_decode(const uint8_t* d_bitmap, const uint32_t* d_payload, uint64_t payload_words,
                                   uint64_t n, uint32_t radius, uint16_t* d_codes, void* d_ws, size_t ws_bytes,
                                   uint32_t* d_status, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (radius == 0 || radius > 32768) return FZB_E_RADIUS;
     if (ws_bytes < fzb_bitshuffle_workspace_bytes(n)) return FZB_E_WORKSPACE;
+    if (reinterpret_cast<uintptr_t>(d_codes) % 16 || reinterpret_cast<uintptr_t>(d_bitmap) % 16) return FZB_E_ARG;
     const uint64_t nb = nblk_of(n), nc = ncta_of(n);
     if (nb == 0) return 0;
     unsigned char* w = static_cast<unsigned char*>(d_ws);
@@ -408,10 +426,9 @@ FZB_API int fzb_bitshuffle_decode(const uint8_t* d_bitmap, const uint32_t* d_pay
     unsigned long long* offs = reinterpret_cast<unsigned long long*>(w + 256 + ((nc * 4 + 255) / 256) * 256);
     const uint32_t* bm = reinterpret_cast<const uint32_t*>(d_bitmap);
     bs_dec_count_kernel<<<(unsigned)nc, BS_THREADS, 0, st>>>(bm, nb, counts);
-    scan_counts_u64_kernel<<<1, 1024, 0, st>>>(counts, nc, offs, tot);
-    bs_check_total_kernel<<<1, 1, 0, st>>>(tot, payload_words, d_status);
-    bs_dec2_kernel<<<(unsigned)nc, BS_THREADS, 0, st>>>(bm, d_payload, payload_words, n, nb, radius, offs, d_codes,
-                                                        d_status);
+    scan_counts_u64_kernel<<<1, 1024, 0, st>>>(counts, nc, offs, tot, payload_words, d_status);
+    bs_dec3_kernel<<<(unsigned)nc, BS_THREADS, 0, st>>>(bm, d_payload, payload_words, n, nb, radius, offs, d_codes,
+                                                       d_status);
     return fzb_check_launch();
 }
 
