@@ -38,13 +38,13 @@
 namespace v6 {
 
 constexpr int G = 8;        // steps per group (staging / flush / handshake granularity)
-constexpr int KR = 64;      // k-indexed ring slots per row (8 chunks of 8)
-constexpr int IP = 68;      // ring pitch in words: multiple of 4 (16 B cp.async) and
+constexpr int KR = 32;      // k-indexed ring slots per row (4 chunks of 8)
+constexpr int IP = 36;      // ring pitch in words: multiple of 4 (16 B cp.async) and
                             // IP-1 odd, so lane b's row at k = c-b hits bank (3b + c) % 32
-constexpr int SD = 4;       // staging distance: group j+SD is put in flight while group j is published
-                            // (needs KR/8 >= SD + 4 chunks: two in use, SD in flight, one draining)
-constexpr int RAWS = SD + 1;   // decode raw-copy slots
+constexpr int SD = 2;       // staging distance: group j+SD is put in flight when group j completes
+                            // (needs KR/8 >= SD + 1 chunks: its slots must already be flushed)
 constexpr int HR = 32;      // halo ring slots (steps)
+constexpr int GRD = 16;     // ghost ring slots between compute warps (steps)
 constexpr int HUW = 33;     // ghost-row entries per step: corner + 32 lanes
 constexpr uint32_t CODE_TAG = 0x7FC00000u;  // decode ring: NaN-tagged code; finite outliers stay raw f32 bits
 constexpr int OFF = 2;      // element k = s - OFF - r - b at step s: every halo a step needs is from step >= 0
@@ -116,128 +116,103 @@ FZB_DEV void wait_min(const uint32_t* cnt, int n, uint32_t target) {
 FZB_DEV int chunk_of(int j, int d) { return (j * G + G - 1 - OFF - d) >> 3; }
 
 // ------------------------------------------------------------------ helper
-// Staging is asynchronous and one group ahead: stage_issue(j) puts group j's
-// new chunk of every row in flight (encode: 16-byte cp.async straight into
-// the ring; decode: 8-byte code quads + their bitmap word into a raw double
-// buffer), stage_finish(j) runs once those copies landed (decode: NaN-tag the
-// codes, splice in outlier values).  Rows are spread as
-// (row = q*16 + lane/2, half = lane&1); n2 % 4 != 0 uses a scalar path.
-template <int PI>
-struct Raw {
-    static constexpr size_t bytes = (size_t)RAWS * PI * 32 * 2 * 12;   // slots x rows x halves x (8 B codes + 4 B bitmap)
-};
-
-FZB_DEV void cp_async8_z(void* smem, const void* gmem, int nbytes) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
-                 "l"(gmem), "r"(nbytes)
-                 : "memory");
-}
+// Staging runs SD groups ahead.  Encode: 16-byte cp.async straight into the
+// ring (one commit group per iteration).  Decode: the stager loads a group's
+// code quads and bitmap words into registers one iteration before it
+// NaN-tags them (splicing in outlier values) and stores them to the ring.
+// Rows are spread as (row = q*16 + lane/2, half = lane&1).  v7 requires
+// n2 % 4 == 0 (the host routes other shapes to v4), so a half-chunk is
+// either entirely inside the field or entirely outside.
 FZB_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 FZB_DEV void cp_async_wait_n() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int PI, bool DEC>
-FZB_DEV void stage_issue(int j, uint32_t* ring, unsigned char* raw, const float* __restrict__ orig,
-                         const uint16_t* __restrict__ codes, const uint32_t* __restrict__ bitmap, const float* recon,
-                         const Geo6& geo, int i0, int j0, int lane, uint32_t pad_code) {
-    const int n0 = geo.n0, n1 = geo.n1, n2 = geo.n2;
-    if (geo.vec) {
-        uint2* rc = reinterpret_cast<uint2*>(raw) + (size_t)(j % RAWS) * PI * 64;
-        uint32_t* rb = reinterpret_cast<uint32_t*>(raw + (size_t)RAWS * PI * 64 * 8) + (size_t)(j % RAWS) * PI * 64;
-#pragma unroll 8
-        for (int q = 0; q < 2 * PI; q++) {
-            const int row = q * 16 + (lane >> 1), half = lane & 1;
-            const int r = row >> 5, b = row & 31;
-            const int k = chunk_of(j, r + b) * 8 + half * 4;
-            const int i = i0 + r, jj = j0 + b;
-            const bool ok = (i < n0) && (jj < n1) && k >= 0 && k < n2;   // n2 % 4 == 0: a half is all-in or all-out
-            const long long t = ok ? ((long long)i * n1 + jj) * n2 + k : 0;
-            if constexpr (!DEC) {
-                cp_async16_zfill(ring + row * IP + (k & (KR - 1)), orig + t, ok ? 16 : 0);
-            } else {
-                cp_async8_z(rc + row * 2 + half, codes + t, ok ? 8 : 0);
-                cp_async4_z(rb + row * 2 + half, bitmap + (t >> 5), ok ? 4 : 0);
-            }
-        }
-    } else {
-#pragma unroll 4
-        for (int q = 0; q < PI * 8; q++) {
-            const int e = q * 32 + lane;
-            const int row = e >> 3, off = e & 7;
-            const int r = row >> 5, b = row & 31;
-            const int k = chunk_of(j, r + b) * 8 + off;
-            const int i = i0 + r, jj = j0 + b;
-            const bool ok = (i < n0) && (jj < n1) && k >= 0 && k < n2;
-            uint32_t* dst = ring + row * IP + (k & (KR - 1));
-            const long long t = ok ? ((long long)i * n1 + jj) * n2 + k : 0;
-            if constexpr (!DEC) {
-                cp_async4_z(dst, orig + t, ok ? 4 : 0);
-            } else {
-                uint32_t w = pad_code;
-                if (ok) {
-                    w = CODE_TAG | (uint32_t)__ldg(codes + t);
-                    if ((__ldg(bitmap + (t >> 5)) >> (t & 31)) & 1u) w = __float_as_uint(recon[t]);
-                }
-                *dst = w;
-            }
+// Lane b of compute warp w owns rows a = w*R + r (r < R) of column j0+b and
+// stages / flushes only those rows' ring lines, so staging needs no
+// cross-lane or cross-warp handshake: a lane only ever reads its own cells.
+struct OwnRow {
+    long long t;   // flat index of element (i0+a, j0+b, k) for k = 0 (row base)
+    bool ok;       // row inside the field
+};
+
+template <int R>
+FZB_DEV void enc_stage_own(int j, uint32_t* ringl, const float* __restrict__ orig, const OwnRow* rows, int d0,
+                           int n2) {
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        const int k = chunk_of(j, d0 + r) * 8;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int kk = k + 4 * h;
+            const bool ok = rows[r].ok && kk >= 0 && kk < n2;   // n2 % 4 == 0: a quad is all-in or all-out
+            cp_async16_zfill(ringl + r * 32 * IP + (kk & (KR - 1)), orig + (ok ? rows[r].t + kk : 0), ok ? 16 : 0);
         }
     }
 }
 
-template <int PI, bool DEC>
-FZB_DEV void stage_finish(int j, uint32_t* ring, const unsigned char* raw, const float* recon, const Geo6& geo, int i0,
-                          int j0, int lane, uint32_t pad_code) {
-    if constexpr (DEC) {
-        if (geo.vec) {
-            const int n0 = geo.n0, n1 = geo.n1, n2 = geo.n2;
-            const uint2* rc = reinterpret_cast<const uint2*>(raw) + (size_t)(j % RAWS) * PI * 64;
-            const uint32_t* rb = reinterpret_cast<const uint32_t*>(raw + (size_t)RAWS * PI * 64 * 8) + (size_t)(j % RAWS) * PI * 64;
-#pragma unroll 4
-            for (int q = 0; q < 2 * PI; q++) {
-                const int row = q * 16 + (lane >> 1), half = lane & 1;
-                const int r = row >> 5, b = row & 31;
-                const int k = chunk_of(j, r + b) * 8 + half * 4;
-                const int i = i0 + r, jj = j0 + b;
-                const bool ok = (i < n0) && (jj < n1) && k >= 0 && k < n2;
-                uint4 w = make_uint4(pad_code, pad_code, pad_code, pad_code);   // code R: exact zeros before k == 0
-                if (ok) {
-                    const uint2 c = rc[row * 2 + half];
-                    w.x = CODE_TAG | (c.x & 0xFFFFu);
-                    w.y = CODE_TAG | (c.x >> 16);
-                    w.z = CODE_TAG | (c.y & 0xFFFFu);
-                    w.w = CODE_TAG | (c.y >> 16);
-                    const long long t = ((long long)i * n1 + jj) * n2 + k;
-                    const uint32_t bits = (rb[row * 2 + half] >> (t & 31)) & 0xFu;   // t % 4 == 0: one word
-                    if (bits) {  // rare: outlier values verbatim (pre-scattered into recon)
-                        if (bits & 1u) w.x = __float_as_uint(recon[t]);
-                        if (bits & 2u) w.y = __float_as_uint(recon[t + 1]);
-                        if (bits & 4u) w.z = __float_as_uint(recon[t + 2]);
-                        if (bits & 8u) w.w = __float_as_uint(recon[t + 3]);
-                    }
-                }
-                *reinterpret_cast<uint4*>(ring + row * IP + (k & (KR - 1))) = w;
-            }
+template <int R>
+struct DecRegs {
+    uint2 c[2 * R];
+    uint32_t bm[2 * R];
+};
+template <int R>
+FZB_DEV void dec_load_own(int j, DecRegs<R>& D, const uint16_t* __restrict__ codes,
+                          const uint32_t* __restrict__ bitmap, const OwnRow* rows, int d0, int n2) {
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        const int k = chunk_of(j, d0 + r) * 8;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int kk = k + 4 * h;
+            const bool ok = rows[r].ok && kk >= 0 && kk < n2;
+            const long long t = rows[r].t + kk;
+            D.c[2 * r + h] = ok ? __ldg(reinterpret_cast<const uint2*>(codes + t)) : make_uint2(0, 0);
+            D.bm[2 * r + h] = ok ? (__ldg(bitmap + (t >> 5)) >> (t & 31)) & 0xFu : 0u;   // t % 4 == 0: one word
         }
     }
-    __threadfence_block();
+}
+template <int R>
+FZB_DEV void dec_write_own(int j, const DecRegs<R>& D, uint32_t* ringl, const float* recon, const OwnRow* rows,
+                           int d0, int n2, uint32_t pad_code) {
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        const int k = chunk_of(j, d0 + r) * 8;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int kk = k + 4 * h;
+            const bool ok = rows[r].ok && kk >= 0 && kk < n2;
+            const long long t = rows[r].t + kk;
+            const uint2 c = D.c[2 * r + h];
+            uint4 w = make_uint4(pad_code, pad_code, pad_code, pad_code);   // code R: exact zeros before k == 0
+            if (ok) {
+                w = make_uint4(CODE_TAG | (c.x & 0xFFFFu), CODE_TAG | (c.x >> 16), CODE_TAG | (c.y & 0xFFFFu),
+                               CODE_TAG | (c.y >> 16));
+                const uint32_t bits = D.bm[2 * r + h];
+                if (bits) {  // rare: outlier values verbatim (pre-scattered into recon)
+                    if (bits & 1u) w.x = __float_as_uint(recon[t]);
+                    if (bits & 2u) w.y = __float_as_uint(recon[t + 1]);
+                    if (bits & 4u) w.z = __float_as_uint(recon[t + 2]);
+                    if (bits & 8u) w.w = __float_as_uint(recon[t + 3]);
+                }
+            }
+            *reinterpret_cast<uint4*>(ringl + r * 32 * IP + (kk & (KR - 1))) = w;
+        }
+    }
 }
 
-template <int PI, bool DEC>
-FZB_DEV void helper_flush(int m_of_j, uint32_t* ring, uint16_t* __restrict__ codes_out, uint32_t* __restrict__ bitmap,
-                          float* recon, const Geo6& geo, int i0, int j0, int lane) {
-    // flush chunk (chunk_of(m_of_j, d) - 1) of every row: complete once group m_of_j is done
-    const int n0 = geo.n0, n1 = geo.n1, n2 = geo.n2;
-    if (geo.vec) {
-#pragma unroll 4
-        for (int q = 0; q < 2 * PI; q++) {
-            const int row = q * 16 + (lane >> 1), half = lane & 1;
-            const int r = row >> 5, b = row & 31;
-            const int m = chunk_of(m_of_j, r + b) - 1;
-            const int k = m * 8 + half * 4;
-            const int i = i0 + r, jj = j0 + b;
-            if ((i < n0) && (jj < n1) && k >= 0 && k < n2) {
-                const long long t = ((long long)i * n1 + jj) * n2 + k;
-                const uint4 w = *reinterpret_cast<const uint4*>(ring + row * IP + (k & (KR - 1)));
+// Flush chunk (chunk_of(j, d) - 1) of the lane's rows: complete once group j is done.
+template <int R, bool DEC>
+FZB_DEV void flush_own(int j, const uint32_t* ringl, uint16_t* __restrict__ codes_out, uint32_t* __restrict__ bitmap,
+                       float* recon, const OwnRow* rows, int d0, int n2) {
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        const int k = (chunk_of(j, d0 + r) - 1) * 8;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int kk = k + 4 * h;
+            if (rows[r].ok && kk >= 0 && kk < n2) {
+                const long long t = rows[r].t + kk;
+                const uint4 w = *reinterpret_cast<const uint4*>(ringl + r * 32 * IP + (kk & (KR - 1)));
                 if constexpr (DEC) {
                     *reinterpret_cast<uint4*>(recon + t) = w;
                 } else {
@@ -246,27 +221,9 @@ FZB_DEV void helper_flush(int m_of_j, uint32_t* ring, uint16_t* __restrict__ cod
                     c.y = (w.z & 0xFFFFu) | (w.w << 16);
                     *reinterpret_cast<uint2*>(codes_out + t) = c;
                     // bit 16 = outlier; t % 4 == 0, so the 4 flags share one bitmap word
-                    const uint32_t ob = ((w.x >> 16) & 1u) | ((w.y >> 15) & 2u) | ((w.z >> 14) & 4u) | ((w.w >> 13) & 8u);
+                    const uint32_t ob =
+                        ((w.x >> 16) & 1u) | ((w.y >> 15) & 2u) | ((w.z >> 14) & 4u) | ((w.w >> 13) & 8u);
                     if (ob) atomicOr(bitmap + (t >> 5), ob << (t & 31));
-                }
-            }
-        }
-    } else {
-#pragma unroll 4
-        for (int q = 0; q < PI * 8; q++) {
-            const int e = q * 32 + lane;
-            const int row = e >> 3, off = e & 7;
-            const int r = row >> 5, b = row & 31;
-            const int k = (chunk_of(m_of_j, r + b) - 1) * 8 + off;
-            const int i = i0 + r, jj = j0 + b;
-            if ((i < n0) && (jj < n1) && k >= 0 && k < n2) {
-                const long long t = ((long long)i * n1 + jj) * n2 + k;
-                const uint32_t w = ring[row * IP + (k & (KR - 1))];
-                if constexpr (DEC) {
-                    recon[t] = __uint_as_float(w);
-                } else {
-                    codes_out[t] = (uint16_t)w;
-                    if (w & 0x10000u) atomicOr(bitmap + (t >> 5), 1u << (t & 31));
                 }
             }
         }
@@ -367,15 +324,22 @@ __device__ __noinline__ uint32_t quantize_word_slow(float vf, double pred, QPara
     return (uint32_t)code | (outl ? 0x10000u : 0u);
 }   // 1.5 * 2^52: x + M - M == rint(x) for |x| < 2^51
 
+// The next step's inputs (ghost-row value + lane -1 halos) carry LL tags.
+// Halo rings are released per group (hready); the ghost row of warps w > 0
+// arrives every step from warp w-1 and is LL-checked.
+FZB_DEV bool ghost_ready(bool polled, uint64_t gh, uint32_t want) { return !polled || (uint32_t)(gh >> 32) == want; }
+FZB_DEV void wait_ghost(bool polled, uint64_t& gh, uint32_t want, const uint64_t* gsrc) {
+    while (!__all_sync(FULL, ghost_ready(polled, gh, want))) gh = ld_ll_cta(gsrc);
+}
+
 template <int W, int R, bool DEC>
 struct Smem7 {
     static constexpr int PI = W * R;
     static constexpr size_t ring = (size_t)PI * 32 * IP * 4;
     static constexpr size_t hu = (size_t)HR * 32 * 8;
     static constexpr size_t hl = (size_t)HR * (PI + 1) * 8;
-    static constexpr size_t gr = (size_t)W * HR * 32 * 8;   // W-1 ghost rings + warp W-1's scratch
-    static constexpr size_t raw = DEC ? Raw<PI>::bytes : 0;
-    static constexpr size_t bytes = ring + hu + hl + gr + raw + 128;
+    static constexpr size_t gr = (size_t)W * GRD * 32 * 8;   // W-1 ghost rings + warp W-1's scratch
+    static constexpr size_t bytes = ring + hu + hl + gr + 128;
 };
 
 // ------------------------------------------------------------------ kernel
@@ -383,21 +347,20 @@ struct Smem7 {
 // Warp w's ghost row (a = w*R - 1) arrives as LL pairs every step: from the
 // helper (w = 0, row i0-1 of the tile above) or from warp w-1 (GR ring).
 template <int W, int R, bool DEC>
-__global__ void __launch_bounds__((W + 2) * 32, 1)
+__global__ void __launch_bounds__((W + 1) * 32, (W <= 4 ? 3 : 1))
 lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in, uint16_t* __restrict__ codes_out,
            uint32_t* __restrict__ bitmap, float* recon, uint64_t* __restrict__ faceI, uint64_t* __restrict__ faceJ,
            const uint32_t* __restrict__ hdr, uint32_t* __restrict__ ticket, const int* __restrict__ order, Geo6 geo,
            const double* __restrict__ d_eb, int radius) {
     using SM = Smem7<W, R, DEC>;
     constexpr int PI = W * R;
-    constexpr int NT = (W + 2) * 32;
+    constexpr int NT = (W + 1) * 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t* ring = reinterpret_cast<uint32_t*>(smem_raw);
     uint64_t* HU = reinterpret_cast<uint64_t*>(smem_raw + SM::ring);
     uint64_t* HL = HU + HR * 32;
     uint64_t* GR = HL + HR * (PI + 1);
-    unsigned char* raw = smem_raw + SM::ring + SM::hu + SM::hl + SM::gr;
-    uint32_t* flags = reinterpret_cast<uint32_t*>(raw + SM::raw);   // [0] tile, [1] staged groups
+    uint32_t* flags = reinterpret_cast<uint32_t*>(smem_raw + SM::ring + SM::hu + SM::hl + SM::gr);   // [0] tile, [1] staged
     uint32_t* done = flags + 2;                                      // [w] groups finished by warp w
     uint32_t* hready = done + W;                                     // halo groups published
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -410,7 +373,7 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
         for (int q = tid; q < nh; q += NT) HU[q] = 0;
     }
     if (tid == 0) flags[0] = (uint32_t)order[atomicAdd(ticket, 1u)];
-    if (tid < W + 3) flags[1 + tid] = 0;
+    if (tid < W + 2) flags[1 + tid] = 0;
     __syncthreads();
     const int tile = (int)flags[0];
     const int nB = geo.nB, S = geo.S;
@@ -420,42 +383,9 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
     const uint32_t epoch = hdr[0];
 
     if (warp == W) {
-        // ================= stager: inputs SD groups ahead, outputs =================
-        // iteration jg: group jg's copies (issued SD iterations earlier) land ->
-        // publish.  Group jg+SD's chunk m(jg+SD) reuses the slots of
-        // m(jg+SD-8), last read by group jg+SD-7: once every warp finished
-        // that group, flush it and put group jg+SD in flight.  One commit per
-        // iteration (empty ones included) keeps wait_group's count fixed.
-        const uint32_t pad = CODE_TAG | (uint32_t)radius;
-        for (int d = 0; d < SD; d++) {
-            if (d < NGRP) stage_issue<PI, DEC>(d, ring, raw, orig, codes_in, bitmap, recon, geo, i0, j0, lane, pad);
-            cp_async_commit();
-        }
+        // ================= halo warp: polls the faces a group at a time, up to 3 groups ahead =================
+        // Group jg's ring slots (steps 8jg-32..) are free once every warp finished group jg-3.
         for (int jg = 0; jg < NGRP; jg++) {
-            cp_async_wait_n<SD - 1>();
-            stage_finish<PI, DEC>(jg, ring, raw, recon, geo, i0, j0, lane, pad);
-            __syncwarp();
-            if (lane == 0) st_rel_cta(flags + 1, (uint32_t)(jg + 1));
-            const int jf = jg + SD - 7;
-            if (jf >= 0) {
-                wait_min(done, W, (uint32_t)(jf + 1));
-                helper_flush<PI, DEC>(jf, ring, codes_out, bitmap, recon, geo, i0, j0, lane);
-            }
-            if (jg + SD < NGRP)
-                stage_issue<PI, DEC>(jg + SD, ring, raw, orig, codes_in, bitmap, recon, geo, i0, j0, lane, pad);
-            cp_async_commit();
-        }
-        for (int jf = (NGRP + SD - 7 > 0 ? NGRP + SD - 7 : 0); jf < NGRP; jf++) {
-            wait_min(done, W, (uint32_t)(jf + 1));
-            helper_flush<PI, DEC>(jf, ring, codes_out, bitmap, recon, geo, i0, j0, lane);
-        }
-        helper_flush<PI, DEC>(NGRP, ring, codes_out, bitmap, recon, geo, i0, j0, lane);
-        return;
-    }
-    if (warp == W + 1) {
-        // ================= halo warp: polls faces up to 3 groups ahead =================
-        for (int jg = 0; jg < NGRP; jg++) {
-            // ring slots of steps 8jg-32.. are free once every warp finished group jg-3
             if (jg >= 3) wait_min(done, W, (uint32_t)(jg - 2));
             helper_halo<PI>(jg, HU, HL, faceI, faceJ, tile, A, B, nB, S, epoch, lane);
             __syncwarp();
@@ -469,7 +399,7 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
     // warps w > 0 (written by warp w-1 every step) is loaded at the start of
     // the step that precedes its use and its LL tag is checked at the end,
     // together with the rare near-tie flag of the reciprocal quantizer; halo
-    // rings (helper-written) are guaranteed per group by `hready`.  Outlier
+    // rings (helper-written) are released per group by `hready`.  Outlier
     // flags ride in bit 16 of the ring word (the stager sets the bitmap).
     const int w = warp, b = lane;
     const QParams P = make_qparams(*d_eb, radius);
@@ -483,9 +413,10 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
         F1[x] = 0.f;
     }
     const bool polled = (w > 0);
-    const uint64_t* ghost_src = polled ? GR + (size_t)(w - 1) * HR * 32 + b : HU + b;   // + slot*32
+    const uint64_t* ghost_src = polled ? GR + (size_t)(w - 1) * GRD * 32 + b : HU + b;   // + slot*32
     // warp W-1 has no consumer in the CTA: its ghost stores go to a scratch ring
-    uint64_t* ghost_dst = GR + (size_t)(w < W - 1 ? w : W - 1) * HR * 32 + b;
+    uint64_t* ghost_dst = GR + (size_t)(w < W - 1 ? w : W - 1) * GRD * 32 + b;
+    const int gmask = polled ? GRD - 1 : HR - 1;   // ghost source ring depth
     const bool pubI = (w == W - 1) && (A < geo.nA - 1);
     uint64_t* fI = faceI + (size_t)tile * S * 32 + b;
     const bool pubJ = (B < nB - 1) && (b == 31);
@@ -499,21 +430,44 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
 #pragma unroll
     for (int x = 0; x <= R; x++) hf[x] = 0.f;
 
+    // ---- own-row staging: SD groups in flight (encode: cp.async groups;
+    //      decode: one group of loads in registers, stored a group early)
+    OwnRow rows[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        const int i = i0 + w * R + r, jj = j0 + b;
+        rows[r].ok = (i < geo.n0) && (jj < geo.n1);
+        rows[r].t = rows[r].ok ? ((long long)i * geo.n1 + jj) * geo.n2 : 0;
+    }
+    const int d0 = w * R + b;
+    const uint32_t pad = CODE_TAG | (uint32_t)radius;
+    DecRegs<R> D;
+    if constexpr (!DEC) {
+        for (int q = 0; q < SD; q++) {
+            if (q < NGRP) enc_stage_own<R>(q, ringl, orig, rows, d0, geo.n2);
+            cp_async_commit();
+        }
+    } else {
+        dec_load_own<R>(0, D, codes_in, bitmap, rows, d0, geo.n2);
+        dec_write_own<R>(0, D, ringl, recon, rows, d0, geo.n2, pad);
+        if (NGRP > 1) dec_load_own<R>(1, D, codes_in, bitmap, rows, d0, geo.n2);
+    }
+
     for (int g = 0; g < NGRP; g++) {
-        if (ld_acq_cta(flags + 1) < (uint32_t)(g + 1))
-            while (ld_acq_cta(flags + 1) < (uint32_t)(g + 1)) __nanosleep(64);
+        if constexpr (!DEC) cp_async_wait_n<SD - 1>();   // this lane's copies of group g landed
         if (ld_acq_cta(hready) < (uint32_t)(g + 1))
             while (ld_acq_cta(hready) < (uint32_t)(g + 1)) __nanosleep(32);
-        // stay within 3 groups of warp w+1: the ghost ring holds HR = 32 steps
-        if (w + 1 < W && ld_acq_cta(done + w + 1) + 2 < (uint32_t)g)
-            while (ld_acq_cta(done + w + 1) + 2 < (uint32_t)g) __nanosleep(32);
+        // stay within 15 steps of warp w+1 (the ghost ring holds GRD = 16)
+        if (w + 1 < W && ld_acq_cta(done + w + 1) + 1 < (uint32_t)g)
+            while (ld_acq_cta(done + w + 1) + 1 < (uint32_t)g) __nanosleep(32);
 #pragma unroll kStepUnroll
         for (int st = 0; st < G; st++) {
             const int s = g * G + st;
             const int cs = s & (HR - 1);
             LZ_STAMP(0);
             // ---- next step's inputs: ghost (tag checked at the end) and halos
-            uint64_t ghn = ld_ll_cta(ghost_src + cs * 32);
+            const uint32_t want = (uint32_t)(s + 1);
+            uint64_t ghn = ld_ll_cta(ghost_src + (s & gmask) * 32);
             float hfn[R + 1];
 #pragma unroll
             for (int x = 0; x <= R; x++) hfn[x] = __uint_as_float((uint32_t)ld_ll_cta(hlw + cs * (PI + 1) + x));
@@ -565,7 +519,7 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
                 }
                 if (!P.use_recip) slow = ~1u;
                 // ---- the step's one branch: ghost not yet published, or a near-tie
-                if (!__all_sync(FULL, (slow == 0) & (!polled || (uint32_t)(ghn >> 32) == (uint32_t)(s + 1)))) {
+                if (!__all_sync(FULL, (slow == 0) & ghost_ready(polled, ghn, want))) {
 #pragma unroll
                     for (int x = 1; x <= R; x++) {
                         if ((slow >> x) & 1u) {
@@ -576,9 +530,7 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
                             Cn[x] = (double)rec;
                         }
                     }
-                    if (polled)
-                        while (!__all_sync(FULL, (uint32_t)(ghn >> 32) == (uint32_t)(s + 1)))
-                            ghn = ld_ll_cta(ghost_src + cs * 32);
+                    wait_ghost(polled, ghn, want, ghost_src + (s & gmask) * 32);
                 }
 #pragma unroll
                 for (int x = 1; x <= R; x++) *cell[x] = word[x];
@@ -596,13 +548,11 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
                     Fn[x] = is_code ? rc : ov;
                     Cn[x] = (double)Fn[x];
                 }
-                if (polled && !__all_sync(FULL, (uint32_t)(ghn >> 32) == (uint32_t)(s + 1)))
-                    while (!__all_sync(FULL, (uint32_t)(ghn >> 32) == (uint32_t)(s + 1)))
-                        ghn = ld_ll_cta(ghost_src + cs * 32);
+                if (!__all_sync(FULL, ghost_ready(polled, ghn, want))) wait_ghost(polled, ghn, want, ghost_src + (s & gmask) * 32);
             }
             LZ_STAMP(3);
             // ---- publish (predicated, no branches): ghost for warp w+1, faces
-            st_ll_cta(ghost_dst + cs * 32, ll_pack(Fn[R], (uint32_t)(s + 1)));
+            st_ll_cta(ghost_dst + (s & (GRD - 1)) * 32, ll_pack(Fn[R], (uint32_t)(s + 1)));
             st_ll_gpu_if(pubI, fI + (size_t)s * 32, ll_pack(Fn[R], epoch));
 #pragma unroll
             for (int x = 1; x <= R; x++) st_ll_gpu_if(pubJ, fJ + (size_t)s * PI + (x - 1), ll_pack(Fn[x], epoch));
@@ -621,9 +571,20 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
             }
             gh = ghn;
         }
+        // ---- own rows: flush what group g completed, stage group g+SD (decode: g+1 / load g+2)
+        flush_own<R, DEC>(g, ringl, codes_out, bitmap, recon, rows, d0, geo.n2);
+        if constexpr (!DEC) {
+            if (g + SD < NGRP) enc_stage_own<R>(g + SD, ringl, orig, rows, d0, geo.n2);
+            cp_async_commit();
+        } else {
+            if (g + 1 < NGRP) dec_write_own<R>(g + 1, D, ringl, recon, rows, d0, geo.n2, pad);
+            if (g + 2 < NGRP) dec_load_own<R>(g + 2, D, codes_in, bitmap, rows, d0, geo.n2);
+        }
         __syncwarp();
         if (b == 0) st_rel_cta(done + w, (uint32_t)(g + 1));
     }
+    // the last chunk of every row completes with the last group
+    flush_own<R, DEC>(NGRP, ringl, codes_out, bitmap, recon, rows, d0, geo.n2);
 }
 
 __global__ void lz7_prep_kernel(uint32_t* hdr) {
@@ -672,7 +633,7 @@ int launch7(const float* orig, const uint16_t* codes_in, uint16_t* codes_out, ui
     const size_t smem = Smem7<W, R, DEC>::bytes;
     auto kfn = lz7_kernel<W, R, DEC>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kfn<<<(unsigned)L.ntile, (W + 2) * 32, smem, st>>>(orig, codes_in, codes_out, bitmap, recon, faceI, faceJ, hdr,
+    kfn<<<(unsigned)L.ntile, (W + 1) * 32, smem, st>>>(orig, codes_in, codes_out, bitmap, recon, faceI, faceJ, hdr,
                                                       hdr + 1, order, g, d_eb, radius);
     return fzb_check_launch();
 }
