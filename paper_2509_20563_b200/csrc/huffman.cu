@@ -22,6 +22,7 @@
 //    truncation / invalid-code / trailing / padding checks reproduce
 //    encode.py:299-316 exactly.
 #include "common.cuh"
+#include "scan.cuh"
 
 #include <cooperative_groups.h>
 namespace cg = cooperative_groups;
@@ -446,48 +447,6 @@ FZB_DEV int decode_one(BitReader& r, unsigned long long total_bits, const DecTab
     return l;
 }
 
-// one sync iteration: start[t] (from end of t-1 of the previous iteration)
-__global__ void __launch_bounds__(HD_THREADS) hf_sync_kernel(const uint32_t* __restrict__ stream, unsigned long long total_bits,
-                                                             uint64_t nsub, const DecTables* __restrict__ Tg,
-                                                             const uint32_t* __restrict__ lut_g,
-                                                             const uint16_t* __restrict__ sym_sorted,
-                                                             const unsigned long long* __restrict__ prev_start,
-                                                             const unsigned long long* __restrict__ prev_end,
-                                                             const uint32_t* __restrict__ prev_cnt,
-                                                             const uint32_t* __restrict__ prev_err,
-                                                             unsigned long long* __restrict__ start,
-                                                             unsigned long long* __restrict__ end,
-                                                             uint32_t* __restrict__ cnt, uint32_t* __restrict__ err,
-                                                             uint32_t* __restrict__ changed, int first_iter) {
-    __shared__ uint32_t lut[1 << LUT_BITS];
-    __shared__ DecTables T;
-    for (int q = threadIdx.x; q < (1 << LUT_BITS); q += blockDim.x) lut[q] = lut_g[q];
-    if (threadIdx.x == 0) T = *Tg;
-    __syncthreads();
-    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= nsub) return;
-    unsigned long long s;
-    if (first_iter) s = t * SUB;
-    else s = (t == 0) ? 0ull : prev_end[t - 1];
-    if (!first_iter && s == prev_start[t]) {
-        start[t] = s; end[t] = prev_end[t]; cnt[t] = prev_cnt[t]; err[t] = prev_err[t];
-        return;
-    }
-    if (!first_iter) *changed = 1;
-    const unsigned long long lim = (t + 1) * (unsigned long long)SUB;
-    BitReader r;
-    r.init(stream, s);
-    uint32_t c = 0, e = 0;
-    while (r.pos < lim && r.pos < total_bits) {
-        uint32_t sym;
-        const int l = decode_one(r, total_bits, T, lut, sym_sorted, sym);
-        if (l < 0) { e = (uint32_t)(-l); break; }
-        r.skip(l);
-        c++;
-    }
-    start[t] = s; end[t] = e ? lim : r.pos; cnt[t] = c; err[t] = e;
-}
-
 // Persistent, cooperative fixed-point iteration of the subsequence starts:
 // sweep 0 starts every subsequence at its nominal bit offset (speculative);
 // later sweeps restart subsequence t at end[t-1] whenever that differs from
@@ -544,76 +503,80 @@ __global__ void __launch_bounds__(HD_THREADS) hf_sync_coop_kernel(const uint32_t
     if (gt == 0 && it >= max_iter) set_err(status, FZB_ERR_HF_SYNC);
 }
 
-__global__ void scan_cnt_kernel(const uint32_t* __restrict__ cnt, uint64_t m, unsigned long long* __restrict__ offs,
-                                unsigned long long* __restrict__ tot) {
-    __shared__ unsigned long long tmp[33];
-    unsigned long long carry = 0;
-    for (uint64_t b0 = 0; b0 < m; b0 += blockDim.x) {
-        const uint64_t q = b0 + threadIdx.x;
-        const unsigned long long v = q < m ? cnt[q] : 0ull;
-        unsigned long long t;
-        const unsigned long long p = block_exclusive_scan64(v, tmp, &t);
-        if (q < m) offs[q] = carry + p;
-        carry += t;
-    }
-    if (threadIdx.x == 0) *tot = carry;
-}
+// Decode + write, coalesced: every thread decodes its subsequence (from the
+// synchronised start) in rounds of HD_ROUND symbols into shared memory;
+// between rounds each warp copies its 32 threads' chunks to their global
+// offsets (consecutive symbols of one chunk go to consecutive lanes).  The
+// first true-path error with ordinal < n (encode.py:299-310) is folded in
+// with an atomicMin on (subsequence << 2 | kind).
+constexpr int HD_ROUND = 64;
 
-__global__ void __launch_bounds__(HD_THREADS) hf_write_dec_kernel(const uint32_t* __restrict__ stream,
-                                                                  unsigned long long total_bits, uint64_t nsub,
-                                                                  const DecTables* __restrict__ Tg,
-                                                                  const uint32_t* __restrict__ lut_g,
-                                                                  const uint16_t* __restrict__ sym_sorted,
-                                                                  const unsigned long long* __restrict__ start,
-                                                                  const unsigned long long* __restrict__ end,
-                                                                  const unsigned long long* __restrict__ offs,
-                                                                  uint64_t n, uint16_t* __restrict__ out,
-                                                                  unsigned long long* __restrict__ end_pos) {
+__global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_t* __restrict__ stream,
+                                                                   unsigned long long total_bits, uint64_t nsub,
+                                                                   const DecTables* __restrict__ Tg,
+                                                                   const uint32_t* __restrict__ lut_g,
+                                                                   const uint16_t* __restrict__ sym_sorted,
+                                                                   const unsigned long long* __restrict__ start,
+                                                                   const unsigned long long* __restrict__ end,
+                                                                   const uint32_t* __restrict__ cnt,
+                                                                   const uint32_t* __restrict__ err,
+                                                                   const unsigned long long* __restrict__ offs,
+                                                                   uint64_t n, uint16_t* __restrict__ out,
+                                                                   unsigned long long* __restrict__ end_pos,
+                                                                   unsigned long long* __restrict__ best) {
     __shared__ uint32_t lut[1 << LUT_BITS];
     __shared__ DecTables T;
+    __shared__ uint16_t buf[HD_THREADS][HD_ROUND + 2];
     for (int q = threadIdx.x; q < (1 << LUT_BITS); q += blockDim.x) lut[q] = lut_g[q];
     if (threadIdx.x == 0) T = *Tg;
     __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= nsub) return;
-    unsigned long long o = offs[t];
-    if (o >= n) return;
+    unsigned long long o = n, e = 0;
     BitReader r;
-    r.init(stream, start[t]);
-    const unsigned long long e = end[t];
-    while (r.pos < e && o < n) {
-        uint32_t sym;
-        const int l = decode_one(r, total_bits, T, lut, sym_sorted, sym);
-        if (l < 0) break;
-        r.skip(l);
-        out[o] = (uint16_t)sym;
-        o++;
-        if (o == n) *end_pos = r.pos;
+    if (t < nsub) {
+        o = offs[t];
+        e = end[t];
+        const uint32_t er = err[t];
+        if (er && o + cnt[t] < n) atomicMin(best, (t << 2) | er);
+        r.init(stream, start[t]);
+    }
+    while (true) {
+        int k = 0;
+        if (o < n) {
+            while (k < HD_ROUND && r.pos < e && o + (unsigned long long)k < n) {
+                uint32_t sym;
+                const int l = decode_one(r, total_bits, T, lut, sym_sorted, sym);
+                if (l < 0) { e = 0; break; }
+                r.skip(l);
+                buf[threadIdx.x][k++] = (uint16_t)sym;
+                if (o + (unsigned long long)k == n) *end_pos = r.pos;
+            }
+        }
+        const bool more = (k == HD_ROUND) && r.pos < e && o + (unsigned long long)k < n;
+        __syncthreads();
+        // copy-out: warp w owns the chunks of threads 32w..32w+31
+        for (int c = 0; c < 32; c++) {
+            const int kc = __shfl_sync(0xffffffffu, k, c);
+            const unsigned long long oc = __shfl_sync(0xffffffffu, o, c);
+            for (int j = lane; j < kc; j += 32) out[oc + j] = buf[warp * 32 + c][j];
+        }
+        o += k;
+        if (!__syncthreads_or(more)) break;
     }
 }
 
-// Find the first true-path error with ordinal < n, or the end position;
-// apply encode.py:299-316.
-__global__ void hf_final_kernel(uint64_t nsub, const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ err,
-                                const unsigned long long* __restrict__ offs, uint64_t n, uint64_t nbytes,
-                                const uint8_t* __restrict__ bytes, const unsigned long long* __restrict__ end_pos,
-                                uint32_t* __restrict__ status) {
-    __shared__ unsigned long long best;
-    if (threadIdx.x == 0) best = ~0ull;
-    __syncthreads();
-    for (uint64_t t = threadIdx.x; t < nsub; t += blockDim.x)
-        if (err[t]) {
-            const unsigned long long ord = offs[t] + cnt[t];
-            if (ord < n) atomicMin(&best, (t << 2) | err[t]);
-        }
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-    if (best != ~0ull) {
-        set_err(status, (best & 3) == 1 ? FZB_ERR_HF_TRUNCATED : FZB_ERR_HF_CORRUPT);
+// Remaining stream checks of encode.py:299-316 (one thread).
+__global__ void hf_final2_kernel(uint64_t n, uint64_t nbytes, const uint8_t* __restrict__ bytes,
+                                 const unsigned long long* __restrict__ tot,
+                                 const unsigned long long* __restrict__ end_pos,
+                                 const unsigned long long* __restrict__ best, uint32_t* __restrict__ status) {
+    const unsigned long long b = *best;
+    if (b != ~0ull) {
+        set_err(status, (b & 3) == 1 ? FZB_ERR_HF_TRUNCATED : FZB_ERR_HF_CORRUPT);
         return;
     }
-    unsigned long long total = nsub ? offs[nsub - 1] + cnt[nsub - 1] : 0;
-    if (total < n) {  // stream ended on a boundary before n symbols
+    if (*tot < n) {  // stream ended on a boundary before n symbols
         set_err(status, FZB_ERR_HF_TRUNCATED);
         return;
     }
@@ -626,10 +589,6 @@ __global__ void hf_final_kernel(uint64_t nsub, const uint32_t* __restrict__ cnt,
         const uint32_t tail = bytes[nbytes - 1] & ((1u << (8 - (e & 7))) - 1u);
         if (tail) set_err(status, FZB_ERR_HF_PAD);
     }
-}
-
-__global__ void hf_sync_check_kernel(const uint32_t* __restrict__ changed, uint32_t* __restrict__ status) {
-    if (*changed) set_err(status, FZB_ERR_HF_SYNC);
 }
 
 size_t align256(size_t x) { return (x + 255) / 256 * 256; }
@@ -702,7 +661,8 @@ FZB_API size_t fzb_huffman_decode_workspace_bytes(uint64_t nbytes, uint32_t nsym
     const uint64_t nsub = (nbytes * 8 + SUB - 1) / SUB + 1;
     // tables + sym_sorted + lut + 2x(start,end,cnt,err) + offs + scalars
     return align256(sizeof(DecTables)) + align256((size_t)nsym * 2) + align256((1u << LUT_BITS) * 4) +
-           2 * (2 * align256(nsub * 8) + 2 * align256(nsub * 4)) + align256(nsub * 8) + 1024;
+           2 * (2 * align256(nsub * 8) + 2 * align256(nsub * 4)) + align256(nsub * 8) +
+           align256(fzscan::ws_bytes(nsub)) + 1024;
 }
 
 // d_stream must be readable (zero) for 8 bytes past nbytes.
@@ -727,8 +687,10 @@ FZB_API int fzb_huffman_decode(const uint8_t* d_stream, uint64_t nbytes, uint64_
         er_[b] = reinterpret_cast<uint32_t*>(p); p += align256(nsub * 4);
     }
     unsigned long long* offs = reinterpret_cast<unsigned long long*>(p); p += align256(nsub * 8);
-    unsigned long long* scal = reinterpret_cast<unsigned long long*>(p);  // [0]=total [1]=end_pos [2]=changed
+    void* scan_ws = p; p += align256(fzscan::ws_bytes(nsub));
+    unsigned long long* scal = reinterpret_cast<unsigned long long*>(p);  // [0]=total [1]=end_pos [2..3]=changed[3] (u32) [4]=best
     cudaMemsetAsync(scal, 0, 64, st);
+    cudaMemsetAsync(scal + 4, 0xFF, 8, st);
     hf_tables_kernel<<<1, 256, 0, st>>>(d_lengths, nsym, T, sym_sorted, lut);
     const uint32_t* words = reinterpret_cast<const uint32_t*>(d_stream);
     const unsigned blocks = (unsigned)((nsub + HD_THREADS - 1) / HD_THREADS);
@@ -754,10 +716,11 @@ FZB_API int fzb_huffman_decode(const uint8_t* d_stream, uint64_t nbytes, uint64_
                      (void*)&max_iter};
     cudaLaunchCooperativeKernel((const void*)hf_sync_coop_kernel, dim3(gridc), dim3(HD_THREADS), kargs, 0, st);
     const int fin = 0;
-    scan_cnt_kernel<<<1, 1024, 0, st>>>(cn_[fin], nsub, offs, scal);
-    hf_write_dec_kernel<<<blocks, HD_THREADS, 0, st>>>(words, total_bits, nsub, T, lut, sym_sorted, st_[fin], en_[fin],
-                                                       offs, n, d_codes, scal + 1);
-    hf_final_kernel<<<1, 1024, 0, st>>>(nsub, cn_[fin], er_[fin], offs, n, nbytes, d_stream, scal + 1, d_status);
+    fzscan::exclusive(cn_[fin], nsub, offs, scal, scan_ws, st);
+    hf_write_dec2_kernel<<<blocks, HD_THREADS, 0, st>>>(words, total_bits, nsub, T, lut, sym_sorted, st_[fin],
+                                                        en_[fin], cn_[fin], er_[fin], offs, n, d_codes, scal + 1,
+                                                        scal + 4);
+    hf_final2_kernel<<<1, 1, 0, st>>>(n, nbytes, d_stream, scal, scal + 1, scal + 4, d_status);
     return fzb_check_launch();
 }
 

@@ -8,7 +8,7 @@ namespace fzscan {
 
 constexpr int CH = 1024;
 
-__global__ void chunk_sum_kernel(const uint32_t* __restrict__ in, uint64_t m, unsigned long long* __restrict__ part) {
+static __global__ void chunk_sum_kernel(const uint32_t* __restrict__ in, uint64_t m, unsigned long long* __restrict__ part) {
     __shared__ unsigned long long tmp[33];
     const uint64_t q = (uint64_t)blockIdx.x * CH + threadIdx.x;
     const unsigned long long x = q < m ? in[q] : 0ull;
@@ -17,7 +17,7 @@ __global__ void chunk_sum_kernel(const uint32_t* __restrict__ in, uint64_t m, un
     if (threadIdx.x == 0) part[blockIdx.x] = t;
 }
 
-__global__ void part_scan_kernel(unsigned long long* __restrict__ part, uint64_t np, unsigned long long* __restrict__ tot) {
+static __global__ void part_scan_kernel(unsigned long long* __restrict__ part, uint64_t np, unsigned long long* __restrict__ tot) {
     __shared__ unsigned long long tmp[33];
     unsigned long long carry = 0;
     for (uint64_t b0 = 0; b0 < np; b0 += blockDim.x) {
@@ -31,7 +31,7 @@ __global__ void part_scan_kernel(unsigned long long* __restrict__ part, uint64_t
     if (threadIdx.x == 0 && tot) *tot = carry;
 }
 
-__global__ void chunk_apply_kernel(const uint32_t* __restrict__ in, uint64_t m, const unsigned long long* __restrict__ part,
+static __global__ void chunk_apply_kernel(const uint32_t* __restrict__ in, uint64_t m, const unsigned long long* __restrict__ part,
                                    unsigned long long* __restrict__ out) {
     __shared__ unsigned long long tmp[33];
     const uint64_t q = (uint64_t)blockIdx.x * CH + threadIdx.x;
