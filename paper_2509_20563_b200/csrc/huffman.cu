@@ -331,7 +331,7 @@ struct DecTables {
 };
 
 __global__ void hf_tables_kernel(const uint8_t* __restrict__ lengths, uint32_t nsym, DecTables* __restrict__ T,
-                                 uint16_t* __restrict__ sym_sorted, uint32_t* __restrict__ lut) {
+                                 uint16_t* __restrict__ sym_sorted, unsigned long long* __restrict__ lut) {
     __shared__ uint32_t cnt[MAXLEN + 1];
     __shared__ uint32_t run[MAXLEN + 1];
     __shared__ long long s_fc[MAXLEN + 2], s_fi[MAXLEN + 2];
@@ -376,17 +376,34 @@ __global__ void hf_tables_kernel(const uint8_t* __restrict__ lengths, uint32_t n
         }
     }
     __syncthreads();
-    // LUT: canonical decode of every 12-bit window (encode.py:248-253), in parallel
+    // LUT: canonical decode of every 12-bit window (encode.py:248-253), in
+    // parallel.  Entry = as many complete codewords as the window holds (up
+    // to 4 when every symbol fits 12 bits, else 1): symbols in bits 0-47
+    // (12 each; a lone symbol may use 16), count in 48-50, total length in
+    // 51-54, first length in 55-58.  Count 0: the first code is > 12 bits.
     const int maxlen = T->maxlen;
+    const int cap = nsym <= 4096 ? 4 : 1;
     for (uint32_t q = tid; q < (1u << LUT_BITS); q += blockDim.x) {
-        uint32_t e = 0;
-        for (int l = 1; l <= LUT_BITS && l <= maxlen; l++) {
-            const long long code = (long long)(q >> (LUT_BITS - l));
-            if (code < T->limit[l]) {
-                e = (uint32_t)sym_sorted[T->first_idx[l] + code - T->first_code[l]] | ((uint32_t)l << 16);
-                break;
+        unsigned long long e = 0;
+        int pos = 0, cnt = 0, len1 = 0;
+        while (cnt < cap && pos < LUT_BITS) {
+            int got = 0;
+            uint32_t sym = 0;
+            for (int l = 1; l <= LUT_BITS - pos && l <= maxlen; l++) {
+                const long long code = (long long)((q >> (LUT_BITS - pos - l)) & ((1u << l) - 1u));
+                if (code < T->limit[l]) {
+                    sym = sym_sorted[T->first_idx[l] + code - T->first_code[l]];
+                    got = l;
+                    break;
+                }
             }
+            if (!got) break;
+            e |= (unsigned long long)sym << (12 * cnt);
+            if (cnt == 0) len1 = got;
+            cnt++;
+            pos += got;
         }
+        e |= ((unsigned long long)cnt << 48) | ((unsigned long long)pos << 51) | ((unsigned long long)len1 << 55);
         lut[q] = e;
     }
 }
@@ -423,14 +440,18 @@ struct BitReader {
     }
 };
 
+FZB_DEV int lut_cnt(unsigned long long e) { return (int)((e >> 48) & 7u); }
+FZB_DEV int lut_len(unsigned long long e) { return (int)((e >> 51) & 15u); }
+
 // decode one symbol at r.pos; returns length (>0) or -1 truncated / -2 corrupt
-FZB_DEV int decode_one(BitReader& r, unsigned long long total_bits, const DecTables& T, const uint32_t* lut,
+FZB_DEV int decode_one(BitReader& r, unsigned long long total_bits, const DecTables& T, const unsigned long long* lut,
                        const uint16_t* sym_sorted, uint32_t& sym) {
     const uint32_t win = r.peek32();
-    const uint32_t e = lut[win >> (32 - LUT_BITS)];
-    int l = (int)(e >> 16);
-    if (l) {
-        sym = e & 0xFFFFu;
+    const unsigned long long e = lut[win >> (32 - LUT_BITS)];
+    int l;
+    if (lut_cnt(e)) {
+        l = (int)((e >> 55) & 15u);
+        sym = (uint32_t)(e & (lut_cnt(e) == 1 ? 0xFFFFu : 0xFFFu));
     } else {
         l = 0;
         for (int q = LUT_BITS + 1; q <= T.maxlen; q++) {
@@ -455,13 +476,13 @@ FZB_DEV int decode_one(BitReader& r, unsigned long long total_bits, const DecTab
 __global__ void __launch_bounds__(HD_THREADS) hf_sync_coop_kernel(const uint32_t* __restrict__ stream,
                                                                   unsigned long long total_bits, uint64_t nsub,
                                                                   const DecTables* __restrict__ Tg,
-                                                                  const uint32_t* __restrict__ lut_g,
+                                                                  const unsigned long long* __restrict__ lut_g,
                                                                   const uint16_t* __restrict__ sym_sorted,
                                                                   unsigned long long* start, unsigned long long* end,
                                                                   uint32_t* __restrict__ cnt, uint32_t* __restrict__ err,
                                                                   uint32_t* changed, uint32_t* __restrict__ status,
                                                                   int max_iter) {
-    __shared__ uint32_t lut[1 << LUT_BITS];
+    __shared__ unsigned long long lut[1 << LUT_BITS];
     __shared__ DecTables T;
     for (int q = threadIdx.x; q < (1 << LUT_BITS); q += blockDim.x) lut[q] = lut_g[q];
     if (threadIdx.x == 0) T = *Tg;
@@ -482,10 +503,20 @@ __global__ void __launch_bounds__(HD_THREADS) hf_sync_coop_kernel(const uint32_t
                 changed[it % 3] = 1;
             }
             const unsigned long long lim = (t + 1) * (unsigned long long)SUB;
+            // whole windows while every codeword of the window starts before lim
+            const unsigned long long fast_end = (lim < total_bits ? lim : total_bits) - LUT_BITS;
             BitReader r;
             r.init(stream, s);
             uint32_t c = 0, e = 0;
             while (r.pos < lim && r.pos < total_bits) {
+                if (r.pos <= fast_end && fast_end < lim) {
+                    const unsigned long long me = lut[r.peek32() >> (32 - LUT_BITS)];
+                    if (lut_cnt(me)) {
+                        c += lut_cnt(me);
+                        r.skip(lut_len(me));
+                        continue;
+                    }
+                }
                 uint32_t sym;
                 const int l = decode_one(r, total_bits, T, lut, sym_sorted, sym);
                 if (l < 0) { e = (uint32_t)(-l); break; }
@@ -509,12 +540,12 @@ __global__ void __launch_bounds__(HD_THREADS) hf_sync_coop_kernel(const uint32_t
 // offsets (consecutive symbols of one chunk go to consecutive lanes).  The
 // first true-path error with ordinal < n (encode.py:299-310) is folded in
 // with an atomicMin on (subsequence << 2 | kind).
-constexpr int HD_ROUND = 64;
+constexpr int HD_ROUND = 48;   // symbols per thread and round (smem: 128 x 50 x 2 B + 32 KB LUT)
 
 __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_t* __restrict__ stream,
                                                                    unsigned long long total_bits, uint64_t nsub,
                                                                    const DecTables* __restrict__ Tg,
-                                                                   const uint32_t* __restrict__ lut_g,
+                                                                   const unsigned long long* __restrict__ lut_g,
                                                                    const uint16_t* __restrict__ sym_sorted,
                                                                    const unsigned long long* __restrict__ start,
                                                                    const unsigned long long* __restrict__ end,
@@ -524,7 +555,7 @@ __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_
                                                                    uint64_t n, uint16_t* __restrict__ out,
                                                                    unsigned long long* __restrict__ end_pos,
                                                                    unsigned long long* __restrict__ best) {
-    __shared__ uint32_t lut[1 << LUT_BITS];
+    __shared__ unsigned long long lut[1 << LUT_BITS];
     __shared__ DecTables T;
     __shared__ uint16_t buf[HD_THREADS][HD_ROUND + 2];
     for (int q = threadIdx.x; q < (1 << LUT_BITS); q += blockDim.x) lut[q] = lut_g[q];
@@ -544,7 +575,24 @@ __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_
     while (true) {
         int k = 0;
         if (o < n) {
+            // whole LUT windows (up to 4 symbols) while they stay inside the
+            // subsequence, the stream, the round and the first n symbols
+            const unsigned long long fe = (e < total_bits ? e : total_bits);
             while (k < HD_ROUND && r.pos < e && o + (unsigned long long)k < n) {
+                if (k <= HD_ROUND - 4 && r.pos + LUT_BITS <= fe && o + (unsigned long long)k + 4 < n) {
+                    const unsigned long long me = lut[r.peek32() >> (32 - LUT_BITS)];
+                    const int mc = lut_cnt(me);
+                    if (mc >= 2) {
+                        uint16_t* bp = &buf[threadIdx.x][k];
+                        bp[0] = (uint16_t)(me & 0xFFFu);
+                        bp[1] = (uint16_t)((me >> 12) & 0xFFFu);
+                        bp[2] = (uint16_t)((me >> 24) & 0xFFFu);
+                        bp[3] = (uint16_t)((me >> 36) & 0xFFFu);
+                        k += mc;
+                        r.skip(lut_len(me));
+                        continue;
+                    }
+                }
                 uint32_t sym;
                 const int l = decode_one(r, total_bits, T, lut, sym_sorted, sym);
                 if (l < 0) { e = 0; break; }
@@ -660,7 +708,7 @@ FZB_API int fzb_huffman_encode(const uint16_t* d_codes, uint64_t n, const uint8_
 FZB_API size_t fzb_huffman_decode_workspace_bytes(uint64_t nbytes, uint32_t nsym) {
     const uint64_t nsub = (nbytes * 8 + SUB - 1) / SUB + 1;
     // tables + sym_sorted + lut + 2x(start,end,cnt,err) + offs + scalars
-    return align256(sizeof(DecTables)) + align256((size_t)nsym * 2) + align256((1u << LUT_BITS) * 4) +
+    return align256(sizeof(DecTables)) + align256((size_t)nsym * 2) + align256((1u << LUT_BITS) * 8) +
            2 * (2 * align256(nsub * 8) + 2 * align256(nsub * 4)) + align256(nsub * 8) +
            align256(fzscan::ws_bytes(nsub)) + 1024;
 }
@@ -678,7 +726,7 @@ FZB_API int fzb_huffman_decode(const uint8_t* d_stream, uint64_t nbytes, uint64_
     unsigned char* p = static_cast<unsigned char*>(d_ws);
     DecTables* T = reinterpret_cast<DecTables*>(p); p += align256(sizeof(DecTables));
     uint16_t* sym_sorted = reinterpret_cast<uint16_t*>(p); p += align256((size_t)nsym * 2);
-    uint32_t* lut = reinterpret_cast<uint32_t*>(p); p += align256((1u << LUT_BITS) * 4);
+    unsigned long long* lut = reinterpret_cast<unsigned long long*>(p); p += align256((1u << LUT_BITS) * 8);
     unsigned long long* st_[2]; unsigned long long* en_[2]; uint32_t* cn_[2]; uint32_t* er_[2];
     for (int b = 0; b < 2; b++) {
         st_[b] = reinterpret_cast<unsigned long long*>(p); p += align256(nsub * 8);

@@ -997,6 +997,29 @@ __global__ void lz1d_super_kernel(const float* __restrict__ bmin, const float* _
     }
 }
 
+// First index in [a, a + 1024) whose value lies outside [zlo, zhi] (values
+// v[e] = x[a + 32e + lane]; indices >= b count as inside), or -1.  Per-lane
+// bitmasks and one warp min instead of 32 ballot/branch rounds.
+FZB_DEV long long first_outside(const float (&v)[32], long long a, long long b, float zlo, float zhi) {
+    const int lane = threadIdx.x & 31;
+    uint32_t m = 0;
+#pragma unroll
+    for (int e = 0; e < 32; e++) {
+        const long long i = a + e * 32 + lane;
+        m |= (uint32_t)((i < b) & !(v[e] >= zlo && v[e] <= zhi)) << e;
+    }
+    const uint32_t mine = m ? (uint32_t)((__ffs(m) - 1) * 32 + lane) : 0xFFFFFFFFu;
+    const uint32_t best = __reduce_min_sync(0xffffffffu, mine);
+    return best == 0xFFFFFFFFu ? -1 : a + (long long)best;
+}
+
+__global__ void lz1d_touch_kernel(const float* __restrict__ p, long long m) {
+    float acc = 0.f;
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (long long)gridDim.x * blockDim.x)
+        acc += __ldcg(p + q);
+    if (acc == 12345.f) asm volatile("" ::"f"(acc));   // keep the loads
+}
+
 FZB_DEV bool zero_code(double v, double pred, const QParams& P) {
     float rec;
     bool outl;
@@ -1018,6 +1041,32 @@ FZB_DEV bool zkey(long long k, double pred, const QParams& P) {
     const float f = kfloat((uint32_t)k);
     return isfinite(f) && zero_code((double)f, pred, P);
 }
+// Both bounds at once: lanes 0-15 slide a 16-key window for the upper bound,
+// lanes 16-31 one for the lower bound.
+FZB_DEV void zbounds(long long k0, long long cu, long long cl, double pred, const QParams& P, uint32_t& khi,
+                     uint32_t& klo) {
+    const int lane = threadIdx.x & 31, h = lane >> 4, q = lane & 15;
+    long long wu = max(cu - 8, k0);      // upper window [wu, wu + 16)
+    long long el = min(cl + 7, k0);      // lower window (el - 16, el]
+    bool du = false, dl = false;
+    while (!(du && dl)) {
+        const long long key = h == 0 ? wu + q : el - 15 + q;
+        const bool z = zkey(key, pred, P);
+        const unsigned bal = __ballot_sync(0xffffffffu, z);
+        const unsigned mu = bal & 0xFFFFu, ml = bal >> 16;
+        if (!du) {
+            if (mu == 0xFFFFu) wu += 16;
+            else if (mu == 0) wu = max(wu - 16, k0);
+            else { khi = (uint32_t)(wu + __ffs(~mu) - 2); du = true; }   // trues occupy the low lanes
+        }
+        if (!dl) {
+            if (ml == 0xFFFFu) el -= 16;
+            else if (ml == 0) el = min(el + 16, k0);
+            else { klo = (uint32_t)(el - 15 + __ffs(ml) - 1); dl = true; }   // trues occupy the high lanes
+        }
+    }
+}
+
 FZB_DEV uint32_t zupper(long long k0, long long c, double pred, const QParams& P) {
     const int lane = threadIdx.x & 31;
     long long w = max(c - 16, k0);
@@ -1039,16 +1088,44 @@ FZB_DEV uint32_t zlower(long long k0, long long c, double pred, const QParams& P
     }
 }
 
+// Superblock summaries live in shared memory (when they fit), and the
+// element loads of the current block are issued before the zero-interval
+// search so their latency overlaps it.
+constexpr long long WALK_SMEM_SB = 24576;
+#ifdef LZ7_TIMING
+__device__ long long g_walk_stamp[8];
+#endif   // superblocks cached in smem (196 KB)
+
 __global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__ x, long long n,
                                                         uint16_t* __restrict__ codes, uint32_t* __restrict__ bitmap,
                                                         const float* __restrict__ bmin, const float* __restrict__ bmax,
-                                                        long long nblk, const float* __restrict__ smin,
-                                                        const float* __restrict__ smax, long long nsb,
+                                                        long long nblk, const float* __restrict__ smin_g,
+                                                        const float* __restrict__ smax_g, long long nsb,
                                                         const double* __restrict__ d_eb, int radius) {
+    extern __shared__ float s_sum[];
     const int lane = threadIdx.x;
+    const bool cached = nsb <= WALK_SMEM_SB;
+    const float* smin = smin_g;
+    const float* smax = smax_g;
+    if (cached) {
+        for (long long q = lane; q < nsb; q += 32) {
+            s_sum[q] = smin_g[q];
+            s_sum[nsb + q] = smax_g[q];
+        }
+        __syncwarp();
+        smin = s_sum;
+        smax = s_sum + nsb;
+    }
     const QParams P = make_qparams(*d_eb, radius);
     long long t = 0;
     float r = 0.f;
+#ifdef LZ7_TIMING
+    long long ph[6] = {0, 0, 0, 0, 0, 0};
+    long long c0 = clock64();
+#define WSTAMP(i) do { const long long c1 = clock64(); ph[i] += c1 - c0; c0 = c1; } while (0)
+#else
+#define WSTAMP(i) do { } while (0)
+#endif
     while (t < n) {
         {   // event at t
             const double v = (double)__ldg(x + t);
@@ -1063,13 +1140,33 @@ __global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__
             r = rec;
             t++;
         }
+        WSTAMP(0);
         if (t >= n) break;
+        // loads that do not depend on the new interval go out before its search:
+        // the rest of the current block, and the block summaries of the current
+        // and the next superblock (lane = block within the superblock)
+        const long long a0 = t, b0 = (t % BS1) ? min(n, (t / BS1 + 1) * BS1) : t;
+        float pv[32];
+#pragma unroll
+        for (int e = 0; e < 32; e++) {
+            const long long i = a0 + e * 32 + lane;
+            pv[e] = i < b0 ? __ldg(x + i) : 0.f;
+        }
+        const long long sb_cur = b0 / BS2;
+        float pmin[2], pmax[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const long long bb = (sb_cur + h) * 32 + lane;
+            pmin[h] = bb < nblk ? __ldcg(bmin + bb) : INFINITY;
+            pmax[h] = bb < nblk ? __ldcg(bmax + bb) : -INFINITY;
+        }
         const double pred = __dadd_rn(0.0, (double)r);
         const long long k0 = fkey(__double2float_rn(pred));
-        const uint32_t khi = zupper(k0, fkey(__double2float_rn(__dadd_rn(pred, P.eb))), pred, P);
-        const uint32_t klo = zlower(k0, fkey(__double2float_rn(__dsub_rn(pred, P.eb))), pred, P);
+        uint32_t khi = 0, klo = 0;
+        zbounds(k0, fkey(__double2float_rn(__dadd_rn(pred, P.eb))), fkey(__double2float_rn(__dsub_rn(pred, P.eb))),
+                pred, P, khi, klo);
         const float zlo = kfloat(klo), zhi = kfloat(khi);
-        auto inside = [&](float v) { return v >= zlo && v <= zhi; };
+        WSTAMP(1);
         // scan [a, b) (b - a <= 1024) with coalesced loads; returns first outside index or -1
         auto scan = [&](long long a, long long b) -> long long {
             float v[32];
@@ -1078,45 +1175,53 @@ __global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__
                 const long long i = a + e * 32 + lane;
                 v[e] = i < b ? __ldg(x + i) : zlo;
             }
-#pragma unroll
-            for (int e = 0; e < 32; e++) {
-                const unsigned m = __ballot_sync(0xffffffffu, !inside(v[e]));
-                if (m) return a + e * 32 + (__ffs(m) - 1);
-            }
-            return -1;
+            return first_outside(v, a, b, zlo, zhi);
         };
         long long found = -1;
-        if (t % BS1) {
-            const long long be = min(n, (t / BS1 + 1) * BS1);
-            found = scan(t, be);
-            t = be;
+        if (b0 > a0) {
+            found = first_outside(pv, a0, b0, zlo, zhi);
+            t = b0;
         }
+        WSTAMP(2);
         while (found < 0 && t < n) {
+            const long long sb = t / BS2;
             if (t % BS2 == 0) {  // probe 32 superblocks
-                const long long sb = t / BS2 + lane;
-                const bool skip = sb < nsb && smin[sb] >= zlo && smax[sb] <= zhi;
+                const long long sq = sb + lane;
+                const bool skip = sq < nsb && smin[sq] >= zlo && smax[sq] <= zhi;
                 const unsigned ns = __ballot_sync(0xffffffffu, !skip);
-                if (!ns) { t = (t / BS2 + 32) * BS2; continue; }
-                t = (t / BS2 + (__ffs(ns) - 1)) * BS2;
+                if (!ns) { t = (sb + 32) * BS2; continue; }
+                t = (sb + (__ffs(ns) - 1)) * BS2;
                 if (t >= n) break;
             }
-            const long long b0 = t / BS1;
-            const long long bb = b0 + lane;
-            const bool in_sb = (bb / 32) == (b0 / 32);
-            const bool skip = bb < nblk && in_sb && bmin[bb] >= zlo && bmax[bb] <= zhi;
+            // block summaries of superblock t / BS2 (prefetched for the current and the next one)
+            const long long sbt = t / BS2;
+            float lo, hi;
+            if (sbt == sb_cur) { lo = pmin[0]; hi = pmax[0]; }
+            else if (sbt == sb_cur + 1) { lo = pmin[1]; hi = pmax[1]; }
+            else {
+                const long long bb = sbt * 32 + lane;
+                lo = bb < nblk ? __ldcg(bmin + bb) : INFINITY;
+                hi = bb < nblk ? __ldcg(bmax + bb) : -INFINITY;
+            }
+            const long long bfirst = t / BS1;
+            const long long bb = sbt * 32 + lane;
+            const bool skip = bb < bfirst || bb >= nblk || (lo >= zlo && hi <= zhi);
             const unsigned nsk = __ballot_sync(0xffffffffu, !skip);
-            const int first = __ffs(nsk) - 1;
-            const long long fb = b0 + first;
-            if (fb >= nblk) { t = n; break; }
-            if ((fb / 32) != (b0 / 32)) { t = fb * BS1; continue; }  // rest of the superblock is skippable
+            if (!nsk) { t = (sbt + 1) * BS2; continue; }   // rest of the superblock is skippable
+            const long long fb = sbt * 32 + (__ffs(nsk) - 1);
             t = fb * BS1;
             const long long be = min(n, t + BS1);
             found = scan(t, be);
             t = be;
         }
+        WSTAMP(3);
         if (found < 0) break;
         t = found;
     }
+#ifdef LZ7_TIMING
+    if (lane == 0)
+        for (int i = 0; i < 4; i++) g_walk_stamp[i] = ph[i];
+#endif
 }
 
 // ---- 1D decode: events = nonzero code or outlier --------------------------
@@ -1470,8 +1575,12 @@ FZB_API int fzb_lorenzo_encode_f32(const float* d_in, uint32_t n0, uint32_t n1, 
         float* smax = smin + nsb;
         lz1d_summary_kernel<<<kNumSMs * 8, 256, 0, st>>>(d_in, n, d_codes, (int)radius, bmin, bmax, nblk);
         lz1d_super_kernel<<<kNumSMs * 2, 256, 0, st>>>(bmin, bmax, nblk, smin, smax, nsb);
-        lz1d_walk_kernel<<<1, 32, 0, st>>>(d_in, n, d_codes, d_bitmap, bmin, bmax, nblk, smin, smax, nsb, d_eb,
-                                           (int)radius);
+        // the summary pass streamed 4n bytes through L2: pull the (small) block summaries back in
+        lz1d_touch_kernel<<<kNumSMs * 4, 256, 0, st>>>(bmin, 2 * nblk);
+        const size_t wsm = nsb <= WALK_SMEM_SB ? (size_t)nsb * 8 : 0;
+        if (wsm > 48 * 1024) cudaFuncSetAttribute(lz1d_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
+        lz1d_walk_kernel<<<1, 32, wsm, st>>>(d_in, n, d_codes, d_bitmap, bmin, bmax, nblk, smin, smax, nsb, d_eb,
+                                             (int)radius);
         return fzb_check_launch();
     }
     if (!use_v4(n2))
@@ -1530,6 +1639,9 @@ FZB_API int fzb_lorenzo_decode_f32(const uint16_t* d_codes, const uint32_t* d_bi
 #ifdef LZ7_TIMING
 FZB_API int fzb_debug_lz_timing(long long* host_out) {
     return (int)cudaMemcpyFromSymbol(host_out, v6::g_lz_stamp, sizeof(v6::g_lz_stamp));
+}
+FZB_API int fzb_debug_walk_timing(long long* host_out) {
+    return (int)cudaMemcpyFromSymbol(host_out, g_walk_stamp, sizeof(g_walk_stamp));
 }
 #endif
 
