@@ -31,6 +31,8 @@ namespace {
 
 constexpr int MAXLEN = 32;
 constexpr int BT = 1024;  // build threads
+constexpr uint32_t SMEM_BUILD_SYMS = 2048;   // alphabets up to this size build in shared memory
+constexpr size_t SMEM_BUILD_BYTES = (size_t)SMEM_BUILD_SYMS * (8 + 8 + 16 + 4 + 4 + 8) + (size_t)MAXLEN * 2 * SMEM_BUILD_SYMS;
 
 struct BuildWS {
     unsigned long long *bw, *pw, *mw;  // base / packages / merged weights
@@ -38,6 +40,9 @@ struct BuildWS {
     uint8_t* isbase;                   // [MAXLEN][2m] leaf marks per merged list
 };
 
+#ifdef LZ7_TIMING
+__device__ uint32_t g_hf_serial_levels;
+#endif
 FZB_DEV bool key_less(unsigned long long wa, uint32_t ta, unsigned long long wb, uint32_t tb) {
     return wa < wb || (wa == wb && ta < tb);
 }
@@ -51,11 +56,26 @@ __global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long l
     __shared__ long long s_nb[MAXLEN + 1];
     __shared__ uint32_t s_cnt[MAXLEN + 1];
     __shared__ unsigned long long s_first[MAXLEN + 1];
+    extern __shared__ __align__(16) unsigned char sm_build[];
     const int tid = threadIdx.x;
+    const uint32_t NTH = blockDim.x;
+    if (nsym <= SMEM_BUILD_SYMS) {
+        // small alphabets (radius <= 1024): every list lives in shared memory
+        // (generic pointers, so the code below is unchanged)
+        constexpr size_t N2 = SMEM_BUILD_SYMS, M2 = 2 * SMEM_BUILD_SYMS;
+        unsigned char* p = sm_build;
+        ws.bw = reinterpret_cast<unsigned long long*>(p); p += N2 * 8;
+        ws.pw = reinterpret_cast<unsigned long long*>(p); p += N2 * 8;
+        ws.mw = reinterpret_cast<unsigned long long*>(p); p += M2 * 8;
+        ws.bs = reinterpret_cast<uint32_t*>(p); p += N2 * 4;
+        ws.pt = reinterpret_cast<uint32_t*>(p); p += N2 * 4;
+        ws.mt = reinterpret_cast<uint32_t*>(p); p += M2 * 4;
+        ws.isbase = p;   // MAXLEN * 2m bytes, m <= N2
+    }
 
     // 1. compact used symbols (symbol order) and zero outputs
     uint32_t carry = 0;
-    for (uint32_t s0 = 0; s0 < nsym; s0 += BT) {
+    for (uint32_t s0 = 0; s0 < nsym; s0 += NTH) {
         const uint32_t s = s0 + tid;
         const bool used = s < nsym && bins[s] != 0;
         if (s < nsym) { lengths[s] = 0; cw[s] = 0; }
@@ -82,11 +102,11 @@ __global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long l
     // 2. bitonic sort of (w, s) over the next power of two (pad = max key)
     uint32_t np2 = 1;
     while (np2 < m) np2 <<= 1;
-    for (uint32_t q = m + tid; q < np2; q += BT) { ws.bw[q] = ~0ull; ws.bs[q] = 0xFFFFFFFFu; }
+    for (uint32_t q = m + tid; q < np2; q += NTH) { ws.bw[q] = ~0ull; ws.bs[q] = 0xFFFFFFFFu; }
     __syncthreads();
     for (uint32_t k = 2; k <= np2; k <<= 1)
         for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
-            for (uint32_t q = tid; q < np2; q += BT) {
+            for (uint32_t q = tid; q < np2; q += NTH) {
                 const uint32_t ixj = q ^ jj;
                 if (ixj > q) {
                     const bool up = (q & k) == 0;
@@ -102,23 +122,23 @@ __global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long l
             __syncthreads();
         }
     // 3. levels.  M_0 = base.
-    for (uint32_t q = tid; q < m; q += BT) { ws.mw[q] = ws.bw[q]; ws.mt[q] = ws.bs[q]; ws.isbase[q] = 1; }
+    for (uint32_t q = tid; q < m; q += NTH) { ws.mw[q] = ws.bw[q]; ws.mt[q] = ws.bs[q]; ws.isbase[q] = 1; }
     uint32_t mlen = m;
     __syncthreads();
     for (int l = 1; l < MAXLEN; l++) {
         const uint32_t npk = mlen / 2;
-        for (uint32_t q = tid; q < npk; q += BT) {
+        for (uint32_t q = tid; q < npk; q += NTH) {
             ws.pw[q] = ws.mw[2 * q] + ws.mw[2 * q + 1];
             ws.pt[q] = ws.mt[2 * q];
         }
         if (tid == 0) s_unsorted = 0;
         __syncthreads();
-        for (uint32_t q = tid; q + 1 < npk; q += BT)
+        for (uint32_t q = tid; q + 1 < npk; q += NTH)
             if (key_less(ws.pw[q + 1], ws.pt[q + 1], ws.pw[q], ws.pt[q])) s_unsorted = 1;
         __syncthreads();
         uint8_t* ib = ws.isbase + (size_t)l * 2 * m;
         if (!s_unsorted) {
-            for (uint32_t q = tid; q < m; q += BT) {  // base item q: count packages < it
+            for (uint32_t q = tid; q < m; q += NTH) {  // base item q: count packages < it
                 const unsigned long long w = ws.bw[q];
                 const uint32_t t = ws.bs[q];
                 uint32_t lo = 0, hi = npk;
@@ -128,7 +148,7 @@ __global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long l
                 }
                 ws.mw[q + lo] = w; ws.mt[q + lo] = t; ib[q + lo] = 1;
             }
-            for (uint32_t q = tid; q < npk; q += BT) {  // package q: count bases < it
+            for (uint32_t q = tid; q < npk; q += NTH) {  // package q: count bases < it
                 const unsigned long long w = ws.pw[q];
                 const uint32_t t = ws.pt[q];
                 uint32_t lo = 0, hi = m;
@@ -139,6 +159,9 @@ __global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long l
                 ws.mw[q + lo] = w; ws.mt[q + lo] = t; ib[q + lo] = 0;
             }
         } else if (tid == 0) {  // heapq.merge(base, level): two heads, base first unless package < base
+#ifdef LZ7_TIMING
+            atomicAdd(&g_hf_serial_levels, 1u);
+#endif
             uint32_t i = 0, j = 0, o = 0;
             while (i < m || j < npk) {
                 if (j >= npk || (i < m && !key_less(ws.pw[j], ws.pt[j], ws.bw[i], ws.bs[i]))) {
@@ -156,7 +179,7 @@ __global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long l
     for (int l = MAXLEN - 1; l >= 1; l--) {
         const uint8_t* ib = ws.isbase + (size_t)l * 2 * m;
         uint32_t c = 0;
-        for (long long q = tid; q < L; q += BT) c += ib[q];
+        for (long long q = tid; q < L; q += NTH) c += ib[q];
         uint32_t tot;
         block_exclusive_scan(c, tmp, &tot);
         if (tid == 0) s_nb[l] = tot;
@@ -166,7 +189,7 @@ __global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long l
     __syncthreads();
     // 5. lengths and bit count
     unsigned long long bits = 0;
-    for (uint32_t q = tid; q < m; q += BT) {
+    for (uint32_t q = tid; q < m; q += NTH) {
         int len = 0;
         for (int l = 0; l < MAXLEN; l++) len += (long long)q < s_nb[l];
         lengths[ws.bs[q]] = (uint8_t)len;
@@ -179,7 +202,7 @@ __global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long l
     // 6. canonical codewords by (length, symbol)  (encode.py:155-171)
     if (tid <= MAXLEN) s_cnt[tid] = 0;
     __syncthreads();
-    for (uint32_t s = tid; s < nsym; s += BT)
+    for (uint32_t s = tid; s < nsym; s += NTH)
         if (lengths[s]) atomicAdd(&s_cnt[lengths[s]], 1u);
     __syncthreads();
     if (tid == 0) {
@@ -227,7 +250,7 @@ FZB_DEV void load16(const uint16_t* __restrict__ codes, uint64_t n, uint64_t bas
 
 __global__ void __launch_bounds__(HE_THREADS) hf_count_kernel(const uint16_t* __restrict__ codes, uint64_t n,
                                                               const uint8_t* __restrict__ lengths, uint32_t nsym,
-                                                              unsigned long long* __restrict__ cta_bits) {
+                                                              uint32_t* __restrict__ cta_bits) {
     __shared__ unsigned long long tmp[33];
     const uint64_t base = ((uint64_t)blockIdx.x * HE_THREADS + threadIdx.x) * HE_PER;
     uint32_t c[HE_PER];
@@ -238,22 +261,7 @@ __global__ void __launch_bounds__(HE_THREADS) hf_count_kernel(const uint16_t* __
         if (c[e] < nsym) b += __ldg(lengths + c[e]);
     unsigned long long tot;
     block_exclusive_scan64(b, tmp, &tot);
-    if (threadIdx.x == 0) cta_bits[blockIdx.x] = tot;
-}
-
-__global__ void scan_u64_kernel(const unsigned long long* __restrict__ x, uint64_t m,
-                                unsigned long long* __restrict__ offs, unsigned long long* __restrict__ tot) {
-    __shared__ unsigned long long tmp[33];
-    unsigned long long carry = 0;
-    for (uint64_t b0 = 0; b0 < m; b0 += blockDim.x) {
-        const uint64_t q = b0 + threadIdx.x;
-        const unsigned long long v = q < m ? x[q] : 0ull;
-        unsigned long long t;
-        const unsigned long long p = block_exclusive_scan64(v, tmp, &t);
-        if (q < m) offs[q] = carry + p;
-        carry += t;
-    }
-    if (threadIdx.x == 0) *tot = carry;
+    if (threadIdx.x == 0) cta_bits[blockIdx.x] = (uint32_t)tot;   // <= 32 * HE_CHUNK
 }
 
 __global__ void hf_zero_kernel(uint32_t* __restrict__ out, const unsigned long long* __restrict__ bits,
@@ -271,13 +279,21 @@ __global__ void hf_check_kernel(const unsigned long long* __restrict__ got, cons
 
 FZB_DEV uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
-__global__ void __launch_bounds__(HE_THREADS) hf_write_kernel(const uint16_t* __restrict__ codes, uint64_t n,
-                                                              const uint8_t* __restrict__ lengths,
-                                                              const uint32_t* __restrict__ cwords, uint32_t nsym,
-                                                              const unsigned long long* __restrict__ cta_off,
-                                                              const unsigned long long* __restrict__ want_bits,
-                                                              uint32_t* __restrict__ out, uint64_t cap_words) {
+// Write pass: the CTA's bits are packed into shared-memory words (atomicOr
+// between neighbouring threads), then shifted to the CTA's global bit offset
+// (from the count pass + scan) and written with plain coalesced stores; only
+// the two edge words shared with the neighbouring CTAs use global atomicOr.
+// Big-endian words == the MSB-first byte stream of encode.py:220-231.
+constexpr int HE_WORDS = HE_CHUNK;   // <= 32 bits per code -> at most HE_CHUNK words per CTA
+
+__global__ void __launch_bounds__(HE_THREADS) hf_write2_kernel(const uint16_t* __restrict__ codes, uint64_t n,
+                                                               const uint8_t* __restrict__ lengths,
+                                                               const uint32_t* __restrict__ cwords, uint32_t nsym,
+                                                               const unsigned long long* __restrict__ cta_off,
+                                                               uint32_t* __restrict__ out, uint64_t cap_words) {
     __shared__ unsigned long long tmp[33];
+    __shared__ uint32_t buf[HE_WORDS + 1];
+    for (int q = threadIdx.x; q <= HE_WORDS; q += HE_THREADS) buf[q] = 0;
     const uint64_t base = ((uint64_t)blockIdx.x * HE_THREADS + threadIdx.x) * HE_PER;
     uint32_t c[HE_PER];
     load16(codes, n, base, c);
@@ -289,32 +305,47 @@ __global__ void __launch_bounds__(HE_THREADS) hf_write_kernel(const uint16_t* __
         if (c[e] < nsym) { len[e] = __ldg(lengths + c[e]); cwv[e] = __ldg(cwords + c[e]); }
         b += len[e];
     }
-    const unsigned long long o = cta_off[blockIdx.x] + block_exclusive_scan64(b, tmp, nullptr);
-    if (b == 0) return;
-    uint64_t w = o >> 5;
-    int filled = (int)(o & 31);
-    unsigned long long acc = 0;  // MSB-aligned pending bits of word w
-    bool first = true;
+    unsigned long long total;
+    const unsigned long long o = block_exclusive_scan64(b, tmp, &total);   // CTA-local bit offset (syncs)
+    // pack this thread's bits into the shared buffer (bit 0 of the CTA = MSB of buf[0])
+    if (b) {
+        uint32_t w = (uint32_t)(o >> 5);
+        int filled = (int)(o & 31);
+        unsigned long long acc = 0;
+        bool first = true;
 #pragma unroll
-    for (int e = 0; e < HE_PER; e++) {
-        const int l = (int)len[e];
-        if (l == 0) continue;
-        // place l bits right after `filled` bits (acc holds up to 64)
-        acc |= ((unsigned long long)cwv[e] << (64 - l)) >> filled;
-        filled += l;
-        if (filled >= 32) {
-            const uint32_t word = (uint32_t)(acc >> 32);
-            if (w < cap_words) {
-                if (first) atomicOr(out + w, bswap32(word));
-                else out[w] = bswap32(word);
+        for (int e = 0; e < HE_PER; e++) {
+            const int l = (int)len[e];
+            if (l == 0) continue;
+            acc |= ((unsigned long long)cwv[e] << (64 - l)) >> filled;
+            filled += l;
+            if (filled >= 32) {
+                const uint32_t word = (uint32_t)(acc >> 32);
+                if (first) atomicOr(buf + w, word);
+                else buf[w] = word;
+                first = false;
+                acc <<= 32;
+                filled -= 32;
+                w++;
             }
-            first = false;
-            acc <<= 32;
-            filled -= 32;
-            w++;
         }
+        if (filled > 0) atomicOr(buf + w, (uint32_t)(acc >> 32));
     }
-    if (filled > 0 && w < cap_words) atomicOr(out + w, bswap32((uint32_t)(acc >> 32)));
+    __syncthreads();
+    if (total == 0) return;
+    const unsigned long long G = cta_off[blockIdx.x];
+    const int sh = (int)(G & 31);
+    const uint64_t w0 = G >> 5, w1 = (G + total - 1) >> 5;   // global words touched
+    const uint32_t nw = (uint32_t)(w1 - w0 + 1);
+    for (uint32_t q = threadIdx.x; q < nw; q += HE_THREADS) {
+        // global word w0+q = the buffer shifted right by sh bits
+        const uint32_t hi = q > 0 ? buf[q - 1] : 0u, lo = q < (uint32_t)HE_WORDS ? buf[q] : 0u;
+        const uint32_t word = sh ? ((lo >> sh) | (hi << (32 - sh))) : lo;
+        const uint64_t gw = w0 + q;
+        if (gw >= cap_words) continue;
+        if (q == 0 || q == nw - 1) atomicOr(out + gw, bswap32(word));   // shared with the neighbouring CTAs
+        else out[gw] = bswap32(word);
+    }
 }
 
 // ------------------------------------------------------------------ decode
@@ -645,6 +676,12 @@ size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 extern "C" {
 
+#ifdef LZ7_TIMING
+FZB_API int fzb_debug_hf_serial(uint32_t* out) {
+    return (int)cudaMemcpyFromSymbol(out, g_hf_serial_levels, 4);
+}
+#endif
+
 FZB_API size_t fzb_huffman_build_workspace_bytes(uint32_t nsym) {
     size_t np2 = 1;
     while (np2 < nsym) np2 <<= 1;
@@ -669,7 +706,11 @@ FZB_API int fzb_huffman_build(const uint64_t* d_bins, uint32_t nsym, uint8_t* d_
     ws.mw = reinterpret_cast<unsigned long long*>(p); p += align256(m2 * 8);
     ws.mt = reinterpret_cast<uint32_t*>(p); p += align256(m2 * 4);
     ws.isbase = p;
-    huffman_build_kernel<<<1, BT, 0, (cudaStream_t)stream>>>(reinterpret_cast<const unsigned long long*>(d_bins), nsym,
+    const size_t bsm = nsym <= SMEM_BUILD_SYMS ? SMEM_BUILD_BYTES : 0;
+    if (bsm) cudaFuncSetAttribute(huffman_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
+    // small alphabets: fewer threads -> cheaper barriers (the lists are short)
+    const int nth = nsym <= 1024 ? 256 : BT;
+    huffman_build_kernel<<<1, nth, bsm, (cudaStream_t)stream>>>(reinterpret_cast<const unsigned long long*>(d_bins), nsym,
                                                              d_lengths, d_codewords,
                                                              reinterpret_cast<unsigned long long*>(d_bit_count), ws);
     return fzb_check_launch();
@@ -677,7 +718,7 @@ FZB_API int fzb_huffman_build(const uint64_t* d_bins, uint32_t nsym, uint8_t* d_
 
 FZB_API size_t fzb_huffman_encode_workspace_bytes(uint64_t n) {
     const uint64_t nc = (n + HE_CHUNK - 1) / HE_CHUNK;
-    return 256 + 2 * align256(nc * 8) + 256;
+    return 256 + 2 * align256(nc * 8) + align256(fzscan::ws_bytes(nc)) + 256;
 }
 
 FZB_API int fzb_huffman_encode(const uint16_t* d_codes, uint64_t n, const uint8_t* d_lengths,
@@ -693,15 +734,17 @@ FZB_API int fzb_huffman_encode(const uint16_t* d_codes, uint64_t n, const uint8_
     unsigned long long* tot = reinterpret_cast<unsigned long long*>(w);
     unsigned long long* cta_bits = reinterpret_cast<unsigned long long*>(w + 256);
     unsigned long long* cta_off = reinterpret_cast<unsigned long long*>(w + 256 + align256(nc * 8));
+    void* scan_ws = w + 256 + 2 * align256(nc * 8);
     const uint64_t cap_words = out_cap / 4;
     uint32_t* out = reinterpret_cast<uint32_t*>(d_out);
     const unsigned long long* want = reinterpret_cast<const unsigned long long*>(d_bit_count);
-    hf_count_kernel<<<(unsigned)nc, HE_THREADS, 0, st>>>(d_codes, n, d_lengths, nsym, cta_bits);
-    scan_u64_kernel<<<1, 1024, 0, st>>>(cta_bits, nc, cta_off, tot);
+    hf_count_kernel<<<(unsigned)nc, HE_THREADS, 0, st>>>(d_codes, n, d_lengths, nsym,
+                                                        reinterpret_cast<uint32_t*>(cta_bits));
+    fzscan::exclusive(reinterpret_cast<uint32_t*>(cta_bits), nc, cta_off, tot, scan_ws, st);
     hf_check_kernel<<<1, 1, 0, st>>>(tot, want, d_status);
     hf_zero_kernel<<<kNumSMs * 4, 256, 0, st>>>(out, tot, cap_words);
-    hf_write_kernel<<<(unsigned)nc, HE_THREADS, 0, st>>>(d_codes, n, d_lengths, d_codewords, nsym, cta_off, want, out,
-                                                        cap_words);
+    hf_write2_kernel<<<(unsigned)nc, HE_THREADS, 0, st>>>(d_codes, n, d_lengths, d_codewords, nsym, cta_off, out,
+                                                         cap_words);
     return fzb_check_launch();
 }
 

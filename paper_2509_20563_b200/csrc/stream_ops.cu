@@ -117,44 +117,58 @@ __global__ void fill_u16_kernel(uint16_t* __restrict__ d, uint64_t n, uint16_t v
 }
 
 // ----------------------------------------------------------------- histogram
-constexpr int HIST_THREADS = 512;
+constexpr int HIST_THREADS = 256;
 constexpr uint32_t HIST_SMEM_BINS = 16384;
 
-FZB_DEV void hist_add(uint32_t* bins, uint32_t c, uint32_t nbins, uint32_t* status) {
-    const bool ok = c < nbins;
-    if (!ok) set_err(status, FZB_ERR_CODE_RANGE);
-    const unsigned am = __activemask();
-    const unsigned peers = __match_any_sync(am, ok ? c : 0xFFFFFFFFu);
-    if (ok && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(bins + c, (uint32_t)__popc(peers));
-}
-
+// Privatised histogram (encode.py:79-84): each warp owns a sub-histogram in
+// shared memory and every thread merges runs of equal codes before it
+// touches a bin, so the heavily skewed code distribution of smooth fields
+// (most codes are R) costs a handful of atomics instead of one per code.
 __global__ void __launch_bounds__(HIST_THREADS) hist_smem_kernel(const uint16_t* __restrict__ codes, uint64_t n,
-                                                                 uint32_t nbins, unsigned long long* __restrict__ out,
+                                                                 uint32_t nbins, int nsub,
+                                                                 unsigned long long* __restrict__ out,
                                                                  uint32_t* __restrict__ status) {
     extern __shared__ uint32_t sb[];
-    for (uint32_t q = threadIdx.x; q < nbins; q += blockDim.x) sb[q] = 0;
+    for (uint32_t q = threadIdx.x; q < nbins * (uint32_t)nsub; q += blockDim.x) sb[q] = 0;
     __syncthreads();
+    uint32_t* mine = sb + (size_t)((threadIdx.x >> 5) % nsub) * nbins;
+    uint32_t cur = 0xFFFFFFFFu, cnt = 0;
+    bool bad = false;
+    auto put = [&](uint32_t c) {
+        if (c == cur) {
+            cnt++;
+        } else {
+            if (cnt) {
+                if (cur < nbins) atomicAdd(mine + cur, cnt);
+                else bad = true;
+            }
+            cur = c;
+            cnt = 1;
+        }
+    };
     const uint64_t n8 = n / 8;
     const uint4* c8 = reinterpret_cast<const uint4*>(codes);
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n8; q += stride) {
         const uint4 v = __ldcs(c8 + q);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            hist_add(sb, w[u] & 0xFFFFu, nbins, status);
-            hist_add(sb, w[u] >> 16, nbins, status);
-        }
+        put(v.x & 0xFFFFu); put(v.x >> 16);
+        put(v.y & 0xFFFFu); put(v.y >> 16);
+        put(v.z & 0xFFFFu); put(v.z >> 16);
+        put(v.w & 0xFFFFu); put(v.w >> 16);
     }
     if (blockIdx.x == 0)
-        for (uint64_t t = n8 * 8 + threadIdx.x; t < n; t += blockDim.x) {
-            const uint32_t c = codes[t];
-            if (c >= nbins) set_err(status, FZB_ERR_CODE_RANGE);
-            else atomicAdd(sb + c, 1u);
-        }
+        for (uint64_t t = n8 * 8 + threadIdx.x; t < n; t += blockDim.x) put(codes[t]);
+    if (cnt) {
+        if (cur < nbins) atomicAdd(mine + cur, cnt);
+        else bad = true;
+    }
+    if (bad) set_err(status, FZB_ERR_CODE_RANGE);
     __syncthreads();
-    for (uint32_t q = threadIdx.x; q < nbins; q += blockDim.x)
-        if (sb[q]) atomicAdd(out + q, (unsigned long long)sb[q]);
+    for (uint32_t q = threadIdx.x; q < nbins; q += blockDim.x) {
+        uint32_t t = 0;
+        for (int w = 0; w < nsub; w++) t += sb[(size_t)w * nbins + q];
+        if (t) atomicAdd(out + q, (unsigned long long)t);
+    }
 }
 
 __global__ void hist_global_kernel(const uint16_t* __restrict__ codes, uint64_t n, uint32_t nbins,
@@ -281,13 +295,16 @@ FZB_API int fzb_histogram(const uint16_t* d_codes, uint64_t n, uint32_t nbins, u
     if (n == 0) return fzb_check_launch();
     unsigned long long* out = reinterpret_cast<unsigned long long*>(d_bins);
     if (nbins <= HIST_SMEM_BINS && !(reinterpret_cast<uintptr_t>(d_codes) & 15)) {
-        const size_t smem = (size_t)nbins * 4;
+        // one sub-histogram per warp while they fit in 64 KB
+        int nsub = HIST_THREADS / 32;
+        while (nsub > 1 && (size_t)nsub * nbins * 4 > 64 * 1024) nsub >>= 1;
+        const size_t smem = (size_t)nbins * 4 * nsub;
         cudaFuncSetAttribute(hist_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         uint64_t blocks = (n / 8 + HIST_THREADS - 1) / HIST_THREADS;
         const uint64_t cap = (uint64_t)kNumSMs * 4;
         if (blocks > cap) blocks = cap;
         if (blocks == 0) blocks = 1;
-        hist_smem_kernel<<<(unsigned)blocks, HIST_THREADS, smem, st>>>(d_codes, n, nbins, out, d_status);
+        hist_smem_kernel<<<(unsigned)blocks, HIST_THREADS, smem, st>>>(d_codes, n, nbins, nsub, out, d_status);
     } else {
         hist_global_kernel<<<kNumSMs * 8, 256, 0, st>>>(d_codes, n, nbins, out, d_status);
     }
