@@ -1497,7 +1497,7 @@ Cfg7 pick7(uint32_t n0) {
     return {1, 1};
 }
 
-#define FZB_LZ7_CFGS(X) X(8, 2) X(4, 4) X(4, 2) X(8, 1) X(2, 4) X(2, 2) X(1, 2) X(1, 1) X(16, 1) X(4, 1) X(2, 1)
+#define FZB_LZ7_CFGS(X) X(8, 2) X(4, 4) X(4, 2) X(4, 3) X(8, 1) X(2, 4) X(2, 2) X(1, 2) X(1, 1) X(16, 1) X(4, 1) X(2, 1)
 
 template <bool DEC>
 int launch_v7(const float* orig, const uint16_t* codes_in, uint16_t* codes_out, uint32_t* bitmap, float* recon,
@@ -1516,7 +1516,7 @@ int launch_v7(const float* orig, const uint16_t* codes_in, uint16_t* codes_out, 
 size_t v7_ws(uint32_t n0, uint32_t n1, uint32_t n2) {
     // enough for every configuration pick7 may return (tuning overrides included)
     size_t m = 0;
-    for (int pi : {1, 2, 4, 8, 16}) {
+    for (int pi : {1, 2, 4, 8, 12, 16}) {
         if ((uint32_t)pi > n0 && pi > 1) continue;
         size_t t = 0;
         switch (pi) {
@@ -1524,6 +1524,7 @@ size_t v7_ws(uint32_t n0, uint32_t n1, uint32_t n2) {
             case 2: t = v6::WS7<2>(n0, n1, n2).total; break;
             case 4: t = v6::WS7<4>(n0, n1, n2).total; break;
             case 8: t = v6::WS7<8>(n0, n1, n2).total; break;
+            case 12: t = v6::WS7<12>(n0, n1, n2).total; break;
             default: t = v6::WS7<16>(n0, n1, n2).total; break;
         }
         m = t > m ? t : m;

@@ -79,6 +79,11 @@ FZB_DEV uint64_t ld_ll_cta(const uint64_t* p) {
 FZB_DEV void st_ll_cta(uint64_t* p, uint64_t v) {
     asm volatile("st.volatile.shared.u64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "l"(v) : "memory");
 }
+FZB_DEV uint32_t ld_cta_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
+    return v;
+}
 FZB_DEV uint32_t ld_acq_cta(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
@@ -471,6 +476,17 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
             float hfn[R + 1];
 #pragma unroll
             for (int x = 0; x <= R; x++) hfn[x] = __uint_as_float((uint32_t)ld_ll_cta(hlw + cs * (PI + 1) + x));
+            // this step's inputs (encode: v, decode: code word) are independent of the
+            // prediction: read them now so their latency hides under the shuffles and
+            // the 7-term sum (a pinned asm load: the compiler would sink a plain one)
+            const int u = s - OFF - w * R - b;
+            uint32_t* cell[R + 1];
+            uint32_t raw[R + 1];
+#pragma unroll
+            for (int x = 1; x <= R; x++) {
+                cell[x] = ringl + (x - 1) * 32 * IP + ((u - (x - 1)) & (KR - 1));
+                raw[x] = ld_cta_u32(cell[x]);
+            }
             LZ_STAMP(1);
             F1[0] = __uint_as_float((uint32_t)gh);
             C1[0] = (double)F1[0];
@@ -481,12 +497,9 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
                 const float up1 = __shfl_up_sync(FULL, F1[x], 1);
                 Ln[x] = (double)(l0 ? hf[x] : up1);
             }
-            const int u = s - OFF - w * R - b;
             double pred[R + 1];
-            uint32_t* cell[R + 1];
 #pragma unroll
             for (int x = 1; x <= R; x++) {
-                cell[x] = ringl + (x - 1) * 32 * IP + ((u - (x - 1)) & (KR - 1));
                 double p = __dadd_rn(C1[x - 1], Ln[x]);   // up + left (up never -0.0)
                 p = __dadd_rn(p, C1[x]);                   // + self
                 p = __dsub_rn(p, L1[x - 1]);               // - diag
@@ -502,7 +515,7 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
                 uint32_t word[R + 1];
 #pragma unroll
                 for (int x = 1; x <= R; x++) {
-                    const float vf = __uint_as_float(*cell[x]) + 0.0f;   // normalised -0 (same quantisation)
+                    const float vf = __uint_as_float(raw[x]) + 0.0f;   // normalised -0 (same quantisation)
                     const double v = (double)vf;
                     const double q = __dmul_rn(__dsub_rn(v, pred[x]), P.inv2eb);
                     const double t = __dadd_rn(q, RINT_MAGIC);
@@ -525,7 +538,7 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
                         if ((slow >> x) & 1u) {
                             // frac(|q|) within ~1e-9 of .5: the exact IEEE-division quantizer decides
                             float rec;
-                            word[x] = quantize_word_slow(__uint_as_float(*cell[x]) + 0.0f, pred[x], P, &rec);
+                            word[x] = quantize_word_slow(__uint_as_float(raw[x]) + 0.0f, pred[x], P, &rec);
                             Fn[x] = rec;
                             Cn[x] = (double)rec;
                         }
@@ -537,7 +550,7 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
             } else {
 #pragma unroll
                 for (int x = 1; x <= R; x++) {
-                    const uint32_t wv = *cell[x];
+                    const uint32_t wv = raw[x];
                     const bool is_code = (wv & 0x7F800000u) == 0x7F800000u;
                     // (code - R) exactly via the 2^52 mantissa trick, no int->double convert
                     const double cm = __dsub_rn(__longlong_as_double(0x4330000000000000ll | (long long)(wv & 0xFFFFu)),
