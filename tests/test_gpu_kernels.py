@@ -1,0 +1,112 @@
+"""GPU parity for the round-1 kernels (v7 Lorenzo wavefront, bitshuffle
+transpose, Huffman multi-symbol decode, privatised histogram) against the C
+oracle: shapes that hit partial tiles in i and j, every v7 tile
+configuration, small radii (outlier-heavy), signed zeros and constant runs,
+alphabets beyond the 12-bit LUT fast path, and sizes off every block
+boundary.  Integer outputs bit-exact, reconstructions bitwise equal."""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2509_20563_b200 import encode as enc, predict as pr  # noqa: E402
+from paper_2509_20563_b200.core import Field, ResolvedBound  # noqa: E402
+from paper_2509_20563_b200.data import smooth_trig_host  # noqa: E402
+
+
+def _lorenzo_check(oracle, x, dims, e, radius=512):
+    lo, hi = float(x.min()), float(x.max())
+    codes, idx, vals, recon = oracle.lorenzo_quantize(x, dims, e, radius)
+    b = ResolvedBound(e, lo, hi)
+    q = pr.lorenzo_quantize(Field(dims, x), b, radius)
+    assert np.array_equal(q.codes, codes)
+    assert np.array_equal(q.outlier_indices, idx)
+    assert q.outlier_values.tobytes() == vals.tobytes()
+    assert pr.lorenzo_reconstruct(q, b).data.tobytes() == recon.tobytes()
+    return int(idx.size)
+
+
+# n2 % 4 == 0 throughout: these run the v7 wavefront (others fall back to v4)
+V7_SHAPES = [(8, 32, 64), (9, 33, 64), (17, 65, 100), (48, 96, 132), (33, 40, 36), (100, 20, 8), (5, 130, 44)]
+
+
+@pytest.mark.parametrize("dims", V7_SHAPES)
+def test_v7_lorenzo_shapes(oracle, dims):
+    x = smooth_trig_host(dims, sum(dims))
+    _lorenzo_check(oracle, x, dims, 1e-4 * float(x.max() - x.min()))
+
+
+@pytest.mark.parametrize("cfg", ["4x2", "2x2", "1x1", "1x2", "8x1", "4x1", "2x4", "8x2", "4x4", "4x3"])
+def test_v7_tile_configs(oracle, cfg, monkeypatch):
+    dims = (37, 70, 48)
+    monkeypatch.setenv("FZB_LZ_CFG", cfg)
+    x = smooth_trig_host(dims, 11)
+    _lorenzo_check(oracle, x, dims, 1e-3 * float(x.max() - x.min()))
+
+
+@pytest.mark.parametrize("radius", [1, 2, 8, 32768])
+def test_v7_outlier_heavy(oracle, radius):
+    dims = (20, 40, 52)
+    x = smooth_trig_host(dims, 5)
+    k = _lorenzo_check(oracle, x, dims, 1e-5 * float(x.max() - x.min()), radius)
+    if radius <= 8:
+        assert k > 0
+
+
+def test_v7_signed_zeros_and_constant_runs(oracle):
+    dims = (12, 40, 64)
+    rng = np.random.default_rng(3)
+    x = smooth_trig_host(dims, 2).reshape(dims)
+    x[:, :, 10:30] = 0.0
+    x[:, 5:9, :] = -0.0
+    x[3] = 1.25
+    x = x.reshape(-1).astype(np.float32)
+    x[rng.integers(0, x.size, 200)] *= -1
+    _lorenzo_check(oracle, x, dims, 1e-4 * float(x.max() - x.min()))
+
+
+def test_v7_2d(oracle):
+    dims = (130, 1000)
+    x = smooth_trig_host(dims, 9)
+    _lorenzo_check(oracle, x, dims, 1e-4 * float(x.max() - x.min()))
+
+
+@pytest.mark.parametrize("n", [1, 7, 255, 256, 257, 8191, 8192, 8193, 100_003, 1 << 20])
+def test_bitshuffle_sizes(oracle, n):
+    rng = np.random.default_rng(n)
+    codes = np.clip(np.round(rng.normal(512, 3, n)), 0, 1023).astype(np.uint32)
+    codes[rng.integers(0, n, max(1, n // 50))] = rng.integers(0, 1024, max(1, n // 50))
+    bm, pay = enc.bitshuffle_encode(codes, 512)
+    obm, opay = oracle.bitshuffle_encode(codes, 512)
+    assert bm == obm and pay == opay
+    assert np.array_equal(enc.bitshuffle_decode(bm, pay, n, 512), codes)
+
+
+@pytest.mark.parametrize("radius,spread", [(512, 1.0), (512, 60.0), (2048, 300.0), (4096, 900.0)])
+def test_huffman_alphabets(oracle, radius, spread):
+    # radius 4096 -> 8192 symbols: the 12-bit LUT holds one symbol per window
+    rng = np.random.default_rng(int(spread))
+    n = 200_001
+    codes = np.clip(np.round(rng.normal(radius, spread, n)), 0, 2 * radius - 1).astype(np.uint32)
+    h = enc.histogram_exact(codes, radius)
+    assert np.array_equal(h.bins, oracle.histogram(codes, radius))
+    cb, stream, bits = enc.huffman_encode(codes, h)
+    cl, ostream, obits = oracle.huffman_encode(codes, h.bins)
+    assert np.array_equal(cb.code_lengths, cl) and bits == obits and stream == ostream
+    assert np.array_equal(enc.huffman_decode(cb, stream, n), codes)
+
+
+def test_histogram_runs_and_tail(oracle):
+    n = 1_000_003   # not a multiple of 8
+    codes = np.full(n, 512, np.uint32)
+    codes[::97] = 3
+    codes[-5:] = 1023
+    h = enc.histogram_exact(codes, 512)
+    assert np.array_equal(h.bins, oracle.histogram(codes, 512))
