@@ -45,6 +45,9 @@ WORKLOADS = {
                dims=(1800, 3600), kind="trig", rel=1e-4),
     "c4": dict(name="FZMod-Default particle1d 280953867 (HACC-shaped) rel 1e-4", pipeline="default",
                dims=(280953867,), kind="particle", rel=1e-4),
+    # C5 shard: 64 fields over 8 GPUs = 8 per GPU, all in flight at once (compress_batch)
+    "c5": dict(name="C5 shard: 8 x smooth_trig 512x512x512 per GPU (FZMod-Speed, batched) rel 1e-3",
+               pipeline="speed", dims=(512, 512, 512), kind="trig", rel=1e-3, fields=8),
 }
 METRIC = "compress/decompress GB/s per GPU & per box at fixed rel eb; CR+PSNR vs CPU ref"
 
@@ -216,19 +219,33 @@ def run_ours(args, wl):
     dims = wl["dims"]
     n = int(np.prod(dims))
     spec = get_pipeline(wl["pipeline"])
-    x = _device_field(wl, seed=rank).contiguous()
+    F = int(wl.get("fields", 1))
+    if F > 1:
+        X = torch.stack([_device_field(wl, seed=rank * F + f) for f in range(F)]).contiguous()
+        x = X[0]
+    else:
+        x = _device_field(wl, seed=rank).contiguous()
     eng = default_engine()
     out = torch.empty(n, dtype=torch.float32, device=dev)
+    OUT = torch.empty(F, n, dtype=torch.float32, device=dev) if F > 1 else None
     ebs = ErrorBoundSpec(ErrorMode.VALUE_RANGE_RELATIVE, wl["rel"])
+    kw = dict(pipeline_id=spec.id, predictor=spec.predictor, codec=spec.primary_codec, radius=spec.radius())
 
     def device_step():
-        da = eng.compress(x, dims, 1, wl["rel"], pipeline_id=spec.id, predictor=spec.predictor,
-                          codec=spec.primary_codec, radius=spec.radius())
-        sz = eng.sizes(da)
-        eb_abs = wl["rel"] * (sz["hi"] - sz["lo"])
-        eng.decompress_resident(da, sz, eb_abs, out)
+        if F > 1:
+            das = eng.compress_batch(X, dims, 1, wl["rel"], **kw)
+            szs = eng.sizes_batch(das)
+            eng.decompress_batch_resident(das, szs, [wl["rel"] * (z["hi"] - z["lo"]) for z in szs], OUT)
+            nbytes = sum(eng.compressed_bytes(d, z) for d, z in zip(das, szs))
+            da, sz = das[0], szs[0]
+        else:
+            da = eng.compress(x, dims, 1, wl["rel"], **kw)
+            sz = eng.sizes(da)
+            eb_abs = wl["rel"] * (sz["hi"] - sz["lo"])
+            eng.decompress_resident(da, sz, eb_abs, out)
+            nbytes = eng.compressed_bytes(da, sz)
         if world > 1:
-            t = torch.tensor([eng.compressed_bytes(da, sz)], dtype=torch.int64, device=dev)
+            t = torch.tensor([nbytes], dtype=torch.int64, device=dev)
             g = [torch.empty_like(t) for _ in range(world)]
             dist.all_gather(g, t)
         return da, sz
@@ -246,7 +263,7 @@ def run_ours(args, wl):
     assert sz["status"] == 0, f"device status {sz['status']:#x}"
     comp_bytes = eng.compressed_bytes(da, sz)
     eb_abs = wl["rel"] * (sz["hi"] - sz["lo"])
-    maxerr = float((out.double() - x.double()).abs().max())
+    maxerr = float(((OUT[0] if F > 1 else out).double() - x.double()).abs().max())
     assert maxerr <= eb_abs, (maxerr, eb_abs)
 
     # ---- timed device-resident round trips (events on the engine stream)
@@ -266,22 +283,25 @@ def run_ours(args, wl):
     per_fn = {}
     for fn, e0, e1 in trace:
         per_fn.setdefault(fn, []).append(e0.elapsed_time(e1))
-    comp_ms = sum(np.mean(v) for k, v in per_fn.items() if k in (
-        "fzb_minmax_f32", "fzb_resolve_bound", "fzb_lorenzo_encode_f32", "fzb_interp_encode_f32",
+    comp_ms = sum(np.sum(v) / args.steps for k, v in per_fn.items() if k in (
+        "fzb_minmax_f32", "fzb_resolve_bound", "fzb_lorenzo_encode_f32", "fzb_lorenzo_encode_batch_f32",
+        "fzb_interp_encode_f32",
         "fzb_outlier_compact", "fzb_histogram", "fzb_huffman_build", "fzb_huffman_encode", "fzb_bitshuffle_encode",
         "fzb_fill_u16"))
-    dec_ms = sum(np.mean(v) for k, v in per_fn.items() if k in (
+    dec_ms = sum(np.sum(v) / args.steps for k, v in per_fn.items() if k in (
         "fzb_huffman_decode", "fzb_bitshuffle_decode", "fzb_outlier_scatter", "fzb_lorenzo_decode_f32",
+        "fzb_lorenzo_decode_batch_f32",
         "fzb_interp_decode_f32"))
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
-    value = world * 4 * n / (ms_max / 1e3) / 1e9
+    value = world * F * 4 * n / (ms_max / 1e3) / 1e9
 
     # ---- roofline of the dominant kernel
     peak, peak_kind = _peaks()
     algo = {"fzb_lorenzo_encode_f32": 6 * n, "fzb_lorenzo_decode_f32": 6 * n + n // 8,
+            "fzb_lorenzo_encode_batch_f32": F * 6 * n, "fzb_lorenzo_decode_batch_f32": F * (6 * n + n // 8),
             "fzb_bitshuffle_encode": 2 * n + n // 16 + 4 * (sz["size"] if spec.primary_codec == "bitshuffle" else 0),
             "fzb_bitshuffle_decode": 2 * n + n // 16 + 4 * (sz["size"] if spec.primary_codec == "bitshuffle" else 0),
             "fzb_huffman_encode": 2 * n + (sz["size"] + 7) // 8, "fzb_huffman_decode": 2 * n + (sz["size"] + 7) // 8,
@@ -304,25 +324,36 @@ def run_ours(args, wl):
                 "stage_ms": {k.replace("fzb_", ""): round(float(np.mean(v)), 4) for k, v in per_fn.items()}}
 
     # ---- e2e through the public API from pinned host memory
-    xh = torch.empty(n, dtype=torch.float32, pin_memory=True)
-    xh.copy_(x)
-    field = Field(dims, xh.numpy())
-    for _ in range(2):
+    hosts = []
+    for f in range(F):
+        xh = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        xh.copy_(X[f] if F > 1 else x)
+        hosts.append(Field(dims, xh.numpy()))
+    field = hosts[0]
+
+    def e2e_step():
+        if F > 1:
+            arcs = fz.compress_batch(hosts, ebs, wl["pipeline"])
+            recs = fz.decompress_batch(arcs)
+            return arcs[0], recs[0], arcs
         a = fz.compress(field, ebs, wl["pipeline"])
-        r = fz.decompress(a)
+        return a, fz.decompress(a), [a]
+
+    for _ in range(2):
+        a, r, arcs = e2e_step()
     barrier()
     e2e_times = []
     for _ in range(max(1, min(args.steps, 5))):
         s0 = time.perf_counter()
-        a = fz.compress(field, ebs, wl["pipeline"])
-        r = fz.decompress(a)
+        a, r, arcs = e2e_step()
         e2e_times.append(time.perf_counter() - s0)
     e2e_s = torch.tensor([float(np.mean(e2e_times))], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-    e2e = world * 4 * n / float(e2e_s.item()) / 1e9
+    e2e = world * F * 4 * n / float(e2e_s.item()) / 1e9
     archive_bytes = len(fz.serialize_archive(a))
     assert archive_bytes == comp_bytes, (archive_bytes, comp_bytes)
+    e2e_comp = sum(len(fz.serialize_archive(q)) for q in arcs)
     q = quality_arrays(field.data, r.data, a.resolved_bound().eb_abs)
     assert q.bound_satisfied
 
@@ -330,14 +361,14 @@ def run_ours(args, wl):
             "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32 data, f64 predictor arithmetic", "data": "synthetic",
             "config": {"workload": wl["name"], "pipeline": wl["pipeline"], "dims": list(dims), "rel_eb": wl["rel"],
-                       "fields_per_gpu": 1, "l2": "working set (805 MB) > 126 MB L2, no flush needed",
+                       "fields_per_gpu": F, "l2": "working set (805 MB per field) > 126 MB L2, no flush needed",
                        "parallelism": f"whole-field shard x{world}"},
             "compress_gbs": round(4 * n / (comp_ms / 1e3) / 1e9, 3) if comp_ms else None,
             "decompress_gbs": round(4 * n / (dec_ms / 1e3) / 1e9, 3) if dec_ms else None,
             "cr": round(4 * n / comp_bytes, 4), "psnr_db": round(q.psnr_db, 4), "max_abs_err": q.max_abs_err,
             "eb_abs": a.resolved_bound().eb_abs,
-            "e2e": {"value": round(e2e, 3), "unit": "GB/s", "h2d_bytes_per_step": 4 * n + comp_bytes,
-                    "d2h_bytes_per_step": 4 * n + comp_bytes},
+            "e2e": {"value": round(e2e, 3), "unit": "GB/s", "h2d_bytes_per_step": F * 4 * n + e2e_comp,
+                    "d2h_bytes_per_step": F * 4 * n + e2e_comp},
             "roofline": roofline, "gpu_launches": launches, "clocks": clk.summary()}
     if rank == 0 and world == 1 and not args.no_cpu:
         xs = x.cpu().numpy()

@@ -59,6 +59,21 @@ FZB_API int fzb_lorenzo_decode_f32(const uint16_t *d_codes, const uint32_t *d_bi
                                    uint32_t n1, uint32_t n2, const double *d_eb, uint32_t radius, void *d_ws,
                                    size_t ws_bytes, void *stream);
 
+/* Batches of nf same-shaped fields in one wavefront launch (fields
+ * in flight per GPU).  Field f: d_in/d_codes/d_recon + f * field_stride
+ * elements, d_bitmap + f * bitmap_stride_words, bound d_eb[f].  Same outputs
+ * as nf single-field calls; the workspace rules above apply. */
+FZB_API size_t fzb_lorenzo_batch_workspace_bytes(uint32_t nf, uint32_t n0, uint32_t n1, uint32_t n2);
+FZB_API int fzb_lorenzo_encode_batch_f32(const float *d_in, uint32_t nf, uint64_t field_stride, uint32_t n0,
+                                         uint32_t n1, uint32_t n2, const double *d_eb, uint32_t radius,
+                                         uint16_t *d_codes, uint32_t *d_bitmap, uint64_t bitmap_stride_words,
+                                         void *d_ws, size_t ws_bytes, void *stream);
+FZB_API int fzb_lorenzo_decode_batch_f32(const uint16_t *d_codes, const uint32_t *d_bitmap,
+                                         uint64_t bitmap_stride_words, float *d_recon, uint32_t nf,
+                                         uint64_t field_stride, uint32_t n0, uint32_t n1, uint32_t n2,
+                                         const double *d_eb, uint32_t radius, void *d_ws, size_t ws_bytes,
+                                         void *stream);
+
 /* ---- a5-a6: G-Interp (predict.py:147-201, 270-344) ---------------------- */
 /* d_recon: f32[n] workspace (encode) / output (decode); d_anchors f32[prod((d-1)/stride+1)]. */
 FZB_API int fzb_interp_encode_f32(const float *d_in, uint32_t n0, uint32_t n1, uint32_t n2, const double *d_eb,

@@ -14,9 +14,9 @@ from .core import (  # noqa: F401
 from .errors import FZError  # noqa: F401
 from .metrics import QualityReport, RateReport, quality, rate  # noqa: F401
 from .pipeline import (  # noqa: F401
-    PipelineSpec, StageKind, StageSpec, compress, compress_device, compress_via_graph, compress_with_timing,
-    decompress, decompress_device, decompress_via_graph, decompress_with_timing, get_pipeline, load_pipeline_file,
-    register_pipeline, registered_pipelines,
+    PipelineSpec, StageKind, StageSpec, compress, compress_batch, compress_device, compress_via_graph,
+    compress_with_timing, decompress, decompress_batch, decompress_device, decompress_via_graph,
+    decompress_with_timing, get_pipeline, load_pipeline_file, register_pipeline, registered_pipelines,
 )
 
 __version__ = "0.1.0"

@@ -74,6 +74,9 @@ def load():
         "fzb_lorenzo_workspace_bytes": (SZ, [U32, U32, U32]),
         "fzb_lorenzo_encode_f32": (I, [P, U32, U32, U32, P, U32, P, P, P, SZ, P]),
         "fzb_lorenzo_decode_f32": (I, [P, P, P, U32, U32, U32, P, U32, P, SZ, P]),
+        "fzb_lorenzo_batch_workspace_bytes": (SZ, [U32, U32, U32, U32]),
+        "fzb_lorenzo_encode_batch_f32": (I, [P, U32, U64, U32, U32, U32, P, U32, P, P, U64, P, SZ, P]),
+        "fzb_lorenzo_decode_batch_f32": (I, [P, P, U64, P, U32, U64, U32, U32, U32, P, U32, P, SZ, P]),
         "fzb_interp_encode_f32": (I, [P, U32, U32, U32, P, U32, U32, P, P, P, P, P, P]),
         "fzb_interp_decode_f32": (I, [P, P, P, P, U32, U32, U32, P, U32, U32, P, P]),
         "fzb_outlier_workspace_bytes": (SZ, [U64]),
@@ -101,7 +104,9 @@ def load():
 
 EXPORTED = [
     "fzb_abi_version", "fzb_minmax_workspace_bytes", "fzb_minmax_f32", "fzb_resolve_bound",
-    "fzb_lorenzo_workspace_bytes", "fzb_lorenzo_encode_f32", "fzb_lorenzo_decode_f32", "fzb_interp_encode_f32",
+    "fzb_lorenzo_workspace_bytes", "fzb_lorenzo_encode_f32", "fzb_lorenzo_decode_f32",
+    "fzb_lorenzo_batch_workspace_bytes", "fzb_lorenzo_encode_batch_f32", "fzb_lorenzo_decode_batch_f32",
+    "fzb_interp_encode_f32",
     "fzb_interp_decode_f32", "fzb_outlier_workspace_bytes", "fzb_outlier_compact", "fzb_outlier_scatter",
     "fzb_histogram", "fzb_huffman_build_workspace_bytes", "fzb_huffman_build", "fzb_huffman_encode_workspace_bytes",
     "fzb_huffman_encode", "fzb_huffman_decode_workspace_bytes", "fzb_huffman_decode",

@@ -913,13 +913,16 @@ lz_wave4_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ cod
 // (a topological order: both predecessors have strictly smaller keys), so
 // resident CTAs are the ones closest to runnable.  Counting sort, one CTA.
 __global__ void tile_order_kernel(int nA, int nB, int lagI, int lagJ, int* __restrict__ counts,
-                                  int* __restrict__ order) {
+                                  int* __restrict__ order, int nf = 1) {
+    // nf fields of nA x nB tiles: tile t of field f has id f*nA*nB + t and the
+    // key of its field-local (A, B), so equal keys interleave the fields
     __shared__ uint32_t tmp[33];
-    const int ntile = nA * nB;
+    const int nt1 = nA * nB, ntile = nt1 * nf;
     const int K = lagI * (nA - 1) + lagJ * (nB - 1) + 1;
+    auto key = [&](int t) { const int l = t % nt1; return lagI * (l / nB) + lagJ * (l % nB); };
     for (int q = threadIdx.x; q < K; q += blockDim.x) counts[q] = 0;
     __syncthreads();
-    for (int t = threadIdx.x; t < ntile; t += blockDim.x) atomicAdd(&counts[lagI * (t / nB) + lagJ * (t % nB)], 1);
+    for (int t = threadIdx.x; t < ntile; t += blockDim.x) atomicAdd(&counts[key(t)], 1);
     __syncthreads();
     uint32_t carry = 0;
     for (int q0 = 0; q0 < K; q0 += blockDim.x) {
@@ -932,7 +935,7 @@ __global__ void tile_order_kernel(int nA, int nB, int lagI, int lagJ, int* __res
     }
     __syncthreads();
     for (int t = threadIdx.x; t < ntile; t += blockDim.x) {
-        const int pos = atomicAdd(&counts[lagI * (t / nB) + lagJ * (t % nB)], 1);
+        const int pos = atomicAdd(&counts[key(t)], 1);
         order[pos] = t;
     }
 }
@@ -1513,6 +1516,32 @@ int launch_v7(const float* orig, const uint16_t* codes_in, uint16_t* codes_out, 
     return FZB_E_ARG;
 }
 
+template <bool DEC>
+int launch_v7_batch(const float* orig, const uint16_t* codes_in, uint16_t* codes_out, uint32_t* bitmap, float* recon,
+                    uint32_t n0, uint32_t n1, uint32_t n2, const double* d_eb, int radius, void* ws, size_t ws_bytes,
+                    cudaStream_t st, int nf, long long fstride, long long bstride) {
+    const Cfg7 c = pick7(n0);
+#define FZB_LZ7_BCASE(W_, R_)                                                                                      \
+    if (c.W == W_ && c.R == R_)                                                                                     \
+        return v6::launch7<W_, R_, DEC>(orig, codes_in, codes_out, bitmap, recon, n0, n1, n2, d_eb, radius, ws,     \
+                                        ws_bytes, st, nf, fstride, bstride);
+    FZB_LZ7_CFGS(FZB_LZ7_BCASE)
+#undef FZB_LZ7_BCASE
+    return FZB_E_ARG;
+}
+
+size_t v7_ws_batch(uint32_t nf, uint32_t n0, uint32_t n1, uint32_t n2) {
+    const Cfg7 c = pick7(n0);
+    switch (c.W * c.R) {
+        case 1: return v6::WS7<1>(n0, n1, n2, nf).total;
+        case 2: return v6::WS7<2>(n0, n1, n2, nf).total;
+        case 4: return v6::WS7<4>(n0, n1, n2, nf).total;
+        case 8: return v6::WS7<8>(n0, n1, n2, nf).total;
+        case 12: return v6::WS7<12>(n0, n1, n2, nf).total;
+        default: return v6::WS7<16>(n0, n1, n2, nf).total;
+    }
+}
+
 size_t v7_ws(uint32_t n0, uint32_t n1, uint32_t n2) {
     // enough for every configuration pick7 may return (tuning overrides included)
     size_t m = 0;
@@ -1645,5 +1674,64 @@ FZB_API int fzb_debug_walk_timing(long long* host_out) {
     return (int)cudaMemcpyFromSymbol(host_out, g_walk_stamp, sizeof(g_walk_stamp));
 }
 #endif
+
+// ---- batches of same-shaped fields (several fields in flight per
+// GPU).  One wavefront launch interleaves the tiles of all fields in one
+// ticket order, so the GPU idles less than with one field at a time.  Field
+// f lives at d_in + f * field_stride (codes / recon likewise) with its
+// bitmap at d_bitmap + f * bitmap_stride_words and its bound at d_eb[f].
+// Shapes the v7 wavefront does not take (1D, n2 % 4 != 0) run field by field.
+FZB_API size_t fzb_lorenzo_batch_workspace_bytes(uint32_t nf, uint32_t n0, uint32_t n1, uint32_t n2) {
+    const size_t one = fzb_lorenzo_workspace_bytes(n0, n1, n2);
+    canon(n0, n1, n2);
+    if (nf <= 1 || (n0 == 1 && n1 == 1) || use_v4(n2)) return one;
+    const size_t b = v7_ws_batch(nf, n0, n1, n2);
+    return b > one ? b : one;
+}
+
+FZB_API int fzb_lorenzo_encode_batch_f32(const float* d_in, uint32_t nf, uint64_t field_stride, uint32_t n0,
+                                         uint32_t n1, uint32_t n2, const double* d_eb, uint32_t radius,
+                                         uint16_t* d_codes, uint32_t* d_bitmap, uint64_t bitmap_stride_words,
+                                         void* d_ws, size_t ws_bytes, void* stream) {
+    if (radius == 0 || radius > 32768) return FZB_E_RADIUS;
+    uint32_t c0 = n0, c1 = n1, c2 = n2;
+    canon(c0, c1, c2);
+    if (nf == 0 || (long long)c0 * c1 * c2 == 0) return 0;
+    if (nf == 1 || (c0 == 1 && c1 == 1) || use_v4(c2)) {
+        for (uint32_t f = 0; f < nf; f++) {
+            const int rc = fzb_lorenzo_encode_f32(d_in + f * field_stride, n0, n1, n2, d_eb + f, radius,
+                                                  d_codes + f * field_stride, d_bitmap + f * bitmap_stride_words, d_ws,
+                                                  ws_bytes, stream);
+            if (rc) return rc;
+        }
+        return 0;
+    }
+    return launch_v7_batch<false>(d_in, nullptr, d_codes, d_bitmap, nullptr, c0, c1, c2, d_eb, (int)radius, d_ws,
+                                  ws_bytes, (cudaStream_t)stream, (int)nf, (long long)field_stride,
+                                  (long long)bitmap_stride_words);
+}
+
+FZB_API int fzb_lorenzo_decode_batch_f32(const uint16_t* d_codes, const uint32_t* d_bitmap,
+                                         uint64_t bitmap_stride_words, float* d_recon, uint32_t nf,
+                                         uint64_t field_stride, uint32_t n0, uint32_t n1, uint32_t n2,
+                                         const double* d_eb, uint32_t radius, void* d_ws, size_t ws_bytes,
+                                         void* stream) {
+    if (radius == 0 || radius > 32768) return FZB_E_RADIUS;
+    uint32_t c0 = n0, c1 = n1, c2 = n2;
+    canon(c0, c1, c2);
+    if (nf == 0 || (long long)c0 * c1 * c2 == 0) return 0;
+    if (nf == 1 || (c0 == 1 && c1 == 1) || use_v4(c2)) {
+        for (uint32_t f = 0; f < nf; f++) {
+            const int rc = fzb_lorenzo_decode_f32(d_codes + f * field_stride, d_bitmap + f * bitmap_stride_words,
+                                                  d_recon + f * field_stride, n0, n1, n2, d_eb + f, radius, d_ws,
+                                                  ws_bytes, stream);
+            if (rc) return rc;
+        }
+        return 0;
+    }
+    return launch_v7_batch<true>(nullptr, d_codes, nullptr, const_cast<uint32_t*>(d_bitmap), d_recon, c0, c1, c2, d_eb,
+                                 (int)radius, d_ws, ws_bytes, (cudaStream_t)stream, (int)nf, (long long)field_stride,
+                                 (long long)bitmap_stride_words);
+}
 
 }  // extern "C"

@@ -51,7 +51,10 @@ constexpr int OFF = 2;      // element k = s - OFF - r - b at step s: every halo
 
 struct Geo6 {
     int n0, n1, n2, nA, nB, S;
-    int vec;  // n2 % 4 == 0: 16-byte staging / flush
+    int vec;             // n2 % 4 == 0: 16-byte staging / flush
+    int nt1;             // tiles per field (batched launches: global tile id T = field * nt1 + tile)
+    long long fstride;   // elements between consecutive fields
+    long long bstride;   // bitmap words between consecutive fields
 };
 
 
@@ -380,7 +383,16 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
     if (tid == 0) flags[0] = (uint32_t)order[atomicAdd(ticket, 1u)];
     if (tid < W + 2) flags[1 + tid] = 0;
     __syncthreads();
-    const int tile = (int)flags[0];
+    // global tile id -> (field, tile): faces are indexed by the global id (the
+    // neighbours a tile reads never cross a field), data by the field offset
+    const int T = (int)flags[0];
+    const int fld = T / geo.nt1, tile = T % geo.nt1;
+    orig += (size_t)fld * geo.fstride;
+    codes_in += (size_t)fld * geo.fstride;
+    codes_out += (size_t)fld * geo.fstride;
+    recon += (size_t)fld * geo.fstride;
+    bitmap += (size_t)fld * geo.bstride;
+    d_eb += fld;
     const int nB = geo.nB, S = geo.S;
     const int A = tile / nB, B = tile % nB;
     const int i0 = A * PI, j0 = B * 32;
@@ -392,7 +404,7 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
         // Group jg's ring slots (steps 8jg-32..) are free once every warp finished group jg-3.
         for (int jg = 0; jg < NGRP; jg++) {
             if (jg >= 3) wait_min(done, W, (uint32_t)(jg - 2));
-            helper_halo<PI>(jg, HU, HL, faceI, faceJ, tile, A, B, nB, S, epoch, lane);
+            helper_halo<PI>(jg, HU, HL, faceI, faceJ, T, A, B, nB, S, epoch, lane);
             __syncwarp();
             if (lane == 0) st_rel_cta(hready, (uint32_t)(jg + 1));
         }
@@ -423,9 +435,9 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
     uint64_t* ghost_dst = GR + (size_t)(w < W - 1 ? w : W - 1) * GRD * 32 + b;
     const int gmask = polled ? GRD - 1 : HR - 1;   // ghost source ring depth
     const bool pubI = (w == W - 1) && (A < geo.nA - 1);
-    uint64_t* fI = faceI + (size_t)tile * S * 32 + b;
+    uint64_t* fI = faceI + (size_t)T * S * 32 + b;
     const bool pubJ = (B < nB - 1) && (b == 31);
-    uint64_t* fJ = faceJ + (size_t)tile * S * PI + w * R;
+    uint64_t* fJ = faceJ + (size_t)T * S * PI + w * R;
     const bool l0 = (b == 0);
     const uint64_t* hlw = HL + w * R;   // + slot*(PI+1): entries x = 0..R (row w*R-1+x)
     uint32_t* ringl = ring + (w * R * 32 + b) * IP;
@@ -608,9 +620,9 @@ __global__ void lz7_prep_kernel(uint32_t* hdr) {
 template <int PI>
 struct WS7 {
     size_t ntile, S, K, off_order, off_counts, off_fI, off_fJ, total;
-    WS7(int n0, int n1, int n2) {
+    WS7(int n0, int n1, int n2, int nf = 1) {
         const size_t nA = (n0 + PI - 1) / PI, nB = (n1 + 31) / 32;
-        ntile = nA * nB;
+        ntile = nA * nB * (size_t)nf;   // all fields of a batch
         // last element: k = n2-1 at a + b = PI + 30; whole groups (the compute warps run them)
         S = ((size_t)n2 + PI + 30 + OFF + G - 1) / G * G;
         K = (size_t)(PI + 8) * (nA - 1) + (size_t)(32 + 8) * (nB - 1) + 1;
@@ -625,9 +637,10 @@ struct WS7 {
 
 template <int W, int R, bool DEC>
 int launch7(const float* orig, const uint16_t* codes_in, uint16_t* codes_out, uint32_t* bitmap, float* recon, int n0,
-            int n1, int n2, const double* d_eb, int radius, void* ws, size_t ws_bytes, cudaStream_t st) {
+            int n1, int n2, const double* d_eb, int radius, void* ws, size_t ws_bytes, cudaStream_t st, int nf = 1,
+            long long fstride = 0, long long bstride = 0) {
     constexpr int PI = W * R;
-    WS7<PI> L(n0, n1, n2);
+    WS7<PI> L(n0, n1, n2, nf);
     if (ws_bytes < L.total) return FZB_E_WORKSPACE;
     Geo6 g;
     g.n0 = n0; g.n1 = n1; g.n2 = n2;
@@ -635,6 +648,9 @@ int launch7(const float* orig, const uint16_t* codes_in, uint16_t* codes_out, ui
     g.nB = (n1 + 31) / 32;
     g.S = (int)L.S;
     g.vec = (n2 % 4 == 0) ? 1 : 0;
+    g.nt1 = g.nA * g.nB;
+    g.fstride = fstride;
+    g.bstride = bstride;
     unsigned char* w = static_cast<unsigned char*>(ws);
     uint32_t* hdr = reinterpret_cast<uint32_t*>(w);
     int* order = reinterpret_cast<int*>(w + L.off_order);
@@ -642,7 +658,7 @@ int launch7(const float* orig, const uint16_t* codes_in, uint16_t* codes_out, ui
     uint64_t* faceI = reinterpret_cast<uint64_t*>(w + L.off_fI);
     uint64_t* faceJ = reinterpret_cast<uint64_t*>(w + L.off_fJ);
     lz7_prep_kernel<<<1, 1, 0, st>>>(hdr);
-    tile_order_kernel<<<1, 1024, 0, st>>>(g.nA, g.nB, PI + 8, 32 + 8, counts, order);
+    tile_order_kernel<<<1, 1024, 0, st>>>(g.nA, g.nB, PI + 8, 32 + 8, counts, order, nf);
     const size_t smem = Smem7<W, R, DEC>::bytes;
     auto kfn = lz7_kernel<W, R, DEC>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

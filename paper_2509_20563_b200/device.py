@@ -169,8 +169,12 @@ class Engine:
     # ----------------------------------------------------------- compress
     def compress(self, x: torch.Tensor, dims, eb_mode: int, magnitude: float, *, pipeline_id: int = 0,
                  predictor: str = "lorenzo", codec: str = "huffman", radius: int = 512,
-                 anchor_stride: int = 16) -> DeviceArchive:
-        """Enqueue the whole compression of a device-resident f32 field."""
+                 anchor_stride: int = 16, tag: str = "", pre: dict | None = None) -> DeviceArchive:
+        """Enqueue the whole compression of a device-resident f32 field.
+
+        `tag` suffixes every cached buffer (several fields alive at once);
+        `pre` = {status, lohi, eb, codes, bitmap} skips the bound and
+        predictor stages (compress_batch ran them for a whole batch)."""
 
         if x.device.type != "cuda" or x.dtype != torch.float32 or not x.is_contiguous():
             raise ValueError("Engine.compress needs a contiguous float32 CUDA tensor")
@@ -182,62 +186,67 @@ class Engine:
             raise E.RadiusTooLarge(f"radius {radius} outside the 16-bit code range of the device path")
         n0, n1, n2 = pad3(dims)
         L, sp = self.lib, self.sp
-        status = self.buf("status", 8, zero=True)
-        lohi = self.buf("lohi", 8)
-        eb = self.buf("eb", 8)
-        mmws = self.buf("mmws", L.fzb_minmax_workspace_bytes(n))
-        self._call("fzb_minmax_f32", _p(x), n, _p(lohi), _p(mmws), mmws.numel(), _p(status), sp, nk=2)
-        self._call("fzb_resolve_bound", _p(lohi), int(eb_mode), float(magnitude), _p(eb), sp)
-        codes = self.buf("codes", 2 * n + 16)
-        bitmap = self.buf("bitmap", 4 * ((n + 31) // 32), zero=True)
-        use_anchors = predictor == "interp" and interp_applicable(dims, anchor_stride)
-        bufs = dict(status=status, lohi=lohi, eb=eb, codes=codes)
         if predictor not in ("lorenzo", "interp"):
             raise ValueError(f"unknown predictor '{predictor}'")
-        if use_anchors:
+        use_anchors = predictor == "interp" and interp_applicable(dims, anchor_stride)
+        if pre is None:
+            status = self.buf("status" + tag, 8, zero=True)
+            lohi = self.buf("lohi" + tag, 8)
+            eb = self.buf("eb" + tag, 8)
+            mmws = self.buf("mmws" + tag, L.fzb_minmax_workspace_bytes(n))
+            self._call("fzb_minmax_f32", _p(x), n, _p(lohi), _p(mmws), mmws.numel(), _p(status), sp, nk=2)
+            self._call("fzb_resolve_bound", _p(lohi), int(eb_mode), float(magnitude), _p(eb), sp)
+            codes = self.buf("codes" + tag, 2 * n + 16)
+            bitmap = self.buf("bitmap" + tag, 4 * ((n + 31) // 32), zero=True)
+        else:
+            status, lohi, eb, codes, bitmap = (pre[k] for k in ("status", "lohi", "eb", "codes", "bitmap"))
+        bufs = dict(status=status, lohi=lohi, eb=eb, codes=codes)
+        if pre is not None:
+            pass
+        elif use_anchors:
             self._call("fzb_fill_u16", _p(codes), n, radius, sp)
-            recon = self.buf("recon_ws", 4 * n)
+            recon = self.buf("recon_ws" + tag, 4 * n)
             a = anchor_stride
             na = ((n0 - 1) // a + 1) * ((n1 - 1) // a + 1) * ((n2 - 1) // a + 1)
-            anchors = self.buf("anchors", 4 * na)
+            anchors = self.buf("anchors" + tag, 4 * na)
             w = (ctypes.c_double * 4)(*CUBIC)
             self._call("fzb_interp_encode_f32", _p(x), n0, n1, n2, _p(eb), radius, a, w, _p(codes), _p(recon),
                        _p(bitmap), _p(anchors), sp, nk=1 + 3 * int(np.log2(a)))
             bufs["anchors"] = anchors
             bufs["n_anchors"] = na
         else:
-            lzws = self.buf("lzws", L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
+            lzws = self.buf("lzws" + tag, L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
             self._call("fzb_lorenzo_encode_f32", _p(x), n0, n1, n2, _p(eb), radius, _p(codes), _p(bitmap),
                        _p(lzws), lzws.numel(), sp, nk=2)
-        oidx = self.buf("oidx", 8 * n)
-        oval = self.buf("oval", 4 * n)
-        ocount = self.buf("ocount", 8)
-        ocws = self.buf("ocws", L.fzb_outlier_workspace_bytes(n))
+        oidx = self.buf("oidx" + tag, 8 * n)
+        oval = self.buf("oval" + tag, 4 * n)
+        ocount = self.buf("ocount" + tag, 8)
+        ocws = self.buf("ocws" + tag, L.fzb_outlier_workspace_bytes(n))
         self._call("fzb_outlier_compact", _p(bitmap), n, _p(x), _p(oidx), _p(oval), _p(ocount), _p(ocws),
                    ocws.numel(), sp, nk=3)
         bufs.update(oidx=oidx, oval=oval, ocount=ocount)
         nsym = 2 * radius
         if codec == "huffman":
-            bins = self.buf("bins", 8 * nsym)
+            bins = self.buf("bins" + tag, 8 * nsym)
             self._call("fzb_histogram", _p(codes), n, nsym, _p(bins), _p(status), sp)
-            lengths = self.buf("lengths", nsym)
-            cw = self.buf("cw", 4 * nsym)
-            bitcount = self.buf("bitcount", 8)
-            bws = self.buf("hbws", L.fzb_huffman_build_workspace_bytes(nsym))
+            lengths = self.buf("lengths" + tag, nsym)
+            cw = self.buf("cw" + tag, 4 * nsym)
+            bitcount = self.buf("bitcount" + tag, 8)
+            bws = self.buf("hbws" + tag, L.fzb_huffman_build_workspace_bytes(nsym))
             self._call("fzb_huffman_build", _p(bins), nsym, _p(lengths), _p(cw), _p(bitcount), _p(bws), bws.numel(),
                        sp)
             cap = 4 * n + 16
-            out = self.buf("hfout", cap)
-            hws = self.buf("hews", L.fzb_huffman_encode_workspace_bytes(n))
+            out = self.buf("hfout" + tag, cap)
+            hws = self.buf("hews" + tag, L.fzb_huffman_encode_workspace_bytes(n))
             self._call("fzb_huffman_encode", _p(codes), n, _p(lengths), _p(cw), nsym, _p(bitcount), _p(out), cap,
                        _p(hws), hws.numel(), _p(status), sp, nk=5)
             bufs.update(lengths=lengths, bitcount=bitcount, hfout=out)
         elif codec == "bitshuffle":
             nb = (n + 255) // 256
-            bsmap = self.buf("bsmap", 16 * nb)
-            pay = self.buf("bspay", 512 * nb)
-            nwords = self.buf("nwords", 8)
-            bws = self.buf("bsws", L.fzb_bitshuffle_workspace_bytes(n))
+            bsmap = self.buf("bsmap" + tag, 16 * nb)
+            pay = self.buf("bspay" + tag, 512 * nb)
+            nwords = self.buf("nwords" + tag, 8)
+            bws = self.buf("bsws" + tag, L.fzb_bitshuffle_workspace_bytes(n))
             self._call("fzb_bitshuffle_encode", _p(codes), n, _p(bsmap), _p(pay), _p(nwords), _p(bws), bws.numel(),
                        sp, nk=3)
             bufs.update(bsmap=bsmap, bspay=pay, nwords=nwords)
@@ -330,48 +339,139 @@ class Engine:
             body += 16 * ((da.n + 255) // 256) + 4 * sz["size"]
         return 41 + 9 * nseg + body
 
-    def decompress_resident(self, da: DeviceArchive, sz: dict, eb_abs: float, out: torch.Tensor) -> torch.Tensor:
+    def decompress_resident(self, da: DeviceArchive, sz: dict, eb_abs: float, out: torch.Tensor, tag: str = "",
+                            batch: dict | None = None) -> torch.Tensor:
         """Decode straight from the device-resident segments of `da` (no H2D):
-        the device half of the round trip measured by bench.py."""
+        the device half of the round trip measured by bench.py.  With `batch`
+        = {codes, bitmap} views the codes/flags land there and the predictor
+        inverse is left to decompress_batch_resident (one batched launch)."""
         L, sp, b, n = self.lib, self.sp, da.bufs, da.n
-        status = self.buf("dstatus", 8, zero=True)
-        codes = self.buf("dcodes", 2 * n + 16)
+        status = self.buf("dstatus" + tag, 8, zero=True)
+        codes = self.buf("dcodes" + tag, 2 * n + 16) if batch is None else batch["codes"]
         nsym = 2 * da.radius
         if da.codec == "huffman":
             nbytes = (sz["size"] + 7) // 8
-            hws = self.buf("hdws", L.fzb_huffman_decode_workspace_bytes(nbytes, nsym))
+            hws = self.buf("hdws" + tag, L.fzb_huffman_decode_workspace_bytes(nbytes, nsym))
             self._call("fzb_huffman_decode", _p(b["hfout"]), nbytes, n, _p(b["lengths"]), nsym, _p(codes), _p(hws),
                        hws.numel(), _p(status), sp, nk=10)
         else:
-            bws = self.buf("dbsws", L.fzb_bitshuffle_workspace_bytes(n))
+            bws = self.buf("dbsws" + tag, L.fzb_bitshuffle_workspace_bytes(n))
             self._call("fzb_bitshuffle_decode", _p(b["bsmap"]), _p(b["bspay"]), sz["size"], n, da.radius, _p(codes),
                        _p(bws), bws.numel(), _p(status), sp, nk=4)
         n0, n1, n2 = pad3(da.dims)
-        bitmap = self.buf("dbitmap", 4 * ((n + 31) // 32), zero=True)
-        ebt = self.buf("deb_res", 8)
+        if batch is None:
+            bitmap = self.buf("dbitmap" + tag, 4 * ((n + 31) // 32), zero=True)
+        else:
+            bitmap = batch["bitmap"]
+        ebt = self.buf("deb_res" + tag, 8)
         with torch.cuda.stream(self.stream):
             ebt[:8].view(torch.float64).fill_(eb_abs)
         if sz["k"]:
             self._call("fzb_outlier_scatter", _p(b["oidx"]), _p(b["oval"]), sz["k"], n, _p(codes), da.radius,
                        _p(out), _p(bitmap), _p(status), sp)
+        if batch is not None:
+            return out
         if da.use_anchors:
             w = (ctypes.c_double * 4)(*CUBIC)
             self._call("fzb_interp_decode_f32", _p(codes), _p(bitmap), _p(b["anchors"]), _p(out), n0, n1, n2, _p(ebt),
                        da.radius, 16, w, sp, nk=13)
         else:
-            lzws = self.buf("dlzws", L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
+            lzws = self.buf("dlzws" + tag, L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
             self._call("fzb_lorenzo_decode_f32", _p(codes), _p(bitmap), _p(out), n0, n1, n2, _p(ebt), da.radius,
                        _p(lzws), lzws.numel(), sp, nk=5)
         return out
 
+    # ------------------------------------------------------------- batches
+    def compress_batch(self, X: torch.Tensor, dims, eb_mode: int, magnitude: float, *, pipeline_id: int = 0,
+                       predictor: str = "lorenzo", codec: str = "huffman", radius: int = 512) -> list:
+        """F same-shaped device fields (X: [F, n] contiguous f32) -> F DeviceArchives.
+        Bounds per field, ONE batched Lorenzo wavefront for all fields (their
+        tiles interleave), then each field's outliers and codec."""
+        F, n = int(X.shape[0]), int(X.shape[1])
+        if predictor != "lorenzo":
+            return [self.compress(X[f], dims, eb_mode, magnitude, pipeline_id=pipeline_id, predictor=predictor,
+                                  codec=codec, radius=radius, tag=f"#{f}") for f in range(F)]
+        L, sp = self.lib, self.sp
+        n0, n1, n2 = pad3(dims)
+        nw = (n + 31) // 32
+        ebs = self.buf("b_eb", 8 * F)
+        codes = self.buf("b_codes", 2 * F * n + 16)
+        bitmap = self.buf("b_bitmap", 4 * F * nw, zero=True)
+        pres = []
+        for f in range(F):
+            tag = f"#{f}"
+            status = self.buf("status" + tag, 8, zero=True)
+            lohi = self.buf("lohi" + tag, 8)
+            mmws = self.buf("mmws" + tag, L.fzb_minmax_workspace_bytes(n))
+            ebv = ebs[8 * f:8 * f + 8]
+            self._call("fzb_minmax_f32", _p(X[f]), n, _p(lohi), _p(mmws), mmws.numel(), _p(status), sp, nk=2)
+            self._call("fzb_resolve_bound", _p(lohi), int(eb_mode), float(magnitude), _p(ebv), sp)
+            pres.append(dict(status=status, lohi=lohi, eb=ebv, codes=codes[2 * n * f:2 * n * (f + 1)],
+                             bitmap=bitmap[4 * nw * f:4 * nw * (f + 1)]))
+        ws = self.buf("b_lzws", L.fzb_lorenzo_batch_workspace_bytes(F, n0, n1, n2), zero_new=True)
+        self._call("fzb_lorenzo_encode_batch_f32", _p(X), F, n, n0, n1, n2, _p(ebs), radius, _p(codes), _p(bitmap),
+                   nw, _p(ws), ws.numel(), sp, nk=2)
+        return [self.compress(X[f], dims, eb_mode, magnitude, pipeline_id=pipeline_id, predictor=predictor,
+                              codec=codec, radius=radius, tag=f"#{f}", pre=pres[f]) for f in range(F)]
+
+    def sizes_batch(self, das: list) -> list:
+        """One D2H for every field's status, lo/hi, outlier count and codec size."""
+        F = len(das)
+        s = self.pinned("scalb", 32 * F)
+        with torch.cuda.stream(self.stream):
+            for f, da in enumerate(das):
+                b = da.bufs
+                o = 32 * f
+                s[o:o + 8].copy_(b["status"][:8], non_blocking=True)
+                s[o + 8:o + 16].copy_(b["lohi"][:8], non_blocking=True)
+                s[o + 16:o + 24].copy_(b["ocount"][:8], non_blocking=True)
+                s[o + 24:o + 32].copy_(b["bitcount" if da.codec == "huffman" else "nwords"][:8], non_blocking=True)
+        self._sync()
+        v = s[:32 * F].numpy()
+        out = []
+        for f in range(F):
+            r = v[32 * f:32 * f + 32]
+            out.append(dict(status=int(r[0:4].view(np.uint32)[0]), lo=float(r[8:12].view(np.float32)[0]),
+                            hi=float(r[12:16].view(np.float32)[0]), k=int(r[16:24].view(np.uint64)[0]),
+                            size=int(r[24:32].view(np.uint64)[0])))
+        return out
+
+    def decompress_batch_resident(self, das: list, szs: list, eb_abs: list, OUT: torch.Tensor) -> torch.Tensor:
+        """Inverse of compress_batch on the resident segments: each field's codec
+        decode + outlier scatter, then ONE batched Lorenzo decode into OUT [F, n]."""
+        F, n = len(das), das[0].n
+        if das[0].predictor != "lorenzo" or das[0].use_anchors:
+            for f in range(F):
+                self.decompress_resident(das[f], szs[f], eb_abs[f], OUT[f], tag=f"#{f}")
+            return OUT
+        L, sp = self.lib, self.sp
+        n0, n1, n2 = pad3(das[0].dims)
+        nw = (n + 31) // 32
+        codes = self.buf("bd_codes", 2 * F * n + 16)
+        bitmap = self.buf("bd_bitmap", 4 * F * nw, zero=True)
+        ebs = self.buf("bd_eb", 8 * F)
+        with torch.cuda.stream(self.stream):
+            ebs[:8 * F].view(torch.float64).copy_(torch.tensor(eb_abs, dtype=torch.float64), non_blocking=False)
+        for f in range(F):
+            self.decompress_resident(das[f], szs[f], eb_abs[f], OUT[f], tag=f"#{f}",
+                                     batch=dict(codes=codes[2 * n * f:2 * n * (f + 1)],
+                                                bitmap=bitmap[4 * nw * f:4 * nw * (f + 1)]))
+        ws = self.buf("bd_lzws", L.fzb_lorenzo_batch_workspace_bytes(F, n0, n1, n2), zero_new=True)
+        self._call("fzb_lorenzo_decode_batch_f32", _p(codes), _p(bitmap), nw, _p(OUT), F, n, n0, n1, n2, _p(ebs),
+                   das[0].radius, _p(ws), ws.numel(), sp, nk=2)
+        return OUT
+
     # --------------------------------------------------------- decompress
-    def decode_codes(self, codec: str, segs: dict, n: int, radius: int) -> torch.Tensor:
+    def decode_codes(self, codec: str, segs: dict, n: int, radius: int, tag: str = "",
+                     codes_out: torch.Tensor | None = None) -> torch.Tensor:
         """Primary-codec decode (pipeline.py:415-430) into device u16 codes.
-        Host-side length checks mirror encode.py:299-305 and 359-375."""
+        Host-side length checks mirror encode.py:299-305 and 359-375.  `tag`
+        gives a batch member its own buffers (queued uploads never share a
+        staging buffer); `codes_out` places the codes in a batch slice."""
 
         L, sp = self.lib, self.sp
-        codes = self.buf("dcodes", 2 * n + 16)
-        status = self.buf("dstatus", 8, zero=True)
+        codes = self.buf("dcodes" + tag, 2 * n + 16) if codes_out is None else codes_out
+        status = self.buf("dstatus" + tag, 8, zero=True)
         nsym = 2 * radius
         if codec == "huffman":
             cl = segs["codebook"]
@@ -382,9 +482,9 @@ class Engine:
                 return codes
             if not cl.size or int(cl.max()) == 0:
                 raise E.CorruptStream("empty codebook with nonzero symbol count")
-            lengths = self.upload("dlengths", cl)
-            s = self.upload("dstream", stream, pad=16)
-            hws = self.buf("hdws", L.fzb_huffman_decode_workspace_bytes(len(stream), nsym))
+            lengths = self.upload("dlengths" + tag, cl)
+            s = self.upload("dstream" + tag, stream, pad=16)
+            hws = self.buf("hdws" + tag, L.fzb_huffman_decode_workspace_bytes(len(stream), nsym))
             self._call("fzb_huffman_decode", _p(s), len(stream), n, _p(lengths), nsym, _p(codes), _p(hws),
                        hws.numel(), _p(status), sp, nk=10)
         else:
@@ -401,47 +501,52 @@ class Engine:
                 if len(payload):
                     raise E.BitmapPayloadMismatch("bitmap marks 0 words, payload has more")
                 return codes
-            bm = self.upload("dbsmap", bitmap, pad=16)
-            pay = self.upload("dbspay", payload, pad=16)
-            bws = self.buf("dbsws", L.fzb_bitshuffle_workspace_bytes(n))
+            bm = self.upload("dbsmap" + tag, bitmap, pad=16)
+            pay = self.upload("dbspay" + tag, payload, pad=16)
+            bws = self.buf("dbsws" + tag, L.fzb_bitshuffle_workspace_bytes(n))
             self._call("fzb_bitshuffle_decode", _p(bm), _p(pay), len(payload) // 4, n, radius, _p(codes), _p(bws),
                        bws.numel(), _p(status), sp, nk=4)
         return codes
 
     def reconstruct(self, predictor: str, codes: torch.Tensor, idx: np.ndarray, vals: np.ndarray, anchors: bytes,
                     dims, eb_abs: float, radius: int, anchor_stride: int = 16,
-                    out: torch.Tensor | None = None) -> torch.Tensor:
-        """Outlier scatter + predictor inverse (pipeline.py:433-436) -> device f32 recon."""
+                    out: torch.Tensor | None = None, tag: str = "",
+                    bitmap_out: torch.Tensor | None = None) -> torch.Tensor:
+        """Outlier scatter + predictor inverse (pipeline.py:433-436) -> device f32 recon.
+        With `bitmap_out` (a batch slice) only the outlier scatter runs: the
+        caller issues one batched Lorenzo decode for all members."""
 
         L, sp = self.lib, self.sp
         dims = tuple(int(d) for d in dims)
         n = int(np.prod(dims))
         n0, n1, n2 = pad3(dims)
         recon = out if out is not None else torch.empty(n, dtype=torch.float32, device=self.device)
-        status = self.buf("dstatus", 8)
-        bitmap = self.buf("dbitmap", 4 * ((n + 31) // 32), zero=True)
-        ebt = self.upload("deb", np.array([eb_abs], np.float64))
+        status = self.buf("dstatus" + tag, 8)
+        bitmap = self.buf("dbitmap" + tag, 4 * ((n + 31) // 32), zero=True) if bitmap_out is None else bitmap_out
+        ebt = self.upload("deb" + tag, np.array([eb_abs], np.float64))
         k = int(idx.size)
         if k:
-            di = self.upload("didx", np.ascontiguousarray(idx, np.uint64))
-            dv = self.upload("dval", np.ascontiguousarray(vals, np.float32))
+            di = self.upload("didx" + tag, np.ascontiguousarray(idx, np.uint64))
+            dv = self.upload("dval" + tag, np.ascontiguousarray(vals, np.float32))
             self._call("fzb_outlier_scatter", _p(di), _p(dv), k, n, _p(codes), radius, _p(recon), _p(bitmap),
                        _p(status), sp)
+        if bitmap_out is not None:
+            return recon
         if predictor == "interp" and len(anchors):
-            da = self.upload("danchors", anchors)
+            da = self.upload("danchors" + tag, anchors)
             w = (ctypes.c_double * 4)(*CUBIC)
             self._call("fzb_interp_decode_f32", _p(codes), _p(bitmap), _p(da), _p(recon), n0, n1, n2, _p(ebt), radius,
                        anchor_stride, w, sp, nk=1 + 3 * int(np.log2(anchor_stride)))
         else:
-            lzws = self.buf("dlzws", L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
+            lzws = self.buf("dlzws" + tag, L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
             self._call("fzb_lorenzo_decode_f32", _p(codes), _p(bitmap), _p(recon), n0, n1, n2, _p(ebt), radius,
                        _p(lzws), lzws.numel(), sp, nk=5)
         return recon
 
-    def decode_status(self) -> int:
+    def decode_status(self, tag: str = "") -> int:
         st = self.pinned("dscal", 64)
         with torch.cuda.stream(self.stream):
-            st[:8].copy_(self.buf("dstatus", 8)[:8], non_blocking=True)
+            st[:8].copy_(self.buf("dstatus" + tag, 8)[:8], non_blocking=True)
         self._sync()
         return int(st[:4].numpy().view(np.uint32)[0])
 

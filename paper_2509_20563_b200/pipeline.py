@@ -240,6 +240,11 @@ def compress_device(x: torch.Tensor, dims, eb: ErrorBoundSpec, pipeline) -> Arch
     da = eng.compress(x, dims, int(eb.mode), float(eb.magnitude), pipeline_id=spec.id, predictor=pred,
                       codec=spec.primary_codec, radius=spec.radius(),
                       anchor_stride=cfg.anchor_stride if cfg else 16)
+    return _archive_of(eng, da, spec, eb, dims)
+
+
+def _archive_of(eng, da, spec: PipelineSpec, eb: ErrorBoundSpec, dims) -> Archive:
+    """finish() one device result into an Archive (pipeline.py:300-342)."""
     try:
         lo, hi, segs = eng.finish(da)
     except E.FZError as e:
@@ -393,6 +398,119 @@ def decompress_with_timing(a: Archive, pipeline=None):
 
 def decompress(a: Archive, pipeline=None) -> Field:
     return decompress_with_timing(a, pipeline)[0]
+
+
+# ------------------------------------------------------------------- batches
+# Several same-shaped fields at once ("several fields in flight
+# per GPU"): one batched Lorenzo wavefront interleaves all members' tiles, so
+# the GPU is busier than with one field at a time.  Archives and
+# reconstructions are identical to per-field compress()/decompress().
+
+def _batchable(spec: PipelineSpec, dims, n: int) -> bool:
+    return spec.predictor == "lorenzo" and len(dims) > 1 and n % 64 == 0
+
+
+def compress_batch(fields: list, eb: ErrorBoundSpec, pipeline) -> list:
+    """compress() of every field; same-shaped Lorenzo fields share one launch."""
+    spec = get_pipeline(pipeline)
+    _check_stage_params(spec)
+    if not fields:
+        return []
+    dims = tuple(fields[0].dims)
+    n = fields[0].len
+    if len(fields) == 1 or any(tuple(f.dims) != dims for f in fields) or not _batchable(spec, dims, n):
+        return [compress(f, eb, pipeline) for f in fields]
+    eng = default_engine()
+    X = eng.buf("cb_in", 4 * n * len(fields))[: 4 * n * len(fields)].view(torch.float32).view(len(fields), n)
+    for i, f in enumerate(fields):
+        src = torch.from_numpy(f.data)
+        if not src.is_pinned():
+            src = eng.pinned(f"cb_stage#{i}", 4 * n)[: 4 * n].view(torch.float32).copy_(src)
+        with torch.cuda.stream(eng.stream):
+            X[i].copy_(src, non_blocking=True)
+    das = eng.compress_batch(X, dims, int(eb.mode), float(eb.magnitude), pipeline_id=spec.id,
+                             predictor=spec.predictor, codec=spec.primary_codec, radius=spec.radius())
+    return [_archive_of(eng, da, spec, eb, dims) for da in das]
+
+
+def decompress_batch(archives: list, pipeline=None) -> list:
+    """decompress() of every archive; same-shaped Lorenzo archives share one
+    batched wavefront (each member's codec decode and outlier scatter first)."""
+    if not archives:
+        return []
+    a0 = archives[0]
+    spec = get_pipeline(pipeline if pipeline is not None else a0.pipeline_id)
+    n = a0.element_count
+    same = all(a.dims == a0.dims and a.pipeline_id == a0.pipeline_id and a.radius == a0.radius and len(a.segments)
+               for a in archives)
+    if len(archives) == 1 or not same or not _batchable(spec, a0.dims, n) or \
+            any(SEG_ANCHOR_GRID in _unwrap(a) for a in archives):
+        return [decompress(a, pipeline) for a in archives]
+    eng = default_engine()
+    F = len(archives)
+    nw = (n + 31) // 32
+    codes = eng.buf("db_codes", 2 * F * n + 16)
+    bitmap = eng.buf("db_bitmap", 4 * F * nw, zero=True)
+    OUT = eng.buf("db_out", 4 * F * n)[: 4 * F * n].view(torch.float32).view(F, n)
+    radius = a0.radius
+    codec = spec.primary_codec
+    ebs = []
+    for f, a in enumerate(archives):
+        tag = f"#{f}"
+        segs = _unwrap(a)
+        try:
+            if codec == "huffman":
+                if SEG_HUFFMAN_CODEBOOK not in segs or SEG_HUFFMAN_BITSTREAM not in segs:
+                    raise E.CorruptPayload("Huffman segments missing")
+                from .encode import HuffmanCodebook
+                cb = HuffmanCodebook.from_bytes(segs[SEG_HUFFMAN_CODEBOOK])
+                if cb.code_lengths.size != 2 * radius:
+                    raise E.CorruptPayload(f"codebook covers {cb.code_lengths.size} symbols, alphabet is {2 * radius}")
+                eng.decode_codes("huffman", {"codebook": cb.code_lengths, "stream": segs[SEG_HUFFMAN_BITSTREAM]}, n,
+                                 radius, tag=tag, codes_out=codes[2 * n * f:2 * n * (f + 1)])
+            else:
+                if SEG_BITSHUFFLE_BITMAP not in segs or SEG_BITSHUFFLE_PAYLOAD not in segs:
+                    raise E.CorruptPayload("bitshuffle segments missing")
+                eng.decode_codes("bitshuffle", {"bitmap": segs[SEG_BITSHUFFLE_BITMAP],
+                                                "payload": segs[SEG_BITSHUFFLE_PAYLOAD]}, n, radius, tag=tag,
+                                 codes_out=codes[2 * n * f:2 * n * (f + 1)])
+        except Exception as e:
+            raise E.StageError("decode-codes", e) from e
+        try:
+            idx, vals = _outliers(segs, n)
+        except Exception as e:
+            raise E.StageError("decode-outliers", e) from e
+        if idx.size > 1 and not bool(np.all(idx[1:] > idx[:-1])):
+            raise E.MalformedCodes("outlier indices not strictly increasing")
+        eb_abs = a.resolved_bound().eb_abs
+        ebs.append(eb_abs)
+        eng.reconstruct("lorenzo", codes[2 * n * f:2 * n * (f + 1)], idx, vals, b"", a.dims, eb_abs, radius,
+                        out=OUT[f], tag=tag, bitmap_out=bitmap[4 * nw * f:4 * nw * (f + 1)])
+    from .device import pad3
+    n0, n1, n2 = pad3(a0.dims)
+    ebt = eng.upload("db_eb", np.asarray(ebs, np.float64))
+    ws = eng.buf("db_lzws", eng.lib.fzb_lorenzo_batch_workspace_bytes(F, n0, n1, n2), zero_new=True)
+    from .device import _p
+    eng._call("fzb_lorenzo_decode_batch_f32", _p(codes), _p(bitmap), nw, _p(OUT), F, n, n0, n1, n2, _p(ebt), radius,
+              _p(ws), ws.numel(), eng.sp, nk=2)
+    from . import _lib
+    out = []
+    for f, a in enumerate(archives):
+        status = eng.decode_status(f"#{f}")
+        if status:
+            try:
+                _lib.raise_codec_status(status)
+            except E.FZError as e:
+                raise E.StageError("decode-codes", e) from e
+            if status & (_lib.ERR_OUTLIER_CODE | _lib.ERR_OUTLIER_ORDER):
+                raise E.MalformedCodes("outlier position without sentinel code")
+            raise RuntimeError(f"device status {status:#x}")
+        host = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        with torch.cuda.stream(eng.stream):
+            host.copy_(OUT[f], non_blocking=True)
+        out.append((a.dims, host))
+    eng._sync()
+    return [Field.trusted(d, h.numpy()) for d, h in out]
 
 
 def worker_count(requested: int | None = None) -> int:

@@ -110,3 +110,19 @@ def test_histogram_runs_and_tail(oracle):
     codes[-5:] = 1023
     h = enc.histogram_exact(codes, 512)
     assert np.array_equal(h.bins, oracle.histogram(codes, 512))
+
+
+# ------------------------------------------------------------------ batches
+
+@pytest.mark.parametrize("preset,dims", [("speed", (24, 40, 64)), ("default", (17, 65, 64)), ("default", (96, 128))])
+def test_batch_archives_identical(preset, dims):
+    import paper_2509_20563_b200 as fz
+    eb = fz.ErrorBoundSpec(fz.ErrorMode.VALUE_RANGE_RELATIVE, 1e-4)
+    fields = [fz.Field(dims, smooth_trig_host(dims, s)) for s in range(3)]
+    single = [fz.serialize_archive(fz.compress(f, eb, preset)) for f in fields]
+    batch = fz.compress_batch(fields, eb, preset)
+    assert [fz.serialize_archive(a) for a in batch] == single
+    parsed = [fz.parse_archive(b) for b in single]
+    recs = fz.decompress_batch(parsed)
+    for a, r in zip(parsed, recs):
+        assert r.data.tobytes() == fz.decompress(a).data.tobytes()
