@@ -50,7 +50,8 @@ FZB_API int fzb_resolve_bound(const float *d_lohi, int eb_mode, double magnitude
  * zero-fill it once when it is allocated, then pass it unchanged (any later
  * geometry that fits may reuse it; never share one between two streams). */
 FZB_API size_t fzb_lorenzo_workspace_bytes(uint32_t n0, uint32_t n1, uint32_t n2);
-/* codes u16[n]; d_bitmap u32[ceil(n/32)] zeroed by caller; outliers set bits. */
+/* codes u16[n]; d_bitmap u32[ceil(n/32)] zeroed by caller; outliers set bits.
+ * Inputs must be finite, as fzpipe's Field enforces (core.py:98-100). */
 FZB_API int fzb_lorenzo_encode_f32(const float *d_in, uint32_t n0, uint32_t n1, uint32_t n2, const double *d_eb,
                                    uint32_t radius, uint16_t *d_codes, uint32_t *d_bitmap, void *d_ws,
                                    size_t ws_bytes, void *stream);
