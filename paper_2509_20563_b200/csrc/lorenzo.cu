@@ -1670,6 +1670,9 @@ FZB_API int fzb_lorenzo_decode_f32(const uint16_t* d_codes, const uint32_t* d_bi
 FZB_API int fzb_debug_lz_timing(long long* host_out) {
     return (int)cudaMemcpyFromSymbol(host_out, v6::g_lz_stamp, sizeof(v6::g_lz_stamp));
 }
+FZB_API int fzb_debug_tile_times(unsigned long long* host_out) {
+    return (int)cudaMemcpyFromSymbol(host_out, v6::g_tile_t, sizeof(v6::g_tile_t));
+}
 FZB_API int fzb_debug_walk_timing(long long* host_out) {
     return (int)cudaMemcpyFromSymbol(host_out, g_walk_stamp, sizeof(g_walk_stamp));
 }

@@ -306,6 +306,12 @@ constexpr double RINT_MAGIC = 6755399441055744.0;
 // warps at 4 points of every step; read back with fzb_debug_lz_timing.
 #ifdef LZ7_TIMING
 __device__ long long g_lz_stamp[8][1024][4];
+__device__ unsigned long long g_tile_t[1 << 16][4];   // per global tile: claim, first step, end (ns), smid
+FZB_DEV unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 #define LZ_STAMP(i)                                                                                    \
     do {                                                                                               \
         const long long c_ = clock64();                                                                \
@@ -381,6 +387,14 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
         for (int q = tid; q < nh; q += NT) HU[q] = 0;
     }
     if (tid == 0) flags[0] = (uint32_t)order[atomicAdd(ticket, 1u)];
+#ifdef LZ7_TIMING
+    if (tid == 0 && flags[0] < (1u << 16)) {
+        g_tile_t[flags[0]][0] = gtimer();
+        unsigned sm;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+        g_tile_t[flags[0]][3] = sm;
+    }
+#endif
     if (tid < W + 2) flags[1 + tid] = 0;
     __syncthreads();
     // global tile id -> (field, tile): faces are indexed by the global id (the
@@ -474,6 +488,9 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
         if constexpr (!DEC) cp_async_wait_n<SD - 1>();   // this lane's copies of group g landed
         if (ld_acq_cta(hready) < (uint32_t)(g + 1))
             while (ld_acq_cta(hready) < (uint32_t)(g + 1)) __nanosleep(32);
+#ifdef LZ7_TIMING
+        if (g == 0 && w == 0 && b == 0 && T < (1 << 16)) g_tile_t[T][1] = gtimer();
+#endif
         // stay within 15 steps of warp w+1 (the ghost ring holds GRD = 16)
         if (w + 1 < W && ld_acq_cta(done + w + 1) + 1 < (uint32_t)g)
             while (ld_acq_cta(done + w + 1) + 1 < (uint32_t)g) __nanosleep(32);
@@ -610,6 +627,9 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
     }
     // the last chunk of every row completes with the last group
     flush_own<R, DEC>(NGRP, ringl, codes_out, bitmap, recon, rows, d0, geo.n2);
+#ifdef LZ7_TIMING
+    if (w == W - 1 && b == 0 && T < (1 << 16)) g_tile_t[T][2] = gtimer();
+#endif
 }
 
 __global__ void lz7_prep_kernel(uint32_t* hdr) {
