@@ -136,6 +136,15 @@ FZB_DEV void block_bitmap(uint32_t gor, int w, int i, uint32_t BM[4]) {
     for (int k = 0; k < 4; k++) BM[k] = __shfl_sync(0xffffffffu, mine, k);
 }
 
+// Predicated read-only load (no branch around it): 0 when !p.
+FZB_DEV uint32_t ldg_if(bool p, const uint32_t* ptr) {
+    uint32_t v;
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; mov.b32 %0, 0; @q ld.global.nc.u32 %0, [%1]; }"
+                 : "=r"(v)
+                 : "l"(ptr), "r"((int)p));
+    return v;
+}
+
 FZB_DEV uint4 load_codes(const uint16_t* __restrict__ codes, uint64_t n, uint64_t blk, int lane) {
     const uint64_t t0 = blk * 256 + 8 * lane;
     if (t0 + 8 <= n) return __ldg(reinterpret_cast<const uint4*>(codes + t0));
@@ -269,6 +278,111 @@ __global__ void __launch_bounds__(BS_THREADS) bs_enc3_kernel(const uint16_t* __r
     }
 }
 
+// Persistent variant: each CTA claims chunks of BS_BPC blocks by ticket (so
+// look-back predecessors are always claimed earlier) and issues the next
+// chunk's loads before the current chunk's transposes, look-back and payload
+// stores, keeping HBM reads in flight across the whole CTA lifetime.
+__global__ void __launch_bounds__(BS_THREADS) bs_enc4_kernel(const uint16_t* __restrict__ codes, uint64_t n,
+                                                             uint64_t nblocks, uint32_t nchunks,
+                                                             uint32_t* __restrict__ bitmap,
+                                                             uint32_t* __restrict__ payload,
+                                                             unsigned long long* __restrict__ state,
+                                                             uint32_t* __restrict__ ticket,
+                                                             unsigned long long* __restrict__ nwords) {
+    __shared__ uint32_t s_off[BS_BPC];
+    __shared__ unsigned long long s_agg, s_excl;
+    __shared__ uint32_t s_cta[2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gw = lane >> 2, gi = lane & 3;
+    const uint32_t xsel = (uint32_t)(gi | ((1 ^ gi) << 4) | ((2 ^ gi) << 8) | ((3 ^ gi) << 12));
+    if (threadIdx.x == 0) s_cta[0] = atomicAdd(ticket, 1u);
+    __syncthreads();
+    uint32_t cta = s_cta[0];
+    uint4 r[BS_BPW];
+    if (cta < nchunks) {
+        const uint64_t blk0 = (uint64_t)cta * BS_BPC + warp * BS_BPW;
+#pragma unroll
+        for (int q = 0; q < BS_BPW; q++)
+            r[q] = (blk0 + q < nblocks) ? load_codes(codes, n, blk0 + q, lane) : make_uint4(0, 0, 0, 0);
+    }
+    for (int it = 0; cta < nchunks; it++) {
+        const uint64_t blk0 = (uint64_t)cta * BS_BPC + warp * BS_BPW;
+        uint32_t gor[BS_BPW];
+#pragma unroll
+        for (int q = 0; q < BS_BPW; q++) {
+            gor[q] = group_or(r[q]);
+            uint32_t c = __popc(gor[q]);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            if (lane == 0) s_off[warp * BS_BPW + q] = c >> 2;
+        }
+        __syncthreads();   // (A) s_off complete; previous iteration fully done with s_excl / s_cta
+        if (warp == 0) {
+            const uint32_t a = s_off[lane];
+            uint32_t incl = a;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            s_off[lane] = incl - a;
+            if (lane == 31) {
+                s_agg = incl;
+                if (cta != 0) {
+                    __threadfence();
+                    atomicExch(state + cta, LB_AGG | (unsigned long long)incl);
+                }
+                s_cta[(it + 1) & 1] = atomicAdd(ticket, 1u);   // next chunk
+            }
+        }
+        uint32_t Wd[BS_BPW][4];
+#pragma unroll
+        for (int q = 0; q < BS_BPW; q++) {
+            uint32_t E[4];
+            codes_to_planes(r[q], E);
+            planes_to_words(E, gi, xsel, Wd[q]);
+        }
+        __syncthreads();   // (B) s_off prefix, s_agg, next ticket visible
+        const uint32_t nxt = s_cta[(it + 1) & 1];
+        if (nxt < nchunks) {   // next chunk's loads go out before the look-back and the stores
+            const uint64_t nb0 = (uint64_t)nxt * BS_BPC + warp * BS_BPW;
+#pragma unroll
+            for (int q = 0; q < BS_BPW; q++)
+                r[q] = (nb0 + q < nblocks) ? load_codes(codes, n, nb0 + q, lane) : make_uint4(0, 0, 0, 0);
+        }
+        if (warp == 0) {
+            const unsigned long long agg = s_agg;
+            const unsigned long long excl = lookback(cta, agg, state);
+            if (lane == 0) {
+                s_excl = excl;
+                if (cta == nchunks - 1) *nwords = excl + agg;
+            }
+        }
+        __syncthreads();   // (C) s_excl visible
+#pragma unroll
+        for (int q = 0; q < BS_BPW; q++) {
+            const uint64_t blk = blk0 + q;
+            if (blk >= nblocks) break;
+            uint32_t BM[4];
+            block_bitmap(gor[q], gw, gi, BM);
+            if (lane < 4) bitmap[blk * 4 + lane] = sel4(BM, lane);
+            const unsigned long long base = s_excl + s_off[warp * BS_BPW + q];
+            uint32_t before = 0;
+#pragma unroll
+            for (int k = 0; k < 4; k++) before += (k < gi) ? __popc(BM[k]) : 0u;
+            const uint32_t bmi = sel4(BM, gi);
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                if ((gor[q] >> (4 * gi + c)) & 1u) {
+                    const uint32_t rank = before + __popc(bmi & ((1u << (8 * c + gw)) - 1u));
+                    payload[base + rank] = Wd[q][c];
+                }
+            }
+        }
+        cta = nxt;
+    }
+}
+
 // Per-CTA word counts of the decoder (bitmap popcounts), then one scan.
 __global__ void __launch_bounds__(BS_THREADS) bs_dec_count_kernel(const uint32_t* __restrict__ bitmap, uint64_t nblocks,
                                                                   uint32_t* __restrict__ counts) {
@@ -329,37 +443,51 @@ __global__ void __launch_bounds__(BS_THREADS) bs_dec3_kernel(const uint32_t* __r
     const unsigned long long cbase = offs[blockIdx.x];
     const uint32_t two_r = 2u * radius;
     bool pad_bad = false, range_bad = false;
+    // phase 1: every block's payload loads in flight at once (branch-free:
+    // predicated loads at 32-bit offsets from the block's payload base)
+    const int lg = 31 - __clz(two_r);   // planes >= lg nonzero <=> some code may be >= 2^lg
+    uint32_t W[BS_BPW][4];
+    uint32_t high = 0;   // bitmap bits of planes >= lg (range check needed)
 #pragma unroll
     for (int q = 0; q < BS_BPW; q++) {
         const uint64_t blk = cblk + warp * BS_BPW + q;
-        if (blk >= nblocks) break;
-        const uint4 bmv = __ldg(reinterpret_cast<const uint4*>(bitmap) + blk);
+        const bool inb = blk < nblocks;
+        const uint4 bmv = inb ? __ldg(reinterpret_cast<const uint4*>(bitmap) + blk) : make_uint4(0, 0, 0, 0);
         const uint32_t BM[4] = {bmv.x, bmv.y, bmv.z, bmv.w};
         const unsigned long long base = cbase + s_off[warp * BS_BPW + q];
+        const uint32_t* pb = payload + base;
+        const long long room = (long long)payload_words - (long long)base;   // words left from base
         uint32_t before = 0;
 #pragma unroll
         for (int k = 0; k < 4; k++) before += (k < gi) ? __popc(BM[k]) : 0u;
         const uint32_t bmi = sel4(BM, gi);
-        uint32_t W[4];
 #pragma unroll
         for (int c = 0; c < 4; c++) {
-            W[c] = 0u;
             const uint32_t bit = 8 * c + gw;
-            if ((bmi >> bit) & 1u) {
-                const unsigned long long pos = base + before + __popc(bmi & ((1u << bit) - 1u));
-                if (pos < payload_words) W[c] = __ldg(payload + pos);
-            }
+            const uint32_t rank = before + __popc(bmi & ((1u << bit) - 1u));
+            W[q][c] = ldg_if(((bmi >> bit) & 1u) && (long long)rank < room, pb + rank);
+            high |= (4 * gi + c >= lg) ? ((bmi >> bit) & 1u) : 0u;
         }
+    }
+    // no nonzero word in planes >= lg: every code < 2^lg <= 2R, no range check
+    const bool check_range = __any_sync(0xffffffffu, high != 0);
+    // phase 2: transposes and 16-byte code stores
+#pragma unroll
+    for (int q = 0; q < BS_BPW; q++) {
+        const uint64_t blk = cblk + warp * BS_BPW + q;
+        if (blk >= nblocks) break;
         uint32_t E[4];
-        words_to_planes(W, gi, xsel, E);
+        words_to_planes(W[q], gi, xsel, E);
         const uint4 rc = planes_to_codes(E);
         const uint64_t t0 = blk * 256 + 8 * lane;
         const uint32_t c8[8] = {rc.x & 0xFFFFu, rc.x >> 16, rc.y & 0xFFFFu, rc.y >> 16,
                                 rc.z & 0xFFFFu, rc.z >> 16, rc.w & 0xFFFFu, rc.w >> 16};
         if (t0 + 8 <= n) {
             *reinterpret_cast<uint4*>(codes + t0) = rc;
+            if (check_range) {
 #pragma unroll
-            for (int j = 0; j < 8; j++) range_bad |= c8[j] >= two_r;
+                for (int j = 0; j < 8; j++) range_bad |= c8[j] >= two_r;
+            }
         } else {
 #pragma unroll
             for (int j = 0; j < 8; j++) {
@@ -403,9 +531,25 @@ FZB_API int fzb_bitshuffle_encode(const uint16_t* d_codes, uint64_t n, uint8_t* 
     uint32_t* ticket = reinterpret_cast<uint32_t*>(w);
     unsigned long long* state = reinterpret_cast<unsigned long long*>(w + 256);
     cudaMemsetAsync(w, 0, 256 + nc * 8, st);
-    bs_enc3_kernel<<<(unsigned)nc, BS_THREADS, 0, st>>>(d_codes, n, nb, reinterpret_cast<uint32_t*>(d_bitmap),
-                                                       d_payload, state, ticket,
-                                                       reinterpret_cast<unsigned long long*>(d_nwords));
+    static int grid_cap = 0;   // resident CTAs of the persistent encoder (device-wide)
+    if (!grid_cap) {
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bs_enc4_kernel, BS_THREADS, 0);
+        grid_cap = sms * (per > 0 ? per : 1);
+    }
+    const char* e = getenv("FZB_BS_ENC");
+    if (e && e[0] == '3') {
+        bs_enc3_kernel<<<(unsigned)nc, BS_THREADS, 0, st>>>(d_codes, n, nb, reinterpret_cast<uint32_t*>(d_bitmap),
+                                                           d_payload, state, ticket,
+                                                           reinterpret_cast<unsigned long long*>(d_nwords));
+    } else {
+        const unsigned grid = (unsigned)(nc < (uint64_t)grid_cap ? nc : (uint64_t)grid_cap);
+        bs_enc4_kernel<<<grid, BS_THREADS, 0, st>>>(d_codes, n, nb, (uint32_t)nc, reinterpret_cast<uint32_t*>(d_bitmap),
+                                                    d_payload, state, ticket,
+                                                    reinterpret_cast<unsigned long long*>(d_nwords));
+    }
     return fzb_check_launch();
 }
 
