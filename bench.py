@@ -356,6 +356,11 @@ def run_ours(args, wl):
     e2e_comp = sum(len(fz.serialize_archive(q)) for q in arcs)
     q = quality_arrays(field.data, r.data, a.resolved_bound().eb_abs)
     assert q.bound_satisfied
+    # the device-side metric (numpy-exact pairwise MSE) must agree bit for bit
+    from paper_2509_20563_b200.metrics import quality_device
+    q_dev = quality_device(torch.from_numpy(np.ascontiguousarray(field.data)).to(dev),
+                           torch.from_numpy(np.ascontiguousarray(r.data)).to(dev), dims, a.resolved_bound().eb_abs)
+    assert q_dev == q, (q_dev, q)
 
     line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True, "scaling": "weak",
@@ -366,6 +371,7 @@ def run_ours(args, wl):
             "compress_gbs": round(4 * n / (comp_ms / 1e3) / 1e9, 3) if comp_ms else None,
             "decompress_gbs": round(4 * n / (dec_ms / 1e3) / 1e9, 3) if dec_ms else None,
             "cr": round(4 * n / comp_bytes, 4), "psnr_db": round(q.psnr_db, 4), "max_abs_err": q.max_abs_err,
+            "quality_device_bit_identical": q_dev == q,
             "eb_abs": a.resolved_bound().eb_abs,
             "e2e": {"value": round(e2e, 3), "unit": "GB/s", "h2d_bytes_per_step": F * 4 * n + e2e_comp,
                     "d2h_bytes_per_step": F * 4 * n + e2e_comp},

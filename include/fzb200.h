@@ -136,6 +136,15 @@ FZB_API int fzb_bitshuffle_decode(const uint8_t *d_bitmap, const uint32_t *d_pay
 /* ---- utilities ----------------------------------------------------------- */
 FZB_API int fzb_fill_u16(uint16_t *d_dst, uint64_t n, uint16_t value, void *stream);
 
+/* ---- verification: metrics.quality (metrics.py:49-75) bit-identical ------ */
+/* Sums the leaves of numpy's pairwise-sum tree of d*d (d = f64(orig) -
+ * f64(recon)); d_leaf_len <= 128.  d_red[0] = bits of max|d|, d_red[1] /
+ * d_red[2] = order-preserving keys of min / max(orig); initialise to
+ * {0, ~0ull, 0}.  The host folds the leaf sums up the same tree. */
+FZB_API int fzb_quality_leaves(const float *d_orig, const float *d_recon, const uint64_t *d_leaf_off,
+                               const uint16_t *d_leaf_len, uint64_t nleaves, double *d_leaf_sum,
+                               unsigned long long *d_red, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

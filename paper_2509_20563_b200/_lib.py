@@ -82,6 +82,7 @@ def load():
         "fzb_outlier_workspace_bytes": (SZ, [U64]),
         "fzb_outlier_compact": (I, [P, U64, P, P, P, P, P, SZ, P]),
         "fzb_outlier_scatter": (I, [P, P, U64, U64, P, U32, P, P, P, P]),
+        "fzb_quality_leaves": (I, [P, P, P, P, U64, P, P, P]),
         "fzb_histogram": (I, [P, U64, U32, P, P, P]),
         "fzb_huffman_build_workspace_bytes": (SZ, [U32]),
         "fzb_huffman_build": (I, [P, U32, P, P, P, P, SZ, P]),
@@ -108,6 +109,7 @@ EXPORTED = [
     "fzb_lorenzo_batch_workspace_bytes", "fzb_lorenzo_encode_batch_f32", "fzb_lorenzo_decode_batch_f32",
     "fzb_interp_encode_f32",
     "fzb_interp_decode_f32", "fzb_outlier_workspace_bytes", "fzb_outlier_compact", "fzb_outlier_scatter",
+    "fzb_quality_leaves",
     "fzb_histogram", "fzb_huffman_build_workspace_bytes", "fzb_huffman_build", "fzb_huffman_encode_workspace_bytes",
     "fzb_huffman_encode", "fzb_huffman_decode_workspace_bytes", "fzb_huffman_decode",
     "fzb_bitshuffle_workspace_bytes", "fzb_bitshuffle_encode", "fzb_bitshuffle_decode", "fzb_fill_u16",

@@ -257,6 +257,85 @@ __global__ void outlier_scatter_kernel(const unsigned long long* __restrict__ id
 
 }  // namespace
 
+// ---------------------------------------------------------------- quality
+// fzpipe metrics.quality (metrics.py:49-75) on device, bit-identical: the
+// MSE is np.mean(d * d) with d = f64(orig) - f64(recon), and numpy sums a
+// contiguous f64 array pairwise (halve at multiples of 8 down to blocks of
+// <= 128, each block summed by 8 strided accumulators then
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus the tail in order).  The host
+// builds that split tree (it depends on n only); this kernel sums its
+// leaves, one warp per leaf, and reduces max|d|, min/max(orig) exactly.
+constexpr int QL_WARPS = 8;
+
+FZB_DEV unsigned long long f32_key(float v) {   // order-preserving f32 -> u32
+    const uint32_t u = __float_as_uint(v);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__global__ void __launch_bounds__(QL_WARPS * 32) quality_leaf_kernel(const float* __restrict__ orig,
+                                                                     const float* __restrict__ recon,
+                                                                     const uint64_t* __restrict__ leaf_off,
+                                                                     const uint16_t* __restrict__ leaf_len,
+                                                                     uint64_t nleaves, double* __restrict__ leaf_sum,
+                                                                     unsigned long long* __restrict__ red) {
+    __shared__ double sq[QL_WARPS][128];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const uint64_t leaf = (uint64_t)blockIdx.x * QL_WARPS + wl;
+    double maxe = 0.0;
+    uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
+    if (leaf < nleaves) {
+        const uint64_t off = leaf_off[leaf];
+        const int m = leaf_len[leaf];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int i = q * 32 + lane;
+            if (i < m) {
+                const float o = orig[off + i];
+                const double d = __dsub_rn((double)o, (double)recon[off + i]);
+                sq[wl][i] = __dmul_rn(d, d);
+                maxe = fmax(maxe, fabs(d));
+                const uint32_t k = (uint32_t)f32_key(o);
+                kmin = min(kmin, k);
+                kmax = max(kmax, k);
+            }
+        }
+        __syncwarp();
+        double res = 0.0;
+        if (m < 8) {
+            if (lane == 0)
+                for (int i = 0; i < m; i++) res = __dadd_rn(res, sq[wl][i]);
+        } else {
+            double r = 0.0;
+            const int full = m - (m & 7);
+            if (lane < 8) {
+                r = sq[wl][lane];
+                for (int i = 8 + lane; i < full; i += 8) r = __dadd_rn(r, sq[wl][i]);
+            }
+            const double r1 = __shfl_down_sync(0xffffffffu, r, 1);
+            const double p01 = __dadd_rn(r, r1);                              // lanes 0,2,4,6: r_j + r_j+1
+            const double p23 = __shfl_down_sync(0xffffffffu, p01, 2);
+            const double q03 = __dadd_rn(p01, p23);                           // lanes 0,4
+            const double q47 = __shfl_down_sync(0xffffffffu, q03, 4);
+            if (lane == 0) {
+                res = __dadd_rn(q03, q47);
+                for (int i = full; i < m; i++) res = __dadd_rn(res, sq[wl][i]);
+            }
+        }
+        if (lane == 0) leaf_sum[leaf] = res;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        maxe = fmax(maxe, __shfl_xor_sync(0xffffffffu, maxe, o));
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if (lane == 0 && leaf < nleaves) {
+        atomicMax(red + 0, (unsigned long long)__double_as_longlong(maxe));   // >= 0: bit order == value order
+        atomicMin(red + 1, (unsigned long long)kmin);
+        atomicMax(red + 2, (unsigned long long)kmax);
+    }
+}
+
 extern "C" {
 
 FZB_API int fzb_abi_version(void) { return 1; }
@@ -346,6 +425,19 @@ FZB_API int fzb_outlier_scatter(const uint64_t* d_idx, const float* d_vals, uint
     outlier_scatter_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
         reinterpret_cast<const unsigned long long*>(d_idx), d_vals, k, n, d_codes, (int)radius, d_recon, d_bitmap,
         d_status);
+    return fzb_check_launch();
+}
+
+// Leaves of numpy's pairwise-sum tree (offsets, lengths <= 128, in order) of
+// d*d, plus red[0] = max|d| (f64 bits), red[1] / red[2] = ordered keys of
+// min / max(orig).  red must be initialised to {0, ~0, 0} by the caller.
+FZB_API int fzb_quality_leaves(const float* d_orig, const float* d_recon, const uint64_t* d_leaf_off,
+                               const uint16_t* d_leaf_len, uint64_t nleaves, double* d_leaf_sum,
+                               unsigned long long* d_red, void* stream) {
+    if (nleaves == 0) return 0;
+    const uint64_t blocks = (nleaves + QL_WARPS - 1) / QL_WARPS;
+    quality_leaf_kernel<<<(unsigned)blocks, QL_WARPS * 32, 0, (cudaStream_t)stream>>>(
+        d_orig, d_recon, d_leaf_off, d_leaf_len, nleaves, d_leaf_sum, d_red);
     return fzb_check_launch();
 }
 

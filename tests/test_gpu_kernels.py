@@ -126,3 +126,28 @@ def test_batch_archives_identical(preset, dims):
     recs = fz.decompress_batch(parsed)
     for a, r in zip(parsed, recs):
         assert r.data.tobytes() == fz.decompress(a).data.tobytes()
+
+
+# ------------------------------------------------------------------ quality
+
+@pytest.mark.parametrize("n", [1, 7, 8, 129, 1000, 100_003, 1 << 20, 3_000_017])
+def test_quality_device_bit_identical(n):
+    from paper_2509_20563_b200 import metrics
+    rng = np.random.default_rng(n)
+    o = (rng.normal(0, 1, n) * 3).astype(np.float32)
+    r = (o + rng.uniform(-1e-3, 1e-3, n)).astype(np.float32)
+    r[::7] = o[::7]   # some exact elements
+    host = metrics.quality_arrays(o, r, 1e-3)
+    dev = metrics.quality_device(torch.from_numpy(o).cuda(), torch.from_numpy(r).cuda(), (n,), 1e-3)
+    assert dev == host   # every field equal (floats compared exactly)
+
+
+def test_quality_device_edge_cases():
+    from paper_2509_20563_b200 import metrics
+    z = np.zeros(1000, np.float32)
+    z[::3] = -0.0
+    for o, r in [(z, z.copy()), (z, z + np.float32(1e-3)), (np.linspace(-1, 1, 999, dtype=np.float32),) * 2]:
+        host = metrics.quality_arrays(o, r, None)
+        dev = metrics.quality_device(torch.from_numpy(o).cuda(), torch.from_numpy(np.ascontiguousarray(r)).cuda(),
+                                     (o.size,), None)
+        assert dev == host

@@ -88,3 +88,39 @@ def test_cpu_only_box_fails_loudly():
     f = Field((8,), np.arange(8, dtype=np.float32))
     with pytest.raises(E.DeviceUnavailable):
         compress(f, ErrorBoundSpec(ErrorMode.ABSOLUTE, 0.1), "default")
+
+
+@pytest.mark.parametrize("n", [1, 5, 8, 128, 129, 1000, 100_003])
+def test_pairwise_tree_matches_numpy(n):
+    # the split tree quality_device folds must reproduce numpy's summation
+    from paper_2509_20563_b200.metrics import _pairwise_tree
+    x = np.random.default_rng(n).random(n)
+    off, ln, levels = _pairwise_tree(n)
+    assert int(ln.astype(np.int64).sum()) == n and ln.max() <= 128
+
+    def leaf(o, m):
+        a = x[o:o + m]
+        if m < 8:
+            r = 0.0
+            for v in a:
+                r += v
+            return r
+        r = list(a[:8])
+        full = m - m % 8
+        for i in range(8, full, 8):
+            for j in range(8):
+                r[j] += a[i + j]
+        res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+        for i in range(full, m):
+            res += a[i]
+        return res
+
+    ls = np.array([leaf(int(o), int(m)) for o, m in zip(off, ln)])
+    below = None
+    for lm, ids in reversed(levels):
+        vals = np.empty(lm.size)
+        vals[lm] = ls[ids]
+        if below is not None:
+            vals[~lm] = below[0::2] + below[1::2]
+        below = vals
+    assert below[0] == np.add.reduce(x)
