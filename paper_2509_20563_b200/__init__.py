@@ -8,7 +8,7 @@ There is no CPU fallback on any path.
 """
 
 from .core import (  # noqa: F401
-    Archive, ErrorBoundSpec, ErrorMode, Field, QuantOutput, ResolvedBound, field_from_array, parse_archive,
+    Archive, ErrorBoundSpec, archive_buffer, ErrorMode, Field, QuantOutput, ResolvedBound, field_from_array, parse_archive,
     resolve_bound, serialize_archive,
 )
 from .errors import FZError  # noqa: F401

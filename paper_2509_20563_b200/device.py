@@ -29,10 +29,13 @@ import torch
 
 from . import _lib
 from . import errors as E
+from .core import HEADER as _HEADER, SEGMENT as _SEGMENT
 from .core import (
     SEG_ANCHOR_GRID, SEG_BITSHUFFLE_BITMAP, SEG_BITSHUFFLE_PAYLOAD, SEG_HUFFMAN_BITSTREAM,
     SEG_HUFFMAN_CODEBOOK, SEG_OUTLIER_INDICES, SEG_OUTLIER_VALUES,
 )
+
+HEADER_SIZE, SEGMENT_SIZE = _HEADER.size, _SEGMENT.size
 
 CUBIC = (-1 / 16, 9 / 16, 9 / 16, -1 / 16)  # reference predict.py:47
 
@@ -256,7 +259,11 @@ class Engine:
                              use_anchors)
 
     def finish(self, da: DeviceArchive):
-        """Synchronise once; return (lo, hi, segments) with host payload bytes."""
+        """Synchronise once; return (lo, hi, segments, wire).  The segments are
+        DMA'd straight into a pinned block laid out as the serialized archive
+        (41-byte header + 9-byte segment entries, then the payloads back to
+        back, core.py:285-300): the caller writes the header and the block IS
+        the container, so serializing needs no host-side assembly."""
 
         b = da.bufs
         # scalars in one small D2H
@@ -277,7 +284,7 @@ class Engine:
         if status & _lib.ERR_NONFINITE:
             raise ValueError("non-finite value in field")
         if lo == hi:
-            return lo, hi, []
+            return lo, hi, [], None
         _lib.raise_codec_status(status)
         n = da.n
         parts = [("oidx", 8 * k), ("oval", 4 * k)]
@@ -287,19 +294,20 @@ class Engine:
             parts += [("lengths", 2 * da.radius), ("hfout", (size + 7) // 8)]
         else:
             parts += [("bsmap", 16 * ((n + 255) // 256)), ("bspay", 4 * size)]
-        total = sum(_align(sz, 64) for _, sz in parts)
+        head = HEADER_SIZE + SEGMENT_SIZE * len(parts)
+        total = head + sum(sz for _, sz in parts)
         # a fresh block from torch's pinned caching allocator: the archive's
         # payloads are read-only views into it (no host-side copy); the block
         # returns to the cache when the archive is dropped
-        host = torch.empty(max(total, 64), dtype=torch.uint8, pin_memory=True)
+        host = torch.empty(total, dtype=torch.uint8, pin_memory=True)
         offs = []
-        o = 0
+        o = head
         with torch.cuda.stream(self.stream):
             for name, sz in parts:
                 if sz:
                     host[o:o + sz].copy_(b[name][:sz], non_blocking=True)
                 offs.append((o, sz))
-                o += _align(sz, 64)
+                o += sz
         self._sync()
         mv = memoryview(host.numpy()).toreadonly()
         blobs = [mv[o:o + sz] for o, sz in offs]
@@ -312,7 +320,7 @@ class Engine:
             segs += [(SEG_HUFFMAN_CODEBOOK, blobs[q]), (SEG_HUFFMAN_BITSTREAM, blobs[q + 1])]
         else:
             segs += [(SEG_BITSHUFFLE_BITMAP, blobs[q]), (SEG_BITSHUFFLE_PAYLOAD, blobs[q + 1])]
-        return lo, hi, segs
+        return lo, hi, segs, (host, head)
 
     def sizes(self, da: DeviceArchive) -> dict:
         """One small D2H: status, lo/hi, outlier count, primary-codec size."""

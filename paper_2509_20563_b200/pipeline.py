@@ -26,7 +26,7 @@ from . import secondary
 from .core import (
     SEG_ANCHOR_GRID, SEG_BITSHUFFLE_BITMAP, SEG_BITSHUFFLE_PAYLOAD, SEG_HUFFMAN_BITSTREAM, SEG_HUFFMAN_CODEBOOK,
     SEG_OUTLIER_INDICES, SEG_OUTLIER_VALUES, SEG_SECONDARY_WRAPPED, Archive, ErrorBoundSpec, ErrorMode, Field,
-    ResolvedBound, eb_from_range, register_known_pipeline_id,
+    ResolvedBound, attach_wire, eb_from_range, register_known_pipeline_id,
 )
 from .device import default_engine, interp_applicable
 
@@ -246,7 +246,7 @@ def compress_device(x: torch.Tensor, dims, eb: ErrorBoundSpec, pipeline) -> Arch
 def _archive_of(eng, da, spec: PipelineSpec, eb: ErrorBoundSpec, dims) -> Archive:
     """finish() one device result into an Archive (pipeline.py:300-342)."""
     try:
-        lo, hi, segs = eng.finish(da)
+        lo, hi, segs, wire = eng.finish(da)
     except E.FZError as e:
         raise E.StageError(spec.stage_of(StageKind.PRIMARY_CODEC).name, e) from e
     if lo == hi:
@@ -262,7 +262,11 @@ def _archive_of(eng, da, spec: PipelineSpec, eb: ErrorBoundSpec, dims) -> Archiv
         except Exception as e:
             raise E.StageError(sc.name, e) from e
         segs = head + prim
-    return Archive(spec.id, eb.mode, eb.magnitude, lo, hi, tuple(dims), spec.radius(), tuple(segs))
+        wire = None
+    a = Archive(spec.id, eb.mode, eb.magnitude, lo, hi, tuple(dims), spec.radius(), tuple(segs))
+    if wire is not None:
+        attach_wire(a, wire[0].numpy(), wire[1])
+    return a
 
 
 def compress_with_timing(field: Field, eb: ErrorBoundSpec, pipeline):

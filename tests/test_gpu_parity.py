@@ -253,3 +253,23 @@ def test_full_size_c4_archive_matches_oracle(oracle, preset):
     rec = fz.decompress(a)
     _, orec = oracle.decompress(want)
     assert rec.data.tobytes() == orec.tobytes()
+
+
+@pytest.mark.parametrize("preset", ["default", "speed", "quality"])
+def test_wire_block_is_the_serialized_archive(preset):
+    # the device path lays the archive out serialized in one pinned block:
+    # archive_buffer must equal the reference serialization byte for byte and
+    # parse back (zero-copy) to an equal archive that decompresses identically
+    import paper_2509_20563_b200 as fz
+    from paper_2509_20563_b200.core import header_bytes
+    dims = (40, 48, 64)
+    from paper_2509_20563_b200.data import smooth_trig_host
+    f = fz.Field(dims, smooth_trig_host(dims, 3))
+    eb = fz.ErrorBoundSpec(fz.ErrorMode.VALUE_RANGE_RELATIVE, 1e-4)
+    a = fz.compress(f, eb, preset)
+    buf = fz.archive_buffer(a)
+    ref = header_bytes(a) + b"".join(bytes(p) for _, p in a.segments)
+    assert bytes(buf) == ref == fz.serialize_archive(a)
+    b = fz.parse_archive(buf)
+    assert b == a
+    assert fz.decompress(b).data.tobytes() == fz.decompress(a).data.tobytes()
