@@ -151,3 +151,23 @@ def test_quality_device_edge_cases():
         dev = metrics.quality_device(torch.from_numpy(o).cuda(), torch.from_numpy(np.ascontiguousarray(r)).cuda(),
                                      (o.size,), None)
         assert dev == host
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_huffman_build_ties_vs_oracle(oracle, seed):
+    # tie-heavy histograms (many equal small counts, 2..300 used symbols) drive
+    # both build paths (single-warp <= 256 used symbols, block otherwise) and
+    # package lists that are not sorted by (weight, tiebreak); the stream
+    # checks the device-built canonical codewords too
+    rng = np.random.default_rng(seed)
+    m = int(rng.integers(2, 300))
+    used = rng.choice(1024, m, replace=False)
+    kind = seed % 3
+    reps = (rng.integers(1, 4, m) if kind == 0 else
+            2 ** rng.integers(0, 12, m) if kind == 1 else rng.geometric(0.05, m))
+    codes = rng.permutation(np.repeat(used, reps)).astype(np.uint32)
+    h = enc.histogram_exact(codes, 512)
+    cb, stream, bits = enc.huffman_encode(codes, h)
+    cl, ostream, obits = oracle.huffman_encode(codes, h.bins)
+    assert np.array_equal(cb.code_lengths, cl) and bits == obits and stream == ostream
+    assert np.array_equal(enc.huffman_decode(cb, stream, codes.size), codes)
