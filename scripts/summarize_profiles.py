@@ -9,7 +9,7 @@ from collections import defaultdict
 
 src, dst = sys.argv[1], sys.argv[2]
 os.makedirs(dst, exist_ok=True)
-SKIP = ("at::", "elementwise", "distribution_", "fill_kernel", "arange")
+SKIP = ("at::", "at_cuda_detail", "elementwise", "distribution_", "fill_kernel", "arange", "quality_leaf")
 
 
 def launches(path):
