@@ -560,35 +560,47 @@ struct DecTables {
     int pad;
 };
 
-__global__ void hf_tables_kernel(const uint8_t* __restrict__ lengths, uint32_t nsym, DecTables* __restrict__ T,
-                                 uint16_t* __restrict__ sym_sorted, unsigned long long* __restrict__ lut) {
+// Decode tables.  Every CTA rebuilds the canonical first-code tables and the
+// (length, symbol)-ordered list of the short (<= LUT_BITS) symbols in shared
+// memory and fills its slice of the LUT from there; CTA 0 also writes the
+// global tables and the full sorted symbol list.
+constexpr int HT_BLOCKS = 16;
+__global__ void __launch_bounds__(256) hf_tables_kernel(const uint8_t* __restrict__ lengths, uint32_t nsym,
+                                                        DecTables* __restrict__ T, uint16_t* __restrict__ sym_sorted,
+                                                        unsigned long long* __restrict__ lut) {
     __shared__ uint32_t cnt[MAXLEN + 1];
     __shared__ uint32_t run[MAXLEN + 1];
-    __shared__ long long s_fc[MAXLEN + 2], s_fi[MAXLEN + 2];
+    __shared__ long long s_fc[MAXLEN + 2], s_fi[MAXLEN + 2], s_lim[MAXLEN + 2];
+    __shared__ int s_maxlen;
+    __shared__ uint16_t s_sym[1 << LUT_BITS];   // symbols of length <= LUT_BITS, (len, sym) order
     const int tid = threadIdx.x;
+    const bool lead = blockIdx.x == 0;
     if (tid <= MAXLEN) { cnt[tid] = 0; run[tid] = 0; }
     __syncthreads();
     for (uint32_t s = tid; s < nsym; s += blockDim.x)
         if (lengths[s] && lengths[s] <= MAXLEN) atomicAdd(&cnt[lengths[s]], 1u);
-    for (uint32_t q = tid; q < (1u << LUT_BITS); q += blockDim.x) lut[q] = 0;
     __syncthreads();
     if (tid == 0) {
         int maxlen = 0;
         for (int l = 1; l <= MAXLEN; l++) if (cnt[l]) maxlen = l;
         long long code = 0, idx = 0;
-        for (int l = 0; l <= MAXLEN + 1; l++) { T->first_code[l] = 0; T->first_idx[l] = 0; T->limit[l] = 0; }
+        for (int l = 0; l <= MAXLEN + 1; l++) { s_fc[l] = 0; s_fi[l] = 0; s_lim[l] = 0; }
         for (int l = 1; l <= maxlen; l++) {  // encode.py:265-273
             code <<= 1;
-            T->first_code[l] = code; s_fc[l] = code;
-            T->first_idx[l] = idx; s_fi[l] = idx;
-            T->limit[l] = code + cnt[l];
+            s_fc[l] = code;
+            s_fi[l] = idx;
+            s_lim[l] = code + cnt[l];
             code += cnt[l];
             idx += cnt[l];
         }
-        T->maxlen = maxlen;
+        s_maxlen = maxlen;
+        if (lead) {
+            for (int l = 0; l <= MAXLEN + 1; l++) { T->first_code[l] = s_fc[l]; T->first_idx[l] = s_fi[l]; T->limit[l] = s_lim[l]; }
+            T->maxlen = maxlen;
+        }
     }
     __syncthreads();
-    // sym_sorted in (len, sym) order + LUT for short codes
+    // (len, sym) order: the short symbols into shared memory (CTA 0: all of them to global)
     if (tid < 32) {
         const int lane = tid;
         for (uint32_t s0 = 0; s0 < nsym; s0 += 32) {
@@ -597,8 +609,9 @@ __global__ void hf_tables_kernel(const uint8_t* __restrict__ lengths, uint32_t n
             const unsigned peers = __match_any_sync(0xffffffffu, len);
             const uint32_t rank = __popc(peers & lanemask_lt());
             if (len && len <= MAXLEN) {
-                const long long r = run[len] + rank;
-                sym_sorted[s_fi[len] + r] = (uint16_t)s;
+                const long long at = s_fi[len] + run[len] + rank;
+                if (len <= LUT_BITS) s_sym[at] = (uint16_t)s;   // short symbols come first in (len, sym) order
+                if (lead) sym_sorted[at] = (uint16_t)s;
             }
             __syncwarp();
             if (len && len <= MAXLEN && rank == 0) run[len] += __popc(peers);
@@ -606,34 +619,34 @@ __global__ void hf_tables_kernel(const uint8_t* __restrict__ lengths, uint32_t n
         }
     }
     __syncthreads();
-    // LUT: canonical decode of every 12-bit window (encode.py:248-253), in
-    // parallel.  Entry = as many complete codewords as the window holds (up
-    // to 4 when every symbol fits 12 bits, else 1): symbols in bits 0-47
-    // (12 each; a lone symbol may use 16), count in 48-50, total length in
-    // 51-54, first length in 55-58.  Count 0: the first code is > 12 bits.
-    const int maxlen = T->maxlen;
+    // LUT: canonical decode of every 12-bit window (encode.py:248-253).
+    // Entry = as many complete codewords as the window holds (up to 4 when
+    // every symbol fits 12 bits, else 1): symbols in bits 0-47 (12 each; a
+    // lone symbol may use 16), count in 48-50, total length in 51-54, first
+    // length in 55-58.  Count 0: the first code is > 12 bits.
+    const int maxlen = s_maxlen;
     const int cap = nsym <= 4096 ? 4 : 1;
-    for (uint32_t q = tid; q < (1u << LUT_BITS); q += blockDim.x) {
+    for (uint32_t q = blockIdx.x * blockDim.x + tid; q < (1u << LUT_BITS); q += gridDim.x * blockDim.x) {
         unsigned long long e = 0;
-        int pos = 0, cnt = 0, len1 = 0;
-        while (cnt < cap && pos < LUT_BITS) {
+        int pos = 0, c = 0, len1 = 0;
+        while (c < cap && pos < LUT_BITS) {
             int got = 0;
             uint32_t sym = 0;
             for (int l = 1; l <= LUT_BITS - pos && l <= maxlen; l++) {
                 const long long code = (long long)((q >> (LUT_BITS - pos - l)) & ((1u << l) - 1u));
-                if (code < T->limit[l]) {
-                    sym = sym_sorted[T->first_idx[l] + code - T->first_code[l]];
+                if (code < s_lim[l]) {
+                    sym = s_sym[s_fi[l] + code - s_fc[l]];
                     got = l;
                     break;
                 }
             }
             if (!got) break;
-            e |= (unsigned long long)sym << (12 * cnt);
-            if (cnt == 0) len1 = got;
-            cnt++;
+            e |= (unsigned long long)sym << (12 * c);
+            if (c == 0) len1 = got;
+            c++;
             pos += got;
         }
-        e |= ((unsigned long long)cnt << 48) | ((unsigned long long)pos << 51) | ((unsigned long long)len1 << 55);
+        e |= ((unsigned long long)c << 48) | ((unsigned long long)pos << 51) | ((unsigned long long)len1 << 55);
         lut[q] = e;
     }
 }
@@ -770,7 +783,7 @@ __global__ void __launch_bounds__(HD_THREADS) hf_sync_coop_kernel(const uint32_t
 // offsets (consecutive symbols of one chunk go to consecutive lanes).  The
 // first true-path error with ordinal < n (encode.py:299-310) is folded in
 // with an atomicMin on (subsequence << 2 | kind).
-constexpr int HD_ROUND = 48;   // symbols per thread and round (smem: 128 x 50 x 2 B + 32 KB LUT)
+constexpr int HD_ROUND = 48;   // symbols per thread and round (smem: 128 x 52 x 2 B + 32 KB LUT)
 
 __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_t* __restrict__ stream,
                                                                    unsigned long long total_bits, uint64_t nsub,
@@ -787,51 +800,64 @@ __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_
                                                                    unsigned long long* __restrict__ best) {
     __shared__ unsigned long long lut[1 << LUT_BITS];
     __shared__ DecTables T;
-    __shared__ uint16_t buf[HD_THREADS][HD_ROUND + 2];
+    __shared__ uint16_t buf[HD_THREADS][HD_ROUND + 4];
     for (int q = threadIdx.x; q < (1 << LUT_BITS); q += blockDim.x) lut[q] = lut_g[q];
     if (threadIdx.x == 0) T = *Tg;
     __syncthreads();
+    (void)end;
+    (void)total_bits;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long o = n, e = 0;
+    unsigned long long o = n;
+    uint32_t todo = 0;   // symbols this thread emits: the sync pass counted them (complete codewords only)
     BitReader r;
     if (t < nsub) {
         o = offs[t];
-        e = end[t];
+        const uint32_t c = cnt[t];
         const uint32_t er = err[t];
-        if (er && o + cnt[t] < n) atomicMin(best, (t << 2) | er);
-        r.init(stream, start[t]);
-    }
-    while (true) {
-        int k = 0;
+        if (er && o + c < n) atomicMin(best, (t << 2) | er);
         if (o < n) {
-            // whole LUT windows (up to 4 symbols) while they stay inside the
-            // subsequence, the stream, the round and the first n symbols
-            const unsigned long long fe = (e < total_bits ? e : total_bits);
-            while (k < HD_ROUND && r.pos < e && o + (unsigned long long)k < n) {
-                if (k <= HD_ROUND - 4 && r.pos + LUT_BITS <= fe && o + (unsigned long long)k + 4 < n) {
-                    const unsigned long long me = lut[r.peek32() >> (32 - LUT_BITS)];
-                    const int mc = lut_cnt(me);
-                    if (mc >= 2) {
-                        uint16_t* bp = &buf[threadIdx.x][k];
-                        bp[0] = (uint16_t)(me & 0xFFFu);
-                        bp[1] = (uint16_t)((me >> 12) & 0xFFFu);
-                        bp[2] = (uint16_t)((me >> 24) & 0xFFFu);
-                        bp[3] = (uint16_t)((me >> 36) & 0xFFFu);
-                        k += mc;
-                        r.skip(lut_len(me));
-                        continue;
+            todo = (uint32_t)min((unsigned long long)c, n - o);
+            r.init(stream, start[t]);
+        }
+    }
+    const bool last = todo && o + todo == n;   // emits symbol n-1: records where it ends
+    uint16_t* bp = buf[threadIdx.x];
+    while (true) {
+        const int want = (int)min(todo, (uint32_t)HD_ROUND);
+        int k = 0;
+        while (k < want) {
+            const uint32_t win = r.peek32();
+            const unsigned long long me = lut[win >> (32 - LUT_BITS)];
+            const int mc = lut_cnt(me);
+            if (mc >= 2 && k + mc <= want) {   // up to 4 whole codewords from one window
+                bp[k] = (uint16_t)(me & 0xFFFu);
+                bp[k + 1] = (uint16_t)((me >> 12) & 0xFFFu);
+                bp[k + 2] = (uint16_t)((me >> 24) & 0xFFFu);
+                bp[k + 3] = (uint16_t)((me >> 36) & 0xFFFu);
+                k += mc;
+                r.skip(lut_len(me));
+                continue;
+            }
+            uint32_t sym = 0;
+            int l = 0;
+            if (mc) {
+                l = (int)((me >> 55) & 15u);
+                sym = (uint32_t)(me & (mc == 1 ? 0xFFFFu : 0xFFFu));
+            } else {   // > LUT_BITS: the canonical first_code / limit walk (encode.py:248-253)
+                for (int q = LUT_BITS + 1; q <= T.maxlen; q++) {
+                    const long long code = (long long)(win >> (32 - q));
+                    if (code < T.limit[q]) {
+                        sym = sym_sorted[T.first_idx[q] + code - T.first_code[q]];
+                        l = q;
+                        break;
                     }
                 }
-                uint32_t sym;
-                const int l = decode_one(r, total_bits, T, lut, sym_sorted, sym);
-                if (l < 0) { e = 0; break; }
-                r.skip(l);
-                buf[threadIdx.x][k++] = (uint16_t)sym;
-                if (o + (unsigned long long)k == n) *end_pos = r.pos;
             }
+            r.skip(l);
+            bp[k++] = (uint16_t)sym;
         }
-        const bool more = (k == HD_ROUND) && r.pos < e && o + (unsigned long long)k < n;
+        todo -= (uint32_t)k;
         __syncthreads();
         // copy-out: warp w owns the chunks of threads 32w..32w+31
         for (int c = 0; c < 32; c++) {
@@ -840,8 +866,9 @@ __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_
             for (int j = lane; j < kc; j += 32) out[oc + j] = buf[warp * 32 + c][j];
         }
         o += k;
-        if (!__syncthreads_or(more)) break;
+        if (!__syncthreads_or(todo != 0)) break;
     }
+    if (last) *end_pos = r.pos;
 }
 
 // Remaining stream checks of encode.py:299-316 (one thread).
@@ -986,7 +1013,7 @@ FZB_API int fzb_huffman_decode(const uint8_t* d_stream, uint64_t nbytes, uint64_
     unsigned long long* scal = reinterpret_cast<unsigned long long*>(p);  // [0]=total [1]=end_pos [2..3]=changed[3] (u32) [4]=best
     cudaMemsetAsync(scal, 0, 64, st);
     cudaMemsetAsync(scal + 4, 0xFF, 8, st);
-    hf_tables_kernel<<<1, 256, 0, st>>>(d_lengths, nsym, T, sym_sorted, lut);
+    hf_tables_kernel<<<HT_BLOCKS, 256, 0, st>>>(d_lengths, nsym, T, sym_sorted, lut);
     const uint32_t* words = reinterpret_cast<const uint32_t*>(d_stream);
     const unsigned blocks = (unsigned)((nsub + HD_THREADS - 1) / HD_THREADS);
     uint32_t* changed = reinterpret_cast<uint32_t*>(scal + 2);
