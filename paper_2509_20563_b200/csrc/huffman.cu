@@ -567,7 +567,8 @@ struct DecTables {
 constexpr int HT_BLOCKS = 16;
 __global__ void __launch_bounds__(256) hf_tables_kernel(const uint8_t* __restrict__ lengths, uint32_t nsym,
                                                         DecTables* __restrict__ T, uint16_t* __restrict__ sym_sorted,
-                                                        unsigned long long* __restrict__ lut) {
+                                                        unsigned long long* __restrict__ lut,
+                                                        uint32_t* __restrict__ lut2) {
     __shared__ uint32_t cnt[MAXLEN + 1];
     __shared__ uint32_t run[MAXLEN + 1];
     __shared__ long long s_fc[MAXLEN + 2], s_fi[MAXLEN + 2], s_lim[MAXLEN + 2];
@@ -648,6 +649,25 @@ __global__ void __launch_bounds__(256) hf_tables_kernel(const uint8_t* __restric
         }
         e |= ((unsigned long long)c << 48) | ((unsigned long long)pos << 51) | ((unsigned long long)len1 << 55);
         lut[q] = e;
+        // sync LUT: every whole codeword of the window (no symbols): count in
+        // bits 0-3, total length 4-7, codeword-start mask 8-19 (bit i: a
+        // codeword starts i bits into the window), first length 20-23
+        uint32_t e2 = 0, mask = 0;
+        int p2 = 0, c2 = 0, f2 = 0;
+        while (p2 < LUT_BITS) {
+            int got = 0;
+            for (int l = 1; l <= LUT_BITS - p2 && l <= maxlen; l++) {
+                const long long code = (long long)((q >> (LUT_BITS - p2 - l)) & ((1u << l) - 1u));
+                if (code < s_lim[l]) { got = l; break; }
+            }
+            if (!got) break;
+            mask |= 1u << p2;
+            if (c2 == 0) f2 = got;
+            c2++;
+            p2 += got;
+        }
+        e2 = (uint32_t)c2 | ((uint32_t)p2 << 4) | (mask << 8) | ((uint32_t)f2 << 20);
+        lut2[q] = e2;
     }
 }
 
@@ -716,20 +736,45 @@ FZB_DEV int decode_one(BitReader& r, unsigned long long total_bits, const DecTab
 // later sweeps restart subsequence t at end[t-1] whenever that differs from
 // its recorded start (in-place, Gauss-Seidel).  A sweep that changes nothing
 // proves start[t] == end[t-1] for every t, i.e. the true codeword path.
+// Every subsequence keeps the bitmap of its codeword starts (256 bits): a
+// restarted decode stops as soon as it lands on a start of the previous
+// path -- from there both paths coincide (Huffman codes resynchronise in a
+// few codewords), so the previous bits, count, end and error carry over and
+// a restart costs a few codewords instead of a whole subsequence.
+constexpr int SYNC_WORDS = SUB / 32;
+
+FZB_DEV uint32_t bits12(const uint32_t* bm, int rel) {
+    const int w = rel >> 5, o = rel & 31;
+    uint32_t v = bm[w] >> o;
+    if (o > 20) v |= bm[w + 1] << (32 - o);
+    return v & 0xFFFu;
+}
+FZB_DEV void setbits(uint32_t* bm, int rel, uint32_t m) {
+    const int w = rel >> 5, o = rel & 31;
+    bm[w] |= m << o;
+    if (o > 20) bm[w + 1] |= m >> (32 - o);
+}
+
 __global__ void __launch_bounds__(HD_THREADS) hf_sync_coop_kernel(const uint32_t* __restrict__ stream,
                                                                   unsigned long long total_bits, uint64_t nsub,
                                                                   const DecTables* __restrict__ Tg,
-                                                                  const unsigned long long* __restrict__ lut_g,
-                                                                  const uint16_t* __restrict__ sym_sorted,
+                                                                  const uint32_t* __restrict__ lut2_g,
+                                                                  uint32_t* __restrict__ bmaps,
                                                                   unsigned long long* start, unsigned long long* end,
                                                                   uint32_t* __restrict__ cnt, uint32_t* __restrict__ err,
                                                                   uint32_t* changed, uint32_t* __restrict__ status,
                                                                   int max_iter) {
-    __shared__ unsigned long long lut[1 << LUT_BITS];
+    __shared__ uint32_t lut2[1 << LUT_BITS];
     __shared__ DecTables T;
-    for (int q = threadIdx.x; q < (1 << LUT_BITS); q += blockDim.x) lut[q] = lut_g[q];
+    __shared__ uint32_t nbm[HD_THREADS][SYNC_WORDS + 1];
+    __shared__ uint32_t obm[HD_THREADS][SYNC_WORDS + 1];
+    for (int q = threadIdx.x; q < (1 << LUT_BITS); q += blockDim.x) lut2[q] = lut2_g[q];
     if (threadIdx.x == 0) T = *Tg;
     __syncthreads();
+    uint32_t* nb = nbm[threadIdx.x];
+    uint32_t* ob = obm[threadIdx.x];
+    nb[SYNC_WORDS] = 0;
+    ob[SYNC_WORDS] = 0;
     cg::grid_group grid = cg::this_grid();
     const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
@@ -738,38 +783,81 @@ __global__ void __launch_bounds__(HD_THREADS) hf_sync_coop_kernel(const uint32_t
         if (gt == 0) changed[(it + 1) % 3] = 0;  // last read two sweeps ago
         for (uint64_t t = gt; t < nsub; t += gs) {
             unsigned long long s;
-            if (it == 0) {
+            const bool fresh = it == 0;
+            if (fresh) {
                 s = t * SUB;
             } else {
                 s = (t == 0) ? 0ull : *(volatile unsigned long long*)(end + t - 1);
                 if (s == start[t]) continue;
                 changed[it % 3] = 1;
+                const uint4* src = reinterpret_cast<const uint4*>(bmaps + t * SYNC_WORDS);
+                const uint4 a = src[0], b = src[1];
+                ob[0] = a.x; ob[1] = a.y; ob[2] = a.z; ob[3] = a.w;
+                ob[4] = b.x; ob[5] = b.y; ob[6] = b.z; ob[7] = b.w;
             }
-            const unsigned long long lim = (t + 1) * (unsigned long long)SUB;
-            // whole windows while every codeword of the window starts before lim
-            const unsigned long long fast_end = (lim < total_bits ? lim : total_bits) - LUT_BITS;
+#pragma unroll
+            for (int w = 0; w < SYNC_WORDS; w++) nb[w] = 0;
+            const unsigned long long base = t * SUB, lim = base + SUB;
+            const unsigned long long stop = lim < total_bits ? lim : total_bits;
             BitReader r;
             r.init(stream, s);
-            uint32_t c = 0, e = 0;
-            while (r.pos < lim && r.pos < total_bits) {
-                if (r.pos <= fast_end && fast_end < lim) {
-                    const unsigned long long me = lut[r.peek32() >> (32 - LUT_BITS)];
-                    if (lut_cnt(me)) {
-                        c += lut_cnt(me);
-                        r.skip(lut_len(me));
-                        continue;
+            uint32_t e = 0;
+            int conv = -1;   // relative bit where the new path joins the previous one
+            while (r.pos < stop) {
+                const uint32_t win = r.peek32();
+                const int rel = (int)(r.pos - base);
+                const uint32_t me = lut2[win >> (32 - LUT_BITS)];
+                const int c = (int)(me & 15u);
+                if (c && r.pos + LUT_BITS <= stop) {   // every codeword of the window starts before lim
+                    const uint32_t mask = (me >> 8) & 0xFFFu;
+                    if (!fresh) {
+                        const uint32_t common = bits12(ob, rel) & mask;
+                        if (common) {
+                            const int i = __ffs(common) - 1;
+                            setbits(nb, rel, mask & ((1u << i) - 1u));
+                            conv = rel + i;
+                            break;
+                        }
                     }
+                    setbits(nb, rel, mask);
+                    r.skip((int)((me >> 4) & 15u));
+                    continue;
                 }
-                uint32_t sym;
-                const int l = decode_one(r, total_bits, T, lut, sym_sorted, sym);
-                if (l < 0) { e = (uint32_t)(-l); break; }
+                if (!fresh && ((ob[rel >> 5] >> (rel & 31)) & 1u)) { conv = rel; break; }
+                int l = 0;
+                if (c) {
+                    l = (int)((me >> 20) & 15u);
+                } else {   // first codeword longer than LUT_BITS (encode.py:248-253)
+                    for (int q = LUT_BITS + 1; q <= T.maxlen; q++) {
+                        const long long code = (long long)(win >> (32 - q));
+                        if (code < T.limit[q]) { l = q; break; }
+                    }
+                    if (!l) { e = (r.pos + (unsigned long long)T.maxlen >= total_bits) ? 1u : 2u; break; }
+                }
+                if (r.pos + (unsigned long long)l > total_bits) { e = 1u; break; }
+                nb[rel >> 5] |= 1u << (rel & 31);
                 r.skip(l);
-                c++;
             }
+            uint32_t c = 0;
+            if (conv >= 0) {   // the previous path's later codewords, end and error carry over
+#pragma unroll
+                for (int w = 0; w < SYNC_WORDS; w++) {
+                    const int lo = conv - 32 * w;
+                    const uint32_t keep = lo <= 0 ? 0xFFFFFFFFu : (lo >= 32 ? 0u : (0xFFFFFFFFu << lo));
+                    nb[w] |= ob[w] & keep;
+                    c += __popc(nb[w]);
+                }
+            } else {
+#pragma unroll
+                for (int w = 0; w < SYNC_WORDS; w++) c += __popc(nb[w]);
+                err[t] = e;
+            }
+            uint4* dst = reinterpret_cast<uint4*>(bmaps + t * SYNC_WORDS);
+            dst[0] = make_uint4(nb[0], nb[1], nb[2], nb[3]);
+            dst[1] = make_uint4(nb[4], nb[5], nb[6], nb[7]);
             start[t] = s;
             cnt[t] = c;
-            err[t] = e;
-            *(volatile unsigned long long*)(end + t) = e ? lim : r.pos;
+            if (conv < 0) *(volatile unsigned long long*)(end + t) = e ? lim : r.pos;
         }
         grid.sync();
         if (it > 0 && *(volatile uint32_t*)(changed + (it % 3)) == 0) break;
@@ -983,8 +1071,9 @@ FZB_API size_t fzb_huffman_decode_workspace_bytes(uint64_t nbytes, uint32_t nsym
     const uint64_t nsub = (nbytes * 8 + SUB - 1) / SUB + 1;
     // tables + sym_sorted + lut + 2x(start,end,cnt,err) + offs + scalars
     return align256(sizeof(DecTables)) + align256((size_t)nsym * 2) + align256((1u << LUT_BITS) * 8) +
-           2 * (2 * align256(nsub * 8) + 2 * align256(nsub * 4)) + align256(nsub * 8) +
-           align256(fzscan::ws_bytes(nsub)) + 1024;
+           align256((1u << LUT_BITS) * 4) + align256(nsub * SYNC_WORDS * 4) +
+           2 * align256(nsub * 8) + 2 * align256(nsub * 4) + align256(nsub * 8) + align256(fzscan::ws_bytes(nsub)) +
+           1024;
 }
 
 // d_stream must be readable (zero) for 8 bytes past nbytes.
@@ -1001,19 +1090,19 @@ FZB_API int fzb_huffman_decode(const uint8_t* d_stream, uint64_t nbytes, uint64_
     DecTables* T = reinterpret_cast<DecTables*>(p); p += align256(sizeof(DecTables));
     uint16_t* sym_sorted = reinterpret_cast<uint16_t*>(p); p += align256((size_t)nsym * 2);
     unsigned long long* lut = reinterpret_cast<unsigned long long*>(p); p += align256((1u << LUT_BITS) * 8);
-    unsigned long long* st_[2]; unsigned long long* en_[2]; uint32_t* cn_[2]; uint32_t* er_[2];
-    for (int b = 0; b < 2; b++) {
-        st_[b] = reinterpret_cast<unsigned long long*>(p); p += align256(nsub * 8);
-        en_[b] = reinterpret_cast<unsigned long long*>(p); p += align256(nsub * 8);
-        cn_[b] = reinterpret_cast<uint32_t*>(p); p += align256(nsub * 4);
-        er_[b] = reinterpret_cast<uint32_t*>(p); p += align256(nsub * 4);
-    }
+    uint32_t* lut2 = reinterpret_cast<uint32_t*>(p); p += align256((1u << LUT_BITS) * 4);
+    uint32_t* bmaps = reinterpret_cast<uint32_t*>(p); p += align256(nsub * SYNC_WORDS * 4);
+    unsigned long long* st_[1]; unsigned long long* en_[1]; uint32_t* cn_[1]; uint32_t* er_[1];
+    st_[0] = reinterpret_cast<unsigned long long*>(p); p += align256(nsub * 8);
+    en_[0] = reinterpret_cast<unsigned long long*>(p); p += align256(nsub * 8);
+    cn_[0] = reinterpret_cast<uint32_t*>(p); p += align256(nsub * 4);
+    er_[0] = reinterpret_cast<uint32_t*>(p); p += align256(nsub * 4);
     unsigned long long* offs = reinterpret_cast<unsigned long long*>(p); p += align256(nsub * 8);
     void* scan_ws = p; p += align256(fzscan::ws_bytes(nsub));
     unsigned long long* scal = reinterpret_cast<unsigned long long*>(p);  // [0]=total [1]=end_pos [2..3]=changed[3] (u32) [4]=best
     cudaMemsetAsync(scal, 0, 64, st);
     cudaMemsetAsync(scal + 4, 0xFF, 8, st);
-    hf_tables_kernel<<<HT_BLOCKS, 256, 0, st>>>(d_lengths, nsym, T, sym_sorted, lut);
+    hf_tables_kernel<<<HT_BLOCKS, 256, 0, st>>>(d_lengths, nsym, T, sym_sorted, lut, lut2);
     const uint32_t* words = reinterpret_cast<const uint32_t*>(d_stream);
     const unsigned blocks = (unsigned)((nsub + HD_THREADS - 1) / HD_THREADS);
     uint32_t* changed = reinterpret_cast<uint32_t*>(scal + 2);
@@ -1033,7 +1122,7 @@ FZB_API int fzb_huffman_decode(const uint8_t* d_stream, uint64_t nbytes, uint64_
     unsigned long long* ep = en_[0];
     uint32_t* cp = cn_[0];
     uint32_t* erp = er_[0];
-    void* kargs[] = {(void*)&words, (void*)&total_bits, (void*)&nsub, (void*)&T, (void*)&lut, (void*)&sym_sorted,
+    void* kargs[] = {(void*)&words, (void*)&total_bits, (void*)&nsub, (void*)&T, (void*)&lut2, (void*)&bmaps,
                      (void*)&sp, (void*)&ep, (void*)&cp, (void*)&erp, (void*)&changed, (void*)&d_status,
                      (void*)&max_iter};
     cudaLaunchCooperativeKernel((const void*)hf_sync_coop_kernel, dim3(gridc), dim3(HD_THREADS), kargs, 0, st);
