@@ -36,6 +36,13 @@ extern "C" {
 #define FZB_E_ARG (-1003)       /* invalid argument */
 
 FZB_API int fzb_abi_version(void);
+/* Record a CUDA event on a stream; external = 1 makes it an event-record node
+ * when the stream is being captured into a CUDA graph (per-kernel timing of
+ * replayed graphs). */
+FZB_API int fzb_event_create(void **event);
+FZB_API int fzb_event_destroy(void *event);
+FZB_API int fzb_event_record(void *event, void *stream, int external);
+FZB_API int fzb_event_elapsed_ms(void *start, void *stop, float *ms);
 
 /* ---- a1: bound resolution (pipeline.py:360-364, core.py:155-170) ------- */
 /* Exact f32 min/max of d_in[0..n) -> d_lohi[0..1]; sets FZB_ERR_NONFINITE. */

@@ -68,6 +68,10 @@ def load():
                              ctypes.c_size_t)
     sig = {
         "fzb_abi_version": (I, []),
+        "fzb_event_create": (I, [P]),
+        "fzb_event_destroy": (I, [P]),
+        "fzb_event_record": (I, [P, P, I]),
+        "fzb_event_elapsed_ms": (I, [P, P, P]),
         "fzb_minmax_workspace_bytes": (SZ, [U64]),
         "fzb_minmax_f32": (I, [P, U64, P, P, SZ, P, P]),
         "fzb_resolve_bound": (I, [P, I, D, P, P]),
@@ -104,7 +108,7 @@ def load():
 
 
 EXPORTED = [
-    "fzb_abi_version", "fzb_minmax_workspace_bytes", "fzb_minmax_f32", "fzb_resolve_bound",
+    "fzb_abi_version", "fzb_event_create", "fzb_event_destroy", "fzb_event_record", "fzb_event_elapsed_ms", "fzb_minmax_workspace_bytes", "fzb_minmax_f32", "fzb_resolve_bound",
     "fzb_lorenzo_workspace_bytes", "fzb_lorenzo_encode_f32", "fzb_lorenzo_decode_f32",
     "fzb_lorenzo_batch_workspace_bytes", "fzb_lorenzo_encode_batch_f32", "fzb_lorenzo_decode_batch_f32",
     "fzb_interp_encode_f32",

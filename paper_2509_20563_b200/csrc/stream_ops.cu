@@ -340,6 +340,19 @@ extern "C" {
 
 FZB_API int fzb_abi_version(void) { return 1; }
 
+// Timing inside CUDA graphs: an event recorded during stream capture with
+// cudaEventRecordExternal becomes an event-record node, so a replayed graph
+// still reports per-kernel times (cudaEventElapsedTime after the replay).
+FZB_API int fzb_event_create(void** event) { return (int)cudaEventCreate(reinterpret_cast<cudaEvent_t*>(event)); }
+FZB_API int fzb_event_destroy(void* event) { return (int)cudaEventDestroy((cudaEvent_t)event); }
+FZB_API int fzb_event_record(void* event, void* stream, int external) {
+    return (int)cudaEventRecordWithFlags((cudaEvent_t)event, (cudaStream_t)stream,
+                                         external ? cudaEventRecordExternal : cudaEventRecordDefault);
+}
+FZB_API int fzb_event_elapsed_ms(void* start, void* stop, float* ms) {
+    return (int)cudaEventElapsedTime(ms, (cudaEvent_t)start, (cudaEvent_t)stop);
+}
+
 FZB_API size_t fzb_minmax_workspace_bytes(uint64_t) { return (size_t)MM_BLOCKS * 2 * sizeof(float); }
 
 FZB_API int fzb_minmax_f32(const float* d_in, uint64_t n, float* d_lohi, void* d_ws, size_t ws_bytes,

@@ -69,6 +69,28 @@ def _align(n: int, a: int = 256) -> int:
     return (int(n) + a - 1) // a * a
 
 
+class _NodeEvent:
+    """A CUDA event recorded as an event-record node of a captured graph
+    (torch.cuda.Event creates its handle lazily, at the first record)."""
+
+    def __init__(self, lib):
+        self.lib = lib
+        h = ctypes.c_void_p()
+        _lib.check(lib.fzb_event_create(ctypes.byref(h)), "fzb_event_create")
+        self.h = h
+
+    def elapsed_time(self, end: "_NodeEvent") -> float:
+        ms = ctypes.c_float()
+        _lib.check(self.lib.fzb_event_elapsed_ms(self.h, end.h, ctypes.byref(ms)), "fzb_event_elapsed_ms")
+        return float(ms.value)
+
+    def __del__(self):
+        try:
+            self.lib.fzb_event_destroy(self.h)
+        except Exception:
+            pass
+
+
 @dataclass
 class DeviceArchive:
     """Device-resident compression result (before `Engine.finish`)."""
@@ -99,6 +121,10 @@ class Engine:
         self._inflight: list = []  # pinned sources of queued H2D copies (dropped at the next sync)
         self.launches = 0  # kernels issued through the C ABI (counted per entry point)
         self.trace = None  # list -> (entry point, start event, end event) per call
+        self._graphs: dict = {}  # captured CUDA graphs (see compress_graphed / decompress_graphed)
+        self._capturing = False
+        self.trace_only = None  # set of entry points to time (None: all); each timed call costs two events
+        self._pending: list = []  # traced calls of replayed graphs, timed at the next sync
 
     # ------------------------------------------------------------ buffers
     def buf(self, name: str, nbytes: int, zero: bool = False, zero_new: bool = False) -> torch.Tensor:
@@ -128,17 +154,27 @@ class Engine:
     def _sync(self):
         self.stream.synchronize()
         self._inflight.clear()
+        if self._pending:   # graph replays done: their event-record nodes hold this replay's times
+            if self.trace is not None:
+                self.trace.extend((fn, e0.elapsed_time(e1)) for fn, e0, e1 in self._pending)
+            self._pending.clear()
 
     @property
     def sp(self):
         return ctypes.c_void_p(self.stream.cuda_stream)
 
     def _call(self, fn: str, *args, nk: int = 1):
-        if self.trace is not None:
+        if self.trace is not None and (self.trace_only is None or fn in self.trace_only):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(self.stream)
-            rc = getattr(self.lib, fn)(*args)
-            e1.record(self.stream)
+            if self._capturing:   # event-record nodes inside the graph
+                e0, e1 = _NodeEvent(self.lib), _NodeEvent(self.lib)
+                _lib.check(self.lib.fzb_event_record(e0.h, self.sp, 1), "fzb_event_record")
+                rc = getattr(self.lib, fn)(*args)
+                _lib.check(self.lib.fzb_event_record(e1.h, self.sp, 1), "fzb_event_record")
+            else:
+                e0.record(self.stream)
+                rc = getattr(self.lib, fn)(*args)
+                e1.record(self.stream)
             self.trace.append((fn, e0, e1))
         else:
             rc = getattr(self.lib, fn)(*args)
@@ -389,6 +425,59 @@ class Engine:
                        _p(lzws), lzws.numel(), sp, nk=5)
         return out
 
+    # ------------------------------------------------------------- graphs
+    # The device half of a pipeline is a fixed DAG of C-ABI launches whose
+    # arguments depend only on the shape, the bound magnitude and (decode) the
+    # segment sizes: captured once into a CUDA graph, it replays with one
+    # launch instead of ~10-30 ctypes calls (CUDA graphs in place of the
+    # reference's CUDASTF task graph, graph.py:96-172).  Needs an engine on a
+    # non-default stream (graph_engine()); the input tensor is the graph's
+    # static input, so callers copy new data into the same tensor.
+    def _graphed(self, key, enqueue):
+        ent = self._graphs.get(key)
+        if ent is not None and ent[4] != self.trace_only:   # captured with other timing nodes
+            ent = None
+        if ent is None:
+            if self.stream.cuda_stream == 0:
+                raise ValueError("CUDA graph capture needs an engine on a non-default stream (graph_engine())")
+            res = enqueue()          # eager warm-up: allocates every cached buffer the capture will use
+            self._sync()
+            l0 = self.launches
+            g = torch.cuda.CUDAGraph()
+            traced = self.trace
+            self.trace = []          # always capture timing nodes: replays can be traced later
+            self._capturing = True
+            try:
+                with torch.cuda.graph(g, stream=self.stream):
+                    res = enqueue()
+            finally:
+                self._capturing = False
+                tr, self.trace = self.trace, traced
+            ent = (g, res, self.launches - l0, tr, self.trace_only)
+            self._graphs[key] = ent
+            if len(self._graphs) > 16:   # a few shapes at a time
+                self._graphs.pop(next(iter(self._graphs)))
+        g, res, nk, tr, _ = ent
+        with torch.cuda.stream(self.stream):
+            g.replay()
+        self.launches += nk
+        if self.trace is not None:
+            self._pending.extend(tr)
+        return res
+
+    def compress_graphed(self, x: torch.Tensor, dims, eb_mode: int, magnitude: float, **kw) -> DeviceArchive:
+        """compress() as one CUDA-graph launch (captured on first use per
+        input tensor / shape / bound / pipeline)."""
+        key = ("c", x.data_ptr(), tuple(dims), int(eb_mode), float(magnitude), tuple(sorted(kw.items())))
+        return self._graphed(key, lambda: self.compress(x, dims, eb_mode, magnitude, **kw))
+
+    def decompress_graphed(self, da: DeviceArchive, sz: dict, eb_abs: float, out: torch.Tensor) -> torch.Tensor:
+        """decompress_resident() as one CUDA-graph launch (per archive buffers
+        and segment sizes)."""
+        key = ("d", id(da.bufs["codes"]), da.pipeline_id, da.dims, da.codec, da.predictor, int(sz["size"]),
+               int(sz["k"]), float(eb_abs), out.data_ptr())
+        return self._graphed(key, lambda: self.decompress_resident(da, sz, eb_abs, out))
+
     # ------------------------------------------------------------- batches
     def compress_batch(self, X: torch.Tensor, dims, eb_mode: int, magnitude: float, *, pipeline_id: int = 0,
                        predictor: str = "lorenzo", codec: str = "huffman", radius: int = 512) -> list:
@@ -560,6 +649,21 @@ class Engine:
 
 
 _engines: dict = {}
+
+
+_graph_engines: dict = {}
+
+
+def graph_engine() -> Engine:
+    """Per-device engine on a private stream, for the CUDA-graph paths."""
+    dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
+    if dev < 0:
+        raise E.DeviceUnavailable("no CUDA device: the B200 path has no CPU fallback")
+    eng = _graph_engines.get(dev)
+    if eng is None:
+        eng = Engine(torch.device("cuda", dev), torch.cuda.Stream(dev))
+        _graph_engines[dev] = eng
+    return eng
 
 
 def default_engine() -> Engine:

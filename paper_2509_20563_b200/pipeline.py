@@ -28,7 +28,7 @@ from .core import (
     SEG_OUTLIER_INDICES, SEG_OUTLIER_VALUES, SEG_SECONDARY_WRAPPED, Archive, ErrorBoundSpec, ErrorMode, Field,
     ResolvedBound, attach_wire, eb_from_range, register_known_pipeline_id,
 )
-from .device import default_engine, interp_applicable
+from .device import default_engine, graph_engine, interp_applicable
 
 log = logging.getLogger(__name__)
 
@@ -226,20 +226,22 @@ def _to_device(field) -> torch.Tensor:
     return buf[: 4 * field.len].view(torch.float32)
 
 
-def compress_device(x: torch.Tensor, dims, eb: ErrorBoundSpec, pipeline) -> Archive:
-    """Compress a device-resident f32 tensor (the timed path)."""
+def compress_device(x: torch.Tensor, dims, eb: ErrorBoundSpec, pipeline, *, graph: bool = False) -> Archive:
+    """Compress a device-resident f32 tensor (the timed path).  graph=True
+    replays the whole device DAG as one captured CUDA graph (graph_engine();
+    `x` is then the graph's static input: keep passing the same tensor)."""
 
     spec = get_pipeline(pipeline)
     _check_stage_params(spec)
-    eng = default_engine()
+    eng = graph_engine() if graph else default_engine()
     pred = spec.predictor
     cfg = spec.interp_config() if pred == "interp" else None
     if pred == "interp" and not interp_applicable(dims, cfg.anchor_stride):
         log.warning("interpolation needs a 2D or 3D field with every extent >= %d, got dims %s; "
                     "falling back to Lorenzo", cfg.anchor_stride + 1, tuple(dims))
-    da = eng.compress(x, dims, int(eb.mode), float(eb.magnitude), pipeline_id=spec.id, predictor=pred,
-                      codec=spec.primary_codec, radius=spec.radius(),
-                      anchor_stride=cfg.anchor_stride if cfg else 16)
+    run = eng.compress_graphed if graph else eng.compress
+    da = run(x, dims, int(eb.mode), float(eb.magnitude), pipeline_id=spec.id, predictor=pred,
+             codec=spec.primary_codec, radius=spec.radius(), anchor_stride=cfg.anchor_stride if cfg else 16)
     return _archive_of(eng, da, spec, eb, dims)
 
 
@@ -283,9 +285,16 @@ def compress(field: Field, eb: ErrorBoundSpec, pipeline) -> Archive:
 
 
 def compress_via_graph(field: Field, eb: ErrorBoundSpec, pipeline, workers: int | None = None) -> Archive:
-    """Graph variant (pipeline.py:650-660).  On the GPU every stage is already
-    a stream-ordered DAG; archives are byte-identical to compress()."""
-    return compress(field, eb, pipeline)
+    """Graph variant (pipeline.py:650-660): the device DAG runs as one CUDA
+    graph, captured per shape / bound / pipeline on first use and replayed
+    for later fields (the H2D lands in the graph's static input).  Archives
+    are byte-identical to compress(); `workers` has no GPU meaning."""
+    eng = graph_engine()
+    x = eng.buf("graph_in_%s" % "x".join(map(str, field.dims)), 4 * field.len)[: 4 * field.len].view(torch.float32)
+    src = torch.from_numpy(field.data)
+    with torch.cuda.stream(eng.stream):
+        x.copy_(src, non_blocking=src.is_pinned())
+    return compress_device(x, field.dims, eb, pipeline, graph=True)
 
 
 # ---------------------------------------------------------------- decompress

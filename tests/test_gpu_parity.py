@@ -273,3 +273,47 @@ def test_wire_block_is_the_serialized_archive(preset):
     b = fz.parse_archive(buf)
     assert b == a
     assert fz.decompress(b).data.tobytes() == fz.decompress(a).data.tobytes()
+
+
+@pytest.mark.parametrize("preset,dims", [("default", (40, 48, 64)), ("speed", (33, 40, 64)), ("quality", (96, 160)),
+                                         ("default", (20_000,))])
+def test_cuda_graph_round_trip(preset, dims):
+    # the captured device DAG replays on new input data (static input
+    # tensor) and yields the eager path's archive and reconstruction
+    import torch
+    from paper_2509_20563_b200.data import smooth_trig_host
+    from paper_2509_20563_b200.device import graph_engine, pad3
+    from paper_2509_20563_b200.pipeline import get_pipeline
+    eng = graph_engine()
+    spec = get_pipeline(preset)
+    kw = dict(pipeline_id=spec.id, predictor=spec.predictor, codec=spec.primary_codec, radius=spec.radius())
+    n = int(np.prod(dims))
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    out = torch.empty(n, dtype=torch.float32, device="cuda")
+    eb = fz.ErrorBoundSpec(fz.ErrorMode.VALUE_RANGE_RELATIVE, 1e-4)
+    for seed in range(3):
+        host = smooth_trig_host(dims, seed)
+        with torch.cuda.stream(eng.stream):
+            x.copy_(torch.from_numpy(host))
+        da = eng.compress_graphed(x, dims, 1, 1e-4, **kw)
+        lo, hi, segs, _ = eng.finish(da)
+        ref = fz.compress(fz.Field(dims, host), eb, preset)
+        assert [(k, bytes(p)) for k, p in segs] == [(k, bytes(p)) for k, p in ref.segments]
+        sz = eng.sizes(da)
+        eng.decompress_graphed(da, sz, 1e-4 * (sz["hi"] - sz["lo"]), out)
+        eng._sync()
+        assert out.cpu().numpy().tobytes() == fz.decompress(ref).data.tobytes()
+
+
+@pytest.mark.parametrize("preset", ["default", "speed", "quality"])
+def test_graph_variants_bytes_equal_sequential(preset):
+    # pipeline.py:650-660 / 583-591 graph variants: bytewise identical to the
+    # sequential calls (test_pipeline.py:281-297); here they replay CUDA graphs
+    from paper_2509_20563_b200.data import smooth_trig_host
+    dims = (48, 40, 64)
+    eb = fz.ErrorBoundSpec(fz.ErrorMode.VALUE_RANGE_RELATIVE, 1e-4)
+    for seed in range(2):
+        f = fz.Field(dims, smooth_trig_host(dims, seed))
+        a = fz.compress_via_graph(f, eb, preset)
+        assert fz.serialize_archive(a) == fz.serialize_archive(fz.compress(f, eb, preset))
+        assert fz.decompress_via_graph(a).data.tobytes() == fz.decompress(a).data.tobytes()
