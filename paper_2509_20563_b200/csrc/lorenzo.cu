@@ -1123,7 +1123,7 @@ __global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__
     long long t = 0;
     float r = 0.f;
 #ifdef LZ7_TIMING
-    long long ph[6] = {0, 0, 0, 0, 0, 0};
+    long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long c0 = clock64();
 #define WSTAMP(i) do { const long long c1 = clock64(); ph[i] += c1 - c0; c0 = c1; } while (0)
 #else
@@ -1187,6 +1187,9 @@ __global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__
         }
         WSTAMP(2);
         while (found < 0 && t < n) {
+#ifdef LZ7_TIMING
+            ph[4]++;
+#endif
             const long long sb = t / BS2;
             if (t % BS2 == 0) {  // probe 32 superblocks
                 const long long sq = sb + lane;
@@ -1202,6 +1205,9 @@ __global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__
             if (sbt == sb_cur) { lo = pmin[0]; hi = pmax[0]; }
             else if (sbt == sb_cur + 1) { lo = pmin[1]; hi = pmax[1]; }
             else {
+#ifdef LZ7_TIMING
+                ph[5]++;
+#endif
                 const long long bb = sbt * 32 + lane;
                 lo = bb < nblk ? __ldcg(bmin + bb) : INFINITY;
                 hi = bb < nblk ? __ldcg(bmax + bb) : -INFINITY;
@@ -1214,6 +1220,9 @@ __global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__
             const long long fb = sbt * 32 + (__ffs(nsk) - 1);
             t = fb * BS1;
             const long long be = min(n, t + BS1);
+#ifdef LZ7_TIMING
+            ph[6]++;
+#endif
             found = scan(t, be);
             t = be;
         }
@@ -1223,7 +1232,7 @@ __global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__
     }
 #ifdef LZ7_TIMING
     if (lane == 0)
-        for (int i = 0; i < 4; i++) g_walk_stamp[i] = ph[i];
+        for (int i = 0; i < 8; i++) g_walk_stamp[i] = ph[i];
 #endif
 }
 

@@ -22,4 +22,5 @@ buf = np.zeros(8, np.int64)
 lib.fzb_debug_walk_timing(buf.ctypes.data_as(ctypes.c_void_p))
 ev = int((codes[:n] != 512).sum()) + int(bitmap.view(torch.uint32).to(torch.int64).bitwise_count().sum()) if hasattr(torch.Tensor, 'bitwise_count') else int((codes[:n] != 512).sum())
 print("encode ms", e0.elapsed_time(e1), "events~", ev, "phases (Mcycles): event", buf[0] / 1e6, "interval", buf[1] / 1e6,
-      "block-rest", buf[2] / 1e6, "probe+scan", buf[3] / 1e6)
+      "block-rest", buf[2] / 1e6, "probe+scan", buf[3] / 1e6, "| loop iters", buf[4], "summary loads", buf[5],
+      "block scans", buf[6])
