@@ -45,6 +45,10 @@ struct BuildWS {
 
 #ifdef LZ7_TIMING
 __device__ uint32_t g_hf_serial_levels;
+__device__ long long g_hf_build_stamp[8];
+#define HB_STAMP(i) do { if ((threadIdx.x & 31) == 0) g_hf_build_stamp[i] = clock64(); } while (0)
+#else
+#define HB_STAMP(i) do { } while (0)
 #endif
 FZB_DEV bool key_less(unsigned long long wa, uint32_t ta, unsigned long long wb, uint32_t tb) {
     return wa < wb || (wa == wb && ta < tb);
@@ -81,6 +85,7 @@ FZB_DEV void build_warp(uint32_t m, uint32_t nsym, const unsigned long long* in_
                         unsigned long long* s_first) {
     extern __shared__ __align__(16) unsigned char sm_build[];
     const int lane = threadIdx.x & 31;
+    HB_STAMP(0);
     // the compacted (w, s) list may alias this layout: move it through registers
     unsigned long long rw[WARP_BUILD_MAX / 32];
     uint32_t rs[WARP_BUILD_MAX / 32];
@@ -126,6 +131,7 @@ FZB_DEV void build_warp(uint32_t m, uint32_t nsym, const unsigned long long* in_
             }
             __syncwarp();
         }
+    HB_STAMP(1);
     // 3. levels.  M_0 = base.  Once M_l == M_{l-1} (weights, tiebreaks and
     // leaf marks) every later level repeats it: stop and reuse its marks.
     unsigned long long* mw2 = reinterpret_cast<unsigned long long*>(sm_build + WB_MW2);
@@ -189,6 +195,10 @@ FZB_DEV void build_warp(uint32_t m, uint32_t nsym, const unsigned long long* in_
             }
         }
     }
+    HB_STAMP(2);
+#ifdef LZ7_TIMING
+    if (lane == 0) g_hf_build_stamp[7] = lfix;
+#endif
     // 4. selected prefixes, top level down
     long long L = 2 * ((long long)m - 1);
     for (int l = MAXLEN - 1; l >= 1; l--) {
@@ -203,6 +213,7 @@ FZB_DEV void build_warp(uint32_t m, uint32_t nsym, const unsigned long long* in_
     }
     if (lane == 0) s_nb[0] = L;
     __syncwarp();
+    HB_STAMP(3);
     // 5. lengths and bit count
     unsigned long long bits = 0;
     if (lane <= MAXLEN) s_cnt[lane] = 0;
@@ -218,6 +229,7 @@ FZB_DEV void build_warp(uint32_t m, uint32_t nsym, const unsigned long long* in_
     for (int o = 16; o; o >>= 1) bits += __shfl_xor_sync(0xffffffffu, bits, o);
     if (lane == 0) *bit_count = bits;
     __syncwarp();
+    HB_STAMP(4);
     // 6. canonical codewords by (length, symbol)  (encode.py:155-171)
     if (lane == 0) {
         unsigned long long code = 0;
@@ -240,6 +252,7 @@ FZB_DEV void build_warp(uint32_t m, uint32_t nsym, const unsigned long long* in_
         if (len && rank == 0) s_cnt[len] += __popc(peers);
         __syncwarp();
     }
+    HB_STAMP(5);
 }
 
 __global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long long* __restrict__ bins, uint32_t nsym,
@@ -991,6 +1004,9 @@ size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 extern "C" {
 
 #ifdef LZ7_TIMING
+FZB_API int fzb_debug_hf_build(long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, g_hf_build_stamp, sizeof(g_hf_build_stamp));
+}
 FZB_API int fzb_debug_hf_serial(uint32_t* out) {
     return (int)cudaMemcpyFromSymbol(out, g_hf_serial_levels, 4);
 }

@@ -29,3 +29,12 @@ for name, used in cases.items():
         if it >= 2:
             ts.append(e0.elapsed_time(e1) * 1e3)
     print(name, "build us median %.1f min %.1f" % (np.median(ts), np.min(ts)))
+    if os.environ.get("FZB_SO"):   # -DLZ7_TIMING build: cycle stamps of the single-warp path
+        import ctypes
+        dbg = ctypes.CDLL(os.environ["FZB_SO"])
+        buf = np.zeros(8, np.int64)
+        dbg.fzb_debug_hf_build(buf.ctypes.data_as(ctypes.c_void_p))
+        d = np.diff(buf[:6])
+        print("   cycles: sort", d[0], "levels", d[1], "prefixes", d[2], "lengths", d[3], "codewords", d[4],
+              "fixed point at level", buf[7])
+
