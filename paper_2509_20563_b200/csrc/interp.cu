@@ -13,12 +13,32 @@
 
 namespace {
 
+// q / d for 32-bit q by a multiply-high (round-up method, exact for every
+// 32-bit q): the lattice index decomposition ran two 64-bit divisions per
+// target, the bulk of the passes' instructions.
+struct FastDiv {
+    uint32_t d, m;
+    int l;
+};
+FastDiv fastdiv(uint32_t d) {
+    FastDiv f;
+    f.d = d;
+    f.l = 0;
+    while ((1ull << f.l) < d) f.l++;
+    f.m = (uint32_t)((((1ull << 32) * ((1ull << f.l) - d)) / d) + 1);
+    return f;
+}
+FZB_DEV uint32_t fdiv(uint32_t q, const FastDiv& f) {
+    return (uint32_t)(((unsigned long long)__umulhi(f.m, q) + q) >> f.l);
+}
+
 struct Pass {
     long long n0, n1, n2;
     long long h;
     // target lattice: start/step/count per axis
     long long s0, d0, c0, s1, d1, c1, s2, d2, c2;
     long long total;
+    FastDiv f1, f2;   // by c1, c2 (valid when total < 2^32)
 };
 
 FZB_DEV double interp_pred(const float* __restrict__ r, long long t, long long c, long long n, long long sh,
@@ -44,10 +64,20 @@ __global__ void __launch_bounds__(256) interp_pass_kernel(const float* __restric
     const double w[4] = {w0, w1, w2, w3};
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < p.total; q += stride) {
-        const long long q2 = q % p.c2;
-        const long long r1 = q / p.c2;
-        const long long q1 = r1 % p.c1;
-        const long long q0 = r1 / p.c1;
+        long long q0, q1, q2;
+        if (p.total <= 0xFFFFFFFFll) {
+            const uint32_t u = (uint32_t)q;
+            const uint32_t r1 = fdiv(u, p.f2);
+            q2 = (long long)(u - r1 * p.f2.d);
+            const uint32_t z0 = fdiv(r1, p.f1);
+            q1 = (long long)(r1 - z0 * p.f1.d);
+            q0 = z0;
+        } else {
+            q2 = q % p.c2;
+            const long long r1 = q / p.c2;
+            q1 = r1 % p.c1;
+            q0 = r1 / p.c1;
+        }
         const long long i = p.s0 + q0 * p.d0, j = p.s1 + q1 * p.d1, k = p.s2 + q2 * p.d2;
         const long long t = (i * p.n1 + j) * p.n2 + k;
         double pred;
@@ -101,6 +131,10 @@ Pass make_pass(long long n0, long long n1, long long n2, long long h, int axis) 
     p.c1 = cnt(p.s1, p.d1, n1);
     p.c2 = cnt(p.s2, p.d2, n2);
     p.total = p.c0 * p.c1 * p.c2;
+    if (p.total > 0 && p.total <= 0xFFFFFFFFll) {
+        p.f1 = fastdiv((uint32_t)p.c1);
+        p.f2 = fastdiv((uint32_t)p.c2);
+    }
     return p;
 }
 
