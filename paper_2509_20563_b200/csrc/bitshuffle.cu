@@ -20,6 +20,7 @@
 // decoupled look-back *before* the transposes, which then hide the
 // look-back latency.  The decoder runs the same network backwards.
 #include "common.cuh"
+#include "scan.cuh"
 
 namespace {
 
@@ -383,36 +384,27 @@ __global__ void __launch_bounds__(BS_THREADS) bs_enc4_kernel(const uint16_t* __r
     }
 }
 
-// Per-CTA word counts of the decoder (bitmap popcounts), then one scan.
-__global__ void __launch_bounds__(BS_THREADS) bs_dec_count_kernel(const uint32_t* __restrict__ bitmap, uint64_t nblocks,
-                                                                  uint32_t* __restrict__ counts) {
-    __shared__ uint32_t tmp[33];
-    uint32_t c = 0;
-    const uint64_t w0 = (uint64_t)blockIdx.x * BS_BPC * 4;
-    for (int e = threadIdx.x; e < BS_BPC * 4; e += blockDim.x)
-        if (w0 + e < nblocks * 4) c += __popc(bitmap[w0 + e]);
-    uint32_t tot;
-    block_exclusive_scan(c, tmp, &tot);
-    if (threadIdx.x == 0) counts[blockIdx.x] = tot;
+// Per-chunk word counts of the decoder (bitmap popcounts): one warp per
+// chunk of BS_BPC blocks (128 bitmap words, one uint4 per lane).
+__global__ void __launch_bounds__(256) bs_dec_count2_kernel(const uint32_t* __restrict__ bitmap, uint64_t nblocks,
+                                                            uint64_t nchunks, uint32_t* __restrict__ counts) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t c = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (c >= nchunks) return;
+    const uint64_t blk = c * BS_BPC + lane;   // BS_BPC == 32: one block (4 words) per lane
+    uint32_t v = 0;
+    if (blk < nblocks) {
+        const uint4 bm = __ldg(reinterpret_cast<const uint4*>(bitmap) + blk);
+        v = __popc(bm.x) + __popc(bm.y) + __popc(bm.z) + __popc(bm.w);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) counts[c] = v;
 }
 
-__global__ void scan_counts_u64_kernel(const uint32_t* __restrict__ cnt, uint64_t m,
-                                       unsigned long long* __restrict__ offs, unsigned long long* __restrict__ tot,
-                                       uint64_t payload_words, uint32_t* __restrict__ status) {
-    __shared__ unsigned long long tmp[33];
-    unsigned long long carry = 0;
-    for (uint64_t b0 = 0; b0 < m; b0 += blockDim.x) {
-        const uint64_t q = b0 + threadIdx.x;
-        const unsigned long long x = q < m ? cnt[q] : 0ull;
-        unsigned long long t;
-        const unsigned long long p = block_exclusive_scan64(x, tmp, &t);
-        if (q < m) offs[q] = carry + p;
-        carry += t;
-    }
-    if (threadIdx.x == 0) {
-        *tot = carry;
-        if (carry != payload_words) set_err(status, FZB_ERR_BS_MISMATCH);   // encode.py:372-375
-    }
+__global__ void bs_check_kernel(const unsigned long long* __restrict__ tot, uint64_t payload_words,
+                                uint32_t* __restrict__ status) {
+    if (*tot != payload_words) set_err(status, FZB_ERR_BS_MISMATCH);   // encode.py:372-375
 }
 
 __global__ void __launch_bounds__(BS_THREADS) bs_dec3_kernel(const uint32_t* __restrict__ bitmap,
@@ -513,7 +505,7 @@ extern "C" {
 
 FZB_API size_t fzb_bitshuffle_workspace_bytes(uint64_t n) {
     const uint64_t c = ncta_of(n);
-    return 512 + ((c * 4 + 255) / 256) * 256 + c * 8 + 256;
+    return 512 + ((c * 4 + 255) / 256) * 256 + ((c * 8 + 255) / 256) * 256 + fzscan::ws_bytes(c) + 512;
 }
 
 // Reference: encode.py:324-353.  d_codes needs 16-byte alignment.
@@ -569,8 +561,10 @@ FZB_API int fzb_bitshuffle_decode(const uint8_t* d_bitmap, const uint32_t* d_pay
     uint32_t* counts = reinterpret_cast<uint32_t*>(w + 256);
     unsigned long long* offs = reinterpret_cast<unsigned long long*>(w + 256 + ((nc * 4 + 255) / 256) * 256);
     const uint32_t* bm = reinterpret_cast<const uint32_t*>(d_bitmap);
-    bs_dec_count_kernel<<<(unsigned)nc, BS_THREADS, 0, st>>>(bm, nb, counts);
-    scan_counts_u64_kernel<<<1, 1024, 0, st>>>(counts, nc, offs, tot, payload_words, d_status);
+    void* scan_ws = w + 256 + ((nc * 4 + 255) / 256) * 256 + ((nc * 8 + 255) / 256) * 256;
+    bs_dec_count2_kernel<<<(unsigned)((nc + 7) / 8), 256, 0, st>>>(bm, nb, nc, counts);
+    fzscan::exclusive(counts, nc, offs, tot, scan_ws, st);
+    bs_check_kernel<<<1, 1, 0, st>>>(tot, payload_words, d_status);
     bs_dec3_kernel<<<(unsigned)nc, BS_THREADS, 0, st>>>(bm, d_payload, payload_words, n, nb, radius, offs, d_codes,
                                                        d_status);
     return fzb_check_launch();
