@@ -294,6 +294,10 @@ def run_ours(args, wl):
             gda = geng.compress_graphed(x, dims, 1, wl["rel"], **kw)
             gsz = geng.sizes(gda)
             geng.decompress_graphed(gda, gsz, wl["rel"] * (gsz["hi"] - gsz["lo"]), gout)
+            if world > 1:   # the container-offset collective, as in device_step
+                t = torch.tensor([geng.compressed_bytes(gda, gsz)], dtype=torch.int64, device=dev)
+                g = [torch.empty_like(t) for _ in range(world)]
+                dist.all_gather(g, t)
             return gda, gsz
 
         for _ in range(max(args.warmup, 3)):
