@@ -437,12 +437,8 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
     const double R_d = (double)radius;
     // state per row x: 0 = ghost row (w*R - 1), 1..R = rows w*R .. w*R+R-1
     double C1[R + 1], C2[R + 1], L1[R + 1], L2[R + 1];
-    float F1[R + 1];   // f32 copy of C1 (what moves through the shuffles)
 #pragma unroll
-    for (int x = 0; x <= R; x++) {
-        C1[x] = C2[x] = L1[x] = L2[x] = 0.0;
-        F1[x] = 0.f;
-    }
+    for (int x = 0; x <= R; x++) C1[x] = C2[x] = L1[x] = L2[x] = 0.0;
     const bool polled = (w > 0);
     const uint64_t* ghost_src = polled ? GR + (size_t)(w - 1) * GRD * 32 + b : HU + b;   // + slot*32
     // warp W-1 has no consumer in the CTA: its ghost stores go to a scratch ring
@@ -458,8 +454,9 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
     // step s consumes step s-1's ghost value and lane -1 halos (step -1: zeros)
     uint64_t gh = 0;
     float hf[R + 1];
+    float upn[R + 1];   // this step's left neighbours, shuffled at the end of the previous step
 #pragma unroll
-    for (int x = 0; x <= R; x++) hf[x] = 0.f;
+    for (int x = 0; x <= R; x++) hf[x] = upn[x] = 0.f;
 
     // ---- own-row staging: SD groups in flight (encode: cp.async groups;
     //      decode: one group of loads in registers, stored a group early)
@@ -517,15 +514,12 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
                 raw[x] = ld_cta_u32(cell[x]);
             }
             LZ_STAMP(1);
-            F1[0] = __uint_as_float((uint32_t)gh);
-            C1[0] = (double)F1[0];
-            // ---- left neighbours: lane b-1's previous values; lane 0 <- lane -1 halo
+            C1[0] = (double)__uint_as_float((uint32_t)gh);
+            // ---- left neighbours: lane b-1's previous values (shuffled at the end of the
+            //      previous step, off this step's chain); lane 0 <- lane -1 halo
             double Ln[R + 1];
 #pragma unroll
-            for (int x = 0; x <= R; x++) {
-                const float up1 = __shfl_up_sync(FULL, F1[x], 1);
-                Ln[x] = (double)(l0 ? hf[x] : up1);
-            }
+            for (int x = 0; x <= R; x++) Ln[x] = (double)(l0 ? hf[x] : upn[x]);
             double pred[R + 1];
 #pragma unroll
             for (int x = 1; x <= R; x++) {
@@ -593,6 +587,11 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
                 if (!__all_sync(FULL, ghost_ready(polled, ghn, want))) wait_ghost(polled, ghn, want, ghost_src + (s & gmask) * 32);
             }
             LZ_STAMP(3);
+            // ---- the next step's left neighbours first: the shuffles' latency then
+            //      hides under the publishes and the history shift
+            upn[0] = __shfl_up_sync(FULL, __uint_as_float((uint32_t)ghn), 1);
+#pragma unroll
+            for (int x = 1; x <= R; x++) upn[x] = __shfl_up_sync(FULL, Fn[x], 1);
             // ---- publish (predicated, no branches): ghost for warp w+1, faces
             st_ll_cta(ghost_dst + (s & (GRD - 1)) * 32, ll_pack(Fn[R], (uint32_t)(s + 1)));
             st_ll_gpu_if(pubI, fI + (size_t)s * 32, ll_pack(Fn[R], epoch));
@@ -607,10 +606,7 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
                 hf[x] = hfn[x];
             }
 #pragma unroll
-            for (int x = 1; x <= R; x++) {
-                C1[x] = Cn[x];
-                F1[x] = Fn[x];
-            }
+            for (int x = 1; x <= R; x++) C1[x] = Cn[x];
             gh = ghn;
         }
         // ---- own rows: flush what group g completed, stage group g+SD (decode: g+1 / load g+2)
