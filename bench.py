@@ -1,6 +1,6 @@
 """Benchmark: FZModules hot path on B200 vs the CPU reference.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2|c1|c3|c4]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2|c1|c3|c4|c5|c5d]
 
 Workload (default) = BASELINE.json configs[1]: FZMod-Speed (Lorenzo +
 bitshuffle) on a synthetic smooth_trig 512^3 f32 Nyx-shaped field at rel eb
@@ -48,6 +48,8 @@ WORKLOADS = {
     # C5 shard: 64 fields over 8 GPUs = 8 per GPU, all in flight at once (compress_batch)
     "c5": dict(name="C5 shard: 8 x smooth_trig 512x512x512 per GPU (FZMod-Speed, batched) rel 1e-3",
                pipeline="speed", dims=(512, 512, 512), kind="trig", rel=1e-3, fields=8),
+    "c5d": dict(name="C5 shard: 8 x smooth_trig 512x512x512 per GPU (FZMod-Default, batched) rel 1e-3",
+                pipeline="default", dims=(512, 512, 512), kind="trig", rel=1e-3, fields=8),
 }
 METRIC = "compress/decompress GB/s per GPU & per box at fixed rel eb; CR+PSNR vs CPU ref"
 
