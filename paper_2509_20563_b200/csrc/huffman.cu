@@ -581,7 +581,9 @@ constexpr int HT_BLOCKS = 16;
 __global__ void __launch_bounds__(256) hf_tables_kernel(const uint8_t* __restrict__ lengths, uint32_t nsym,
                                                         DecTables* __restrict__ T, uint16_t* __restrict__ sym_sorted,
                                                         unsigned long long* __restrict__ lut,
-                                                        uint32_t* __restrict__ lut2) {
+                                                        uint32_t* __restrict__ lut2,
+                                                        unsigned long long* __restrict__ lut_s,
+                                                        uint16_t* __restrict__ lut_m) {
     __shared__ uint32_t cnt[MAXLEN + 1];
     __shared__ uint32_t run[MAXLEN + 1];
     __shared__ long long s_fc[MAXLEN + 2], s_fi[MAXLEN + 2], s_lim[MAXLEN + 2];
@@ -662,6 +664,13 @@ __global__ void __launch_bounds__(256) hf_tables_kernel(const uint8_t* __restric
         }
         e |= ((unsigned long long)c << 48) | ((unsigned long long)pos << 51) | ((unsigned long long)len1 << 55);
         lut[q] = e;
+        {   // write-pass LUT: the same codewords with 16-bit symbol fields
+            unsigned long long es = 0;
+            if (c == 1) es = e & 0xFFFFull;
+            for (int z = 0; z < c && c > 1; z++) es |= ((e >> (12 * z)) & 0xFFFull) << (16 * z);
+            lut_s[q] = es;
+            lut_m[q] = (uint16_t)(c | (pos << 3) | (len1 << 7));
+        }
         // sync LUT: every whole codeword of the window (no symbols): count in
         // bits 0-3, total length 4-7, codeword-start mask 8-19 (bit i: a
         // codeword starts i bits into the window), first length 20-23
@@ -717,33 +726,6 @@ struct BitReader {
 };
 
 FZB_DEV int lut_cnt(unsigned long long e) { return (int)((e >> 48) & 7u); }
-FZB_DEV int lut_len(unsigned long long e) { return (int)((e >> 51) & 15u); }
-
-// decode one symbol at r.pos; returns length (>0) or -1 truncated / -2 corrupt
-FZB_DEV int decode_one(BitReader& r, unsigned long long total_bits, const DecTables& T, const unsigned long long* lut,
-                       const uint16_t* sym_sorted, uint32_t& sym) {
-    const uint32_t win = r.peek32();
-    const unsigned long long e = lut[win >> (32 - LUT_BITS)];
-    int l;
-    if (lut_cnt(e)) {
-        l = (int)((e >> 55) & 15u);
-        sym = (uint32_t)(e & (lut_cnt(e) == 1 ? 0xFFFFu : 0xFFFu));
-    } else {
-        l = 0;
-        for (int q = LUT_BITS + 1; q <= T.maxlen; q++) {
-            const long long code = (long long)(win >> (32 - q));
-            if (code < T.limit[q]) {
-                sym = sym_sorted[T.first_idx[q] + code - T.first_code[q]];
-                l = q;
-                break;
-            }
-        }
-        if (!l) return (r.pos + (unsigned long long)T.maxlen >= total_bits) ? -1 : -2;
-    }
-    if (r.pos + (unsigned long long)l > total_bits) return -1;
-    return l;
-}
-
 // Persistent, cooperative fixed-point iteration of the subsequence starts:
 // sweep 0 starts every subsequence at its nominal bit offset (speculative);
 // later sweeps restart subsequence t at end[t-1] whenever that differs from
@@ -884,91 +866,101 @@ __global__ void __launch_bounds__(HD_THREADS) hf_sync_coop_kernel(const uint32_t
 // offsets (consecutive symbols of one chunk go to consecutive lanes).  The
 // first true-path error with ordinal < n (encode.py:299-310) is folded in
 // with an atomicMin on (subsequence << 2 | kind).
-constexpr int HD_ROUND = 48;   // symbols per thread and round (smem: 128 x 52 x 2 B + 32 KB LUT)
+// Decode + write.  Every thread decodes the symbols the sync pass counted
+// for its subsequence (complete codewords only) and streams them to its
+// output range through a register word of 4 symbols: interior 8-byte
+// chunks go out as one aligned 64-bit store, the chunks shared with the
+// neighbouring threads' ranges as 16-bit stores.  No shared-memory staging,
+// no block barriers.  The first true-path error with ordinal < n
+// (encode.py:299-310) is folded in with an atomicMin on (subsequence << 2 | kind).
+FZB_DEV void put_chunk(uint16_t* __restrict__ out, unsigned long long base, unsigned long long acc, int from, int to) {
+    if (from == 0 && to == 4) {
+        *reinterpret_cast<unsigned long long*>(out + base) = acc;
+    } else {
+        for (int z = from; z < to; z++) out[base + z] = (uint16_t)(acc >> (16 * z));
+    }
+}
 
 __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_t* __restrict__ stream,
                                                                    unsigned long long total_bits, uint64_t nsub,
                                                                    const DecTables* __restrict__ Tg,
-                                                                   const unsigned long long* __restrict__ lut_g,
+                                                                   const unsigned long long* __restrict__ lut_s_g,
+                                                                   const uint16_t* __restrict__ lut_m_g,
                                                                    const uint16_t* __restrict__ sym_sorted,
                                                                    const unsigned long long* __restrict__ start,
-                                                                   const unsigned long long* __restrict__ end,
                                                                    const uint32_t* __restrict__ cnt,
                                                                    const uint32_t* __restrict__ err,
                                                                    const unsigned long long* __restrict__ offs,
                                                                    uint64_t n, uint16_t* __restrict__ out,
                                                                    unsigned long long* __restrict__ end_pos,
                                                                    unsigned long long* __restrict__ best) {
-    __shared__ unsigned long long lut[1 << LUT_BITS];
+    __shared__ unsigned long long ls[1 << LUT_BITS];
+    __shared__ uint16_t lm[1 << LUT_BITS];
     __shared__ DecTables T;
-    __shared__ uint16_t buf[HD_THREADS][HD_ROUND + 4];
-    for (int q = threadIdx.x; q < (1 << LUT_BITS); q += blockDim.x) lut[q] = lut_g[q];
+    for (int q = threadIdx.x; q < (1 << LUT_BITS); q += blockDim.x) {
+        ls[q] = lut_s_g[q];
+        lm[q] = lut_m_g[q];
+    }
     if (threadIdx.x == 0) T = *Tg;
     __syncthreads();
-    (void)end;
     (void)total_bits;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long o = n;
-    uint32_t todo = 0;   // symbols this thread emits: the sync pass counted them (complete codewords only)
-    BitReader r;
-    if (t < nsub) {
-        o = offs[t];
-        const uint32_t c = cnt[t];
-        const uint32_t er = err[t];
-        if (er && o + c < n) atomicMin(best, (t << 2) | er);
-        if (o < n) {
-            todo = (uint32_t)min((unsigned long long)c, n - o);
-            r.init(stream, start[t]);
-        }
-    }
+    if (t >= nsub) return;
+    const unsigned long long o = offs[t];
+    const uint32_t c0 = cnt[t];
+    const uint32_t er = err[t];
+    if (er && o + c0 < n) atomicMin(best, (t << 2) | er);
+    if (o >= n) return;
+    uint32_t todo = (uint32_t)min((unsigned long long)c0, n - o);   // symbols this thread emits
     const bool last = todo && o + todo == n;   // emits symbol n-1: records where it ends
-    uint16_t* bp = buf[threadIdx.x];
-    while (true) {
-        const int want = (int)min(todo, (uint32_t)HD_ROUND);
-        int k = 0;
-        while (k < want) {
-            const uint32_t win = r.peek32();
-            const unsigned long long me = lut[win >> (32 - LUT_BITS)];
-            const int mc = lut_cnt(me);
-            if (mc >= 2 && k + mc <= want) {   // up to 4 whole codewords from one window
-                bp[k] = (uint16_t)(me & 0xFFFu);
-                bp[k + 1] = (uint16_t)((me >> 12) & 0xFFFu);
-                bp[k + 2] = (uint16_t)((me >> 24) & 0xFFFu);
-                bp[k + 3] = (uint16_t)((me >> 36) & 0xFFFu);
-                k += mc;
-                r.skip(lut_len(me));
-                continue;
-            }
+    BitReader r;
+    r.init(stream, start[t]);
+    unsigned long long base = o & ~3ull;   // current 4-symbol chunk
+    int from = (int)(o & 3);               // first slot of the chunk that is ours
+    int p = from;                          // next free slot
+    unsigned long long acc = 0;
+    while (todo) {
+        const uint32_t win = r.peek32();
+        const uint32_t idx = win >> (32 - LUT_BITS);
+        const uint32_t md = lm[idx];
+        int c = (int)(md & 7u);
+        unsigned long long e;
+        int len;
+        if (c >= 2 && (uint32_t)c <= todo) {   // up to 4 whole codewords from one window
+            e = ls[idx];
+            len = (int)((md >> 3) & 15u);
+        } else if (c) {
+            e = ls[idx] & 0xFFFFull;
+            len = (int)((md >> 7) & 15u);
+            c = 1;
+        } else {   // > LUT_BITS: the canonical first_code / limit walk (encode.py:248-253)
             uint32_t sym = 0;
-            int l = 0;
-            if (mc) {
-                l = (int)((me >> 55) & 15u);
-                sym = (uint32_t)(me & (mc == 1 ? 0xFFFFu : 0xFFFu));
-            } else {   // > LUT_BITS: the canonical first_code / limit walk (encode.py:248-253)
-                for (int q = LUT_BITS + 1; q <= T.maxlen; q++) {
-                    const long long code = (long long)(win >> (32 - q));
-                    if (code < T.limit[q]) {
-                        sym = sym_sorted[T.first_idx[q] + code - T.first_code[q]];
-                        l = q;
-                        break;
-                    }
+            len = 0;
+            for (int q = LUT_BITS + 1; q <= T.maxlen; q++) {
+                const long long code = (long long)(win >> (32 - q));
+                if (code < T.limit[q]) {
+                    sym = sym_sorted[T.first_idx[q] + code - T.first_code[q]];
+                    len = q;
+                    break;
                 }
             }
-            r.skip(l);
-            bp[k++] = (uint16_t)sym;
+            e = sym;
+            c = 1;
         }
-        todo -= (uint32_t)k;
-        __syncthreads();
-        // copy-out: warp w owns the chunks of threads 32w..32w+31
-        for (int c = 0; c < 32; c++) {
-            const int kc = __shfl_sync(0xffffffffu, k, c);
-            const unsigned long long oc = __shfl_sync(0xffffffffu, o, c);
-            for (int j = lane; j < kc; j += 32) out[oc + j] = buf[warp * 32 + c][j];
+        r.skip(len);
+        todo -= (uint32_t)c;
+        acc |= e << (16 * p);
+        const unsigned long long spill = p ? e >> (64 - 16 * p) : 0ull;
+        p += c;
+        if (p >= 4) {
+            put_chunk(out, base, acc, from, 4);
+            base += 4;
+            from = 0;
+            acc = spill;
+            p -= 4;
         }
-        o += k;
-        if (!__syncthreads_or(todo != 0)) break;
     }
+    if (p > from) put_chunk(out, base, acc, from, p);
     if (last) *end_pos = r.pos;
 }
 
@@ -1087,7 +1079,8 @@ FZB_API size_t fzb_huffman_decode_workspace_bytes(uint64_t nbytes, uint32_t nsym
     const uint64_t nsub = (nbytes * 8 + SUB - 1) / SUB + 1;
     // tables + sym_sorted + lut + 2x(start,end,cnt,err) + offs + scalars
     return align256(sizeof(DecTables)) + align256((size_t)nsym * 2) + align256((1u << LUT_BITS) * 8) +
-           align256((1u << LUT_BITS) * 4) + align256(nsub * SYNC_WORDS * 4) +
+           align256((1u << LUT_BITS) * 4) + align256((1u << LUT_BITS) * 8) + align256((1u << LUT_BITS) * 2) +
+           align256(nsub * SYNC_WORDS * 4) +
            2 * align256(nsub * 8) + 2 * align256(nsub * 4) + align256(nsub * 8) + align256(fzscan::ws_bytes(nsub)) +
            1024;
 }
@@ -1107,6 +1100,8 @@ FZB_API int fzb_huffman_decode(const uint8_t* d_stream, uint64_t nbytes, uint64_
     uint16_t* sym_sorted = reinterpret_cast<uint16_t*>(p); p += align256((size_t)nsym * 2);
     unsigned long long* lut = reinterpret_cast<unsigned long long*>(p); p += align256((1u << LUT_BITS) * 8);
     uint32_t* lut2 = reinterpret_cast<uint32_t*>(p); p += align256((1u << LUT_BITS) * 4);
+    unsigned long long* lut_s = reinterpret_cast<unsigned long long*>(p); p += align256((1u << LUT_BITS) * 8);
+    uint16_t* lut_m = reinterpret_cast<uint16_t*>(p); p += align256((1u << LUT_BITS) * 2);
     uint32_t* bmaps = reinterpret_cast<uint32_t*>(p); p += align256(nsub * SYNC_WORDS * 4);
     unsigned long long* st_[1]; unsigned long long* en_[1]; uint32_t* cn_[1]; uint32_t* er_[1];
     st_[0] = reinterpret_cast<unsigned long long*>(p); p += align256(nsub * 8);
@@ -1118,7 +1113,7 @@ FZB_API int fzb_huffman_decode(const uint8_t* d_stream, uint64_t nbytes, uint64_
     unsigned long long* scal = reinterpret_cast<unsigned long long*>(p);  // [0]=total [1]=end_pos [2..3]=changed[3] (u32) [4]=best
     cudaMemsetAsync(scal, 0, 64, st);
     cudaMemsetAsync(scal + 4, 0xFF, 8, st);
-    hf_tables_kernel<<<HT_BLOCKS, 256, 0, st>>>(d_lengths, nsym, T, sym_sorted, lut, lut2);
+    hf_tables_kernel<<<HT_BLOCKS, 256, 0, st>>>(d_lengths, nsym, T, sym_sorted, lut, lut2, lut_s, lut_m);
     const uint32_t* words = reinterpret_cast<const uint32_t*>(d_stream);
     const unsigned blocks = (unsigned)((nsub + HD_THREADS - 1) / HD_THREADS);
     uint32_t* changed = reinterpret_cast<uint32_t*>(scal + 2);
@@ -1144,8 +1139,8 @@ FZB_API int fzb_huffman_decode(const uint8_t* d_stream, uint64_t nbytes, uint64_
     cudaLaunchCooperativeKernel((const void*)hf_sync_coop_kernel, dim3(gridc), dim3(HD_THREADS), kargs, 0, st);
     const int fin = 0;
     fzscan::exclusive(cn_[fin], nsub, offs, scal, scan_ws, st);
-    hf_write_dec2_kernel<<<blocks, HD_THREADS, 0, st>>>(words, total_bits, nsub, T, lut, sym_sorted, st_[fin],
-                                                        en_[fin], cn_[fin], er_[fin], offs, n, d_codes, scal + 1,
+    hf_write_dec2_kernel<<<blocks, HD_THREADS, 0, st>>>(words, total_bits, nsub, T, lut_s, lut_m, sym_sorted,
+                                                        st_[fin], cn_[fin], er_[fin], offs, n, d_codes, scal + 1,
                                                         scal + 4);
     hf_final2_kernel<<<1, 1, 0, st>>>(n, nbytes, d_stream, scal, scal + 1, scal + 4, d_status);
     return fzb_check_launch();
