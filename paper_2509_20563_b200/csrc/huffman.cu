@@ -498,14 +498,19 @@ FZB_DEV uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 // Big-endian words == the MSB-first byte stream of encode.py:220-231.
 constexpr int HE_WORDS = HE_CHUNK;   // <= 32 bits per code -> at most HE_CHUNK words per CTA
 
+__global__ void hf_pack_table_kernel(const uint8_t* __restrict__ lengths, const uint32_t* __restrict__ cwords,
+                                     uint32_t nsym, unsigned long long* __restrict__ lc) {
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < nsym; s += gridDim.x * blockDim.x)
+        lc[s] = ((unsigned long long)cwords[s] << 32) | lengths[s];
+}
+
 __global__ void __launch_bounds__(HE_THREADS) hf_write2_kernel(const uint16_t* __restrict__ codes, uint64_t n,
-                                                               const uint8_t* __restrict__ lengths,
-                                                               const uint32_t* __restrict__ cwords, uint32_t nsym,
+                                                               const unsigned long long* __restrict__ lc,
+                                                               uint32_t nsym,
                                                                const unsigned long long* __restrict__ cta_off,
                                                                uint32_t* __restrict__ out, uint64_t cap_words) {
     __shared__ unsigned long long tmp[33];
     __shared__ uint32_t buf[HE_WORDS + 1];
-    for (int q = threadIdx.x; q <= HE_WORDS; q += HE_THREADS) buf[q] = 0;
     const uint64_t base = ((uint64_t)blockIdx.x * HE_THREADS + threadIdx.x) * HE_PER;
     uint32_t c[HE_PER];
     load16(codes, n, base, c);
@@ -514,11 +519,20 @@ __global__ void __launch_bounds__(HE_THREADS) hf_write2_kernel(const uint16_t* _
 #pragma unroll
     for (int e = 0; e < HE_PER; e++) {
         len[e] = 0; cwv[e] = 0;
-        if (c[e] < nsym) { len[e] = __ldg(lengths + c[e]); cwv[e] = __ldg(cwords + c[e]); }
+        if (c[e] < nsym) {   // one 8-byte lookup: codeword << 32 | length
+            const unsigned long long v = __ldg(lc + c[e]);
+            len[e] = (uint32_t)v & 0xFFu;
+            cwv[e] = (uint32_t)(v >> 32);
+        }
         b += len[e];
     }
     unsigned long long total;
     const unsigned long long o = block_exclusive_scan64(b, tmp, &total);   // CTA-local bit offset (syncs)
+    // clear only the words this CTA's bits occupy (low-entropy streams use a
+    // small fraction of the worst-case buffer)
+    for (uint32_t q = threadIdx.x; q <= (uint32_t)((total + 31) >> 5) && q <= (uint32_t)HE_WORDS; q += HE_THREADS)
+        buf[q] = 0;
+    __syncthreads();
     // pack this thread's bits into the shared buffer (bit 0 of the CTA = MSB of buf[0])
     if (b) {
         uint32_t w = (uint32_t)(o >> 5);
@@ -1045,7 +1059,7 @@ FZB_API int fzb_huffman_build(const uint64_t* d_bins, uint32_t nsym, uint8_t* d_
 
 FZB_API size_t fzb_huffman_encode_workspace_bytes(uint64_t n) {
     const uint64_t nc = (n + HE_CHUNK - 1) / HE_CHUNK;
-    return 256 + 2 * align256(nc * 8) + align256(fzscan::ws_bytes(nc)) + 256;
+    return 256 + 2 * align256(nc * 8) + align256(fzscan::ws_bytes(nc)) + align256(65536 * 8) + 256;
 }
 
 FZB_API int fzb_huffman_encode(const uint16_t* d_codes, uint64_t n, const uint8_t* d_lengths,
@@ -1062,6 +1076,8 @@ FZB_API int fzb_huffman_encode(const uint16_t* d_codes, uint64_t n, const uint8_
     unsigned long long* cta_bits = reinterpret_cast<unsigned long long*>(w + 256);
     unsigned long long* cta_off = reinterpret_cast<unsigned long long*>(w + 256 + align256(nc * 8));
     void* scan_ws = w + 256 + 2 * align256(nc * 8);
+    unsigned long long* lc = reinterpret_cast<unsigned long long*>(w + 256 + 2 * align256(nc * 8) +
+                                                                   align256(fzscan::ws_bytes(nc)));
     const uint64_t cap_words = out_cap / 4;
     uint32_t* out = reinterpret_cast<uint32_t*>(d_out);
     const unsigned long long* want = reinterpret_cast<const unsigned long long*>(d_bit_count);
@@ -1070,8 +1086,8 @@ FZB_API int fzb_huffman_encode(const uint16_t* d_codes, uint64_t n, const uint8_
     fzscan::exclusive(reinterpret_cast<uint32_t*>(cta_bits), nc, cta_off, tot, scan_ws, st);
     hf_check_kernel<<<1, 1, 0, st>>>(tot, want, d_status);
     hf_zero_kernel<<<kNumSMs * 4, 256, 0, st>>>(out, tot, cap_words);
-    hf_write2_kernel<<<(unsigned)nc, HE_THREADS, 0, st>>>(d_codes, n, d_lengths, d_codewords, nsym, cta_off, out,
-                                                         cap_words);
+    hf_pack_table_kernel<<<(nsym + 255) / 256, 256, 0, st>>>(d_lengths, d_codewords, nsym, lc);
+    hf_write2_kernel<<<(unsigned)nc, HE_THREADS, 0, st>>>(d_codes, n, lc, nsym, cta_off, out, cap_words);
     return fzb_check_launch();
 }
 

@@ -124,6 +124,7 @@ constexpr uint32_t HIST_SMEM_BINS = 16384;
 // shared memory and every thread merges runs of equal codes before it
 // touches a bin, so the heavily skewed code distribution of smooth fields
 // (most codes are R) costs a handful of atomics instead of one per code.
+constexpr int HIST_UNROLL = 4;
 __global__ void __launch_bounds__(HIST_THREADS) hist_smem_kernel(const uint16_t* __restrict__ codes, uint64_t n,
                                                                  uint32_t nbins, int nsub,
                                                                  unsigned long long* __restrict__ out,
@@ -149,7 +150,22 @@ __global__ void __launch_bounds__(HIST_THREADS) hist_smem_kernel(const uint16_t*
     const uint64_t n8 = n / 8;
     const uint4* c8 = reinterpret_cast<const uint4*>(codes);
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n8; q += stride) {
+    // HIST_UNROLL independent 16-byte loads in flight per thread (the run
+    // merging below is a serial chain; the loads must not wait on it)
+    uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; q + (HIST_UNROLL - 1) * stride < n8; q += HIST_UNROLL * stride) {
+        uint4 v[HIST_UNROLL];
+#pragma unroll
+        for (int u = 0; u < HIST_UNROLL; u++) v[u] = __ldcs(c8 + q + u * stride);
+#pragma unroll
+        for (int u = 0; u < HIST_UNROLL; u++) {
+            put(v[u].x & 0xFFFFu); put(v[u].x >> 16);
+            put(v[u].y & 0xFFFFu); put(v[u].y >> 16);
+            put(v[u].z & 0xFFFFu); put(v[u].z >> 16);
+            put(v[u].w & 0xFFFFu); put(v[u].w >> 16);
+        }
+    }
+    for (; q < n8; q += stride) {
         const uint4 v = __ldcs(c8 + q);
         put(v.x & 0xFFFFu); put(v.x >> 16);
         put(v.y & 0xFFFFu); put(v.y >> 16);
