@@ -882,16 +882,18 @@ __global__ void __launch_bounds__(HD_THREADS) hf_sync_coop_kernel(const uint32_t
 // with an atomicMin on (subsequence << 2 | kind).
 // Decode + write.  Every thread decodes the symbols the sync pass counted
 // for its subsequence (complete codewords only) and streams them to its
-// output range through a register word of 4 symbols: interior 8-byte
-// chunks go out as one aligned 64-bit store, the chunks shared with the
+// output range through two register words of 8 symbols: interior 16-byte
+// chunks go out as one aligned 128-bit store, the chunks shared with the
 // neighbouring threads' ranges as 16-bit stores.  No shared-memory staging,
 // no block barriers.  The first true-path error with ordinal < n
 // (encode.py:299-310) is folded in with an atomicMin on (subsequence << 2 | kind).
-FZB_DEV void put_chunk(uint16_t* __restrict__ out, unsigned long long base, unsigned long long acc, int from, int to) {
-    if (from == 0 && to == 4) {
-        *reinterpret_cast<unsigned long long*>(out + base) = acc;
+FZB_DEV void put_chunk(uint16_t* __restrict__ out, unsigned long long base, unsigned long long lo,
+                       unsigned long long hi, int from, int to) {
+    if (from == 0 && to == 8) {
+        *reinterpret_cast<uint4*>(out + base) =
+            make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32));
     } else {
-        for (int z = from; z < to; z++) out[base + z] = (uint16_t)(acc >> (16 * z));
+        for (int z = from; z < to; z++) out[base + z] = (uint16_t)((z < 4 ? lo : hi) >> (16 * (z & 3)));
     }
 }
 
@@ -929,10 +931,10 @@ __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_
     const bool last = todo && o + todo == n;   // emits symbol n-1: records where it ends
     BitReader r;
     r.init(stream, start[t]);
-    unsigned long long base = o & ~3ull;   // current 4-symbol chunk
-    int from = (int)(o & 3);               // first slot of the chunk that is ours
+    unsigned long long base = o & ~7ull;   // current 8-symbol (16-byte) chunk
+    int from = (int)(o & 7);               // first slot of the chunk that is ours
     int p = from;                          // next free slot
-    unsigned long long acc = 0;
+    unsigned long long lo = 0, hi = 0;
     while (todo) {
         const uint32_t win = r.peek32();
         const uint32_t idx = win >> (32 - LUT_BITS);
@@ -963,18 +965,26 @@ __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_
         }
         r.skip(len);
         todo -= (uint32_t)c;
-        acc |= e << (16 * p);
-        const unsigned long long spill = p ? e >> (64 - 16 * p) : 0ull;
+        // append c <= 4 symbols at slot p of the 128-bit chunk (lo: 0-3, hi: 4-7)
+        unsigned long long spill = 0;
+        if (p < 4) {
+            lo |= e << (16 * p);
+            if (p) hi |= e >> (64 - 16 * p);
+        } else {
+            hi |= e << (16 * (p - 4));
+            if (p > 4) spill = e >> (64 - 16 * (p - 4));
+        }
         p += c;
-        if (p >= 4) {
-            put_chunk(out, base, acc, from, 4);
-            base += 4;
+        if (p >= 8) {
+            put_chunk(out, base, lo, hi, from, 8);
+            base += 8;
             from = 0;
-            acc = spill;
-            p -= 4;
+            lo = spill;
+            hi = 0;
+            p -= 8;
         }
     }
-    if (p > from) put_chunk(out, base, acc, from, p);
+    if (p > from) put_chunk(out, base, lo, hi, from, p);
     if (last) *end_pos = r.pos;
 }
 
