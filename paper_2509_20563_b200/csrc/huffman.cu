@@ -739,7 +739,6 @@ struct BitReader {
     }
 };
 
-FZB_DEV int lut_cnt(unsigned long long e) { return (int)((e >> 48) & 7u); }
 // Persistent, cooperative fixed-point iteration of the subsequence starts:
 // sweep 0 starts every subsequence at its nominal bit offset (speculative);
 // later sweeps restart subsequence t at end[t-1] whenever that differs from
@@ -764,6 +763,130 @@ FZB_DEV void setbits(uint32_t* bm, int rel, uint32_t m) {
     if (o > 20) bm[w + 1] |= m >> (32 - o);
 }
 
+// One subsequence of one sweep (see hf_sync_coop_kernel): fresh = sweep 0
+// (start at the nominal offset), else restart at end[t-1] when it moved.
+FZB_DEV void sync_one(uint64_t t, bool fresh, int slot, const uint32_t* __restrict__ stream,
+                      unsigned long long total_bits, const DecTables& T, const uint32_t* __restrict__ lut2,
+                      uint32_t* nb,
+                      uint32_t* ob, uint32_t* __restrict__ bmaps, unsigned long long* start,
+                      unsigned long long* end, uint32_t* __restrict__ cnt, uint32_t* __restrict__ err,
+                      uint32_t* changed) {
+        unsigned long long s;
+        if (fresh) {
+            s = t * SUB;
+        } else {
+            s = (t == 0) ? 0ull : *(volatile unsigned long long*)(end + t - 1);
+            if (s == start[t]) return;
+            changed[slot] = 1;
+            const uint4* src = reinterpret_cast<const uint4*>(bmaps + t * SYNC_WORDS);
+            const uint4 a = src[0], b = src[1];
+            ob[0] = a.x; ob[1] = a.y; ob[2] = a.z; ob[3] = a.w;
+            ob[4] = b.x; ob[5] = b.y; ob[6] = b.z; ob[7] = b.w;
+        }
+#pragma unroll
+        for (int w = 0; w < SYNC_WORDS; w++) nb[w] = 0;
+        const unsigned long long base = t * SUB, lim = base + SUB;
+        const unsigned long long stop = lim < total_bits ? lim : total_bits;
+        BitReader r;
+        r.init(stream, s);
+        uint32_t e = 0;
+        int conv = -1;   // relative bit where the new path joins the previous one
+        while (r.pos < stop) {
+            const uint32_t win = r.peek32();
+            const int rel = (int)(r.pos - base);
+            const uint32_t me = lut2[win >> (32 - LUT_BITS)];
+            const int c = (int)(me & 15u);
+            if (c && r.pos + LUT_BITS <= stop) {   // every codeword of the window starts before lim
+                const uint32_t mask = (me >> 8) & 0xFFFu;
+                if (!fresh) {
+                    const uint32_t common = bits12(ob, rel) & mask;
+                    if (common) {
+                        const int i = __ffs(common) - 1;
+                        setbits(nb, rel, mask & ((1u << i) - 1u));
+                        conv = rel + i;
+                        break;
+                    }
+                }
+                setbits(nb, rel, mask);
+                r.skip((int)((me >> 4) & 15u));
+                continue;
+            }
+            if (!fresh && ((ob[rel >> 5] >> (rel & 31)) & 1u)) { conv = rel; break; }
+            int l = 0;
+            if (c) {
+                l = (int)((me >> 20) & 15u);
+            } else {   // first codeword longer than LUT_BITS (encode.py:248-253)
+                for (int q = LUT_BITS + 1; q <= T.maxlen; q++) {
+                    const long long code = (long long)(win >> (32 - q));
+                    if (code < T.limit[q]) { l = q; break; }
+                }
+                if (!l) { e = (r.pos + (unsigned long long)T.maxlen >= total_bits) ? 1u : 2u; break; }
+            }
+            if (r.pos + (unsigned long long)l > total_bits) { e = 1u; break; }
+            nb[rel >> 5] |= 1u << (rel & 31);
+            r.skip(l);
+        }
+        uint32_t c = 0;
+        if (conv >= 0) {   // the previous path's later codewords, end and error carry over
+#pragma unroll
+            for (int w = 0; w < SYNC_WORDS; w++) {
+                const int lo = conv - 32 * w;
+                const uint32_t keep = lo <= 0 ? 0xFFFFFFFFu : (lo >= 32 ? 0u : (0xFFFFFFFFu << lo));
+                nb[w] |= ob[w] & keep;
+                c += __popc(nb[w]);
+            }
+        } else {
+#pragma unroll
+            for (int w = 0; w < SYNC_WORDS; w++) c += __popc(nb[w]);
+            err[t] = e;
+        }
+        uint4* dst = reinterpret_cast<uint4*>(bmaps + t * SYNC_WORDS);
+        dst[0] = make_uint4(nb[0], nb[1], nb[2], nb[3]);
+        dst[1] = make_uint4(nb[4], nb[5], nb[6], nb[7]);
+        start[t] = s;
+        cnt[t] = c;
+        if (conv < 0) *(volatile unsigned long long*)(end + t) = e ? lim : r.pos;
+}
+
+#define HF_SYNC_SMEM                                                                      \
+    __shared__ uint32_t lut2[1 << LUT_BITS];                                              \
+    __shared__ DecTables T;                                                               \
+    __shared__ uint32_t nbm[HD_THREADS][SYNC_WORDS + 1];                                  \
+    __shared__ uint32_t obm[HD_THREADS][SYNC_WORDS + 1];                                  \
+    for (int q = threadIdx.x; q < (1 << LUT_BITS); q += blockDim.x) lut2[q] = lut2_g[q]; \
+    if (threadIdx.x == 0) T = *Tg;                                                        \
+    __syncthreads();                                                                      \
+    uint32_t* nb = nbm[threadIdx.x];                                                      \
+    uint32_t* ob = obm[threadIdx.x];                                                      \
+    nb[SYNC_WORDS] = 0;                                                                   \
+    ob[SYNC_WORDS] = 0;
+
+// Sweeps 0, 1 and 2 as plain launches, one thread per subsequence: no grid
+// barrier and no load imbalance (the cooperative kernel's resident grid
+// holds fewer threads than there are subsequences).  Sweep 1 mostly stops
+// after a few codewords on the previous path; sweep 2 usually only
+// verifies (changed[2] stays 0) and the cooperative kernel exits at once.
+template <int IT>
+__global__ void __launch_bounds__(HD_THREADS) hf_sync_sweep_kernel(const uint32_t* __restrict__ stream,
+                                                                   unsigned long long total_bits, uint64_t nsub,
+                                                                   const DecTables* __restrict__ Tg,
+                                                                   const uint32_t* __restrict__ lut2_g,
+                                                                   uint32_t* __restrict__ bmaps,
+                                                                   unsigned long long* start, unsigned long long* end,
+                                                                   uint32_t* __restrict__ cnt,
+                                                                   uint32_t* __restrict__ err, uint32_t* changed) {
+    // short-lived CTAs: the LUT is read through L1 (__ldg) instead of being
+    // copied into shared memory 128 subsequences at a time
+    __shared__ uint32_t nbm[HD_THREADS][SYNC_WORDS + 1];
+    __shared__ uint32_t obm[HD_THREADS][SYNC_WORDS + 1];
+    uint32_t* nb = nbm[threadIdx.x];
+    uint32_t* ob = obm[threadIdx.x];
+    nb[SYNC_WORDS] = 0;
+    ob[SYNC_WORDS] = 0;
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < nsub) sync_one(t, IT == 0, IT, stream, total_bits, *Tg, lut2_g, nb, ob, bmaps, start, end, cnt, err, changed);
+}
+
 __global__ void __launch_bounds__(HD_THREADS) hf_sync_coop_kernel(const uint32_t* __restrict__ stream,
                                                                   unsigned long long total_bits, uint64_t nsub,
                                                                   const DecTables* __restrict__ Tg,
@@ -773,113 +896,23 @@ __global__ void __launch_bounds__(HD_THREADS) hf_sync_coop_kernel(const uint32_t
                                                                   uint32_t* __restrict__ cnt, uint32_t* __restrict__ err,
                                                                   uint32_t* changed, uint32_t* __restrict__ status,
                                                                   int max_iter) {
-    __shared__ uint32_t lut2[1 << LUT_BITS];
-    __shared__ DecTables T;
-    __shared__ uint32_t nbm[HD_THREADS][SYNC_WORDS + 1];
-    __shared__ uint32_t obm[HD_THREADS][SYNC_WORDS + 1];
-    for (int q = threadIdx.x; q < (1 << LUT_BITS); q += blockDim.x) lut2[q] = lut2_g[q];
-    if (threadIdx.x == 0) T = *Tg;
-    __syncthreads();
-    uint32_t* nb = nbm[threadIdx.x];
-    uint32_t* ob = obm[threadIdx.x];
-    nb[SYNC_WORDS] = 0;
-    ob[SYNC_WORDS] = 0;
+    // sweeps 0-2 ran as plain launches (changed[2] = whether sweep 2 moved anything)
+    if (*(volatile uint32_t*)(changed + 2) == 0) return;
+    HF_SYNC_SMEM
     cg::grid_group grid = cg::this_grid();
     const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
-    int it = 0;
+    int it = 3;
     for (; it < max_iter; it++) {
         if (gt == 0) changed[(it + 1) % 3] = 0;  // last read two sweeps ago
-        for (uint64_t t = gt; t < nsub; t += gs) {
-            unsigned long long s;
-            const bool fresh = it == 0;
-            if (fresh) {
-                s = t * SUB;
-            } else {
-                s = (t == 0) ? 0ull : *(volatile unsigned long long*)(end + t - 1);
-                if (s == start[t]) continue;
-                changed[it % 3] = 1;
-                const uint4* src = reinterpret_cast<const uint4*>(bmaps + t * SYNC_WORDS);
-                const uint4 a = src[0], b = src[1];
-                ob[0] = a.x; ob[1] = a.y; ob[2] = a.z; ob[3] = a.w;
-                ob[4] = b.x; ob[5] = b.y; ob[6] = b.z; ob[7] = b.w;
-            }
-#pragma unroll
-            for (int w = 0; w < SYNC_WORDS; w++) nb[w] = 0;
-            const unsigned long long base = t * SUB, lim = base + SUB;
-            const unsigned long long stop = lim < total_bits ? lim : total_bits;
-            BitReader r;
-            r.init(stream, s);
-            uint32_t e = 0;
-            int conv = -1;   // relative bit where the new path joins the previous one
-            while (r.pos < stop) {
-                const uint32_t win = r.peek32();
-                const int rel = (int)(r.pos - base);
-                const uint32_t me = lut2[win >> (32 - LUT_BITS)];
-                const int c = (int)(me & 15u);
-                if (c && r.pos + LUT_BITS <= stop) {   // every codeword of the window starts before lim
-                    const uint32_t mask = (me >> 8) & 0xFFFu;
-                    if (!fresh) {
-                        const uint32_t common = bits12(ob, rel) & mask;
-                        if (common) {
-                            const int i = __ffs(common) - 1;
-                            setbits(nb, rel, mask & ((1u << i) - 1u));
-                            conv = rel + i;
-                            break;
-                        }
-                    }
-                    setbits(nb, rel, mask);
-                    r.skip((int)((me >> 4) & 15u));
-                    continue;
-                }
-                if (!fresh && ((ob[rel >> 5] >> (rel & 31)) & 1u)) { conv = rel; break; }
-                int l = 0;
-                if (c) {
-                    l = (int)((me >> 20) & 15u);
-                } else {   // first codeword longer than LUT_BITS (encode.py:248-253)
-                    for (int q = LUT_BITS + 1; q <= T.maxlen; q++) {
-                        const long long code = (long long)(win >> (32 - q));
-                        if (code < T.limit[q]) { l = q; break; }
-                    }
-                    if (!l) { e = (r.pos + (unsigned long long)T.maxlen >= total_bits) ? 1u : 2u; break; }
-                }
-                if (r.pos + (unsigned long long)l > total_bits) { e = 1u; break; }
-                nb[rel >> 5] |= 1u << (rel & 31);
-                r.skip(l);
-            }
-            uint32_t c = 0;
-            if (conv >= 0) {   // the previous path's later codewords, end and error carry over
-#pragma unroll
-                for (int w = 0; w < SYNC_WORDS; w++) {
-                    const int lo = conv - 32 * w;
-                    const uint32_t keep = lo <= 0 ? 0xFFFFFFFFu : (lo >= 32 ? 0u : (0xFFFFFFFFu << lo));
-                    nb[w] |= ob[w] & keep;
-                    c += __popc(nb[w]);
-                }
-            } else {
-#pragma unroll
-                for (int w = 0; w < SYNC_WORDS; w++) c += __popc(nb[w]);
-                err[t] = e;
-            }
-            uint4* dst = reinterpret_cast<uint4*>(bmaps + t * SYNC_WORDS);
-            dst[0] = make_uint4(nb[0], nb[1], nb[2], nb[3]);
-            dst[1] = make_uint4(nb[4], nb[5], nb[6], nb[7]);
-            start[t] = s;
-            cnt[t] = c;
-            if (conv < 0) *(volatile unsigned long long*)(end + t) = e ? lim : r.pos;
-        }
+        for (uint64_t t = gt; t < nsub; t += gs)
+            sync_one(t, false, it % 3, stream, total_bits, T, lut2, nb, ob, bmaps, start, end, cnt, err, changed);
         grid.sync();
-        if (it > 0 && *(volatile uint32_t*)(changed + (it % 3)) == 0) break;
+        if (*(volatile uint32_t*)(changed + (it % 3)) == 0) break;
     }
     if (gt == 0 && it >= max_iter) set_err(status, FZB_ERR_HF_SYNC);
 }
 
-// Decode + write, coalesced: every thread decodes its subsequence (from the
-// synchronised start) in rounds of HD_ROUND symbols into shared memory;
-// between rounds each warp copies its 32 threads' chunks to their global
-// offsets (consecutive symbols of one chunk go to consecutive lanes).  The
-// first true-path error with ordinal < n (encode.py:299-310) is folded in
-// with an atomicMin on (subsequence << 2 | kind).
 // Decode + write.  Every thread decodes the symbols the sync pass counted
 // for its subsequence (complete codewords only) and streams them to its
 // output range through two register words of 8 symbols: interior 16-byte
@@ -1162,6 +1195,12 @@ FZB_API int fzb_huffman_decode(const uint8_t* d_stream, uint64_t nbytes, uint64_
     void* kargs[] = {(void*)&words, (void*)&total_bits, (void*)&nsub, (void*)&T, (void*)&lut2, (void*)&bmaps,
                      (void*)&sp, (void*)&ep, (void*)&cp, (void*)&erp, (void*)&changed, (void*)&d_status,
                      (void*)&max_iter};
+    hf_sync_sweep_kernel<0><<<blocks, HD_THREADS, 0, st>>>(words, total_bits, nsub, T, lut2, bmaps, sp, ep, cp, erp,
+                                                           changed);
+    hf_sync_sweep_kernel<1><<<blocks, HD_THREADS, 0, st>>>(words, total_bits, nsub, T, lut2, bmaps, sp, ep, cp, erp,
+                                                           changed);
+    hf_sync_sweep_kernel<2><<<blocks, HD_THREADS, 0, st>>>(words, total_bits, nsub, T, lut2, bmaps, sp, ep, cp, erp,
+                                                           changed);
     cudaLaunchCooperativeKernel((const void*)hf_sync_coop_kernel, dim3(gridc), dim3(HD_THREADS), kargs, 0, st);
     const int fin = 0;
     fzscan::exclusive(cn_[fin], nsub, offs, scal, scan_ws, st);
