@@ -739,6 +739,49 @@ struct BitReader {
     }
 };
 
+// Bit reader over one subsequence with every stream word it can need
+// (<= SUB + 64 bits from its start) loaded up front: the refills of the
+// write pass then read registers instead of issuing a dependent global
+// load every 32 bits.  The word queue shifts with compile-time indices so
+// it stays in registers.
+constexpr int PQ = (SUB + 64) / 32 + 2;
+struct BitReaderP {
+    uint32_t q[PQ];
+    unsigned long long pos, buf;
+    int nb;
+    FZB_DEV void init(const uint32_t* __restrict__ words, unsigned long long p, unsigned long long nwords) {
+        pos = p;
+        const unsigned long long wi = p >> 5;
+#pragma unroll
+        for (int k = 0; k < PQ; k++) {
+            const unsigned long long a = wi + k;
+            q[k] = a < nwords ? bswap32(__ldg(words + a)) : 0u;
+        }
+        buf = (((unsigned long long)q[0] << 32) | q[1]) << (p & 31);
+        nb = 64 - (int)(p & 31);
+        shift();
+        shift();
+    }
+    FZB_DEV void shift() {
+#pragma unroll
+        for (int k = 0; k + 1 < PQ; k++) q[k] = q[k + 1];
+        q[PQ - 1] = 0;
+    }
+    FZB_DEV uint32_t peek32() {
+        if (nb < 32) {
+            buf |= (unsigned long long)q[0] << (32 - nb);
+            nb += 32;
+            shift();
+        }
+        return (uint32_t)(buf >> 32);
+    }
+    FZB_DEV void skip(int l) {
+        buf <<= l;
+        nb -= l;
+        pos += l;
+    }
+};
+
 // Persistent, cooperative fixed-point iteration of the subsequence starts:
 // sweep 0 starts every subsequence at its nominal bit offset (speculative);
 // later sweeps restart subsequence t at end[t-1] whenever that differs from
@@ -952,7 +995,6 @@ __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_
     }
     if (threadIdx.x == 0) T = *Tg;
     __syncthreads();
-    (void)total_bits;
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nsub) return;
     const unsigned long long o = offs[t];
@@ -962,8 +1004,8 @@ __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_
     if (o >= n) return;
     uint32_t todo = (uint32_t)min((unsigned long long)c0, n - o);   // symbols this thread emits
     const bool last = todo && o + todo == n;   // emits symbol n-1: records where it ends
-    BitReader r;
-    r.init(stream, start[t]);
+    BitReaderP r;
+    r.init(stream, start[t], (total_bits / 8 + 8) / 4);
     unsigned long long base = o & ~7ull;   // current 8-symbol (16-byte) chunk
     int from = (int)(o & 7);               // first slot of the chunk that is ours
     int p = from;                          // next free slot
