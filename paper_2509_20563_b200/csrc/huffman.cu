@@ -512,6 +512,7 @@ __global__ void __launch_bounds__(HE_THREADS) hf_write2_kernel(const uint16_t* _
     __shared__ unsigned long long tmp[33];
     __shared__ uint32_t buf[HE_WORDS + 1];
     const uint64_t base = ((uint64_t)blockIdx.x * HE_THREADS + threadIdx.x) * HE_PER;
+    const unsigned long long G = __ldg(cta_off + blockIdx.x);   // issued early: read after the packing
     uint32_t c[HE_PER];
     load16(codes, n, base, c);
     uint32_t len[HE_PER], cwv[HE_PER];
@@ -559,7 +560,6 @@ __global__ void __launch_bounds__(HE_THREADS) hf_write2_kernel(const uint16_t* _
     }
     __syncthreads();
     if (total == 0) return;
-    const unsigned long long G = cta_off[blockIdx.x];
     const int sh = (int)(G & 31);
     const uint64_t w0 = G >> 5, w1 = (G + total - 1) >> 5;   // global words touched
     const uint32_t nw = (uint32_t)(w1 - w0 + 1);
