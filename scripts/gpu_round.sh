@@ -10,6 +10,7 @@ timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 timeout 600 python bench.py > $O/bench_c2.json 2> $O/bench_c2.err
 for w in c1 c3 c4 c5; do timeout 600 python bench.py --workload $w --no-cpu > $O/bench_$w.json 2> $O/bench_$w.err; done
+timeout 600 python bench.py --workload c5d --no-cpu > $O/bench_c5d.json 2> $O/bench_c5d.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref_c2.json 2> $O/bench_ref_c2.err
 if [ "$2" != "quick" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c2.csv python bench.py --steps 2 --warmup 1 --no-cpu > $O/ncu_launch.log 2>&1

@@ -124,3 +124,27 @@ def test_pairwise_tree_matches_numpy(n):
             vals[~lm] = below[0::2] + below[1::2]
         below = vals
     assert below[0] == np.add.reduce(x)
+
+
+@pytest.mark.parametrize("preset", ["default", "speed", "quality"])
+def test_zero_copy_parse_and_wire_block(preset):
+    # parse_archive of a read-only view keeps the payloads as views (no copy)
+    # and round-trips; attach_wire lays an archive out exactly as
+    # serialize_archive does, so archive_buffer needs no host assembly
+    name = list(ARCH["names"])[0]
+    blob = ARCH[f"{name}__{preset}__archive"].tobytes()
+    view = memoryview(blob).toreadonly()
+    a = core.parse_archive(view)
+    assert all(isinstance(p, memoryview) for _, p in a.segments)
+    assert core.serialize_archive(a) == blob
+    assert a == core.parse_archive(blob)
+    b = core.parse_archive(blob)
+    head = len(core.header_bytes(b))
+    block = np.zeros(len(blob), np.uint8)
+    block[head:] = np.frombuffer(b"".join(bytes(p) for _, p in b.segments), np.uint8)
+    core.attach_wire(b, block, head)
+    assert bytes(core.archive_buffer(b)) == blob
+    assert core.serialize_archive(b) == blob
+    # a mutable buffer is copied once, as the reference does
+    c = core.parse_archive(bytearray(blob))
+    assert all(isinstance(p, bytes) for _, p in c.segments)
