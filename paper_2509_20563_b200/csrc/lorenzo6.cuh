@@ -587,13 +587,14 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
                 if (!__all_sync(FULL, ghost_ready(polled, ghn, want))) wait_ghost(polled, ghn, want, ghost_src + (s & gmask) * 32);
             }
             LZ_STAMP(3);
-            // ---- the next step's left neighbours first: the shuffles' latency then
-            //      hides under the publishes and the history shift
+            // ---- the ghost row for warp w+1 first (it waits on it), then the next
+            //      step's left neighbours: the shuffles' latency hides under the
+            //      face publishes and the history shift
+            st_ll_cta(ghost_dst + (s & (GRD - 1)) * 32, ll_pack(Fn[R], (uint32_t)(s + 1)));
             upn[0] = __shfl_up_sync(FULL, __uint_as_float((uint32_t)ghn), 1);
 #pragma unroll
             for (int x = 1; x <= R; x++) upn[x] = __shfl_up_sync(FULL, Fn[x], 1);
-            // ---- publish (predicated, no branches): ghost for warp w+1, faces
-            st_ll_cta(ghost_dst + (s & (GRD - 1)) * 32, ll_pack(Fn[R], (uint32_t)(s + 1)));
+            // ---- publish the faces (predicated, no branches)
             st_ll_gpu_if(pubI, fI + (size_t)s * 32, ll_pack(Fn[R], epoch));
 #pragma unroll
             for (int x = 1; x <= R; x++) st_ll_gpu_if(pubJ, fJ + (size_t)s * PI + (x - 1), ll_pack(Fn[x], epoch));
