@@ -206,8 +206,16 @@ __global__ void __launch_bounds__(OC_THREADS) outlier_count_kernel(const uint32_
     __shared__ uint32_t tmp[33];
     const uint64_t base = (uint64_t)blockIdx.x * OC_WORDS;
     uint32_t c = 0;
-    for (int e = threadIdx.x; e < OC_WORDS; e += blockDim.x)
-        if (base + e < nwords) c += __popc(bm[base + e]);
+    if (base + OC_WORDS <= nwords && !(reinterpret_cast<uintptr_t>(bm) & 15)) {
+        const uint4* b4 = reinterpret_cast<const uint4*>(bm + base);
+        for (int e = threadIdx.x; e < OC_WORDS / 4; e += blockDim.x) {
+            const uint4 v = __ldg(b4 + e);
+            c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+        }
+    } else {
+        for (int e = threadIdx.x; e < OC_WORDS; e += blockDim.x)
+            if (base + e < nwords) c += __popc(bm[base + e]);
+    }
     uint32_t tot;
     block_exclusive_scan(c, tmp, &tot);
     if (threadIdx.x == 0) counts[blockIdx.x] = tot;
@@ -230,10 +238,12 @@ __global__ void scan_u32_to_u64_kernel(const uint32_t* __restrict__ cnt, uint64_
 
 __global__ void __launch_bounds__(OC_THREADS) outlier_write_kernel(const uint32_t* __restrict__ bm, uint64_t nwords,
                                                                    const float* __restrict__ x,
+                                                                   const uint32_t* __restrict__ counts,
                                                                    const unsigned long long* __restrict__ offs,
                                                                    unsigned long long* __restrict__ idx,
                                                                    float* __restrict__ vals) {
     __shared__ uint32_t tmp[33];
+    if (counts[blockIdx.x] == 0) return;   // outliers are rare: most CTAs have none
     const uint64_t base = (uint64_t)blockIdx.x * OC_WORDS;
     unsigned long long o = offs[blockIdx.x];
     for (int e0 = 0; e0 < OC_WORDS; e0 += blockDim.x) {
@@ -440,7 +450,7 @@ FZB_API int fzb_outlier_compact(const uint32_t* d_bitmap, uint64_t n, const floa
     unsigned long long* offs = reinterpret_cast<unsigned long long*>(w + 256 + ((nblk * 4 + 255) / 256) * 256);
     outlier_count_kernel<<<(unsigned)nblk, OC_THREADS, 0, st>>>(d_bitmap, nwords, counts);
     scan_u32_to_u64_kernel<<<1, 1024, 0, st>>>(counts, nblk, offs, reinterpret_cast<unsigned long long*>(d_count));
-    outlier_write_kernel<<<(unsigned)nblk, OC_THREADS, 0, st>>>(d_bitmap, nwords, d_in, offs,
+    outlier_write_kernel<<<(unsigned)nblk, OC_THREADS, 0, st>>>(d_bitmap, nwords, d_in, counts, offs,
                                                                reinterpret_cast<unsigned long long*>(d_idx), d_vals);
     return fzb_check_launch();
 }
