@@ -79,6 +79,202 @@ constexpr size_t WB_BW = 0, WB_PW = WB_BW + 8 * WARP_BUILD_MAX, WB_MW = WB_PW + 
                  WB_IB = WB_LB + 4 * WARP_BUILD_MAX, WB_MW2 = WB_IB + (size_t)MAXLEN * 2 * WARP_BUILD_MAX,
                  WB_MT2 = WB_MW2 + 16 * WARP_BUILD_MAX, WARP_BUILD_SMEM = WB_MT2 + 8 * WARP_BUILD_MAX;
 
+// ---- 4-warp build for small used alphabets (m <= WARP_BUILD_MAX): the
+// same steps as build_warp below, with one item (two for m > 128) per thread
+// and named barriers (bar 1, 128 threads) between the phases of a level, so
+// each level costs one rank search per thread instead of a warp's serial
+// sweep over all items.
+constexpr int CB = 128;   // threads of the 4-warp build
+FZB_DEV void cb_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+FZB_DEV void build_cta4(uint32_t m, uint32_t nsym, const unsigned long long* in_w, const uint32_t* in_s,
+                        uint8_t* __restrict__ lengths, uint32_t* __restrict__ cw,
+                        unsigned long long* __restrict__ bit_count, long long* s_nb, uint32_t* s_cnt,
+                        unsigned long long* s_first) {
+    extern __shared__ __align__(16) unsigned char sm_build[];
+    __shared__ uint32_t s_tot[WARP_BUILD_MAX / 32];
+    __shared__ int s_flag;
+    const int tid = threadIdx.x, lane = tid & 31;
+    constexpr int KI = (int)(WARP_BUILD_MAX / CB);   // items per thread
+    unsigned long long rw[KI];
+    uint32_t rs[KI];
+#pragma unroll
+    for (int k = 0; k < KI; k++) {
+        const uint32_t q = k * CB + tid;
+        rw[k] = q < m ? in_w[q] : 0ull;
+        rs[k] = q < m ? in_s[q] : 0u;
+    }
+    cb_sync();
+    BuildWS ws;
+    ws.bw = reinterpret_cast<unsigned long long*>(sm_build + WB_BW);
+    ws.pw = reinterpret_cast<unsigned long long*>(sm_build + WB_PW);
+    ws.mw = reinterpret_cast<unsigned long long*>(sm_build + WB_MW);
+    ws.bs = reinterpret_cast<uint32_t*>(sm_build + WB_BS);
+    ws.pt = reinterpret_cast<uint32_t*>(sm_build + WB_PT);
+    ws.mt = reinterpret_cast<uint32_t*>(sm_build + WB_MT);
+    ws.isbase = sm_build + WB_IB;
+    uint32_t* lbm = reinterpret_cast<uint32_t*>(sm_build + WB_LB);
+    unsigned long long* mw2 = reinterpret_cast<unsigned long long*>(sm_build + WB_MW2);
+    uint32_t* mt2 = reinterpret_cast<uint32_t*>(sm_build + WB_MT2);
+    // 2. bitonic sort of (w, s) over the next power of two (pad = max key)
+    uint32_t np2 = 1;
+    while (np2 < m) np2 <<= 1;
+#pragma unroll
+    for (int k = 0; k < KI; k++) {
+        const uint32_t q = k * CB + tid;
+        if (q < np2) {
+            ws.bw[q] = q < m ? rw[k] : ~0ull;
+            ws.bs[q] = q < m ? rs[k] : 0xFFFFFFFFu;
+        }
+    }
+    cb_sync();
+    for (uint32_t k2 = 2; k2 <= np2; k2 <<= 1)
+        for (uint32_t jj = k2 >> 1; jj > 0; jj >>= 1) {
+            for (uint32_t q = tid; q < np2; q += CB) {
+                const uint32_t ixj = q ^ jj;
+                if (ixj > q) {
+                    const bool up = (q & k2) == 0;
+                    const unsigned long long wa = ws.bw[q], wb = ws.bw[ixj];
+                    const uint32_t ta = ws.bs[q], tb2 = ws.bs[ixj];
+                    if (key_less(wb, tb2, wa, ta) == up) {
+                        ws.bw[q] = wb; ws.bs[q] = tb2;
+                        ws.bw[ixj] = wa; ws.bs[ixj] = ta;
+                    }
+                }
+            }
+            cb_sync();
+        }
+    // 3. levels (see build_warp): prefix-max rank merge, fixed-point exit
+    for (uint32_t q = tid; q < m; q += CB) { ws.mw[q] = ws.bw[q]; ws.mt[q] = ws.bs[q]; ws.isbase[q] = 1; }
+    uint32_t mlen = m;
+    int lfix = MAXLEN - 1;
+    cb_sync();
+    for (int l = 1; l < MAXLEN; l++) {
+        const uint32_t npk = mlen / 2;
+        uint8_t* ib = ws.isbase + (size_t)l * 2 * m;
+        unsigned long long* nw = (l & 1) ? mw2 : ws.mw;
+        uint32_t* nt = (l & 1) ? mt2 : ws.mt;
+        const unsigned long long* ow = (l & 1) ? ws.mw : mw2;
+        const uint32_t* ot = (l & 1) ? ws.mt : mt2;
+        unsigned long long pw_[KI];
+        uint32_t pt_[KI], im_[KI];
+#pragma unroll
+        for (int k = 0; k < KI; k++) {
+            const uint32_t q = k * CB + tid;
+            uint32_t lb = 0;
+            pw_[k] = 0; pt_[k] = 0;
+            if (q < npk) {
+                pw_[k] = ow[2 * q] + ow[2 * q + 1];
+                pt_[k] = ot[2 * q];
+                uint32_t lo = 0, hi = m;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (key_less(ws.bw[mid], ws.bs[mid], pw_[k], pt_[k])) lo = mid + 1; else hi = mid;
+                }
+                lb = lo;
+            }
+            im_[k] = warp_incl_max(lb, lane);   // within the 32-package chunk k*4 + warp
+            if (lane == 31) s_tot[k * (CB / 32) + (tid >> 5)] = im_[k];
+        }
+        cb_sync();
+#pragma unroll
+        for (int k = 0; k < KI; k++) {
+            const uint32_t q = k * CB + tid;
+            const int chunk = k * (CB / 32) + (tid >> 5);
+            uint32_t pre = 0;
+            for (int c = 0; c < chunk; c++) pre = max(pre, s_tot[c]);
+            const uint32_t im = max(im_[k], pre);
+            if (q < npk) {
+                lbm[q] = im;
+                const uint32_t pos = im + q;
+                nw[pos] = pw_[k]; nt[pos] = pt_[k]; ib[pos] = 0;
+            }
+        }
+        cb_sync();
+        for (uint32_t q = tid; q < m; q += CB) {   // base item q lands after the packages with i_j <= q
+            uint32_t lo = 0, hi = npk;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (lbm[mid] <= q) lo = mid + 1; else hi = mid;
+            }
+            const uint32_t pos = q + lo;
+            nw[pos] = ws.bw[q]; nt[pos] = ws.bs[q]; ib[pos] = 1;
+        }
+        const uint32_t plen = mlen;
+        mlen = m + npk;
+        if (tid == 0) s_flag = 1;
+        cb_sync();
+        if (l >= 2 && mlen == plen) {
+            const uint8_t* pib = ib - 2 * m;
+            bool same = true;
+            for (uint32_t q = tid; q < mlen; q += CB) same &= nw[q] == ow[q] && nt[q] == ot[q] && ib[q] == pib[q];
+            if (!same) s_flag = 0;
+            cb_sync();
+            if (s_flag) {
+                lfix = l;
+                break;
+            }
+        }
+    }
+    // 4. selected prefixes, top level down
+    long long L = 2 * ((long long)m - 1);
+    for (int l = MAXLEN - 1; l >= 1; l--) {
+        const uint8_t* ib = ws.isbase + (size_t)min(l, lfix) * 2 * m;
+        uint32_t c = 0;
+        for (long long q = tid; q < L; q += CB) c += ib[q];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) s_tot[tid >> 5] = c;
+        cb_sync();
+        const uint32_t tot = s_tot[0] + s_tot[1] + s_tot[2] + s_tot[3];
+        cb_sync();
+        if (tid == 0) s_nb[l] = tot;
+        L = 2 * (L - (long long)tot);
+    }
+    if (tid == 0) s_nb[0] = L;
+    if (tid <= MAXLEN) s_cnt[tid] = 0;
+    cb_sync();
+    // 5. lengths and bit count
+    unsigned long long bits = 0;
+    for (uint32_t q = tid; q < m; q += CB) {
+        int len = 0;
+        for (int l = 0; l < MAXLEN; l++) len += (long long)q < s_nb[l];
+        lengths[ws.bs[q]] = (uint8_t)len;
+        bits += ws.bw[q] * (unsigned long long)len;
+        atomicAdd(&s_cnt[len], 1u);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) bits += __shfl_xor_sync(0xffffffffu, bits, o);
+    if (lane == 0) reinterpret_cast<unsigned long long*>(mw2)[tid >> 5] = bits;   // scratch
+    cb_sync();
+    if (tid == 0) {
+        const unsigned long long* sb = reinterpret_cast<const unsigned long long*>(mw2);
+        *bit_count = sb[0] + sb[1] + sb[2] + sb[3];
+        unsigned long long code = 0;
+        s_first[0] = 0;
+        for (int l = 1; l <= MAXLEN; l++) {
+            code = (code + (l > 1 ? s_cnt[l - 1] : 0)) << 1;
+            s_first[l] = code;
+        }
+        for (int l = 0; l <= MAXLEN; l++) s_cnt[l] = 0;   // reuse as running rank
+    }
+    __threadfence_block();
+    cb_sync();
+    // 6. canonical codewords by (length, symbol)  (encode.py:155-171): one warp
+    if (tid < 32) {
+        for (uint32_t s0 = 0; s0 < nsym; s0 += 32) {
+            const uint32_t sy = s0 + lane;
+            const int len = sy < nsym ? lengths[sy] : 0;
+            const unsigned peers = __match_any_sync(0xffffffffu, len);
+            const uint32_t rank = __popc(peers & lanemask_lt());
+            if (len) cw[sy] = (uint32_t)(s_first[len] + s_cnt[len] + rank);
+            __syncwarp();
+            if (len && rank == 0) s_cnt[len] += __popc(peers);
+            __syncwarp();
+        }
+    }
+}
+
 FZB_DEV void build_warp(uint32_t m, uint32_t nsym, const unsigned long long* in_w, const uint32_t* in_s,
                         uint8_t* __restrict__ lengths, uint32_t* __restrict__ cw,
                         unsigned long long* __restrict__ bit_count, long long* s_nb, uint32_t* s_cnt,
@@ -308,7 +504,7 @@ __global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long l
         return;
     }
     if (m <= WARP_BUILD_MAX) {
-        if (tid < 32) build_warp(m, nsym, ws.bw, ws.bs, lengths, cw, bit_count, s_nb, s_cnt, s_first);
+        if (tid < CB) build_cta4(m, nsym, ws.bw, ws.bs, lengths, cw, bit_count, s_nb, s_cnt, s_first);
         return;
     }
     // 2. bitonic sort of (w, s) over the next power of two (pad = max key)
