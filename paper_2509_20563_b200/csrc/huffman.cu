@@ -6,8 +6,8 @@
 //    materialised: every merged list's selected items form a prefix, so a
 //    leaf's length is the number of levels whose selected prefix contains
 //    it; only "is this merged slot a leaf" bytes per level are stored.
-//    Up to 256 used symbols one warp builds everything in shared memory
-//    with no block barriers; a level's merge places every package and base
+//    Up to 256 used symbols four warps build everything in shared memory
+//    (named barriers between phases); a level's merge places every package and base
 //    item by rank search, with a prefix max over the packages' ranks so an
 //    unsorted package list still merges exactly as heapq.merge does, and
 //    the level loop stops at the fixed point (a level equal to the previous
@@ -33,7 +33,7 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int MAXLEN = 32;
-constexpr int BT = 256;   // build threads (<= 255 registers: the single-warp path must not spill)
+constexpr int BT = 256;   // build threads (<= 255 registers: the small-alphabet path must not spill)
 constexpr uint32_t SMEM_BUILD_SYMS = 2048;   // alphabets up to this size build in shared memory
 constexpr size_t SMEM_BUILD_BYTES = (size_t)SMEM_BUILD_SYMS * (8 + 8 + 16 + 4 + 4 + 8) + (size_t)MAXLEN * 2 * SMEM_BUILD_SYMS;
 
@@ -54,12 +54,12 @@ FZB_DEV bool key_less(unsigned long long wa, uint32_t ta, unsigned long long wb,
     return wa < wb || (wa == wb && ta < tb);
 }
 
-// ---- single-warp build for small used alphabets (m <= WARP_BUILD_MAX): no
-// block barriers; every step is warp-synchronous.  Each level's merge of
-// the sorted base list B with the package list P reproduces heapq.merge
-// (encode.py:196) for ANY P order: P[j] is emitted once the base pointer
-// reaches i_j = max_{j' <= j} lb(P[j']) (lb = #B < P[j], keys never tie
-// across the lists), so P[j] lands at i_j + j and B[q] at q + #{j: i_j <= q}.
+// ---- small used alphabets (m <= WARP_BUILD_MAX) build in shared memory
+// with the layout below.  Each level's merge of the sorted base list B with
+// the package list P reproduces heapq.merge (encode.py:196) for ANY P
+// order: P[j] is emitted once the base pointer reaches i_j = max_{j' <= j}
+// lb(P[j']) (lb = #B < P[j], keys never tie across the lists), so P[j]
+// lands at i_j + j and B[q] at q + #{j: i_j <= q}.
 constexpr uint32_t WARP_BUILD_MAX = 256;
 
 FZB_DEV uint32_t warp_incl_max(uint32_t v, int lane) {
@@ -79,11 +79,11 @@ constexpr size_t WB_BW = 0, WB_PW = WB_BW + 8 * WARP_BUILD_MAX, WB_MW = WB_PW + 
                  WB_IB = WB_LB + 4 * WARP_BUILD_MAX, WB_MW2 = WB_IB + (size_t)MAXLEN * 2 * WARP_BUILD_MAX,
                  WB_MT2 = WB_MW2 + 16 * WARP_BUILD_MAX, WARP_BUILD_SMEM = WB_MT2 + 8 * WARP_BUILD_MAX;
 
-// ---- 4-warp build for small used alphabets (m <= WARP_BUILD_MAX): the
-// same steps as build_warp below, with one item (two for m > 128) per thread
-// and named barriers (bar 1, 128 threads) between the phases of a level, so
-// each level costs one rank search per thread instead of a warp's serial
-// sweep over all items.
+// ---- 4-warp build for small used alphabets (m <= WARP_BUILD_MAX): one item
+// (two for m > 128) per thread and named barriers (bar 1, 128 threads)
+// between the phases of a level, so each level costs one rank search per
+// thread instead of a warp's serial sweep over all items (the single-warp
+// build it replaced took 2x as long).
 constexpr int CB = 128;   // threads of the 4-warp build
 FZB_DEV void cb_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
@@ -144,7 +144,12 @@ FZB_DEV void build_cta4(uint32_t m, uint32_t nsym, const unsigned long long* in_
             }
             cb_sync();
         }
-    // 3. levels (see build_warp): prefix-max rank merge, fixed-point exit
+    // 3. levels.  M_0 = base.  A level's merge places every package and base
+    // item by rank search; the prefix max over the packages' base ranks
+    // reproduces heapq.merge (encode.py:196) for ANY package order: P[j] is
+    // emitted once the base pointer reaches i_j = max_{j' <= j} lb(P[j']), so
+    // P[j] lands at i_j + j and B[q] at q + #{j: i_j <= q}.  Once M_l == M_{l-1}
+    // every later level repeats it: stop and reuse its leaf marks.
     for (uint32_t q = tid; q < m; q += CB) { ws.mw[q] = ws.bw[q]; ws.mt[q] = ws.bs[q]; ws.isbase[q] = 1; }
     uint32_t mlen = m;
     int lfix = MAXLEN - 1;
@@ -273,182 +278,6 @@ FZB_DEV void build_cta4(uint32_t m, uint32_t nsym, const unsigned long long* in_
             __syncwarp();
         }
     }
-}
-
-FZB_DEV void build_warp(uint32_t m, uint32_t nsym, const unsigned long long* in_w, const uint32_t* in_s,
-                        uint8_t* __restrict__ lengths, uint32_t* __restrict__ cw,
-                        unsigned long long* __restrict__ bit_count, long long* s_nb, uint32_t* s_cnt,
-                        unsigned long long* s_first) {
-    extern __shared__ __align__(16) unsigned char sm_build[];
-    const int lane = threadIdx.x & 31;
-    HB_STAMP(0);
-    // the compacted (w, s) list may alias this layout: move it through registers
-    unsigned long long rw[WARP_BUILD_MAX / 32];
-    uint32_t rs[WARP_BUILD_MAX / 32];
-#pragma unroll
-    for (int k = 0; k < (int)(WARP_BUILD_MAX / 32); k++) {
-        const uint32_t q = k * 32 + lane;
-        rw[k] = q < m ? in_w[q] : 0ull;
-        rs[k] = q < m ? in_s[q] : 0u;
-    }
-    __syncwarp();
-    BuildWS ws;
-    ws.bw = reinterpret_cast<unsigned long long*>(sm_build + WB_BW);
-    ws.pw = reinterpret_cast<unsigned long long*>(sm_build + WB_PW);
-    ws.mw = reinterpret_cast<unsigned long long*>(sm_build + WB_MW);
-    ws.bs = reinterpret_cast<uint32_t*>(sm_build + WB_BS);
-    ws.pt = reinterpret_cast<uint32_t*>(sm_build + WB_PT);
-    ws.mt = reinterpret_cast<uint32_t*>(sm_build + WB_MT);
-    ws.isbase = sm_build + WB_IB;
-    uint32_t* lbm = reinterpret_cast<uint32_t*>(sm_build + WB_LB);
-#pragma unroll
-    for (int k = 0; k < (int)(WARP_BUILD_MAX / 32); k++) {
-        const uint32_t q = k * 32 + lane;
-        if (q < m) { ws.bw[q] = rw[k]; ws.bs[q] = rs[k]; }
-    }
-    // 2. bitonic sort of (w, s) over the next power of two (pad = max key)
-    uint32_t np2 = 1;
-    while (np2 < m) np2 <<= 1;
-    for (uint32_t q = m + lane; q < np2; q += 32) { ws.bw[q] = ~0ull; ws.bs[q] = 0xFFFFFFFFu; }
-    __syncwarp();
-    for (uint32_t k = 2; k <= np2; k <<= 1)
-        for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
-            for (uint32_t q = lane; q < np2; q += 32) {
-                const uint32_t ixj = q ^ jj;
-                if (ixj > q) {
-                    const bool up = (q & k) == 0;
-                    const unsigned long long wa = ws.bw[q], wb = ws.bw[ixj];
-                    const uint32_t ta = ws.bs[q], tb2 = ws.bs[ixj];
-                    if (key_less(wb, tb2, wa, ta) == up) {
-                        ws.bw[q] = wb; ws.bs[q] = tb2;
-                        ws.bw[ixj] = wa; ws.bs[ixj] = ta;
-                    }
-                }
-            }
-            __syncwarp();
-        }
-    HB_STAMP(1);
-    // 3. levels.  M_0 = base.  Once M_l == M_{l-1} (weights, tiebreaks and
-    // leaf marks) every later level repeats it: stop and reuse its marks.
-    unsigned long long* mw2 = reinterpret_cast<unsigned long long*>(sm_build + WB_MW2);
-    uint32_t* mt2 = reinterpret_cast<uint32_t*>(sm_build + WB_MT2);
-    for (uint32_t q = lane; q < m; q += 32) { ws.mw[q] = ws.bw[q]; ws.mt[q] = ws.bs[q]; ws.isbase[q] = 1; }
-    uint32_t mlen = m;
-    int lfix = MAXLEN - 1;
-    __syncwarp();
-    for (int l = 1; l < MAXLEN; l++) {
-        const uint32_t npk = mlen / 2;
-        uint8_t* ib = ws.isbase + (size_t)l * 2 * m;
-        unsigned long long* nw = (l & 1) ? mw2 : ws.mw;   // this level's merged list
-        uint32_t* nt = (l & 1) ? mt2 : ws.mt;
-        const unsigned long long* ow = (l & 1) ? ws.mw : mw2;   // the previous level's
-        const uint32_t* ot = (l & 1) ? ws.mt : mt2;
-        uint32_t carry = 0;
-        for (uint32_t q0 = 0; q0 < npk; q0 += 32) {
-            const uint32_t q = q0 + lane;
-            uint32_t lb = 0;
-            unsigned long long w = 0;
-            uint32_t t = 0;
-            if (q < npk) {
-                w = ow[2 * q] + ow[2 * q + 1];
-                t = ot[2 * q];
-                uint32_t lo = 0, hi = m;
-                while (lo < hi) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (key_less(ws.bw[mid], ws.bs[mid], w, t)) lo = mid + 1; else hi = mid;
-                }
-                lb = lo;
-            }
-            const uint32_t im = max(warp_incl_max(lb, lane), carry);
-            carry = __shfl_sync(0xffffffffu, im, 31);
-            if (q < npk) { ws.pw[q] = w; ws.pt[q] = t; lbm[q] = im; }
-        }
-        __syncwarp();
-        for (uint32_t q = lane; q < npk; q += 32) {
-            const uint32_t pos = lbm[q] + q;
-            nw[pos] = ws.pw[q]; nt[pos] = ws.pt[q]; ib[pos] = 0;
-        }
-        for (uint32_t q = lane; q < m; q += 32) {   // packages before base q: #{j : i_j <= q}
-            uint32_t lo = 0, hi = npk;
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (lbm[mid] <= q) lo = mid + 1; else hi = mid;
-            }
-            const uint32_t pos = q + lo;
-            nw[pos] = ws.bw[q]; nt[pos] = ws.bs[q]; ib[pos] = 1;
-        }
-        const uint32_t plen = mlen;
-        mlen = m + npk;
-        __syncwarp();
-        if (l >= 2 && mlen == plen) {
-            const uint8_t* pib = ib - 2 * m;
-            bool same = true;
-            for (uint32_t q = lane; q < mlen; q += 32)
-                same &= nw[q] == ow[q] && nt[q] == ot[q] && ib[q] == pib[q];
-            if (__all_sync(0xffffffffu, same)) {
-                lfix = l;
-                break;
-            }
-        }
-    }
-    HB_STAMP(2);
-#ifdef LZ7_TIMING
-    if (lane == 0) g_hf_build_stamp[7] = lfix;
-#endif
-    // 4. selected prefixes, top level down
-    long long L = 2 * ((long long)m - 1);
-    for (int l = MAXLEN - 1; l >= 1; l--) {
-        const uint8_t* ib = ws.isbase + (size_t)min(l, lfix) * 2 * m;
-        uint32_t c = 0;
-        for (long long q0 = 0; q0 < L; q0 += 32) {
-            const long long q = q0 + lane;
-            c += __popc(__ballot_sync(0xffffffffu, q < L && ib[q]));
-        }
-        if (lane == 0) s_nb[l] = c;
-        L = 2 * (L - (long long)c);
-    }
-    if (lane == 0) s_nb[0] = L;
-    __syncwarp();
-    HB_STAMP(3);
-    // 5. lengths and bit count
-    unsigned long long bits = 0;
-    if (lane <= MAXLEN) s_cnt[lane] = 0;
-    __syncwarp();
-    for (uint32_t q = lane; q < m; q += 32) {
-        int len = 0;
-        for (int l = 0; l < MAXLEN; l++) len += (long long)q < s_nb[l];
-        lengths[ws.bs[q]] = (uint8_t)len;
-        bits += ws.bw[q] * (unsigned long long)len;
-        atomicAdd(&s_cnt[len], 1u);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) bits += __shfl_xor_sync(0xffffffffu, bits, o);
-    if (lane == 0) *bit_count = bits;
-    __syncwarp();
-    HB_STAMP(4);
-    // 6. canonical codewords by (length, symbol)  (encode.py:155-171)
-    if (lane == 0) {
-        unsigned long long code = 0;
-        s_first[0] = 0;
-        for (int l = 1; l <= MAXLEN; l++) {
-            code = (code + (l > 1 ? s_cnt[l - 1] : 0)) << 1;
-            s_first[l] = code;
-        }
-        for (int l = 0; l <= MAXLEN; l++) s_cnt[l] = 0;   // reuse as running rank
-    }
-    __syncwarp();
-    __threadfence_block();   // lengths[] written above by other lanes
-    for (uint32_t s0 = 0; s0 < nsym; s0 += 32) {
-        const uint32_t s = s0 + lane;
-        const int len = s < nsym ? lengths[s] : 0;
-        const unsigned peers = __match_any_sync(0xffffffffu, len);
-        const uint32_t rank = __popc(peers & lanemask_lt());
-        if (len) cw[s] = (uint32_t)(s_first[len] + s_cnt[len] + rank);
-        __syncwarp();
-        if (len && rank == 0) s_cnt[len] += __popc(peers);
-        __syncwarp();
-    }
-    HB_STAMP(5);
 }
 
 __global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long long* __restrict__ bins, uint32_t nsym,
@@ -1323,7 +1152,7 @@ FZB_API int fzb_huffman_build(const uint64_t* d_bins, uint32_t nsym, uint8_t* d_
     ws.mw = reinterpret_cast<unsigned long long*>(p); p += align256(m2 * 8);
     ws.mt = reinterpret_cast<uint32_t*>(p); p += align256(m2 * 4);
     ws.isbase = p;
-    // the single-warp path (<= WARP_BUILD_MAX used symbols) always builds in shared memory
+    // the small-alphabet path (<= WARP_BUILD_MAX used symbols) always builds in shared memory
     const size_t bsm = nsym <= SMEM_BUILD_SYMS ? SMEM_BUILD_BYTES : WARP_BUILD_SMEM;
     static bool attr_set = false;
     if (!attr_set) {
