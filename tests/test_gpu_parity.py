@@ -317,3 +317,51 @@ def test_graph_variants_bytes_equal_sequential(preset):
         a = fz.compress_via_graph(f, eb, preset)
         assert fz.serialize_archive(a) == fz.serialize_archive(fz.compress(f, eb, preset))
         assert fz.decompress_via_graph(a).data.tobytes() == fz.decompress(a).data.tobytes()
+
+
+# ------------------------------------------------------------------ edge cases
+
+EDGE_DIMS = [(1,), (2,), (7,), (33,), (1, 1, 1), (1, 1, 5), (2, 2, 2), (3, 3), (1, 64), (64, 1), (17, 17),
+             (4, 5, 6), (16, 17, 18), (1, 2, 3), (5, 1, 9)]
+
+
+@pytest.mark.parametrize("dims", EDGE_DIMS)
+@pytest.mark.parametrize("preset", ["default", "speed", "quality"])
+def test_tiny_and_ragged_fields_match_oracle(oracle, dims, preset):
+    # tiny / degenerate extents: every kernel's partial-tile, partial-block and
+    # single-element paths (and the interp -> Lorenzo fallback) vs the oracle
+    rng = np.random.default_rng(sum(dims) + len(preset))
+    x = (np.cumsum(rng.normal(0, 1, int(np.prod(dims)))) * 0.1).astype(np.float32)
+    want = oracle.compress(x, dims, 1, 1e-3, preset)
+    a = fz.compress(Field(dims, x), ErrorBoundSpec(REL, 1e-3), preset)
+    assert fz.serialize_archive(a) == want
+    rec = fz.decompress(a)
+    _, orec = oracle.decompress(want)
+    assert rec.data.tobytes() == orec.tobytes()
+
+
+@pytest.mark.parametrize("preset", ["default", "speed", "quality"])
+@pytest.mark.parametrize("case", ["constant", "abs_tiny_eb", "abs_huge_eb", "two_values"])
+def test_bound_edge_cases_match_oracle(oracle, preset, case):
+    # constant field (header-only archive), an absolute bound so small that
+    # almost everything is an outlier, one so large that every code is zero,
+    # and a two-valued field
+    dims = (24, 40, 36)
+    n = int(np.prod(dims))
+    x = np.sin(np.arange(n, dtype=np.float64) * 0.01).astype(np.float32)
+    mode, mag = 1, 1e-3
+    if case == "constant":
+        x = np.full(n, 3.25, np.float32)
+    elif case == "abs_tiny_eb":
+        mode, mag = 0, 1e-9
+    elif case == "abs_huge_eb":
+        mode, mag = 0, 10.0
+    else:
+        x = np.where(np.arange(n) % 3 == 0, -1.5, 2.0).astype(np.float32)
+    want = oracle.compress(x, dims, mode, mag, preset)
+    eb = ErrorBoundSpec(ABS if mode == 0 else REL, mag)
+    a = fz.compress(Field(dims, x), eb, preset)
+    assert fz.serialize_archive(a) == want
+    rec = fz.decompress(a)
+    _, orec = oracle.decompress(want)
+    assert rec.data.tobytes() == orec.tobytes()
