@@ -1149,11 +1149,24 @@ __global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__
         // the rest of the current block, and the block summaries of the current
         // and the next superblock (lane = block within the superblock)
         const long long a0 = t, b0 = (t % BS1) ? min(n, (t / BS1 + 1) * BS1) : t;
+        // the rest of the current block: its whole aligned 1024-element block in
+        // 8 16-byte loads per lane when it is complete (elements before a0 are
+        // masked at the search), else 32 scalar loads
+        const long long blk_a = (a0 / BS1) * BS1;
+        const bool vec_rest = b0 > a0 && blk_a + BS1 <= n && !((reinterpret_cast<uintptr_t>(x + blk_a)) & 15);
         float pv[32];
+        if (vec_rest) {
 #pragma unroll
-        for (int e = 0; e < 32; e++) {
-            const long long i = a0 + e * 32 + lane;
-            pv[e] = i < b0 ? __ldg(x + i) : 0.f;
+            for (int e = 0; e < 8; e++) {
+                const float4 q = __ldg(reinterpret_cast<const float4*>(x + blk_a) + e * 32 + lane);
+                pv[4 * e] = q.x; pv[4 * e + 1] = q.y; pv[4 * e + 2] = q.z; pv[4 * e + 3] = q.w;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 32; e++) {
+                const long long i = a0 + e * 32 + lane;
+                pv[e] = i < b0 ? __ldg(x + i) : 0.f;
+            }
         }
         const long long sb_cur = b0 / BS2;
         float pmin[2], pmax[2];
@@ -1172,6 +1185,23 @@ __global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__
         WSTAMP(1);
         // scan [a, b) (b - a <= 1024) with coalesced loads; returns first outside index or -1
         auto scan = [&](long long a, long long b) -> long long {
+            if (b - a == BS1 && !((reinterpret_cast<uintptr_t>(x + a)) & 15)) {
+                // a whole aligned block: 8 16-byte loads per lane (elements
+                // a + 128*e + 4*lane + c) instead of 32 scalar ones
+                uint32_t m = 0;
+#pragma unroll
+                for (int e = 0; e < 8; e++) {
+                    const float4 q = __ldg(reinterpret_cast<const float4*>(x + a) + e * 32 + lane);
+                    const float qq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                    for (int c = 0; c < 4; c++) m |= (uint32_t)!(qq[c] >= zlo && qq[c] <= zhi) << (4 * e + c);
+                }
+                // bit 4e+c <-> index a + 128e + 4*lane + c: increasing with the bit within a lane
+                const uint32_t mine = m ? (uint32_t)(128 * ((__ffs(m) - 1) >> 2) + 4 * lane + ((__ffs(m) - 1) & 3))
+                                        : 0xFFFFFFFFu;
+                const uint32_t best = __reduce_min_sync(0xffffffffu, mine);
+                return best == 0xFFFFFFFFu ? -1 : a + (long long)best;
+            }
             float v[32];
 #pragma unroll
             for (int e = 0; e < 32; e++) {
@@ -1182,7 +1212,20 @@ __global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__
         };
         long long found = -1;
         if (b0 > a0) {
-            found = first_outside(pv, a0, b0, zlo, zhi);
+            if (vec_rest) {   // bit 4e+c <-> index blk_a + 128e + 4*lane + c
+                uint32_t m = 0;
+#pragma unroll
+                for (int e = 0; e < 32; e++) {
+                    const long long i = blk_a + 128 * (e >> 2) + 4 * lane + (e & 3);
+                    m |= (uint32_t)((i >= a0) & !(pv[e] >= zlo && pv[e] <= zhi)) << e;
+                }
+                const uint32_t mine = m ? (uint32_t)(128 * ((__ffs(m) - 1) >> 2) + 4 * lane + ((__ffs(m) - 1) & 3))
+                                        : 0xFFFFFFFFu;
+                const uint32_t best = __reduce_min_sync(0xffffffffu, mine);
+                found = best == 0xFFFFFFFFu ? -1 : blk_a + (long long)best;
+            } else {
+                found = first_outside(pv, a0, b0, zlo, zhi);
+            }
             t = b0;
         }
         WSTAMP(2);
