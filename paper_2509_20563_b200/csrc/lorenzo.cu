@@ -1356,16 +1356,35 @@ __global__ void lz1d_event_chain_kernel(const long long* __restrict__ evpos, con
         const bool o0 = (bitmap[p0 >> 5] >> (p0 & 31)) & 1u;
         if (!(e == 0 || o0)) continue;
         float r = 0.f;
-        for (unsigned long long q = e; q < nev; q++) {
-            const long long p = evpos[q];
-            const bool outl = (bitmap[p >> 5] >> (p & 31)) & 1u;
-            if (q != e && outl) break;
-            if (outl) {
-                r = recon[p];  // pre-scattered outlier value
-            } else {
-                const double pred = (p == 0) ? 0.0 : __dadd_rn(0.0, (double)r);
-                r = dequantize(pred, (int)codes[p], P);
-                recon[p] = r;
+        // the chain depends on r only: positions, flags and codes of the next
+        // EV_AHEAD events are loaded together, so each event costs its
+        // dequantization instead of three dependent global loads
+        constexpr int EV_AHEAD = 8;
+        bool done = false;
+        for (unsigned long long q0 = e; q0 < nev && !done; q0 += EV_AHEAD) {
+            long long pp[EV_AHEAD];
+            uint32_t ww[EV_AHEAD];
+            uint16_t cc[EV_AHEAD];
+#pragma unroll
+            for (int u = 0; u < EV_AHEAD; u++) pp[u] = q0 + u < nev ? evpos[q0 + u] : -1;
+#pragma unroll
+            for (int u = 0; u < EV_AHEAD; u++) {
+                ww[u] = pp[u] >= 0 ? bitmap[pp[u] >> 5] : 0u;
+                cc[u] = pp[u] >= 0 ? codes[pp[u]] : (uint16_t)radius;
+            }
+#pragma unroll
+            for (int u = 0; u < EV_AHEAD; u++) {
+                const long long p = pp[u];
+                if (p < 0) { done = true; break; }
+                const bool outl = (ww[u] >> (p & 31)) & 1u;
+                if (q0 + u != e && outl) { done = true; break; }
+                if (outl) {
+                    r = recon[p];  // pre-scattered outlier value
+                } else {
+                    const double pred = (p == 0) ? 0.0 : __dadd_rn(0.0, (double)r);
+                    r = dequantize(pred, (int)cc[u], P);
+                    recon[p] = r;
+                }
             }
         }
     }
@@ -1377,7 +1396,8 @@ __global__ void lz1d_fill_kernel(const uint16_t* __restrict__ codes, const uint3
     const int lane = threadIdx.x & 31;
     const long long ch = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (ch >= nch) return;
-    const long long base = ch * EVC + lane * 32;
+    const long long base0 = ch * EVC;
+    const long long base = base0 + lane * 32;
     const uint32_t m = event_mask(codes, bitmap, n, base, radius);
     // last event position at or before the end of each lane's group
     long long last = m ? base + 31 - __clz(m) : -1;
@@ -1392,12 +1412,17 @@ __global__ void lz1d_fill_kernel(const uint16_t* __restrict__ codes, const uint3
         const unsigned long long o = offs[ch];
         carry = o > 0 ? evpos[o - 1] : -1;
     }
-    if (base >= n) return;
-    // a zero-code element reconstructs to f32(0.0 + r): same value, -0 -> +0
-    float cur = carry >= 0 ? recon[carry] + 0.0f : 0.f;
-    for (int e = 0; e < 32 && base + e < n; e++) {
-        if ((m >> e) & 1u) cur = recon[base + e] + 0.0f;
-        else recon[base + e] = cur;
+    // coalesced writes: row j is group j's 32 elements, one per lane; a
+    // zero-code element reconstructs to f32(0.0 + r): the value of the last
+    // event at or before it (or the carry), -0 -> +0; events keep their value
+    for (int j = 0; j < 32; j++) {
+        const long long gb = base0 + 32 * (long long)j;
+        if (gb >= n) break;
+        const uint32_t mj = __shfl_sync(0xffffffffu, m, j);
+        const long long cj = __shfl_sync(0xffffffffu, carry, j);
+        const uint32_t upto = mj & (0xFFFFFFFFu >> (31 - lane));   // events at positions <= lane
+        const long long src = upto ? gb + 31 - __clz(upto) : cj;
+        if (gb + lane < n && !((mj >> lane) & 1u)) recon[gb + lane] = src >= 0 ? recon[src] + 0.0f : 0.f;
     }
 }
 
