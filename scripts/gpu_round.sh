@@ -16,6 +16,7 @@ if [ "$2" != "quick" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c2.csv python bench.py --steps 2 --warmup 1 --no-cpu > $O/ncu_launch.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c1.csv python scripts/prof_roundtrip.py 100x500x500 default 1e-4 > $O/ncu_launch_c1.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c3.csv python scripts/prof_roundtrip.py 1800x3600 quality 1e-4 > $O/ncu_launch_c3.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c4.csv python scripts/prof_roundtrip.py 280953867 default 1e-4 > $O/ncu_launch_c4.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"lz7_kernel|bs_enc4|bs_dec3" -c 4 -o $O/c2_full python scripts/prof_roundtrip.py 512x512x512 speed 1e-3 > $O/ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"hf_|huffman_build|hist_" -c 9 -o $O/c1_full python scripts/prof_roundtrip.py 100x500x500 default 1e-4 > $O/ncu_full_c1.log 2>&1
 fi
