@@ -1,3 +1,5 @@
+// Host restatement check: the walker's short zero-code predicate equals
+// quantize(v, pred) == (radius, not outlier) (run by tests/test_zero_code.py).
 #include <math.h>
 #include <stdio.h>
 #include <stdint.h>
