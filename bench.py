@@ -459,8 +459,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--pipeline", choices=["speed", "default", "quality"],
+                    help="override the workload's preset (SURVEY 8d: C4 on all three)")
+    ap.add_argument("--rel", type=float, help="override the workload's relative error bound")
     args = ap.parse_args()
-    wl = WORKLOADS[args.workload]
+    wl = dict(WORKLOADS[args.workload])
+    if args.pipeline or args.rel:
+        wl["pipeline"] = args.pipeline or wl["pipeline"]
+        wl["rel"] = args.rel or wl["rel"]
+        wl["name"] = f"{wl['name']} [override: {wl['pipeline']} rel {wl['rel']:g}]"
     if args.impl == "reference":
         run_reference(args, wl)
     else:
