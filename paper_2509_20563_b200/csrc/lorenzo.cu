@@ -1006,11 +1006,9 @@ __global__ void lz1d_super_kernel(const float* __restrict__ bmin, const float* _
 FZB_DEV long long first_outside(const float (&v)[32], long long a, long long b, float zlo, float zhi) {
     const int lane = threadIdx.x & 31;
     uint32_t m = 0;
+    const int len = (int)(b - a);   // <= 1024: 32-bit offsets
 #pragma unroll
-    for (int e = 0; e < 32; e++) {
-        const long long i = a + e * 32 + lane;
-        m |= (uint32_t)((i < b) & !(v[e] >= zlo && v[e] <= zhi)) << e;
-    }
+    for (int e = 0; e < 32; e++) m |= (uint32_t)((e * 32 + lane < len) & !(v[e] >= zlo && v[e] <= zhi)) << e;
     const uint32_t mine = m ? (uint32_t)((__ffs(m) - 1) * 32 + lane) : 0xFFFFFFFFu;
     const uint32_t best = __reduce_min_sync(0xffffffffu, mine);
     return best == 0xFFFFFFFFu ? -1 : a + (long long)best;
@@ -1225,11 +1223,10 @@ __global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__
         if (b0 > a0) {
             if (vec_rest) {   // bit 4e+c <-> index blk_a + 128e + 4*lane + c
                 uint32_t m = 0;
+                const int d0 = (int)(a0 - blk_a);   // < 1024: 32-bit offsets
 #pragma unroll
-                for (int e = 0; e < 32; e++) {
-                    const long long i = blk_a + 128 * (e >> 2) + 4 * lane + (e & 3);
-                    m |= (uint32_t)((i >= a0) & !(pv[e] >= zlo && pv[e] <= zhi)) << e;
-                }
+                for (int e = 0; e < 32; e++)
+                    m |= (uint32_t)((128 * (e >> 2) + 4 * lane + (e & 3) >= d0) & !(pv[e] >= zlo && pv[e] <= zhi)) << e;
                 const uint32_t mine = m ? (uint32_t)(128 * ((__ffs(m) - 1) >> 2) + 4 * lane + ((__ffs(m) - 1) & 3))
                                         : 0xFFFFFFFFu;
                 const uint32_t best = __reduce_min_sync(0xffffffffu, mine);
