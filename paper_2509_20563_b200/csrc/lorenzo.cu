@@ -951,6 +951,7 @@ __global__ void tile_order_kernel(int nA, int nB, int lagI, int lagJ, int* __res
 // element scans.
 constexpr int BS1 = 1024;        // elements per summary block
 constexpr int BS2 = 32 * BS1;    // elements per superblock
+static_assert(BS1 == 1 << 10 && BS2 == 1 << 15, "the walker indexes blocks with shifts (t >= 0)");
 
 __global__ void lz1d_summary_kernel(const float* __restrict__ x, long long n, uint16_t* __restrict__ codes,
                                     int radius, float* __restrict__ bmin, float* __restrict__ bmax,
@@ -1157,11 +1158,11 @@ __global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__
         // loads that do not depend on the new interval go out before its search:
         // the rest of the current block, and the block summaries of the current
         // and the next superblock (lane = block within the superblock)
-        const long long a0 = t, b0 = (t % BS1) ? min(n, (t / BS1 + 1) * BS1) : t;
+        const long long a0 = t, b0 = (t & (BS1 - 1)) ? min(n, ((t >> 10) + 1) << 10) : t;
         // the rest of the current block: its whole aligned 1024-element block in
         // 8 16-byte loads per lane when it is complete (elements before a0 are
         // masked at the search), else 32 scalar loads
-        const long long blk_a = (a0 / BS1) * BS1;
+        const long long blk_a = a0 & ~(long long)(BS1 - 1);
         const bool vec_rest = b0 > a0 && blk_a + BS1 <= n && !((reinterpret_cast<uintptr_t>(x + blk_a)) & 15);
         float pv[32];
         if (vec_rest) {
@@ -1177,7 +1178,7 @@ __global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__
                 pv[e] = i < b0 ? __ldg(x + i) : 0.f;
             }
         }
-        const long long sb_cur = b0 / BS2;
+        const long long sb_cur = b0 >> 15;
         float pmin[2], pmax[2];
 #pragma unroll
         for (int h = 0; h < 2; h++) {
@@ -1241,8 +1242,8 @@ __global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__
 #ifdef LZ7_TIMING
             ph[4]++;
 #endif
-            const long long sb = t / BS2;
-            if (t % BS2 == 0) {  // probe 32 superblocks
+            const long long sb = t >> 15;
+            if ((t & (BS2 - 1)) == 0) {  // probe 32 superblocks
                 const long long sq = sb + lane;
                 const bool skip = sq < nsb && smin[sq] >= zlo && smax[sq] <= zhi;
                 const unsigned ns = __ballot_sync(0xffffffffu, !skip);
@@ -1251,7 +1252,7 @@ __global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__
                 if (t >= n) break;
             }
             // block summaries of superblock t / BS2 (prefetched for the current and the next one)
-            const long long sbt = t / BS2;
+            const long long sbt = t >> 15;
             float lo, hi;
             if (sbt == sb_cur) { lo = pmin[0]; hi = pmax[0]; }
             else if (sbt == sb_cur + 1) { lo = pmin[1]; hi = pmax[1]; }
@@ -1263,7 +1264,7 @@ __global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__
                 lo = bb < nblk ? __ldcg(bmin + bb) : INFINITY;
                 hi = bb < nblk ? __ldcg(bmax + bb) : -INFINITY;
             }
-            const long long bfirst = t / BS1;
+            const long long bfirst = t >> 10;
             const long long bb = sbt * 32 + lane;
             const bool skip = bb < bfirst || bb >= nblk || (lo >= zlo && hi <= zhi);
             const unsigned nsk = __ballot_sync(0xffffffffu, !skip);
