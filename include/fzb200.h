@@ -98,10 +98,16 @@ FZB_API size_t fzb_outlier_workspace_bytes(uint64_t n);
 FZB_API int fzb_outlier_compact(const uint32_t *d_bitmap, uint64_t n, const float *d_in, uint64_t *d_idx,
                                 float *d_vals, uint64_t *d_count, void *d_ws, size_t ws_bytes, void *stream);
 /* Scatter k outliers into d_recon + d_bitmap (zeroed by caller) and check the
- * QuantOutput invariants (core.py:207-215) against d_codes. */
+ * QuantOutput invariants (core.py:207-215) against d_codes.  d_codes may be
+ * NULL: the sentinel check is then left to fzb_outlier_check, so the scatter
+ * can run beside the codec decode (the reference's decompress graph,
+ * pipeline.py:490-580: huffman-decode || outlier-scatter). */
 FZB_API int fzb_outlier_scatter(const uint64_t *d_idx, const float *d_vals, uint64_t k, uint64_t n,
                                 const uint16_t *d_codes, uint32_t radius, float *d_recon, uint32_t *d_bitmap,
                                 uint32_t *d_status, void *stream);
+/* core.py:214-215: every outlier position must hold the sentinel code. */
+FZB_API int fzb_outlier_check(const uint64_t *d_idx, uint64_t k, uint64_t n, const uint16_t *d_codes,
+                              uint32_t radius, uint32_t *d_status, void *stream);
 
 /* ---- a7: histogram (encode.py:79-111) ----------------------------------- */
 /* d_bins u64[nbins] is zeroed here; codes >= nbins set FZB_ERR_CODE_RANGE. */

@@ -86,6 +86,7 @@ def load():
         "fzb_outlier_workspace_bytes": (SZ, [U64]),
         "fzb_outlier_compact": (I, [P, U64, P, P, P, P, P, SZ, P]),
         "fzb_outlier_scatter": (I, [P, P, U64, U64, P, U32, P, P, P, P]),
+        "fzb_outlier_check": (I, [P, U64, U64, P, U32, P, P]),
         "fzb_quality_leaves": (I, [P, P, P, P, U64, P, P, P]),
         "fzb_histogram": (I, [P, U64, U32, P, P, P]),
         "fzb_huffman_build_workspace_bytes": (SZ, [U32]),
@@ -113,6 +114,7 @@ EXPORTED = [
     "fzb_lorenzo_batch_workspace_bytes", "fzb_lorenzo_encode_batch_f32", "fzb_lorenzo_decode_batch_f32",
     "fzb_interp_encode_f32",
     "fzb_interp_decode_f32", "fzb_outlier_workspace_bytes", "fzb_outlier_compact", "fzb_outlier_scatter",
+    "fzb_outlier_check",
     "fzb_quality_leaves",
     "fzb_histogram", "fzb_huffman_build_workspace_bytes", "fzb_huffman_build", "fzb_huffman_encode_workspace_bytes",
     "fzb_huffman_encode", "fzb_huffman_decode_workspace_bytes", "fzb_huffman_decode",

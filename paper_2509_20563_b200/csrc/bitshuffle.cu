@@ -523,10 +523,12 @@ FZB_API int fzb_bitshuffle_encode(const uint16_t* d_codes, uint64_t n, uint8_t* 
     uint32_t* ticket = reinterpret_cast<uint32_t*>(w);
     unsigned long long* state = reinterpret_cast<unsigned long long*>(w + 256);
     cudaMemsetAsync(w, 0, 256 + nc * 8, st);
-    static int grid_cap = 0;   // resident CTAs of the persistent encoder (device-wide)
+    static int grid_cap_dev[64] = {0};   // resident CTAs of the persistent encoder, per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& grid_cap = grid_cap_dev[dev & 63];
     if (!grid_cap) {
-        int dev = 0, sms = 0, per = 0;
-        cudaGetDevice(&dev);
+        int sms = 0, per = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bs_enc4_kernel, BS_THREADS, 0);
         grid_cap = sms * (per > 0 ? per : 1);

@@ -1154,11 +1154,8 @@ FZB_API int fzb_huffman_build(const uint64_t* d_bins, uint32_t nsym, uint8_t* d_
     ws.isbase = p;
     // the small-alphabet path (<= WARP_BUILD_MAX used symbols) always builds in shared memory
     const size_t bsm = nsym <= SMEM_BUILD_SYMS ? SMEM_BUILD_BYTES : WARP_BUILD_SMEM;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(huffman_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BUILD_BYTES);
-        attr_set = true;
-    }
+    // the attribute is per device context: set it on every launch (cheap)
+    cudaFuncSetAttribute(huffman_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BUILD_BYTES);
     // small alphabets: fewer threads -> cheaper barriers (the lists are short)
     const int nth = BT;
     huffman_build_kernel<<<1, nth, bsm, (cudaStream_t)stream>>>(reinterpret_cast<const unsigned long long*>(d_bins), nsym,
@@ -1243,13 +1240,15 @@ FZB_API int fzb_huffman_decode(const uint8_t* d_stream, uint64_t nbytes, uint64_
     const uint32_t* words = reinterpret_cast<const uint32_t*>(d_stream);
     const unsigned blocks = (unsigned)((nsub + HD_THREADS - 1) / HD_THREADS);
     uint32_t* changed = reinterpret_cast<uint32_t*>(scal + 2);
-    static int coop_blocks = 0;
+    static int coop_blocks_dev[64] = {0};   // resident cooperative grid, per device
+    int cdev = 0;
+    cudaGetDevice(&cdev);
+    int& coop_blocks = coop_blocks_dev[cdev & 63];
     if (coop_blocks == 0) {
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hf_sync_coop_kernel, HD_THREADS, 0);
-        int dev = 0, nsm = kNumSMs;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        int nsm = kNumSMs;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cdev);
         coop_blocks = (per_sm > 0 ? per_sm : 1) * nsm;
     }
     unsigned gridc = (unsigned)coop_blocks;

@@ -275,9 +275,20 @@ __global__ void outlier_scatter_kernel(const unsigned long long* __restrict__ id
             continue;
         }
         if (q > 0 && idx[q - 1] >= t) set_err(status, FZB_ERR_OUTLIER_ORDER);  // core.py:212-213
-        if (codes[t] != radius) set_err(status, FZB_ERR_OUTLIER_CODE);          // core.py:214-215
+        if (codes != nullptr && codes[t] != radius) set_err(status, FZB_ERR_OUTLIER_CODE);  // core.py:214-215
         recon[t] = vals[q];
         atomicOr(bm + (t >> 5), 1u << (t & 31));
+    }
+}
+
+// core.py:214-215 on its own: the sentinel check of the outlier list against
+// decoded codes, for DAGs where the scatter runs beside the codec decode.
+__global__ void outlier_check_kernel(const unsigned long long* __restrict__ idx, uint64_t k, uint64_t n,
+                                     const uint16_t* __restrict__ codes, int radius, uint32_t* __restrict__ status) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < k; q += stride) {
+        const unsigned long long t = idx[q];
+        if (t < n && codes[t] != radius) set_err(status, FZB_ERR_OUTLIER_CODE);
     }
 }
 
@@ -464,6 +475,16 @@ FZB_API int fzb_outlier_scatter(const uint64_t* d_idx, const float* d_vals, uint
     outlier_scatter_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
         reinterpret_cast<const unsigned long long*>(d_idx), d_vals, k, n, d_codes, (int)radius, d_recon, d_bitmap,
         d_status);
+    return fzb_check_launch();
+}
+
+FZB_API int fzb_outlier_check(const uint64_t* d_idx, uint64_t k, uint64_t n, const uint16_t* d_codes,
+                              uint32_t radius, uint32_t* d_status, void* stream) {
+    if (k == 0) return 0;
+    unsigned blocks = (unsigned)((k + 255) / 256);
+    if (blocks > (unsigned)kNumSMs * 8) blocks = kNumSMs * 8;
+    outlier_check_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const unsigned long long*>(d_idx), k, n, d_codes, (int)radius, d_status);
     return fzb_check_launch();
 }
 

@@ -125,6 +125,8 @@ class Engine:
         self._capturing = False
         self.trace_only = None  # set of entry points to time (None: all); each timed call costs two events
         self._pending: list = []  # traced calls of replayed graphs, timed at the next sync
+        self.marks = None  # dict label -> CUDA event at a stage boundary (the *_with_timing paths)
+        self._side = None  # second stream of the fork/join DAGs (created on first use)
 
     # ------------------------------------------------------------ buffers
     def buf(self, name: str, nbytes: int, zero: bool = False, zero_new: bool = False) -> torch.Tensor:
@@ -163,28 +165,60 @@ class Engine:
     def sp(self):
         return ctypes.c_void_p(self.stream.cuda_stream)
 
-    def _call(self, fn: str, *args, nk: int = 1):
+    # ------------------------------------------------- fork/join + stage marks
+    def side(self) -> torch.cuda.Stream:
+        if self._side is None:
+            self._side = torch.cuda.Stream(self.device)
+        return self._side
+
+    def _fork(self) -> torch.cuda.Stream:
+        """Second branch of a DAG: the side stream waits for the main stream
+        (inside a capture this becomes a graph dependency edge)."""
+        side = self.side()
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        side.wait_event(ev)
+        return side
+
+    def _join(self, side: torch.cuda.Stream):
+        ev = torch.cuda.Event()
+        ev.record(side)
+        self.stream.wait_event(ev)
+
+    def _mark(self, label: str, st: torch.cuda.Stream | None = None):
+        if self.marks is not None and not self._capturing:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(st or self.stream)
+            self.marks[label] = ev
+
+    def _call(self, fn: str, *args, nk: int = 1, st: torch.cuda.Stream | None = None):
+        st = st or self.stream
         if self.trace is not None and (self.trace_only is None or fn in self.trace_only):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             if self._capturing:   # event-record nodes inside the graph
                 e0, e1 = _NodeEvent(self.lib), _NodeEvent(self.lib)
-                _lib.check(self.lib.fzb_event_record(e0.h, self.sp, 1), "fzb_event_record")
+                ssp = ctypes.c_void_p(st.cuda_stream)
+                _lib.check(self.lib.fzb_event_record(e0.h, ssp, 1), "fzb_event_record")
                 rc = getattr(self.lib, fn)(*args)
-                _lib.check(self.lib.fzb_event_record(e1.h, self.sp, 1), "fzb_event_record")
+                _lib.check(self.lib.fzb_event_record(e1.h, ssp, 1), "fzb_event_record")
             else:
-                e0.record(self.stream)
+                e0.record(st)
                 rc = getattr(self.lib, fn)(*args)
-                e1.record(self.stream)
+                e1.record(st)
             self.trace.append((fn, e0, e1))
         else:
             rc = getattr(self.lib, fn)(*args)
         self.launches += nk
         _lib.check(rc, fn)
 
-    def upload(self, name: str, data, pad: int = 0) -> torch.Tensor:
-        """H2D copy of host bytes (zero padded).  Payloads that already live in
-        pinned memory (archives produced by `finish`) are DMA-ed directly;
-        anything else goes through a cached pinned staging buffer."""
+    def upload(self, name: str, data, pad: int = 0, st: torch.cuda.Stream | None = None,
+               stage: str | None = None) -> torch.Tensor:
+        """H2D copy of host bytes (zero padded) on stream `st`.  Payloads that
+        already live in pinned memory (archives produced by `finish`) are
+        DMA-ed directly; anything else goes through a cached pinned staging
+        buffer.  `stage` forces the staging buffer `stage + name` (graph
+        replays copy from the captured staging address)."""
+        st = st or self.stream
         if isinstance(data, np.ndarray):
             raw = np.ascontiguousarray(data).view(np.uint8).reshape(-1)
         else:
@@ -192,15 +226,15 @@ class Engine:
         nb = raw.size
         dev = self.buf(name, nb + pad)
         if pad:
-            with torch.cuda.stream(self.stream):
+            with torch.cuda.stream(st):
                 dev[max(nb - (nb % 4), 0):nb + pad].zero_()
         if nb:
-            src = _pinned_view(raw)
+            src = None if stage is not None else _pinned_view(raw)
             if src is None:
-                h = self.pinned(name, nb)
+                h = self.pinned((stage or "") + name, nb)
                 h.numpy()[:nb] = raw
                 src = h[:nb]
-            with torch.cuda.stream(self.stream):
+            with torch.cuda.stream(st):
                 dev[:nb].copy_(src, non_blocking=True)
             self._inflight.append(src)  # keep the source alive until the next sync
         return dev
@@ -229,6 +263,7 @@ class Engine:
             raise ValueError(f"unknown predictor '{predictor}'")
         use_anchors = predictor == "interp" and interp_applicable(dims, anchor_stride)
         if pre is None:
+            self._mark("bound")
             status = self.buf("status" + tag, 8, zero=True)
             lohi = self.buf("lohi" + tag, 8)
             eb = self.buf("eb" + tag, 8)
@@ -240,6 +275,7 @@ class Engine:
         else:
             status, lohi, eb, codes, bitmap = (pre[k] for k in ("status", "lohi", "eb", "codes", "bitmap"))
         bufs = dict(status=status, lohi=lohi, eb=eb, codes=codes)
+        self._mark("predict")
         if pre is not None:
             pass
         elif use_anchors:
@@ -257,17 +293,23 @@ class Engine:
             lzws = self.buf("lzws" + tag, L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
             self._call("fzb_lorenzo_encode_f32", _p(x), n0, n1, n2, _p(eb), radius, _p(codes), _p(bitmap),
                        _p(lzws), lzws.numel(), sp, nk=2)
+        # the reference compress graph (pipeline.py:594-647) forks after the
+        # predictor: serialize-outliers || analysis -> primary-encode
         oidx = self.buf("oidx" + tag, 8 * n)
         oval = self.buf("oval" + tag, 4 * n)
         ocount = self.buf("ocount" + tag, 8)
         ocws = self.buf("ocws" + tag, L.fzb_outlier_workspace_bytes(n))
+        side = self._fork()
         self._call("fzb_outlier_compact", _p(bitmap), n, _p(x), _p(oidx), _p(oval), _p(ocount), _p(ocws),
-                   ocws.numel(), sp, nk=3)
+                   ocws.numel(), ctypes.c_void_p(side.cuda_stream), nk=3, st=side)
+        self._mark("outliers_end", side)
         bufs.update(oidx=oidx, oval=oval, ocount=ocount)
+        self._mark("predict_end")
         nsym = 2 * radius
         if codec == "huffman":
             bins = self.buf("bins" + tag, 8 * nsym)
             self._call("fzb_histogram", _p(codes), n, nsym, _p(bins), _p(status), sp)
+            self._mark("primary")
             lengths = self.buf("lengths" + tag, nsym)
             cw = self.buf("cw" + tag, 4 * nsym)
             bitcount = self.buf("bitcount" + tag, 8)
@@ -281,6 +323,7 @@ class Engine:
                        _p(hws), hws.numel(), _p(status), sp, nk=5)
             bufs.update(lengths=lengths, bitcount=bitcount, hfout=out)
         elif codec == "bitshuffle":
+            self._mark("primary")
             nb = (n + 255) // 256
             bsmap = self.buf("bsmap" + tag, 16 * nb)
             pay = self.buf("bspay" + tag, 512 * nb)
@@ -291,6 +334,8 @@ class Engine:
             bufs.update(bsmap=bsmap, bspay=pay, nwords=nwords)
         else:
             raise ValueError(f"unknown primary codec '{codec}'")
+        self._mark("primary_end")
+        self._join(side)
         return DeviceArchive(pipeline_id, int(eb_mode), float(magnitude), dims, radius, predictor, codec, n, bufs,
                              use_anchors)
 
@@ -338,12 +383,14 @@ class Engine:
         host = torch.empty(total, dtype=torch.uint8, pin_memory=True)
         offs = []
         o = head
+        self._mark("d2h")
         with torch.cuda.stream(self.stream):
             for name, sz in parts:
                 if sz:
                     host[o:o + sz].copy_(b[name][:sz], non_blocking=True)
                 offs.append((o, sz))
                 o += sz
+        self._mark("d2h_end")
         self._sync()
         mv = memoryview(host.numpy()).toreadonly()
         blobs = [mv[o:o + sz] for o, sz in offs]
@@ -393,6 +440,16 @@ class Engine:
         status = self.buf("dstatus" + tag, 8, zero=True)
         codes = self.buf("dcodes" + tag, 2 * n + 16) if batch is None else batch["codes"]
         nsym = 2 * da.radius
+        n0, n1, n2 = pad3(da.dims)
+        if batch is None:
+            bitmap = self.buf("dbitmap" + tag, 4 * ((n + 31) // 32), zero=True)
+        else:
+            bitmap = batch["bitmap"]
+        # outlier-scatter || codec decode (reference decompress graph, pipeline.py:490-580)
+        side = self._fork()
+        if sz["k"]:
+            self._call("fzb_outlier_scatter", _p(b["oidx"]), _p(b["oval"]), sz["k"], n, None, da.radius,
+                       _p(out), _p(bitmap), _p(status), ctypes.c_void_p(side.cuda_stream), st=side)
         if da.codec == "huffman":
             nbytes = (sz["size"] + 7) // 8
             hws = self.buf("hdws" + tag, L.fzb_huffman_decode_workspace_bytes(nbytes, nsym))
@@ -402,17 +459,12 @@ class Engine:
             bws = self.buf("dbsws" + tag, L.fzb_bitshuffle_workspace_bytes(n))
             self._call("fzb_bitshuffle_decode", _p(b["bsmap"]), _p(b["bspay"]), sz["size"], n, da.radius, _p(codes),
                        _p(bws), bws.numel(), _p(status), sp, nk=4)
-        n0, n1, n2 = pad3(da.dims)
-        if batch is None:
-            bitmap = self.buf("dbitmap" + tag, 4 * ((n + 31) // 32), zero=True)
-        else:
-            bitmap = batch["bitmap"]
+        self._join(side)
+        if sz["k"]:
+            self._call("fzb_outlier_check", _p(b["oidx"]), sz["k"], n, _p(codes), da.radius, _p(status), sp)
         ebt = self.buf("deb_res" + tag, 8)
         with torch.cuda.stream(self.stream):
             ebt[:8].view(torch.float64).fill_(eb_abs)
-        if sz["k"]:
-            self._call("fzb_outlier_scatter", _p(b["oidx"]), _p(b["oval"]), sz["k"], n, _p(codes), da.radius,
-                       _p(out), _p(bitmap), _p(status), sp)
         if batch is not None:
             return out
         if da.use_anchors:
@@ -453,11 +505,15 @@ class Engine:
             finally:
                 self._capturing = False
                 tr, self.trace = self.trace, traced
-            ent = (g, res, self.launches - l0, tr, self.trace_only)
+            # the graph holds raw pointers into every cached buffer it touched;
+            # buf() may later replace a buffer for a larger shape, so the entry
+            # keeps this capture's tensors alive (the replaced ones stay valid)
+            keep = tuple(self._dev.values())
+            ent = (g, res, self.launches - l0, tr, self.trace_only, keep)
             self._graphs[key] = ent
             if len(self._graphs) > 16:   # a few shapes at a time
                 self._graphs.pop(next(iter(self._graphs)))
-        g, res, nk, tr, _ = ent
+        g, res, nk, tr = ent[:4]
         with torch.cuda.stream(self.stream):
             g.replay()
         self.launches += nk
@@ -560,7 +616,8 @@ class Engine:
 
     # --------------------------------------------------------- decompress
     def decode_codes(self, codec: str, segs: dict, n: int, radius: int, tag: str = "",
-                     codes_out: torch.Tensor | None = None) -> torch.Tensor:
+                     codes_out: torch.Tensor | None = None, zero_status: bool = True,
+                     stage: str | None = None) -> torch.Tensor:
         """Primary-codec decode (pipeline.py:415-430) into device u16 codes.
         Host-side length checks mirror encode.py:299-305 and 359-375.  `tag`
         gives a batch member its own buffers (queued uploads never share a
@@ -568,7 +625,7 @@ class Engine:
 
         L, sp = self.lib, self.sp
         codes = self.buf("dcodes" + tag, 2 * n + 16) if codes_out is None else codes_out
-        status = self.buf("dstatus" + tag, 8, zero=True)
+        status = self.buf("dstatus" + tag, 8, zero=zero_status)
         nsym = 2 * radius
         if codec == "huffman":
             cl = segs["codebook"]
@@ -579,8 +636,8 @@ class Engine:
                 return codes
             if not cl.size or int(cl.max()) == 0:
                 raise E.CorruptStream("empty codebook with nonzero symbol count")
-            lengths = self.upload("dlengths" + tag, cl)
-            s = self.upload("dstream" + tag, stream, pad=16)
+            lengths = self.upload("dlengths" + tag, cl, stage=stage)
+            s = self.upload("dstream" + tag, stream, pad=16, stage=stage)
             hws = self.buf("hdws" + tag, L.fzb_huffman_decode_workspace_bytes(len(stream), nsym))
             self._call("fzb_huffman_decode", _p(s), len(stream), n, _p(lengths), nsym, _p(codes), _p(hws),
                        hws.numel(), _p(status), sp, nk=10)
@@ -598,8 +655,8 @@ class Engine:
                 if len(payload):
                     raise E.BitmapPayloadMismatch("bitmap marks 0 words, payload has more")
                 return codes
-            bm = self.upload("dbsmap" + tag, bitmap, pad=16)
-            pay = self.upload("dbspay" + tag, payload, pad=16)
+            bm = self.upload("dbsmap" + tag, bitmap, pad=16, stage=stage)
+            pay = self.upload("dbspay" + tag, payload, pad=16, stage=stage)
             bws = self.buf("dbsws" + tag, L.fzb_bitshuffle_workspace_bytes(n))
             self._call("fzb_bitshuffle_decode", _p(bm), _p(pay), len(payload) // 4, n, radius, _p(codes), _p(bws),
                        bws.numel(), _p(status), sp, nk=4)
@@ -639,6 +696,92 @@ class Engine:
             self._call("fzb_lorenzo_decode_f32", _p(codes), _p(bitmap), _p(recon), n0, n1, n2, _p(ebt), radius,
                        _p(lzws), lzws.numel(), sp, nk=5)
         return recon
+
+    def decompress_dag(self, codec: str, predictor: str, segs: dict, idx: np.ndarray, vals: np.ndarray,
+                       anchors, dims, eb_abs: float, radius: int, anchor_stride: int = 16,
+                       stage: str | None = None) -> torch.Tensor:
+        """The reference's four-task decompress graph (pipeline.py:490-580) on
+        two streams: [side] outlier H2D + scatter (and the anchor grid H2D)
+        || [main] codec H2D + decode, joined before the sentinel check and
+        the predictor inverse.  Returns the device reconstruction (a cached
+        buffer).  Host-side structural checks happen in decode_codes before
+        anything is enqueued.  `stage`: copy every payload through named
+        pinned staging buffers (graph replays)."""
+        L, sp = self.lib, self.sp
+        dims = tuple(int(d) for d in dims)
+        n = int(np.prod(dims))
+        n0, n1, n2 = pad3(dims)
+        recon = self.buf("drecon", 4 * n)[:4 * n].view(torch.float32)
+        status = self.buf("dstatus", 8, zero=True)
+        bitmap = self.buf("dbitmap", 4 * ((n + 31) // 32), zero=True)
+        k = int(idx.size)
+        side = self._fork()
+        self._mark("decode-outliers", side)
+        if k:
+            di = self.upload("didx", np.ascontiguousarray(idx, np.uint64), st=side, stage=stage)
+            dv = self.upload("dval", np.ascontiguousarray(vals, np.float32), st=side, stage=stage)
+            self._call("fzb_outlier_scatter", _p(di), _p(dv), k, n, None, radius, _p(recon), _p(bitmap), _p(status),
+                       ctypes.c_void_p(side.cuda_stream), st=side)
+        use_anchors = predictor == "interp" and len(anchors)
+        if use_anchors:
+            danch = self.upload("danchors", anchors, st=side, stage=stage)
+        ebt = self.upload("deb", np.array([eb_abs], np.float64), st=side, stage=stage)
+        self._mark("decode-outliers_end", side)
+        self._mark("decode-codes")
+        codes = self.decode_codes(codec, segs, n, radius, zero_status=False, stage=stage)
+        self._mark("decode-codes_end")
+        self._join(side)
+        self._mark("reconstruct")
+        if k:
+            self._call("fzb_outlier_check", _p(di), k, n, _p(codes), radius, _p(status), sp)
+        if use_anchors:
+            w = (ctypes.c_double * 4)(*CUBIC)
+            self._call("fzb_interp_decode_f32", _p(codes), _p(bitmap), _p(danch), _p(recon), n0, n1, n2, _p(ebt),
+                       radius, anchor_stride, w, sp, nk=1 + 3 * int(np.log2(anchor_stride)))
+        else:
+            lzws = self.buf("dlzws", L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
+            self._call("fzb_lorenzo_decode_f32", _p(codes), _p(bitmap), _p(recon), n0, n1, n2, _p(ebt), radius,
+                       _p(lzws), lzws.numel(), sp, nk=5)
+        return recon
+
+    def decompress_dag_graphed(self, codec: str, predictor: str, segs: dict, idx, vals, anchors, dims,
+                               eb_abs: float, radius: int, anchor_stride: int = 16) -> torch.Tensor:
+        """decompress_dag as one CUDA-graph launch: the archive's payloads are
+        copied into this shape's pinned staging buffers on the host, then the
+        captured DAG (H2D nodes from those buffers, both branches, the join)
+        replays.  Captured per payload sizes."""
+        if codec == "huffman":
+            sizes = (len(segs["codebook"]) if hasattr(segs["codebook"], "__len__") else 0, len(segs["stream"]))
+        else:
+            sizes = (len(segs["bitmap"]), len(segs["payload"]))
+        key = ("dh", codec, predictor, tuple(dims), radius, anchor_stride, sizes, int(idx.size), len(anchors))
+        stage = "gs%x:" % (hash(key) & 0xFFFFFFFF)
+        run = lambda: self.decompress_dag(codec, predictor, segs, idx, vals, anchors, dims, eb_abs, radius,
+                                          anchor_stride, stage=stage)
+        if key in self._graphs:   # stage this archive's payloads where the graph's H2D nodes read
+            self._stage_only(codec, segs, idx, vals, anchors, eb_abs, predictor, stage)
+        return self._graphed(key, run)
+
+    def _stage_only(self, codec, segs, idx, vals, anchors, eb_abs, predictor, stage):
+        def put(name, data):
+            if isinstance(data, np.ndarray):
+                raw = np.ascontiguousarray(data).view(np.uint8).reshape(-1)
+            else:
+                raw = np.frombuffer(data, np.uint8) if len(data) else np.zeros(0, np.uint8)
+            if raw.size:
+                self.pinned(stage + name, raw.size).numpy()[:raw.size] = raw
+        if idx.size:
+            put("didx", np.ascontiguousarray(idx, np.uint64))
+            put("dval", np.ascontiguousarray(vals, np.float32))
+        if predictor == "interp" and len(anchors):
+            put("danchors", anchors)
+        put("deb", np.array([eb_abs], np.float64))
+        if codec == "huffman":
+            put("dlengths", segs["codebook"])
+            put("dstream", segs["stream"])
+        else:
+            put("dbsmap", segs["bitmap"])
+            put("dbspay", segs["payload"])
 
     def decode_status(self, tag: str = "") -> int:
         st = self.pinned("dscal", 64)

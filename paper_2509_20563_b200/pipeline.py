@@ -226,10 +226,13 @@ def _to_device(field) -> torch.Tensor:
     return buf[: 4 * field.len].view(torch.float32)
 
 
-def compress_device(x: torch.Tensor, dims, eb: ErrorBoundSpec, pipeline, *, graph: bool = False) -> Archive:
+def compress_device(x: torch.Tensor, dims, eb: ErrorBoundSpec, pipeline, *, graph: bool = False,
+                    timings: dict | None = None) -> Archive:
     """Compress a device-resident f32 tensor (the timed path).  graph=True
     replays the whole device DAG as one captured CUDA graph (graph_engine();
-    `x` is then the graph's static input: keep passing the same tensor)."""
+    `x` is then the graph's static input: keep passing the same tensor).
+    `timings` receives per-stage seconds keyed by stage name, as the
+    reference's compress_with_timing (pipeline.py:345-379)."""
 
     spec = get_pipeline(pipeline)
     _check_stage_params(spec)
@@ -240,22 +243,56 @@ def compress_device(x: torch.Tensor, dims, eb: ErrorBoundSpec, pipeline, *, grap
         log.warning("interpolation needs a 2D or 3D field with every extent >= %d, got dims %s; "
                     "falling back to Lorenzo", cfg.anchor_stride + 1, tuple(dims))
     run = eng.compress_graphed if graph else eng.compress
-    da = run(x, dims, int(eb.mode), float(eb.magnitude), pipeline_id=spec.id, predictor=pred,
-             codec=spec.primary_codec, radius=spec.radius(), anchor_stride=cfg.anchor_stride if cfg else 16)
-    return _archive_of(eng, da, spec, eb, dims)
+    if timings is not None and not graph:
+        eng.marks = {}
+    try:
+        da = run(x, dims, int(eb.mode), float(eb.magnitude), pipeline_id=spec.id, predictor=pred,
+                 codec=spec.primary_codec, radius=spec.radius(), anchor_stride=cfg.anchor_stride if cfg else 16)
+        return _archive_of(eng, da, spec, eb, dims, timings)
+    finally:
+        eng.marks = None
 
 
-def _archive_of(eng, da, spec: PipelineSpec, eb: ErrorBoundSpec, dims) -> Archive:
+def _span(marks: dict, a: str, b: str) -> float:
+    return marks[a].elapsed_time(marks[b]) / 1e3 if a in marks and b in marks else 0.0
+
+
+def _device_error_stage(spec: PipelineSpec, status: int) -> str:
+    """The stage a compress-side device status bit belongs to: a code outside
+    the alphabet is the histogram's CodeOutOfRange (encode.py:79-84) when an
+    analysis stage runs, everything else the primary codec's."""
+    from . import _lib
+    an = spec.stage_of(StageKind.ANALYSIS)
+    if an is not None and status & _lib.ERR_CODE_RANGE:
+        return an.name
+    return spec.stage_of(StageKind.PRIMARY_CODEC).name
+
+
+def _archive_of(eng, da, spec: PipelineSpec, eb: ErrorBoundSpec, dims, timings: dict | None = None) -> Archive:
     """finish() one device result into an Archive (pipeline.py:300-342)."""
     try:
         lo, hi, segs, wire = eng.finish(da)
     except E.FZError as e:
-        raise E.StageError(spec.stage_of(StageKind.PRIMARY_CODEC).name, e) from e
+        st = eng.sizes(da)["status"]
+        raise E.StageError(_device_error_stage(spec, st), e) from e
     if lo == hi:
         return Archive(spec.id, eb.mode, eb.magnitude, lo, hi, tuple(dims), spec.radius(), ())
     ResolvedBound(eb_from_range(eb.mode, eb.magnitude, lo, hi), lo, hi)
+    if timings is not None and eng.marks is not None:
+        m = eng.marks
+        for st in spec.stages:
+            if st.kind == StageKind.PREPROCESS:
+                timings[st.name] = 0.0   # identity (pipeline.py:260-264)
+        timings[spec.stage_of(StageKind.PREDICT).name] = _span(m, "predict", "predict_end")
+        an = spec.stage_of(StageKind.ANALYSIS)
+        if an is not None:
+            timings[an.name] = _span(m, "predict_end", "primary")
+        # primary codec: build + encode, and the D2H that makes its segments host bytes
+        timings[spec.stage_of(StageKind.PRIMARY_CODEC).name] = \
+            _span(m, "primary", "primary_end") + _span(m, "d2h", "d2h_end")
     sc = spec.stage_of(StageKind.SECONDARY_CODEC)
     if sc is not None:
+        t0 = time.perf_counter()
         nprim = 2
         head, prim = segs[:-nprim], segs[-nprim:]
         try:
@@ -265,6 +302,8 @@ def _archive_of(eng, da, spec: PipelineSpec, eb: ErrorBoundSpec, dims) -> Archiv
             raise E.StageError(sc.name, e) from e
         segs = head + prim
         wire = None
+        if timings is not None:
+            timings[sc.name] = time.perf_counter() - t0
     a = Archive(spec.id, eb.mode, eb.magnitude, lo, hi, tuple(dims), spec.radius(), tuple(segs))
     if wire is not None:
         attach_wire(a, wire[0].numpy(), wire[1])
@@ -272,23 +311,26 @@ def _archive_of(eng, da, spec: PipelineSpec, eb: ErrorBoundSpec, dims) -> Archiv
 
 
 def compress_with_timing(field: Field, eb: ErrorBoundSpec, pipeline):
-    t0 = time.perf_counter()
+    """pipeline.py:345-379: the archive plus per-stage seconds keyed by the
+    spec's stage names (CUDA-event spans of each stage's kernels; the
+    primary codec includes the D2H of its segments).  A constant field
+    returns an empty dict, as the reference does."""
+    timings: dict = {}
     x = _to_device(field)
-    t1 = time.perf_counter()
-    a = compress_device(x, field.dims, eb, pipeline)
-    t2 = time.perf_counter()
-    return a, {"h2d": t1 - t0, "device": t2 - t1}
+    a = compress_device(x, field.dims, eb, pipeline, timings=timings)
+    return a, timings
 
 
 def compress(field: Field, eb: ErrorBoundSpec, pipeline) -> Archive:
-    return compress_with_timing(field, eb, pipeline)[0]
+    return compress_device(_to_device(field), field.dims, eb, pipeline)
 
 
 def compress_via_graph(field: Field, eb: ErrorBoundSpec, pipeline, workers: int | None = None) -> Archive:
-    """Graph variant (pipeline.py:650-660): the device DAG runs as one CUDA
-    graph, captured per shape / bound / pipeline on first use and replayed
-    for later fields (the H2D lands in the graph's static input).  Archives
-    are byte-identical to compress(); `workers` has no GPU meaning."""
+    """Graph variant (pipeline.py:650-660): the device DAG (predict ->
+    serialize-outliers || analysis -> primary-encode) runs as one CUDA graph,
+    captured per shape / bound / pipeline on first use and replayed for
+    later fields (the H2D lands in the graph's static input).  Archives are
+    byte-identical to compress(); `workers` has no GPU meaning."""
     eng = graph_engine()
     x = eng.buf("graph_in_%s" % "x".join(map(str, field.dims)), 4 * field.len)[: 4 * field.len].view(torch.float32)
     src = torch.from_numpy(field.data)
@@ -324,44 +366,61 @@ def _outliers(segs: dict, n: int):
     return idx, vals
 
 
-def decompress_device(a: Archive, pipeline=None, out: torch.Tensor | None = None) -> torch.Tensor:
-    """Decompress into a device f32 tensor (the timed path)."""
+def _codec_segments(spec: PipelineSpec, segs: dict, radius: int):
+    """Host-side structural checks of _decode_codes (pipeline.py:415-430)."""
+    codec = spec.primary_codec
+    if codec == "huffman":
+        if SEG_HUFFMAN_CODEBOOK not in segs or SEG_HUFFMAN_BITSTREAM not in segs:
+            raise E.CorruptPayload("Huffman segments missing")
+        from .encode import HuffmanCodebook
+        cb = HuffmanCodebook.from_bytes(segs[SEG_HUFFMAN_CODEBOOK])
+        if cb.code_lengths.size != 2 * radius:
+            raise E.CorruptPayload(f"codebook covers {cb.code_lengths.size} symbols, alphabet is {2 * radius}")
+        if radius > 32768:
+            raise E.RadiusTooLarge(f"radius {radius} exceeds the device path's 16-bit codes")
+        return {"codebook": cb.code_lengths, "stream": segs[SEG_HUFFMAN_BITSTREAM]}
+    if codec == "bitshuffle":
+        if SEG_BITSHUFFLE_BITMAP not in segs or SEG_BITSHUFFLE_PAYLOAD not in segs:
+            raise E.CorruptPayload("bitshuffle segments missing")
+        if radius > 32768:
+            raise E.RadiusTooLarge(f"radius {radius} exceeds 16-bit code width")
+        return {"bitmap": segs[SEG_BITSHUFFLE_BITMAP], "payload": segs[SEG_BITSHUFFLE_PAYLOAD]}
+    raise ValueError(f"unknown primary codec '{codec}'")
 
+
+def _raise_decode_status(status: int):
+    from . import _lib
+    if not status:
+        return
+    try:
+        _lib.raise_codec_status(status)
+    except E.FZError as e:
+        raise E.StageError("decode-codes", e) from e
+    if status & (_lib.ERR_OUTLIER_CODE | _lib.ERR_OUTLIER_ORDER):
+        raise E.MalformedCodes("outlier position without sentinel code")
+    if status & _lib.ERR_HF_SYNC:
+        raise RuntimeError("Huffman decoder did not synchronise (increase iterations)")
+    raise RuntimeError(f"device status {status:#x}")
+
+
+def _decompress_dev(a: Archive, pipeline=None, *, graph: bool = False, timings: dict | None = None):
+    """Shared body of decompress_device / decompress_with_timing /
+    decompress_via_graph: host checks, then the two-stream device DAG.
+    Returns (engine, device recon) or (None, constant value)."""
     spec = get_pipeline(pipeline if pipeline is not None else a.pipeline_id)
-    eng = default_engine()
     n = a.element_count
     if len(a.segments) == 0:
         if a.data_min != a.data_max:
             raise E.CorruptPayload("no segments but the header spans a value range")
-        t = out if out is not None else torch.empty(n, dtype=torch.float32, device=eng.device)
-        t.fill_(a.data_min)
-        return t
+        return None, a.data_min
     bound = a.resolved_bound()
+    t0 = time.perf_counter()
     segs = _unwrap(a)
+    if timings is not None:
+        timings["unwrap"] = time.perf_counter() - t0
     radius = a.radius
-    codec = spec.primary_codec
-    # decode-codes (host-side structural checks first, as encode.py does)
     try:
-        if codec == "huffman":
-            if SEG_HUFFMAN_CODEBOOK not in segs or SEG_HUFFMAN_BITSTREAM not in segs:
-                raise E.CorruptPayload("Huffman segments missing")
-            from .encode import HuffmanCodebook
-            cb = HuffmanCodebook.from_bytes(segs[SEG_HUFFMAN_CODEBOOK])
-            if cb.code_lengths.size != 2 * radius:
-                raise E.CorruptPayload(f"codebook covers {cb.code_lengths.size} symbols, alphabet is {2 * radius}")
-            if radius > 32768:
-                raise E.RadiusTooLarge(f"radius {radius} exceeds the device path's 16-bit codes")
-            codes = eng.decode_codes("huffman", {"codebook": cb.code_lengths, "stream": segs[SEG_HUFFMAN_BITSTREAM]},
-                                     n, radius)
-        elif codec == "bitshuffle":
-            if SEG_BITSHUFFLE_BITMAP not in segs or SEG_BITSHUFFLE_PAYLOAD not in segs:
-                raise E.CorruptPayload("bitshuffle segments missing")
-            if radius > 32768:
-                raise E.RadiusTooLarge(f"radius {radius} exceeds 16-bit code width")
-            codes = eng.decode_codes("bitshuffle", {"bitmap": segs[SEG_BITSHUFFLE_BITMAP],
-                                                    "payload": segs[SEG_BITSHUFFLE_PAYLOAD]}, n, radius)
-        else:
-            raise ValueError(f"unknown primary codec '{codec}'")
+        csegs = _codec_segments(spec, segs, radius)
     except Exception as e:
         raise E.StageError("decode-codes", e) from e
     try:
@@ -380,37 +439,71 @@ def decompress_device(a: Archive, pipeline=None, out: torch.Tensor | None = None
         if len(anchors) != want:
             raise E.StageError("reconstruct", E.AnchorSizeMismatch(
                 f"anchor payload is {len(anchors)} bytes, expected {want}"))
-    recon = eng.reconstruct(pred, codes, idx, vals, anchors, a.dims, bound.eb_abs, radius, stride, out=out)
-    status = eng.decode_status()
-    if status:
-        from . import _lib
+    eng = graph_engine() if graph else default_engine()
+    if timings is not None and not graph:
+        eng.marks = {}
+    try:
+        dag = eng.decompress_dag_graphed if graph else eng.decompress_dag
         try:
-            _lib.raise_codec_status(status)
+            recon = dag(spec.primary_codec, pred, csegs, idx, vals, anchors, a.dims, bound.eb_abs, radius, stride)
         except E.FZError as e:
             raise E.StageError("decode-codes", e) from e
-        if status & (_lib.ERR_OUTLIER_CODE | _lib.ERR_OUTLIER_ORDER):
-            raise E.MalformedCodes("outlier position without sentinel code")
-        if status & _lib.ERR_HF_SYNC:
-            raise RuntimeError("Huffman decoder did not synchronise (increase iterations)")
-    return recon
+        return eng, recon
+    finally:
+        if timings is not None and eng.marks is not None:
+            eng._mark("reconstruct_end")
+            eng.stream.synchronize()
+            m = eng.marks
+            timings["decode-codes"] = _span(m, "decode-codes", "decode-codes_end")
+            timings["decode-outliers"] = _span(m, "decode-outliers", "decode-outliers_end")
+            timings["reconstruct"] = _span(m, "reconstruct", "reconstruct_end")
+        eng.marks = None
+
+
+def decompress_device(a: Archive, pipeline=None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Decompress into a device f32 tensor (the timed path)."""
+    eng, recon = _decompress_dev(a, pipeline)
+    if eng is None:
+        dev = default_engine().device
+        t = out if out is not None else torch.empty(a.element_count, dtype=torch.float32, device=dev)
+        t.fill_(recon)
+        return t
+    _raise_decode_status(eng.decode_status())
+    if out is not None:
+        with torch.cuda.stream(eng.stream):
+            out.copy_(recon)
+        return out
+    with torch.cuda.stream(eng.stream):
+        return recon.clone()
+
+
+def _to_host(a: Archive, eng, recon, t_reconstruct: dict | None = None) -> Field:
+    if eng is None:
+        return Field(a.dims, np.full(a.element_count, recon, np.float32))
+    t0 = time.perf_counter()
+    host = torch.empty(recon.numel(), dtype=torch.float32, pin_memory=True)
+    with torch.cuda.stream(eng.stream):
+        host.copy_(recon, non_blocking=True)
+    eng._sync()
+    if t_reconstruct is not None and "reconstruct" in t_reconstruct:
+        t_reconstruct["reconstruct"] += time.perf_counter() - t0
+    _raise_decode_status(eng.decode_status())
+    # the decoder output is finite by construction; skip Field's O(n) host re-validation
+    return Field.trusted(a.dims, host.numpy())
 
 
 def decompress_with_timing(a: Archive, pipeline=None):
-    t0 = time.perf_counter()
-    eng = default_engine()
-    rec = decompress_device(a, pipeline)
-    t1 = time.perf_counter()
-    host = torch.empty(rec.numel(), dtype=torch.float32, pin_memory=True)
-    with torch.cuda.stream(eng.stream):
-        host.copy_(rec, non_blocking=True)
-    eng._sync()
-    t2 = time.perf_counter()
-    # the decoder output is finite by construction; skip Field's O(n) host re-validation
-    return Field.trusted(a.dims, host.numpy()), {"device": t1 - t0, "d2h": t2 - t1}
+    """pipeline.py:439-466: the field plus seconds for "unwrap",
+    "decode-codes", "decode-outliers" (both branches of the two-stream DAG,
+    which overlap) and "reconstruct" (predictor inverse + D2H)."""
+    timings: dict = {}
+    eng, recon = _decompress_dev(a, pipeline, timings=timings)
+    return _to_host(a, eng, recon, timings), timings
 
 
 def decompress(a: Archive, pipeline=None) -> Field:
-    return decompress_with_timing(a, pipeline)[0]
+    eng, recon = _decompress_dev(a, pipeline)
+    return _to_host(a, eng, recon)
 
 
 # ------------------------------------------------------------------- batches
@@ -472,6 +565,8 @@ def decompress_batch(archives: list, pipeline=None) -> list:
         tag = f"#{f}"
         segs = _unwrap(a)
         try:
+            if radius > 32768:
+                raise E.RadiusTooLarge(f"radius {radius} exceeds the device path's 16-bit codes")
             if codec == "huffman":
                 if SEG_HUFFMAN_CODEBOOK not in segs or SEG_HUFFMAN_BITSTREAM not in segs:
                     raise E.CorruptPayload("Huffman segments missing")
@@ -539,5 +634,11 @@ def worker_count(requested: int | None = None) -> int:
 
 
 def decompress_via_graph(a: Archive, workers: int | None = None) -> Field:
-    """Graph variant (pipeline.py:583-591); bitwise equal to decompress()."""
-    return decompress(a)
+    """Graph variant (pipeline.py:583-591): the four-task decompress graph
+    (parse -> huffman-decode || outlier-scatter -> predict-reconstruct) as a
+    captured two-stream CUDA graph, replayed for later archives of the same
+    shape and payload sizes; bitwise equal to decompress().  As in the
+    reference, it applies to every pipeline here (a bitshuffle decode is the
+    same fork with another codec branch); `workers` has no GPU meaning."""
+    eng, recon = _decompress_dev(a, graph=True)
+    return _to_host(a, eng, recon)
