@@ -64,17 +64,29 @@ def _trig_terms(dims, seed, terms=4, max_cycles=2.0):
 
 
 def smooth_trig_host(dims, seed: int = 0) -> np.ndarray:
+    """fzpipe data._smooth_trig (data.py:85-106) bit for bit: the same per-
+    element operation order, evaluated in slabs of the slowest axis to bound
+    the f64 temporaries (every element's arithmetic is independent)."""
     dims = tuple(int(d) for d in dims)
     coords = [np.arange(d, dtype=np.float64) / d for d in dims]
-    acc = np.zeros(dims, np.float64)
-    for freqs, phase, amp in _trig_terms(dims, seed):
-        arg = np.full(dims, phase)
-        for ax, d in enumerate(dims):
-            shape = [1] * len(dims)
-            shape[ax] = d
-            arg = arg + (2.0 * np.pi * freqs[ax] * coords[ax]).reshape(shape)
-        acc += amp * np.sin(arg)
-    return acc.astype(np.float32).reshape(-1)
+    terms = _trig_terms(dims, seed)
+    out = np.empty(dims, np.float32)
+    per = int(np.prod(dims[1:])) if len(dims) > 1 else 1
+    step = max(1, (1 << 22) // per)
+    for s0 in range(0, dims[0], step):
+        s1 = min(dims[0], s0 + step)
+        shp = (s1 - s0,) + dims[1:]
+        acc = np.zeros(shp, np.float64)
+        for freqs, phase, amp in terms:
+            arg = np.full(shp, phase)
+            for ax, d in enumerate(dims):
+                shape = [1] * len(dims)
+                shape[ax] = shp[ax]
+                c = coords[ax][s0:s1] if ax == 0 else coords[ax]
+                arg = arg + (2.0 * np.pi * freqs[ax] * c).reshape(shape)
+            acc += amp * np.sin(arg)
+        out[s0:s1] = acc.astype(np.float32)
+    return out.reshape(-1)
 
 
 def smooth_trig_device(dims, seed: int = 0, device="cuda") -> torch.Tensor:
@@ -104,8 +116,14 @@ def smooth_trig_device(dims, seed: int = 0, device="cuda") -> torch.Tensor:
 
 
 def particle1d_host(n: int, seed: int = 0, box: float = 1000.0, jitter: float = 0.3) -> np.ndarray:
-    u = splitmix_uniform_host(seed, 0, n)
-    return (box * (np.arange(n, dtype=np.float64) + 0.5 + jitter * (2.0 * u - 1.0)) / n).astype(np.float32)
+    """fzpipe data._particle1d (data.py:137-147) bit for bit, in chunks."""
+    out = np.empty(n, np.float32)
+    step = 1 << 22
+    for s0 in range(0, n, step):
+        s1 = min(n, s0 + step)
+        u = splitmix_uniform_host(seed, s0, s1 - s0)
+        out[s0:s1] = box * (np.arange(s0, s1, dtype=np.float64) + 0.5 + jitter * (2.0 * u - 1.0)) / n
+    return out
 
 
 def particle1d_device(n: int, seed: int = 0, box: float = 1000.0, jitter: float = 0.3, device="cuda"):

@@ -1,0 +1,131 @@
+"""Full-size parity at the BASELINE configs, pinned to the reference itself.
+
+tests/golden/fullsize.json holds SHA-256 hashes of fzpipe's own input field,
+archive and reconstruction bytes for C1-C4 (BASELINE.json configs 0-3),
+made by scripts/make_fullsize_golden.py, which imports fzpipe in the build
+container.  CPU tests: the host generators reproduce fzpipe's inputs and
+the C oracle reproduces fzpipe's archives and reconstructions.  GPU tests:
+the CUDA path (public API, the default launch configuration for each
+shape) produces the same bytes -- including C2 512^3 on the throughput
+wavefront configuration and the C5 batched wavefront (8 x 512^3 in one
+launch) against per-field oracle archives.
+"""
+
+import hashlib
+import json
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+G = json.load(open(os.path.join(GOLDEN, "fullsize.json")))
+_INPUTS = {}
+
+
+def sha(b) -> str:
+    return hashlib.sha256(bytes(b)).hexdigest()
+
+
+def _input(case):
+    if case not in _INPUTS:
+        from paper_2509_20563_b200 import data
+        e = G[case]
+        dims = tuple(e["dims"])
+        x = data.particle1d_host(dims[0], e["seed"]) if e["kind"] == "particle1d" else \
+            data.smooth_trig_host(dims, e["seed"])
+        _INPUTS.clear()   # one full-size field in memory at a time
+        _INPUTS[case] = x
+    return _INPUTS[case]
+
+
+CPU_CASES = [("c1", "default"), ("c1", "speed"), ("c1", "quality"), ("c3", "quality"), ("c4", "default"),
+             ("c2", "speed")]
+
+
+@pytest.mark.parametrize("case,preset", CPU_CASES)
+def test_oracle_matches_fzpipe_at_full_size(oracle, case, preset):
+    e = G[case]
+    x = _input(case)
+    assert sha(x.tobytes()) == e["input_sha256"], "host generator differs from fzpipe.data.generate"
+    blob = oracle.compress(x, tuple(e["dims"]), 1, e["rel_eb"], preset)
+    want = e["archives"][preset]
+    assert len(blob) == want["archive_bytes"]
+    assert sha(blob) == want["archive_sha256"]
+    _, rec = oracle.decompress(blob)
+    assert sha(rec.tobytes()) == want["recon_sha256"]
+
+
+GPU_CASES = [(c, p) for c in ("c1", "c2", "c3", "c4") for p in G[c]["archives"]]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case,preset", GPU_CASES)
+def test_gpu_matches_fzpipe_at_full_size(case, preset):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2509_20563_b200 as fz
+    e = G[case]
+    dims = tuple(e["dims"])
+    x = _input(case)
+    f = fz.Field(dims, x)
+    eb = fz.ErrorBoundSpec(fz.ErrorMode.VALUE_RANGE_RELATIVE, e["rel_eb"])
+    want = e["archives"][preset]
+    a = fz.compress(f, eb, preset)
+    blob = fz.serialize_archive(a)
+    assert len(blob) == want["archive_bytes"]
+    assert sha(blob) == want["archive_sha256"]
+    r = fz.decompress(fz.parse_archive(fz.archive_buffer(a)))
+    assert sha(r.data.tobytes()) == want["recon_sha256"]
+    # the captured-graph variants replay the same kernels
+    g = fz.compress_via_graph(f, eb, preset)
+    assert sha(fz.serialize_archive(g)) == want["archive_sha256"]
+    assert sha(fz.decompress_via_graph(g).data.tobytes()) == want["recon_sha256"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["c1", "c2", "c3", "c4"])
+def test_device_generator_matches_fzpipe_input(case):
+    # bench.py generates its inputs on the device: they must be fzpipe's bytes
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2509_20563_b200 import data
+    e = G[case]
+    dims = tuple(e["dims"])
+    d = data.particle1d_device(dims[0], e["seed"]) if e["kind"] == "particle1d" else \
+        data.smooth_trig_device(dims, e["seed"])
+    h = d.cpu().numpy()
+    if sha(h.tobytes()) != e["input_sha256"]:
+        x = _input(case)
+        bad = int(np.count_nonzero(h.view(np.uint32) != x.view(np.uint32)))
+        pytest.fail(f"device generator differs from fzpipe in {bad} of {x.size} elements")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("preset", ["speed", "default"])
+def test_c5_batched_wavefront_matches_oracle_per_field(oracle, preset):
+    # BASELINE configs[4]: same-shaped 512^3 fields through compress_batch
+    # (one batched Lorenzo launch for all members) -> every archive equals
+    # the oracle's for that field; decompress_batch inverts them bit for bit
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2509_20563_b200 as fz
+    from paper_2509_20563_b200 import data
+    dims, F, rel = (512, 512, 512), 8, 1e-3
+    fields = [fz.Field(dims, data.smooth_trig_device(dims, s).cpu().numpy()) for s in range(F)]
+    eb = fz.ErrorBoundSpec(fz.ErrorMode.VALUE_RANGE_RELATIVE, rel)
+    arcs = fz.compress_batch(fields, eb, preset)
+    with ThreadPoolExecutor(max_workers=min(F, os.cpu_count() or 1)) as ex:   # ctypes releases the GIL
+        want = list(ex.map(lambda f: oracle.compress(f.data, dims, 1, rel, preset), fields))
+    for f, a, w in zip(fields, arcs, want):
+        assert fz.serialize_archive(a) == w
+    recs = fz.decompress_batch(arcs)
+    with ThreadPoolExecutor(max_workers=min(F, os.cpu_count() or 1)) as ex:
+        orec = list(ex.map(lambda w: oracle.decompress(w)[1], want))
+    for r, o in zip(recs, orec):
+        assert r.data.tobytes() == o.tobytes()
