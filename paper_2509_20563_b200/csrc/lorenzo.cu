@@ -33,27 +33,12 @@
 
 namespace {
 
-constexpr bool kUseWave3 = false;  // R=2 rows/thread variant (slower on B200; kept for experiments)
 constexpr int G = 8;        // steps per group (staging / progress granularity)
 constexpr int RING = 32;    // ring slots (steps)
 constexpr int PITCH = 33;   // words per row in f32/u32 rings (conflict-free)
 constexpr int CPITCH = 34;  // u16 per row in the encoder code ring
 constexpr uint32_t MARK = 0xFFFFFFFFu;
 constexpr unsigned FULL = 0xffffffffu;
-
-template <int PI>
-struct Tile {
-    static constexpr int NT = PI * 32;
-    static constexpr int HROWS = 33 + PI + 1;                   // HU (33) + HL (PI+1)
-    static constexpr int HITER = (HROWS * G + NT - 1) / NT;     // halo loads per thread
-    static constexpr int RPE = NT / G;                          // staging rows per iteration
-    static constexpr int MINB = PI >= 8 ? 3 : (PI >= 4 ? 6 : 12);
-};
-
-template <int PI>
-FZB_DEV void tile_sync() {
-    if constexpr (PI == 1) __syncwarp(); else __syncthreads();
-}
 
 FZB_DEV void wait_progress(const uint32_t* p, uint32_t need) {
     if (!p) return;
@@ -65,541 +50,28 @@ FZB_DEV void wait_progress(const uint32_t* p, uint32_t need) {
     }
 }
 
-FZB_DEV void cp_async4(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
-}
 FZB_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 struct Geo {
     int n0, n1, n2, nA, nB;
 };
 
-template <int PI, bool DEC>
-struct Smem {
-    static constexpr int NT = PI * 32;
-    static constexpr size_t in_words = (size_t)NT * PITCH;
-    static constexpr size_t out_bytes = DEC ? (size_t)NT * PITCH * 4 : (size_t)NT * CPITCH * 2;
-    static constexpr size_t rr_words = PI > 1 ? 4 * NT : 0;
-    static constexpr size_t hu_words = 33 * PITCH;
-    static constexpr size_t hl_words = (PI + 1) * PITCH;
-    static constexpr size_t bytes = in_words * 4 + ((out_bytes + 15) / 16) * 16 + (rr_words + hu_words + hl_words) * 4 + 16;
-};
-
-// Wavefront tile kernel, both directions (v2).
-//   ENC: orig -> codes (u16) + outlier bits
-//   DEC: codes + outlier bits + pre-scattered outlier values (in recon) -> recon
-// Thread (a, b) owns row (i0+a, j0+b) and handles k = s - a - b at step s.
-// Prediction keeps the reference's 7-term order; absent neighbours (i, j or
-// k == 0) contribute an exact +0.0, which leaves every partial sum bitwise
-// unchanged (pred is never -0.0 after the leading 0.0 + up), so the sum is
-// branch-free.  Neighbours: up via the shared ring (other warp), left and
-// diagonal via __shfl_up of the previous step's (rec, up) of lane b-1.
-template <int PI, bool DEC>
-__global__ void __launch_bounds__(PI * 32, Tile<PI>::MINB)
-lz_wave_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in,
-               uint16_t* __restrict__ codes_out, uint32_t* __restrict__ bitmap, float* __restrict__ recon,
-               float* __restrict__ faceI, float* __restrict__ faceJ, uint32_t* __restrict__ progress,
-               uint32_t* __restrict__ ticket, const int* __restrict__ order, Geo geo,
-               const double* __restrict__ d_eb, int radius) {
-    using T = Tile<PI>;
-    using SM = Smem<PI, DEC>;
-    constexpr int NT = T::NT;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint32_t* IN = reinterpret_cast<uint32_t*>(smem_raw);
-    unsigned char* OUTB = smem_raw + SM::in_words * 4;
-    float* RR = reinterpret_cast<float*>(OUTB + ((SM::out_bytes + 15) / 16) * 16);
-    float* HU = RR + SM::rr_words;
-    float* HL = HU + SM::hu_words;
-    int* s_tile = reinterpret_cast<int*>(HL + SM::hl_words);
-    uint16_t* CR = reinterpret_cast<uint16_t*>(OUTB);  // ENC
-    float* OR = reinterpret_cast<float*>(OUTB);        // DEC
-
-    const int n0 = geo.n0, n1 = geo.n1, n2 = geo.n2, nB = geo.nB;
-    const int tid = threadIdx.x, a = tid >> 5, b = tid & 31;
-    if (tid == 0) *s_tile = order[atomicAdd(ticket, 1u)];
-    __syncthreads();
-    const int tile = *s_tile;
-    const int A = tile / nB, B = tile % nB;
-    const int i0 = A * PI, j0 = B * 32;
-    const int i = i0 + a, j = j0 + b;
-    const bool row_ok = (i < n0) && (j < n1);
-    const QParams P = make_qparams(*d_eb, radius);
-    const double R_d = (double)radius;
-    const int S = n2 + PI - 1 + 31;
-    const int NGRP = (S + G - 1) / G;
-    const uint32_t* progI = (A > 0) ? progress + (tile - nB) : nullptr;
-    const uint32_t* progJ = (B > 0) ? progress + (tile - 1) : nullptr;
-    const bool writeI = row_ok && (a == PI - 1) && (A < geo.nA - 1);
-    const bool writeJ = row_ok && (b == 31) && (B < nB - 1);
-    const bool has_dep = (A < geo.nA - 1) || (B < nB - 1);
-    const long long plane = (long long)n1 * n2;
-    const long long tile_base = (long long)i0 * plane + (long long)j0 * n2;
-    const long long rowbase = tile_base + (long long)a * plane + (long long)b * n2;
-    float* fI = faceI + ((long long)A * n1 + j) * n2;
-    float* fJ = faceJ + ((long long)B * n0 + i) * n2;
-
-    uint32_t st_in[DEC ? G : 1];
-    float st_val[DEC ? G : 1];
-    float st_h[T::HITER];
-
-    // ---- staging: ring input for steps [gg*G, gg*G+G), 8 lanes per row segment
-    auto load_group = [&](int gg) {
-#pragma unroll
-        for (int e = 0; e < G; e++) {
-            const int row = e * T::RPE + (tid >> 3), off = tid & 7;
-            const int ra = row >> 5, rb = row & 31;
-            const int k = gg * G + off - ra - rb;
-            const bool ok = (i0 + ra < n0) && (j0 + rb < n1) && k >= 0 && k < n2;
-            const long long t = tile_base + (long long)ra * plane + (long long)rb * n2 + k;
-            const int slot = (gg * G + off) & (RING - 1);
-            if constexpr (DEC) {
-                st_in[e] = 0u;
-                st_val[e] = 0.f;
-                if (ok) {
-                    if ((__ldg(bitmap + (t >> 5)) >> (t & 31)) & 1u) {
-                        st_in[e] = MARK;
-                        st_val[e] = recon[t];
-                    } else {
-                        st_in[e] = __ldg(codes_in + t);
-                    }
-                }
-            } else {
-                if (ok) cp_async4(IN + row * PITCH + slot, orig + t);
-            }
-        }
-#pragma unroll
-        for (int e = 0; e < T::HITER; e++) {
-            const int h = e * NT + tid;
-            st_h[e] = 0.f;
-            if (h < 33 * G) {
-                const int jj = h / G - 1, off = h % G;
-                const int k = gg * G + off - jj;
-                const int jg = j0 + jj;
-                if (A > 0 && jg >= 0 && jg < n1 && k >= 0 && k < n2)
-                    st_h[e] = __ldcg(faceI + ((long long)(A - 1) * n1 + jg) * n2 + k);
-            } else if (h < T::HROWS * G) {
-                const int hh = h - 33 * G;
-                const int aa = hh / G - 1, off = hh % G;
-                const int k = gg * G + off - aa;
-                const int ig = i0 + aa;
-                if (B > 0 && ig >= 0 && ig < n0 && k >= 0 && k < n2)
-                    st_h[e] = __ldcg(faceJ + ((long long)(B - 1) * n0 + ig) * n2 + k);
-            }
-        }
-    };
-    auto store_group = [&](int gg) {
-        if constexpr (DEC) {
-#pragma unroll
-            for (int e = 0; e < G; e++) {
-                const int row = e * T::RPE + (tid >> 3), off = tid & 7;
-                const int slot = (gg * G + off) & (RING - 1);
-                IN[row * PITCH + slot] = st_in[e];
-                if (st_in[e] == MARK) OR[row * PITCH + slot] = st_val[e];
-            }
-        } else {
-            cp_async_wait_all();
-        }
-#pragma unroll
-        for (int e = 0; e < T::HITER; e++) {
-            const int h = e * NT + tid;
-            if (h < 33 * G) {
-                HU[(h / G) * PITCH + ((gg * G + h % G) & (RING - 1))] = st_h[e];
-            } else if (h < T::HROWS * G) {
-                const int hh = h - 33 * G;
-                HL[(hh / G) * PITCH + ((gg * G + hh % G) & (RING - 1))] = st_h[e];
-            }
-        }
-    };
-    auto need_for = [&](int gg, int lag) -> uint32_t {
-        const long long v = (long long)(gg + 1) * G + lag;
-        return (uint32_t)(v < S ? v : S);
-    };
-
-    // ---- prologue -----------------------------------------------------------
-    if (tid == 0) {
-        wait_progress(progI, need_for(0, PI));
-        wait_progress(progJ, need_for(0, 32));
-    }
-    __syncthreads();
-    load_group(0);
-    store_group(0);
-    // corner r[i0-1, j0-1, 0] sits at step -1 of halo row jj = -1 (slot 31)
-    if (tid == 0) HU[RING - 1] = (A > 0 && B > 0) ? __ldcg(faceI + ((long long)(A - 1) * n1 + (j0 - 1)) * n2) : 0.f;
-
-    // history of the previous step (exact zeros before k == 0)
-    float recL = 0.f, upLf = 0.f;
-    double selfL = 0.0, upL = 0.0, leftL = 0.0, diagL = 0.0;
-
-    for (int g = 0; g < NGRP; g++) {
-        const bool more = (g + 1) < NGRP;
-        if (tid == 0 && more) {
-            wait_progress(progI, need_for(g + 1, PI));
-            wait_progress(progJ, need_for(g + 1, 32));
-        }
-        __syncthreads();
-        if (more) load_group(g + 1);
-
-#pragma unroll
-        for (int st = 0; st < G; st++) {
-            const int s = g * G + st;
-            const int k = s - a - b;
-            const bool act = row_ok && (unsigned)k < (unsigned)n2;
-            const int slot = s & (RING - 1);
-            float upf;
-            if constexpr (PI > 1) upf = (a > 0) ? RR[(k & 3) * NT + tid - 32] : HU[(b + 1) * PITCH + slot];
-            else upf = HU[(b + 1) * PITCH + slot];
-            float leftf = __shfl_up_sync(FULL, recL, 1);
-            float diagf = __shfl_up_sync(FULL, upLf, 1);
-            if (b == 0) {
-                const int ps = (s - 1) & (RING - 1);
-                leftf = HL[(a + 1) * PITCH + slot];
-                diagf = (a > 0) ? HL[a * PITCH + ps] : HU[ps];
-            }
-            // predict.py:100-114, absent terms == +0.0 (see header comment)
-            const double up = (double)(upf + 0.0f);  // the leading "0.0 + x" (normalises -0)
-            const double left = (double)leftf, diag = (double)diagf;
-            double pred = __dadd_rn(up, left);
-            pred = __dadd_rn(pred, selfL);
-            pred = __dsub_rn(pred, diag);
-            pred = __dsub_rn(pred, upL);
-            pred = __dsub_rn(pred, leftL);
-            pred = __dadd_rn(pred, diagL);
-            float rec;
-            double recd;
-            if constexpr (DEC) {
-                const uint32_t c = IN[tid * PITCH + slot];
-                if (c == MARK) {
-                    rec = OR[tid * PITCH + slot];
-                } else {
-                    rec = dequantize(pred, (int)c, P);
-                    OR[tid * PITCH + slot] = rec;
-                }
-                recd = (double)rec;
-            } else {
-                const float vf = __uint_as_float(IN[tid * PITCH + slot]);
-                const double v = (double)vf;
-                // fast path: q = (v-pred)*inv2eb, s = rint(q); exact fallback near .5 ties
-                const double q = __dmul_rn(__dsub_rn(v, pred), P.inv2eb);
-                const double sd = rint(q);
-                const double fr = fabs(__dsub_rn(q, sd));
-                int code;
-                bool outl;
-                if (!P.use_recip || fr >= 0.4999999990686774) {
-                    code = quantize(v, pred, P, rec, outl);
-                } else {
-                    const float rc = __double2float_rn(__dadd_rn(pred, __dmul_rn(P.two_eb, sd)));
-                    const bool ok = fabs(sd) < R_d && fabs(__dsub_rn((double)rc, v)) <= P.eb;
-                    code = ok ? (int)sd + radius : radius;
-                    rec = ok ? rc : vf;
-                    outl = !ok;
-                }
-                recd = (double)rec;
-                CR[tid * CPITCH + slot] = (uint16_t)code;
-                if (outl && act) {
-                    const long long t = rowbase + k;
-                    atomicOr(bitmap + (t >> 5), 1u << (t & 31));
-                }
-            }
-            if constexpr (PI > 1) RR[(k & 3) * NT + tid] = rec;
-            if (act) {
-                if (writeI) fI[k] = rec;
-                if (writeJ) fJ[k] = rec;
-            }
-            recL = act ? rec : 0.f;
-            upLf = act ? upf : 0.f;
-            selfL = act ? recd : 0.0;
-            upL = act ? up : 0.0;
-            leftL = act ? left : 0.0;
-            diagL = act ? diag : 0.0;
-            tile_sync<PI>();
-        }
-        if (tid == 0 && has_dep) st_release(progress + tile, (uint32_t)min((g + 1) * G, S));
-        // flush group g (complete for every row)
-#pragma unroll
-        for (int e = 0; e < G; e++) {
-            const int row = e * T::RPE + (tid >> 3), off = tid & 7;
-            const int ra = row >> 5, rb = row & 31;
-            const int s = g * G + off;
-            const int k = s - ra - rb;
-            if ((i0 + ra < n0) && (j0 + rb < n1) && k >= 0 && k < n2) {
-                const long long t = tile_base + (long long)ra * plane + (long long)rb * n2 + k;
-                if constexpr (DEC) recon[t] = OR[row * PITCH + (s & (RING - 1))];
-                else codes_out[t] = CR[row * CPITCH + (s & (RING - 1))];
-            }
-        }
-        if (more) store_group(g + 1);
-    }
-}
-
-// ---------------------------------------------------------------- v3 (3D)
-// Same wavefront as above, but each thread owns R rows a = w + W*r (ILP R:
-// R independent dependency chains per step, one barrier per R elements) and
-// all staging offsets are 32-bit relative to the tile origin.  Requires
-// PI * n1 * n2 < 2^31 (checked on the host).
-template <int W, int R, bool DEC>
-struct Smem3 {
-    static constexpr int PI = W * R, NROW = PI * 32;
-    static constexpr size_t in_words = (size_t)NROW * PITCH;
-    static constexpr size_t out_bytes = DEC ? (size_t)NROW * PITCH * 4 : (size_t)NROW * CPITCH * 2;
-    static constexpr size_t rr_words = 4 * NROW;
-    static constexpr size_t hu_words = 33 * PITCH;
-    static constexpr size_t hl_words = (PI + 1) * PITCH;
-    static constexpr size_t bytes = in_words * 4 + ((out_bytes + 15) / 16) * 16 + (rr_words + hu_words + hl_words) * 4 + 16;
-};
-
-template <int W, int R, bool DEC>
-__global__ void __launch_bounds__(W * 32, (W >= 4 ? 4 : 8))
-lz_wave3_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in,
-                uint16_t* __restrict__ codes_out, uint32_t* __restrict__ bitmap, float* __restrict__ recon,
-                float* __restrict__ faceI, float* __restrict__ faceJ, uint32_t* __restrict__ progress,
-                uint32_t* __restrict__ ticket, const int* __restrict__ order, Geo geo,
-                const double* __restrict__ d_eb, int radius) {
-    constexpr int PI = W * R, NT = W * 32, NROW = PI * 32;
-    constexpr int SE = R * G;                      // staging elements per thread per group
-    constexpr int HROWS = 33 + PI + 1;
-    constexpr int HITER = (HROWS * G + NT - 1) / NT;
-    using SM = Smem3<W, R, DEC>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint32_t* IN = reinterpret_cast<uint32_t*>(smem_raw);
-    unsigned char* OUTB = smem_raw + SM::in_words * 4;
-    float* RR = reinterpret_cast<float*>(OUTB + ((SM::out_bytes + 15) / 16) * 16);
-    float* HU = RR + SM::rr_words;
-    float* HL = HU + SM::hu_words;
-    int* s_tile = reinterpret_cast<int*>(HL + SM::hl_words);
-    uint16_t* CR = reinterpret_cast<uint16_t*>(OUTB);
-    float* OR = reinterpret_cast<float*>(OUTB);
-
-    const int n0 = geo.n0, n1 = geo.n1, n2 = geo.n2, nB = geo.nB;
-    const int tid = threadIdx.x, w = tid >> 5, b = tid & 31;
-    if (tid == 0) *s_tile = order[atomicAdd(ticket, 1u)];
-    __syncthreads();
-    const int tile = *s_tile;
-    const int A = tile / nB, B = tile % nB;
-    const int i0 = A * PI, j0 = B * 32;
-    const int j = j0 + b;
-    const QParams P = make_qparams(*d_eb, radius);
-    const double R_d = (double)radius;
-    const int S = n2 + PI - 1 + 31;
-    const int NGRP = (S + G - 1) / G;
-    const uint32_t* progI = (A > 0) ? progress + (tile - nB) : nullptr;
-    const uint32_t* progJ = (B > 0) ? progress + (tile - 1) : nullptr;
-    const int plane = n1 * n2;  // fits: PI * plane < 2^31
-    const long long tile_base = (long long)i0 * plane + (long long)j0 * n2;
-    const float* tin = DEC ? nullptr : orig + tile_base;
-    const uint16_t* tcin = DEC ? codes_in + tile_base : nullptr;
-    float* trec = DEC ? recon + tile_base : nullptr;
-    uint16_t* tcout = DEC ? nullptr : codes_out + tile_base;
-
-    bool row_ok[R], wI[R], wJ[R];
-    int roff[R];
-    float* fI[R];
-    float* fJ[R];
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-        const int a = w + W * r, i = i0 + a;
-        row_ok[r] = (i < n0) && (j < n1);
-        wI[r] = row_ok[r] && (a == PI - 1) && (A < geo.nA - 1);
-        wJ[r] = row_ok[r] && (b == 31) && (B < nB - 1);
-        roff[r] = a * plane + b * n2;
-        fI[r] = faceI + ((long long)A * n1 + j) * n2;
-        fJ[r] = faceJ + ((long long)B * n0 + i) * n2;
-    }
-    const int soff = tid & 7;  // staging: 8 lanes per row segment
-
-    uint32_t st_in[DEC ? SE : 1];
-    float st_val[DEC ? SE : 1];
-    float st_h[HITER];
-
-    auto srow = [&](int e) { return e * (NT / G) + (tid >> 3); };
-    auto load_group = [&](int gg) {
-#pragma unroll
-        for (int e = 0; e < SE; e++) {
-            const int row = srow(e), ra = row >> 5, rb = row & 31;
-            const int k = gg * G + soff - ra - rb;
-            const bool ok = (i0 + ra < n0) && (j0 + rb < n1) && (unsigned)k < (unsigned)n2;
-            const int t = ra * plane + rb * n2 + k;
-            if constexpr (DEC) {
-                st_in[e] = 0u;
-                st_val[e] = 0.f;
-                if (ok) {
-                    const long long gt = tile_base + t;
-                    if ((__ldg(bitmap + (gt >> 5)) >> (gt & 31)) & 1u) {
-                        st_in[e] = MARK;
-                        st_val[e] = trec[t];
-                    } else {
-                        st_in[e] = __ldg(tcin + t);
-                    }
-                }
-            } else {
-                if (ok) cp_async4(IN + row * PITCH + ((gg * G + soff) & (RING - 1)), tin + t);
-            }
-        }
-#pragma unroll
-        for (int e = 0; e < HITER; e++) {
-            const int h = e * NT + tid;
-            st_h[e] = 0.f;
-            if (h < 33 * G) {
-                const int jj = h / G - 1, off = h % G;
-                const int k = gg * G + off - jj;
-                const int jg = j0 + jj;
-                if (A > 0 && jg >= 0 && jg < n1 && k >= 0 && k < n2)
-                    st_h[e] = __ldcg(faceI + ((long long)(A - 1) * n1 + jg) * n2 + k);
-            } else if (h < HROWS * G) {
-                const int hh = h - 33 * G;
-                const int aa = hh / G - 1, off = hh % G;
-                const int k = gg * G + off - aa;
-                const int ig = i0 + aa;
-                if (B > 0 && ig >= 0 && ig < n0 && k >= 0 && k < n2)
-                    st_h[e] = __ldcg(faceJ + ((long long)(B - 1) * n0 + ig) * n2 + k);
-            }
-        }
-    };
-    auto store_group = [&](int gg) {
-        if constexpr (DEC) {
-#pragma unroll
-            for (int e = 0; e < SE; e++) {
-                const int row = srow(e);
-                const int slot = (gg * G + soff) & (RING - 1);
-                IN[row * PITCH + slot] = st_in[e];
-                if (st_in[e] == MARK) OR[row * PITCH + slot] = st_val[e];
-            }
-        } else {
-            cp_async_wait_all();
-        }
-#pragma unroll
-        for (int e = 0; e < HITER; e++) {
-            const int h = e * NT + tid;
-            if (h < 33 * G) {
-                HU[(h / G) * PITCH + ((gg * G + h % G) & (RING - 1))] = st_h[e];
-            } else if (h < HROWS * G) {
-                const int hh = h - 33 * G;
-                HL[(hh / G) * PITCH + ((gg * G + hh % G) & (RING - 1))] = st_h[e];
-            }
-        }
-    };
-    auto need_for = [&](int gg, int lag) -> uint32_t {
-        const long long v = (long long)(gg + 1) * G + lag;
-        return (uint32_t)(v < S ? v : S);
-    };
-
-    if (tid == 0) {
-        wait_progress(progI, need_for(0, PI));
-        wait_progress(progJ, need_for(0, 32));
-    }
-    __syncthreads();
-    load_group(0);
-    store_group(0);
-    if (tid == 0) HU[RING - 1] = (A > 0 && B > 0) ? __ldcg(faceI + ((long long)(A - 1) * n1 + (j0 - 1)) * n2) : 0.f;
-
-    float recL[R], upLf[R];
-    double selfL[R], upL[R], leftL[R], diagL[R];
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-        recL[r] = 0.f; upLf[r] = 0.f;
-        selfL[r] = 0.0; upL[r] = 0.0; leftL[r] = 0.0; diagL[r] = 0.0;
-    }
-
-    for (int g = 0; g < NGRP; g++) {
-        const bool more = (g + 1) < NGRP;
-        if (tid == 0 && more) {
-            wait_progress(progI, need_for(g + 1, PI));
-            wait_progress(progJ, need_for(g + 1, 32));
-        }
-        __syncthreads();
-        if (more) load_group(g + 1);
-
-#pragma unroll 2
-        for (int st = 0; st < G; st++) {
-            const int s = g * G + st;
-            const int slot = s & (RING - 1);
-            const int ps = (s - 1) & (RING - 1);
-#pragma unroll
-            for (int r = 0; r < R; r++) {
-                const int a = w + W * r;
-                const int row = a * 32 + b;
-                const int k = s - a - b;
-                const bool act = row_ok[r] && (unsigned)k < (unsigned)n2;
-                const float upf = (a > 0) ? RR[(k & 3) * NROW + row - 32] : HU[(b + 1) * PITCH + slot];
-                float leftf = __shfl_up_sync(FULL, recL[r], 1);
-                float diagf = __shfl_up_sync(FULL, upLf[r], 1);
-                if (b == 0) {
-                    leftf = HL[(a + 1) * PITCH + slot];
-                    diagf = (a > 0) ? HL[a * PITCH + ps] : HU[ps];
-                }
-                const double up = (double)(upf + 0.0f);
-                const double left = (double)leftf, diag = (double)diagf;
-                double pred = __dadd_rn(up, left);
-                pred = __dadd_rn(pred, selfL[r]);
-                pred = __dsub_rn(pred, diag);
-                pred = __dsub_rn(pred, upL[r]);
-                pred = __dsub_rn(pred, leftL[r]);
-                pred = __dadd_rn(pred, diagL[r]);
-                float rec;
-                double recd;
-                if constexpr (DEC) {
-                    const uint32_t c = IN[row * PITCH + slot];
-                    if (c == MARK) {
-                        rec = OR[row * PITCH + slot];
-                    } else {
-                        rec = dequantize(pred, (int)c, P);
-                        OR[row * PITCH + slot] = rec;
-                    }
-                    recd = (double)rec;
-                } else {
-                    const float vf = __uint_as_float(IN[row * PITCH + slot]);
-                    const double v = (double)vf;
-                    const double q = __dmul_rn(__dsub_rn(v, pred), P.inv2eb);
-                    const double sd = rint(q);
-                    const double fr = fabs(__dsub_rn(q, sd));
-                    int code;
-                    bool outl;
-                    if (!P.use_recip || fr >= 0.4999999990686774) {
-                        code = quantize(v, pred, P, rec, outl);
-                        recd = (double)rec;
-                    } else {
-                        const float rc = __double2float_rn(__dadd_rn(pred, __dmul_rn(P.two_eb, sd)));
-                        const double rcd = (double)rc;
-                        const bool ok = fabs(sd) < R_d && fabs(__dsub_rn(rcd, v)) <= P.eb;
-                        code = ok ? (int)sd + radius : radius;
-                        rec = ok ? rc : vf;
-                        recd = ok ? rcd : v;
-                        outl = !ok;
-                    }
-                    CR[row * CPITCH + slot] = (uint16_t)code;
-                    if (outl && act) {
-                        const long long t = tile_base + roff[r] + k;
-                        atomicOr(bitmap + (t >> 5), 1u << (t & 31));
-                    }
-                }
-                RR[(k & 3) * NROW + row] = rec;
-                recL[r] = rec;
-                upLf[r] = upf;
-                if (act) {
-                    if (wI[r]) fI[r][k] = rec;
-                    if (wJ[r]) fJ[r][k] = rec;
-                    selfL[r] = recd;
-                    upL[r] = up;
-                    leftL[r] = left;
-                    diagL[r] = diag;
-                }
-            }
-            __syncthreads();
-        }
-        if (tid == 0) st_release(progress + tile, (uint32_t)min((g + 1) * G, S));
-#pragma unroll
-        for (int e = 0; e < SE; e++) {
-            const int row = srow(e), ra = row >> 5, rb = row & 31;
-            const int s = g * G + soff;
-            const int k = s - ra - rb;
-            if ((i0 + ra < n0) && (j0 + rb < n1) && (unsigned)k < (unsigned)n2) {
-                const int t = ra * plane + rb * n2 + k;
-                if constexpr (DEC) trec[t] = OR[row * PITCH + (s & (RING - 1))];
-                else tcout[t] = CR[row * CPITCH + (s & (RING - 1))];
-            }
-        }
-        if (more) store_group(g + 1);
-    }
+// Workspace header: the first WS_HDR bytes of every Lorenzo workspace, shared
+// by all paths that run on it (an Engine reuses one workspace across shapes,
+// dimensionalities and directions).
+//   word 0     v7 launch epoch = the LL tag of the faces; only ever incremented
+//   word 1     v7 tile ticket
+//   words 2-3  u64 signature of the v7 face layout the workspace holds (0 = none)
+//   word 4     v7: this launch must clear the faces (layout changed)
+//   word 32    v4 tile ticket (v4 progress counters start at WS_HDR)
+// v7 faces are only trusted under the layout that wrote them: every other
+// path lays its data out from WS_HDR on and resets the signature, and a v7
+// launch whose layout differs from the signature zeroes its faces first, so
+// a stale word (another shape's faces, tile order, event counts, summaries)
+// can never carry the current epoch.
+constexpr size_t WS_HDR = 256;
+void invalidate_faces(void* ws, cudaStream_t st) {
+    cudaMemsetAsync(static_cast<unsigned char*>(ws) + 8, 0, 8, st);
 }
 
 // ---------------------------------------------------------------- v4
@@ -1470,59 +942,6 @@ struct WaveWS {
 };
 
 template <int PI, bool DEC>
-int launch_wave(const float* orig, const uint16_t* codes_in, uint16_t* codes_out, uint32_t* bitmap, float* recon,
-                int n0, int n1, int n2, const double* d_eb, int radius, void* ws, size_t ws_bytes, cudaStream_t st) {
-    Geo g;
-    g.n0 = n0; g.n1 = n1; g.n2 = n2;
-    g.nA = (n0 + PI - 1) / PI;
-    g.nB = (n1 + 31) / 32;
-    WaveWS<PI> L(n0, n1, n2);
-    if (ws_bytes < L.total) return FZB_E_WORKSPACE;
-    unsigned char* w = static_cast<unsigned char*>(ws);
-    uint32_t* ticket = reinterpret_cast<uint32_t*>(w);
-    uint32_t* progress = reinterpret_cast<uint32_t*>(w + L.off_prog);
-    int* order = reinterpret_cast<int*>(w + L.off_order);
-    int* counts = reinterpret_cast<int*>(w + L.off_counts);
-    float* faceI = reinterpret_cast<float*>(w + L.off_fI);
-    float* faceJ = reinterpret_cast<float*>(w + L.off_fI + (L.fI * 4 + 255) / 256 * 256);
-    cudaMemsetAsync(w, 0, L.off_order, st);  // ticket + progress
-    tile_order_kernel<<<1, 1024, 0, st>>>(g.nA, g.nB, 2 * G + PI, 2 * G + 32, counts, order);
-    const size_t smem = Smem<PI, DEC>::bytes;
-    auto kfn = lz_wave_kernel<PI, DEC>;
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kfn<<<(unsigned)L.ntile, PI * 32, smem, st>>>(orig, codes_in, codes_out, bitmap, recon, faceI, faceJ, progress,
-                                                 ticket, order, g, d_eb, radius);
-    return fzb_check_launch();
-}
-
-template <int W, int R, bool DEC>
-int launch_wave3(const float* orig, const uint16_t* codes_in, uint16_t* codes_out, uint32_t* bitmap, float* recon,
-                 int n0, int n1, int n2, const double* d_eb, int radius, void* ws, size_t ws_bytes, cudaStream_t st) {
-    constexpr int PI = W * R;
-    Geo g;
-    g.n0 = n0; g.n1 = n1; g.n2 = n2;
-    g.nA = (n0 + PI - 1) / PI;
-    g.nB = (n1 + 31) / 32;
-    WaveWS<PI> L(n0, n1, n2);
-    if (ws_bytes < L.total) return FZB_E_WORKSPACE;
-    unsigned char* w = static_cast<unsigned char*>(ws);
-    uint32_t* ticket = reinterpret_cast<uint32_t*>(w);
-    uint32_t* progress = reinterpret_cast<uint32_t*>(w + L.off_prog);
-    int* order = reinterpret_cast<int*>(w + L.off_order);
-    int* counts = reinterpret_cast<int*>(w + L.off_counts);
-    float* faceI = reinterpret_cast<float*>(w + L.off_fI);
-    float* faceJ = reinterpret_cast<float*>(w + L.off_fI + (L.fI * 4 + 255) / 256 * 256);
-    cudaMemsetAsync(w, 0, L.off_order, st);
-    tile_order_kernel<<<1, 1024, 0, st>>>(g.nA, g.nB, 2 * G + PI, 2 * G + 32, counts, order);
-    const size_t smem = Smem3<W, R, DEC>::bytes;
-    auto kfn = lz_wave3_kernel<W, R, DEC>;
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kfn<<<(unsigned)L.ntile, W * 32, smem, st>>>(orig, codes_in, codes_out, bitmap, recon, faceI, faceJ, progress,
-                                                ticket, order, g, d_eb, radius);
-    return fzb_check_launch();
-}
-
-template <int PI, bool DEC>
 int launch_wave4(const float* orig, const uint16_t* codes_in, uint16_t* codes_out, uint32_t* bitmap, float* recon,
                  int n0, int n1, int n2, const double* d_eb, int radius, void* ws, size_t ws_bytes, cudaStream_t st) {
     Geo g;
@@ -1532,13 +951,13 @@ int launch_wave4(const float* orig, const uint16_t* codes_in, uint16_t* codes_ou
     WaveWS<PI> L(n0, n1, n2);
     if (ws_bytes < L.total) return FZB_E_WORKSPACE;
     unsigned char* w = static_cast<unsigned char*>(ws);
-    uint32_t* ticket = reinterpret_cast<uint32_t*>(w);
+    uint32_t* ticket = reinterpret_cast<uint32_t*>(w + 128);
     uint32_t* progress = reinterpret_cast<uint32_t*>(w + L.off_prog);
     int* order = reinterpret_cast<int*>(w + L.off_order);
     int* counts = reinterpret_cast<int*>(w + L.off_counts);
     float* faceI = reinterpret_cast<float*>(w + L.off_fI);
     float* faceJ = reinterpret_cast<float*>(w + L.off_fI + (L.fI * 4 + 255) / 256 * 256);
-    cudaMemsetAsync(w, 0, L.off_order, st);
+    cudaMemsetAsync(w + 8, 0, L.off_order - 8, st);   // signature, ticket, progress (keeps the v7 epoch)
     tile_order_kernel<<<1, 1024, 0, st>>>(g.nA, g.nB, 2 * G + PI, 2 * G + 32, counts, order);
     const size_t smem = Smem4<PI, DEC>::bytes;
     auto kfn = lz_wave4_kernel<PI, DEC>;
@@ -1663,8 +1082,8 @@ FZB_API size_t fzb_lorenzo_workspace_bytes(uint32_t n0, uint32_t n1, uint32_t n2
     const long long n = (long long)n0 * n1 * n2;
     if (n0 == 1 && n1 == 1) {
         const long long nblk = (n + BS1 - 1) / BS1, nsb = (nblk + 31) / 32, nch = (n + EVC - 1) / EVC;
-        const size_t enc = (size_t)(nblk + nsb) * 8 + 1024;
-        const size_t dec = 1024 + (size_t)nch * 4 + (size_t)nch * 8 + fzscan::ws_bytes(nch) + 256 + (size_t)n * 8;
+        const size_t enc = WS_HDR + (size_t)(nblk + nsb) * 8 + 1024;
+        const size_t dec = WS_HDR + 1024 + (size_t)nch * 4 + (size_t)nch * 8 + fzscan::ws_bytes(nch) + 256 + (size_t)n * 8;
         return enc > dec ? enc : dec;
     }
     size_t w4;
@@ -1691,8 +1110,9 @@ FZB_API int fzb_lorenzo_encode_f32(const float* d_in, uint32_t n0, uint32_t n1, 
     if (n == 0) return 0;
     if (n0 == 1 && n1 == 1) {
         const long long nblk = (n + BS1 - 1) / BS1, nsb = (nblk + 31) / 32;
-        if (ws_bytes < (size_t)(nblk + nsb) * 8) return FZB_E_WORKSPACE;
-        float* bmin = static_cast<float*>(d_ws);
+        if (ws_bytes < WS_HDR + (size_t)(nblk + nsb) * 8) return FZB_E_WORKSPACE;
+        invalidate_faces(d_ws, st);
+        float* bmin = reinterpret_cast<float*>(static_cast<unsigned char*>(d_ws) + WS_HDR);
         float* bmax = bmin + nblk;
         float* smin = bmax + nblk;
         float* smax = smin + nsb;
@@ -1708,8 +1128,6 @@ FZB_API int fzb_lorenzo_encode_f32(const float* d_in, uint32_t n0, uint32_t n1, 
     }
     if (!use_v4(n2))
         return launch_v7<false>(d_in, nullptr, d_codes, d_bitmap, nullptr, n0, n1, n2, d_eb, (int)radius, d_ws, ws_bytes, st);
-    if (kUseWave3 && n0 >= 8 && 8ll * n1 * n2 < (1ll << 31))
-        return launch_wave3<4, 2, false>(d_in, nullptr, d_codes, d_bitmap, nullptr, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
     switch (pick_pi(n0)) {
         case 8: return launch_wave4<8, false>(d_in, nullptr, d_codes, d_bitmap, nullptr, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
         case 4: return launch_wave4<4, false>(d_in, nullptr, d_codes, d_bitmap, nullptr, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
@@ -1732,7 +1150,8 @@ FZB_API int fzb_lorenzo_decode_f32(const uint16_t* d_codes, const uint32_t* d_bi
     if (n0 == 1 && n1 == 1) {
         const long long nch = (n + EVC - 1) / EVC;
         if (ws_bytes < fzb_lorenzo_workspace_bytes(1, 1, (uint32_t)n)) return FZB_E_WORKSPACE;
-        unsigned char* w = static_cast<unsigned char*>(d_ws);
+        invalidate_faces(d_ws, st);
+        unsigned char* w = static_cast<unsigned char*>(d_ws) + WS_HDR;
         auto al = [](size_t x) { return (x + 255) / 256 * 256; };
         unsigned long long* nev = reinterpret_cast<unsigned long long*>(w);
         uint32_t* counts = reinterpret_cast<uint32_t*>(w + 256);
@@ -1749,8 +1168,6 @@ FZB_API int fzb_lorenzo_decode_f32(const uint16_t* d_codes, const uint32_t* d_bi
     }
     if (!use_v4(n2))
         return launch_v7<true>(nullptr, d_codes, nullptr, const_cast<uint32_t*>(d_bitmap), d_recon, n0, n1, n2, d_eb, (int)radius, d_ws, ws_bytes, st);
-    if (kUseWave3 && n0 >= 8 && 8ll * n1 * n2 < (1ll << 31))
-        return launch_wave3<4, 2, true>(nullptr, d_codes, nullptr, const_cast<uint32_t*>(d_bitmap), d_recon, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
     switch (pick_pi(n0)) {
         case 8: return launch_wave4<8, true>(nullptr, d_codes, nullptr, const_cast<uint32_t*>(d_bitmap), d_recon, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);
         case 4: return launch_wave4<4, true>(nullptr, d_codes, nullptr, const_cast<uint32_t*>(d_bitmap), d_recon, n0, n1, n2, d_eb, radius, d_ws, ws_bytes, st);

@@ -629,9 +629,25 @@ lz7_kernel(const float* __restrict__ orig, const uint16_t* __restrict__ codes_in
 #endif
 }
 
-__global__ void lz7_prep_kernel(uint32_t* hdr) {
+// Header words: see WS_HDR in lorenzo.cu.
+__global__ void lz7_prep_kernel(uint32_t* hdr, unsigned long long sig) {
     hdr[0] += 1u;   // launch epoch: face tags of earlier launches never match
     hdr[1] = 0u;    // ticket
+    unsigned long long* cur = reinterpret_cast<unsigned long long*>(hdr + 2);
+    hdr[4] = (*cur != sig) ? 1u : 0u;
+    *cur = sig;
+}
+// Zero the faces when the layout changed (then every tag is 0 < epoch).
+__global__ void lz7_clear_kernel(const uint32_t* __restrict__ hdr, uint4* __restrict__ p, size_t n16) {
+    if (!hdr[4]) return;
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < n16; q += (size_t)gridDim.x * blockDim.x)
+        p[q] = make_uint4(0, 0, 0, 0);
+}
+inline unsigned long long layout_sig(int pi, int n0, int n1, int n2, int nf) {
+    unsigned long long h = 1469598103934665603ull;
+    const long long v[5] = {pi, n0, n1, n2, nf};
+    for (int q = 0; q < 5; q++) h = (h ^ (unsigned long long)v[q]) * 1099511628211ull;
+    return h | 1ull;
 }
 
 template <int PI>
@@ -674,7 +690,8 @@ int launch7(const float* orig, const uint16_t* codes_in, uint16_t* codes_out, ui
     int* counts = reinterpret_cast<int*>(w + L.off_counts);
     uint64_t* faceI = reinterpret_cast<uint64_t*>(w + L.off_fI);
     uint64_t* faceJ = reinterpret_cast<uint64_t*>(w + L.off_fJ);
-    lz7_prep_kernel<<<1, 1, 0, st>>>(hdr);
+    lz7_prep_kernel<<<1, 1, 0, st>>>(hdr, layout_sig(PI, n0, n1, n2, nf));
+    lz7_clear_kernel<<<kNumSMs * 4, 256, 0, st>>>(hdr, reinterpret_cast<uint4*>(faceI), (L.total - L.off_fI) / 16);
     tile_order_kernel<<<1, 1024, 0, st>>>(g.nA, g.nB, PI + 8, 32 + 8, counts, order, nf);
     const size_t smem = Smem7<W, R, DEC>::bytes;
     auto kfn = lz7_kernel<W, R, DEC>;
