@@ -63,6 +63,7 @@ struct Geo {
 //   word 1     v7 tile ticket
 //   words 2-3  u64 signature of the v7 face layout the workspace holds (0 = none)
 //   word 4     v7: this launch must clear the faces (layout changed)
+//   words 6-7  1D walker: the walking CTA's current block, read by its prefetch CTA
 //   word 32    v4 tile ticket (v4 progress counters start at WS_HDR)
 // v7 faces are only trusted under the layout that wrote them: every other
 // path lays its data out from WS_HDR on and resets the signature, and a v7
@@ -425,37 +426,6 @@ constexpr int BS1 = 1024;        // elements per summary block
 constexpr int BS2 = 32 * BS1;    // elements per superblock
 static_assert(BS1 == 1 << 10 && BS2 == 1 << 15, "the walker indexes blocks with shifts (t >= 0)");
 
-__global__ void lz1d_summary_kernel(const float* __restrict__ x, long long n, uint16_t* __restrict__ codes,
-                                    int radius, float* __restrict__ bmin, float* __restrict__ bmax,
-                                    long long nblk) {
-    const int lane = threadIdx.x & 31;
-    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-    for (long long blk = warp; blk < nblk; blk += nw) {
-        const long long base = blk * BS1;
-        float lo = INFINITY, hi = -INFINITY;
-#pragma unroll 8
-        for (int e = 0; e < BS1 / 32; e++) {
-            const long long t = base + e * 32 + lane;
-            if (t < n) {
-                const float v = __ldg(x + t);
-                lo = fminf(lo, v);
-                hi = fmaxf(hi, v);
-                codes[t] = (uint16_t)radius;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-        }
-        if (lane == 0) {
-            bmin[blk] = lo;
-            bmax[blk] = hi;
-        }
-    }
-}
-
 __global__ void lz1d_super_kernel(const float* __restrict__ bmin, const float* __restrict__ bmax, long long nblk,
                                   float* __restrict__ smin, float* __restrict__ smax, long long nsb) {
     const int lane = threadIdx.x & 31;
@@ -471,27 +441,6 @@ __global__ void lz1d_super_kernel(const float* __restrict__ bmin, const float* _
         }
         if (lane == 0) { smin[sb] = lo; smax[sb] = hi; }
     }
-}
-
-// First index in [a, a + 1024) whose value lies outside [zlo, zhi] (values
-// v[e] = x[a + 32e + lane]; indices >= b count as inside), or -1.  Per-lane
-// bitmasks and one warp min instead of 32 ballot/branch rounds.
-FZB_DEV long long first_outside(const float (&v)[32], long long a, long long b, float zlo, float zhi) {
-    const int lane = threadIdx.x & 31;
-    uint32_t m = 0;
-    const int len = (int)(b - a);   // <= 1024: 32-bit offsets
-#pragma unroll
-    for (int e = 0; e < 32; e++) m |= (uint32_t)((e * 32 + lane < len) & !(v[e] >= zlo && v[e] <= zhi)) << e;
-    const uint32_t mine = m ? (uint32_t)((__ffs(m) - 1) * 32 + lane) : 0xFFFFFFFFu;
-    const uint32_t best = __reduce_min_sync(0xffffffffu, mine);
-    return best == 0xFFFFFFFFu ? -1 : a + (long long)best;
-}
-
-__global__ void lz1d_touch_kernel(const float* __restrict__ p, long long m) {
-    float acc = 0.f;
-    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (long long)gridDim.x * blockDim.x)
-        acc += __ldcg(p + q);
-    if (acc == 12345.f) asm volatile("" ::"f"(acc));   // keep the loads
 }
 
 // quantize(v, pred) == (radius, not outlier), with the chain cut short: a
@@ -552,27 +501,6 @@ FZB_DEV void zbounds(long long k0, long long cu, long long cl, double pred, cons
     }
 }
 
-FZB_DEV uint32_t zupper(long long k0, long long c, double pred, const QParams& P) {
-    const int lane = threadIdx.x & 31;
-    long long w = max(c - 16, k0);
-    for (;;) {
-        const unsigned m = __ballot_sync(0xffffffffu, zkey(w + lane, pred, P));
-        if (m == 0xffffffffu) { w += 32; continue; }
-        if (m == 0) { w = max(w - 32, k0); continue; }
-        return (uint32_t)(w + __ffs(~m) - 2);  // trues occupy the low lanes
-    }
-}
-FZB_DEV uint32_t zlower(long long k0, long long c, double pred, const QParams& P) {
-    const int lane = threadIdx.x & 31;
-    long long e = min(c + 15, k0);
-    for (;;) {
-        const unsigned m = __ballot_sync(0xffffffffu, zkey(e - 31 + lane, pred, P));
-        if (m == 0xffffffffu) { e -= 32; continue; }
-        if (m == 0) { e = min(e + 32, k0); continue; }
-        return (uint32_t)(e - 31 + __ffs(m) - 1);  // trues occupy the high lanes
-    }
-}
-
 // Superblock summaries live in shared memory (when they fit), and the
 // element loads of the current block are issued before the zero-interval
 // search so their latency overlaps it.
@@ -581,179 +509,436 @@ constexpr long long WALK_SMEM_SB = 24576;
 __device__ long long g_walk_stamp[8];
 #endif   // superblocks cached in smem (196 KB)
 
-__global__ void __launch_bounds__(32) lz1d_walk_kernel(const float* __restrict__ x, long long n,
-                                                        uint16_t* __restrict__ codes, uint32_t* __restrict__ bitmap,
-                                                        const float* __restrict__ bmin, const float* __restrict__ bmax,
-                                                        long long nblk, const float* __restrict__ smin_g,
-                                                        const float* __restrict__ smax_g, long long nsb,
-                                                        const double* __restrict__ d_eb, int radius) {
+constexpr int WIN1 = 4;                // window = 4 x 32 block summaries past the event's block
+constexpr long long PF_AHEAD = 4096;   // blocks (16 MB) the prefetch CTA keeps ahead of the walker
+
+FZB_DEV void walk_load_window(const float* __restrict__ bmin, const float* __restrict__ bmax, long long nblk,
+                              long long b, float (&lo)[WIN1], float (&hi)[WIN1]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < WIN1; j++) {
+        const long long bb = b + 1 + 32 * j + lane;
+        lo[j] = bb < nblk ? __ldcg(bmin + bb) : INFINITY;
+        hi[j] = bb < nblk ? __ldcg(bmax + bb) : -INFINITY;
+    }
+}
+
+// First block >= b0 whose [min, max] leaves [zlo, zhi], or -1 (none).
+FZB_DEV long long walk_far(long long b0, long long nblk, const float* __restrict__ bmin, const float* __restrict__ bmax,
+                           const float* smin, const float* smax, long long nsb, float zlo, float zhi) {
+    const int lane = threadIdx.x & 31;
+    long long b = b0;
+    while (b < nblk) {
+        long long sb = b >> 5;
+        const long long bb = sb * 32 + lane;
+        const bool fail = bb >= b && bb < nblk && !(__ldcg(bmin + bb) >= zlo && __ldcg(bmax + bb) <= zhi);
+        const unsigned fm = __ballot_sync(0xffffffffu, fail);
+        if (fm) return sb * 32 + (__ffs(fm) - 1);
+        // whole superblocks, 32 at a time
+        for (;;) {
+            const long long sq = sb + 1 + lane;
+            const bool stop = sq < nsb && !(smin[sq] >= zlo && smax[sq] <= zhi);
+            const unsigned sm = __ballot_sync(0xffffffffu, stop);
+            if (sm) { b = (sb + __ffs(sm)) * 32; break; }
+            sb += 32;
+            if (sb + 1 >= nsb) return -1;
+        }
+    }
+    return -1;
+}
+
+FZB_DEV void prefetch_line(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+FZB_DEV void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// ---- 1D walker v3: group summaries + the exit block in shared memory -------
+// Per event the chain is: quantize -> exact zero interval -> one ballot over
+// the rest of the event's 32-element group (a register per lane) -> one
+// ballot over the block's group summaries (a register per lane) -> one
+// ballot over the window of block summaries (registers) -> ONE memory round
+// trip for the exit block: its 32 group summaries (one word per lane) and its
+// 1024 elements (cp.async into shared memory) arrive together; a ballot
+// picks the group, one shared-memory load per lane and a ballot the element.
+constexpr long long PF_CHUNK = 16;     // blocks per prefetch chunk (64 KB of x)
+
+__global__ void lz1d_summary2_kernel(const float* __restrict__ x, long long n, uint16_t* __restrict__ codes,
+                                     int radius, float* __restrict__ bmin, float* __restrict__ bmax,
+                                     float* __restrict__ gmin, float* __restrict__ gmax, long long nblk) {
+    // one warp per 1K block; lane l owns group l = elements [32 l, 32 l + 32)
+    const int lane = threadIdx.x & 31;
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    const uint32_t rr = (uint32_t)radius | ((uint32_t)radius << 16);
+    for (long long blk = warp; blk < nblk; blk += nw) {
+        const long long g0 = blk * BS1 + 32 * lane;
+        float lo = INFINITY, hi = -INFINITY;
+        if (g0 + 32 <= n && !((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(codes)) & 15)) {
+            const float4* p = reinterpret_cast<const float4*>(x + g0);
+            float4 q[8];
+#pragma unroll
+            for (int e = 0; e < 8; e++) q[e] = __ldcs(p + e);
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                lo = fminf(lo, fminf(fminf(q[e].x, q[e].y), fminf(q[e].z, q[e].w)));
+                hi = fmaxf(hi, fmaxf(fmaxf(q[e].x, q[e].y), fmaxf(q[e].z, q[e].w)));
+            }
+            uint4* c = reinterpret_cast<uint4*>(codes + g0);   // codes are 64-byte aligned per group
+#pragma unroll
+            for (int e = 0; e < 4; e++) c[e] = make_uint4(rr, rr, rr, rr);
+        } else {
+            for (int e = 0; e < 32; e++) {
+                const long long t = g0 + e;
+                if (t < n) {
+                    const float v = x[t];
+                    lo = fminf(lo, v);
+                    hi = fmaxf(hi, v);
+                    codes[t] = (uint16_t)radius;
+                }
+            }
+        }
+        gmin[blk * 32 + lane] = lo;
+        gmax[blk * 32 + lane] = hi;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane == 0) {
+            bmin[blk] = lo;
+            bmax[blk] = hi;
+        }
+    }
+}
+
+FZB_DEV void cp_async16(void* smem, const void* gmem, int nbytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+                 "l"(gmem), "r"(nbytes)
+                 : "memory");
+}
+
+// The walker's quantizer: the lz7 step's exact shortcut (reciprocal multiply,
+// rint via the 1.5*2^52 magic constant, which also yields the integer code);
+// within 1e-9 of a .5 tie, or without a usable reciprocal, the IEEE-division
+// quantizer decides (same argument as v6::lz7_kernel / common.cuh).
+FZB_DEV int quantize_walk(double v, double pred, const QParams& P, float& rec, bool& outl) {
+    const double q = __dmul_rn(__dsub_rn(v, pred), P.inv2eb);
+    const double tq = __dadd_rn(q, 6755399441055744.0);
+    const double sd = __dsub_rn(tq, 6755399441055744.0);   // rint(q); |q| >= 2^51 -> outlier anyway
+    const double fr = fabs(__dsub_rn(q, sd));
+    if (!P.use_recip || fr >= 0.4999999990686774) return quantize(v, pred, P, rec, outl);
+    const float rc = __double2float_rn(__dadd_rn(pred, __dmul_rn(P.two_eb, sd)));
+    const bool ok = (fabs(sd) < (double)P.radius) & (fabs(__dsub_rn((double)rc, v)) <= P.eb);
+    outl = !ok;
+    rec = ok ? rc : __double2float_rn(v);
+    return ok ? (int)(uint32_t)__double_as_longlong(tq) + P.radius : P.radius;
+}
+
+// Exact zero-code interval [zlo, zhi] of the state whose prediction is pred
+// (never -0.0).  One round: lanes 0-15 test the 16 keys around RN32(pred+eb),
+// lanes 16-31 the 16 around RN32(pred-eb), with zero_code's arithmetic and
+// the state's own RN32(pred) hoisted; the rare near-tie lanes re-divide (one
+// warp-uniform branch).  When a transition falls outside its window
+// (tiny / huge bounds), the sliding search (zbounds) takes over.
+FZB_DEV void zinterval(double pred, const QParams& P, float& zlo, float& zhi) {
+    const int lane = threadIdx.x & 31, q = lane & 15;
+    const float rp = __double2float_rn(pred);
+    const double rcd = (double)__double2float_rn(__dadd_rn(pred, __dmul_rn(P.two_eb, 0.0)));
+    const long long k0 = fkey(rp);
+    const long long cu = fkey(__double2float_rn(__dadd_rn(pred, P.eb)));
+    const long long cl = fkey(__double2float_rn(__dsub_rn(pred, P.eb)));
+    const long long wu = max(cu - 8, k0), el = min(cl + 7, k0);
+    const long long key = lane < 16 ? wu + q : el - 15 + q;
+    const bool valid = key >= 0 && key <= 0xFFFFFFFFll;
+    const float f = valid ? kfloat((uint32_t)key) : 0.f;
+    const double v = (double)f;
+    const double d = __dsub_rn(v, pred);
+    double aq = fabs(__dmul_rn(d, P.inv2eb));
+    const bool near = valid && (!P.use_recip || fabs(__dsub_rn(aq, 0.5)) <= __dmul_rn(aq, 1.7763568394002505e-15) + 1e-300);
+    if (__any_sync(0xffffffffu, near)) {   // rare: exact division for the lanes near a .5 tie
+        if (near) aq = fabs(__ddiv_rn(d, P.two_eb));
+    }
+    const bool z = valid && isfinite(f) && aq < 0.5 && fabs(__dsub_rn(rcd, v)) <= P.eb && P.radius > 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, z);
+    const unsigned mu = bal & 0xFFFFu, ml = bal >> 16;
+    if (mu != 0xFFFFu && mu != 0 && ml != 0xFFFFu && ml != 0) {
+        zhi = kfloat((uint32_t)(wu + __ffs(~mu) - 2));      // trues occupy the low lanes
+        zlo = kfloat((uint32_t)(el - 15 + __ffs(ml) - 1));  // trues occupy the high lanes
+        return;
+    }
+    uint32_t khi = 0, klo = 0;
+    zbounds(k0, cu, cl, pred, P, khi, klo);
+    zlo = kfloat(klo);
+    zhi = kfloat(khi);
+}
+
+// An INNER zero-code interval: [ilo, ihi] with |v - pred| <= eb - m/2 for
+// every f32 v in it, m = eb 2^-20 + (|pred| + eb) 2^-44, which dominates the
+// rounding of the few f64 ops below.  Such a v has |q| < 0.5 - 2^-22 (no tie
+// re-division) and |RN32(pred) - v| <= eb, i.e. a zero code: the interval is
+// a subset of the exact one (zinterval), so a scan with it finds every event,
+// plus -- when an element falls in the sliver between the two, width ~m --
+// a false candidate, which the event step quantizes to code R with the state
+// unchanged.  Six f64 ops instead of a ballot round of zero_code.
+FZB_DEV void zinner(double pred, const QParams& P, float& ilo, float& ihi) {
+    const double m = __dadd_rn(__dmul_rn(P.eb, 9.5367431640625e-07), __dmul_rn(__dadd_rn(fabs(pred), P.eb), 5.684341886080802e-14));
+    const double w = __dsub_rn(P.eb, m);
+    const double hd = __dadd_rn(pred, w), ld = __dsub_rn(pred, w);
+    float hf = __double2float_rn(hd), lf = __double2float_rn(ld);
+    if ((double)hf > hd) hf = kfloat(fkey(hf) - 1u);   // largest f32 <= hd
+    if ((double)lf < ld) lf = kfloat(fkey(lf) + 1u);   // smallest f32 >= ld
+    ilo = lf;
+    ihi = hf;
+}
+
+FZB_DEV void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// lane 0: arm the barrier for `bytes` and start one bulk copy global -> shared
+FZB_DEV void bulk_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(smem)),
+                 "l"(gmem), "r"(bytes), "r"(b)
+                 : "memory");
+}
+FZB_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done)
+                     : "r"(b), "r"(parity)
+                     : "memory");
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(64) lz1d_walk3_kernel(const float* __restrict__ x, long long n,
+                                                         uint16_t* __restrict__ codes, uint32_t* __restrict__ bitmap,
+                                                         const float* __restrict__ bmin, const float* __restrict__ bmax,
+                                                         long long nblk, const float* __restrict__ smin_g,
+                                                         const float* __restrict__ smax_g, long long nsb,
+                                                         const float* __restrict__ gmin, const float* __restrict__ gmax,
+                                                         const double* __restrict__ d_eb, int radius,
+                                                         long long pf_ahead, long long* pos_slot) {
     extern __shared__ float s_sum[];
-    const int lane = threadIdx.x;
+    __shared__ __align__(128) float s_blk[2][BS1];   // double-buffered exit blocks
+    __shared__ __align__(8) uint64_t s_bar[2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    volatile long long* g_pos = reinterpret_cast<volatile long long*>(pos_slot);
+    if (blockIdx.x == 1) {
+        // ---- prefetch CTA (another SM: its bulk prefetches do not queue in
+        //      front of the walker's own bulk copies)
+        if (warp != 0 || pf_ahead <= 0 || !VEC) return;
+        // ---- prefetch warp: keep x and the summaries of [walker, walker + pf_ahead) in L2
+        long long done = 0;
+        for (;;) {
+            const long long cb = *g_pos;
+            if (cb < 0) break;
+            if (done < cb) done = cb & ~(PF_CHUNK - 1);
+            const long long target = min(nblk, cb + pf_ahead);
+            if (lane == 0) {
+                while (done < target) {
+                    const long long m = min(PF_CHUNK * BS1, n - (done << 10));
+                    prefetch_l2(x + (done << 10), (uint32_t)(((m * 4) + 15) & ~15ll));
+                    const long long gm = min(PF_CHUNK, nblk - done) * 32 * 4;
+                    prefetch_l2(gmin + done * 32, (uint32_t)gm);
+                    prefetch_l2(gmax + done * 32, (uint32_t)gm);
+                    if ((done & 255) == 0) {
+                        const uint32_t by = (uint32_t)(((min(256ll, nblk - done) * 4) + 15) & ~15ll);
+                        prefetch_l2(bmin + done, by);
+                        prefetch_l2(bmax + done, by);
+                    }
+                    done += PF_CHUNK;
+                }
+            }
+            done = __shfl_sync(0xffffffffu, done, 0);
+            __nanosleep(256);
+        }
+        return;
+    }
     const bool cached = nsb <= WALK_SMEM_SB;
     const float* smin = smin_g;
     const float* smax = smax_g;
     if (cached) {
-        for (long long q = lane; q < nsb; q += 32) {
+        for (long long q = threadIdx.x; q < nsb; q += blockDim.x) {
             s_sum[q] = smin_g[q];
             s_sum[nsb + q] = smax_g[q];
         }
-        __syncwarp();
         smin = s_sum;
         smax = s_sum + nsb;
     }
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar[0]);
+        mbar_init(&s_bar[1]);
+    }
+    __syncthreads();
+    if (warp == 1) return;
     const QParams P = make_qparams(*d_eb, radius);
-    long long t = 0;
-    float r = 0.f;
 #ifdef LZ7_TIMING
     long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long c0 = clock64();
-#define WSTAMP(i) do { const long long c1 = clock64(); ph[i] += c1 - c0; c0 = c1; } while (0)
+#define WSTAMP3(i) do { const long long c1 = clock64(); ph[i] += c1 - c0; c0 = c1; } while (0)
 #else
-#define WSTAMP(i) do { } while (0)
+#define WSTAMP3(i) do { } while (0)
 #endif
-    while (t < n) {
+    // current block cb (smem buffer `cur`): its group summaries, the window of
+    // block summaries past it, and this lane's element of the event's group;
+    // the *2 registers hold the block being loaded into buffer cur ^ 1
+    float wlo[WIN1], whi[WIN1], wlo2[WIN1], whi2[WIN1];
+    float glo, ghi, glo2, ghi2;
+    float gv;
+    long long cb = 0;
+    int cg = 0, cur = 0;
+    bool bulk[2] = {false, false}, pend[2] = {false, false};
+    uint32_t par[2] = {0u, 0u};
+    // start the loads of block b into buffer k (elements) and the *2 registers
+    auto issue = [&](long long b, int k) {
+        const long long base = b << 10;
+        const bool bk = VEC && base + BS1 <= n;
+        if (bk) {
+            if (lane == 0) bulk_load(s_blk[k], x + base, BS1 * 4, &s_bar[k]);
+        } else if (VEC) {
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                const long long i = base + 128 * e + 4 * lane;
+                const int nb = (int)max(0ll, min(16ll, (n - i) * 4));
+                cp_async16(s_blk[k] + 128 * e + 4 * lane, x + (nb ? i : 0), nb);
+            }
+            v6::cp_async_commit();
+        }
+        if (k) { bulk[1] = bk; pend[1] = VEC; } else { bulk[0] = bk; pend[0] = VEC; }
+        const long long gq = b * 32 + lane;
+        glo2 = (base + 32 * lane < n) ? __ldcg(gmin + gq) : INFINITY;
+        ghi2 = (base + 32 * lane < n) ? __ldcg(gmax + gq) : -INFINITY;
+        walk_load_window(bmin, bmax, nblk, b, wlo2, whi2);
+    };
+    auto wait_buf = [&](int k) {
+        const bool p = k ? pend[1] : pend[0];
+        if (!p) return;
+        const bool bk = k ? bulk[1] : bulk[0];
+        if (bk) {
+            mbar_wait(&s_bar[k], k ? par[1] : par[0]);
+            if (k) par[1] ^= 1u; else par[0] ^= 1u;
+        } else {
+            v6::cp_async_wait_n<0>();
+        }
+        if (k) pend[1] = false; else pend[0] = false;
+        __syncwarp();
+    };
+    auto commit = [&]() {   // the *2 registers become the current block's
+        glo = glo2;
+        ghi = ghi2;
+#pragma unroll
+        for (int j = 0; j < WIN1; j++) { wlo[j] = wlo2[j]; whi[j] = whi2[j]; }
+    };
+    auto group_val = [&](long long b, int g, int k) -> float {
+        const long long i = (b << 10) + 32 * g + lane;
+        if (VEC) return s_blk[k][32 * g + lane];
+        return i < n ? __ldg(x + i) : 0.f;
+    };
+    auto window_first = [&](float lo, float hi) -> long long {
+        long long fb = -1;
+#pragma unroll
+        for (int j = 0; j < WIN1; j++) {
+            const unsigned fm = __ballot_sync(0xffffffffu, !(wlo[j] >= lo && whi[j] <= hi));
+            if (fm && fb < 0) fb = cb + 1 + 32 * j + (__ffs(fm) - 1);
+        }
+        return fb;
+    };
+    issue(0, 0);
+    commit();
+    wait_buf(0);
+    gv = group_val(0, 0, 0);
+    long long t = 0;
+    float xv = __shfl_sync(0xffffffffu, gv, 0);
+    float r = 0.f;
+    for (;;) {
         {   // event at t
-            const double v = (double)__ldg(x + t);
             const double pred = (t == 0) ? 0.0 : __dadd_rn(0.0, (double)r);
             float rec;
             bool outl;
-            const int c = quantize(v, pred, P, rec, outl);
+            const int c = quantize_walk((double)xv, pred, P, rec, outl);
             if (lane == 0) {
                 if (c != radius) codes[t] = (uint16_t)c;
                 if (outl) atomicOr(bitmap + (t >> 5), 1u << (t & 31));
             }
             r = rec;
-            t++;
         }
-        WSTAMP(0);
-        if (t >= n) break;
-        // loads that do not depend on the new interval go out before its search:
-        // the rest of the current block, and the block summaries of the current
-        // and the next superblock (lane = block within the superblock)
-        const long long a0 = t, b0 = (t & (BS1 - 1)) ? min(n, ((t >> 10) + 1) << 10) : t;
-        // the rest of the current block: its whole aligned 1024-element block in
-        // 8 16-byte loads per lane when it is complete (elements before a0 are
-        // masked at the search), else 32 scalar loads
-        const long long blk_a = a0 & ~(long long)(BS1 - 1);
-        const bool vec_rest = b0 > a0 && blk_a + BS1 <= n && !((reinterpret_cast<uintptr_t>(x + blk_a)) & 15);
-        float pv[32];
-        if (vec_rest) {
-#pragma unroll
-            for (int e = 0; e < 8; e++) {
-                const float4 q = __ldg(reinterpret_cast<const float4*>(x + blk_a) + e * 32 + lane);
-                pv[4 * e] = q.x; pv[4 * e + 1] = q.y; pv[4 * e + 2] = q.z; pv[4 * e + 3] = q.w;
-            }
-        } else {
-#pragma unroll
-            for (int e = 0; e < 32; e++) {
-                const long long i = a0 + e * 32 + lane;
-                pv[e] = i < b0 ? __ldg(x + i) : 0.f;
+        WSTAMP3(0);
+        if (t + 1 >= n) break;
+        const double pr = __dadd_rn(0.0, (double)r);
+        const long long gbase = (cb << 10) + 32 * cg;
+        float zlo, zhi;
+        zinner(pr, P, zlo, zhi);
+        WSTAMP3(1);
+        // (1) the rest of the event's group
+        {
+            const unsigned m = __ballot_sync(0xffffffffu, (gbase + lane > t) & (gbase + lane < n) &
+                                                              !(gv >= zlo && gv <= zhi));
+            if (m) {
+                const int f = __ffs(m) - 1;
+                t = gbase + f;
+                xv = __shfl_sync(0xffffffffu, gv, f);
+                WSTAMP3(2);
+                continue;
             }
         }
-        const long long sb_cur = b0 >> 15;
-        float pmin[2], pmax[2];
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const long long bb = (sb_cur + h) * 32 + lane;
-            pmin[h] = bb < nblk ? __ldcg(bmin + bb) : INFINITY;
-            pmax[h] = bb < nblk ? __ldcg(bmax + bb) : -INFINITY;
+        // (2) the rest of the block: its later groups
+        {
+            const unsigned m = __ballot_sync(0xffffffffu, (lane > cg) & !(glo >= zlo && ghi <= zhi));
+            if (m) {
+                cg = __ffs(m) - 1;
+                gv = group_val(cb, cg, cur);
+                const long long gb2 = (cb << 10) + 32 * cg;
+                const unsigned m2 = __ballot_sync(0xffffffffu, (gb2 + lane < n) & !(gv >= zlo && gv <= zhi));
+                const int f = __ffs(m2) - 1;
+                t = gb2 + f;
+                xv = __shfl_sync(0xffffffffu, gv, f);
+                WSTAMP3(2);
+                continue;
+            }
         }
-        const double pred = __dadd_rn(0.0, (double)r);
-        const long long k0 = fkey(__double2float_rn(pred));
-        uint32_t khi = 0, klo = 0;
-        zbounds(k0, fkey(__double2float_rn(__dadd_rn(pred, P.eb))), fkey(__double2float_rn(__dsub_rn(pred, P.eb))),
-                pred, P, khi, klo);
-        const float zlo = kfloat(klo), zhi = kfloat(khi);
-        WSTAMP(1);
-        // scan [a, b) (b - a <= 1024) with coalesced loads; returns first outside index or -1
-        auto scan = [&](long long a, long long b) -> long long {
-            if (b - a == BS1 && !((reinterpret_cast<uintptr_t>(x + a)) & 15)) {
-                // a whole aligned block: 8 16-byte loads per lane (elements
-                // a + 128*e + 4*lane + c) instead of 32 scalar ones
-                uint32_t m = 0;
-#pragma unroll
-                for (int e = 0; e < 8; e++) {
-                    const float4 q = __ldg(reinterpret_cast<const float4*>(x + a) + e * 32 + lane);
-                    const float qq[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-                    for (int c = 0; c < 4; c++) m |= (uint32_t)!(qq[c] >= zlo && qq[c] <= zhi) << (4 * e + c);
-                }
-                // bit 4e+c <-> index a + 128e + 4*lane + c: increasing with the bit within a lane
-                const uint32_t mine = m ? (uint32_t)(128 * ((__ffs(m) - 1) >> 2) + 4 * lane + ((__ffs(m) - 1) & 3))
-                                        : 0xFFFFFFFFu;
-                const uint32_t best = __reduce_min_sync(0xffffffffu, mine);
-                return best == 0xFFFFFFFFu ? -1 : a + (long long)best;
-            }
-            float v[32];
-#pragma unroll
-            for (int e = 0; e < 32; e++) {
-                const long long i = a + e * 32 + lane;
-                v[e] = i < b ? __ldg(x + i) : zlo;
-            }
-            return first_outside(v, a, b, zlo, zhi);
-        };
-        long long found = -1;
-        if (b0 > a0) {
-            if (vec_rest) {   // bit 4e+c <-> index blk_a + 128e + 4*lane + c
-                uint32_t m = 0;
-                const int d0 = (int)(a0 - blk_a);   // < 1024: 32-bit offsets
-#pragma unroll
-                for (int e = 0; e < 32; e++)
-                    m |= (uint32_t)((128 * (e >> 2) + 4 * lane + (e & 3) >= d0) & !(pv[e] >= zlo && pv[e] <= zhi)) << e;
-                const uint32_t mine = m ? (uint32_t)(128 * ((__ffs(m) - 1) >> 2) + 4 * lane + ((__ffs(m) - 1) & 3))
-                                        : 0xFFFFFFFFu;
-                const uint32_t best = __reduce_min_sync(0xffffffffu, mine);
-                found = best == 0xFFFFFFFFu ? -1 : blk_a + (long long)best;
-            } else {
-                found = first_outside(pv, a0, b0, zlo, zhi);
-            }
-            t = b0;
-        }
-        WSTAMP(2);
-        while (found < 0 && t < n) {
+        // (3) the window of block summaries, else the superblocks
+        long long fb = window_first(zlo, zhi);
+        WSTAMP3(2);
+        if (fb < 0) {
 #ifdef LZ7_TIMING
             ph[4]++;
 #endif
-            const long long sb = t >> 15;
-            if ((t & (BS2 - 1)) == 0) {  // probe 32 superblocks
-                const long long sq = sb + lane;
-                const bool skip = sq < nsb && smin[sq] >= zlo && smax[sq] <= zhi;
-                const unsigned ns = __ballot_sync(0xffffffffu, !skip);
-                if (!ns) { t = (sb + 32) * BS2; continue; }
-                t = (sb + (__ffs(ns) - 1)) * BS2;
-                if (t >= n) break;
-            }
-            // block summaries of superblock t / BS2 (prefetched for the current and the next one)
-            const long long sbt = t >> 15;
-            float lo, hi;
-            if (sbt == sb_cur) { lo = pmin[0]; hi = pmax[0]; }
-            else if (sbt == sb_cur + 1) { lo = pmin[1]; hi = pmax[1]; }
-            else {
-#ifdef LZ7_TIMING
-                ph[5]++;
-#endif
-                const long long bb = sbt * 32 + lane;
-                lo = bb < nblk ? __ldcg(bmin + bb) : INFINITY;
-                hi = bb < nblk ? __ldcg(bmax + bb) : -INFINITY;
-            }
-            const long long bfirst = t >> 10;
-            const long long bb = sbt * 32 + lane;
-            const bool skip = bb < bfirst || bb >= nblk || (lo >= zlo && hi <= zhi);
-            const unsigned nsk = __ballot_sync(0xffffffffu, !skip);
-            if (!nsk) { t = (sbt + 1) * BS2; continue; }   // rest of the superblock is skippable
-            const long long fb = sbt * 32 + (__ffs(nsk) - 1);
-            t = fb * BS1;
-            const long long be = min(n, t + BS1);
-#ifdef LZ7_TIMING
-            ph[6]++;
-#endif
-            found = scan(t, be);
-            t = be;
+            fb = walk_far(cb + 1 + 32 * WIN1, nblk, bmin, bmax, smin, smax, nsb, zlo, zhi);
         }
-        WSTAMP(3);
-        if (found < 0) break;
-        t = found;
+        if (fb < 0) break;   // no further event: the rest keeps zero codes
+        wait_buf(cur ^ 1);
+        issue(fb, cur ^ 1);
+        cur ^= 1;
+        commit();
+        cb = fb;
+        if (lane == 0) *g_pos = cb;
+        {
+            const unsigned m = __ballot_sync(0xffffffffu, !(glo >= zlo && ghi <= zhi));   // the summary guarantees one
+            cg = __ffs(m) - 1;
+        }
+        wait_buf(cur);
+        gv = group_val(cb, cg, cur);
+        {
+            const long long gb2 = (cb << 10) + 32 * cg;
+            const unsigned m2 = __ballot_sync(0xffffffffu, (gb2 + lane < n) & !(gv >= zlo && gv <= zhi));
+            const int f = __ffs(m2) - 1;
+            t = gb2 + f;
+            xv = __shfl_sync(0xffffffffu, gv, f);
+        }
+#ifdef LZ7_TIMING
+        ph[6]++;
+#endif
+        WSTAMP3(3);
     }
+    // drain outstanding copies before the CTA exits
+    wait_buf(0);
+    wait_buf(1);
+    if (lane == 0) *g_pos = -1;
 #ifdef LZ7_TIMING
     if (lane == 0)
         for (int i = 0; i < 8; i++) g_walk_stamp[i] = ph[i];
@@ -1073,6 +1258,22 @@ size_t v7_ws(uint32_t n0, uint32_t n1, uint32_t n2) {
     return m;
 }
 
+// 1D encoder workspace: header, block / superblock / group summaries.
+struct Walk1D {
+    size_t o_bmin, o_bmax, o_smin, o_smax, o_gmin, o_gmax, total;
+    explicit Walk1D(long long n) {
+        const size_t nblk = (size_t)((n + BS1 - 1) / BS1), nsb = (nblk + 31) / 32;
+        auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+        o_bmin = WS_HDR;
+        o_bmax = o_bmin + al(nblk * 4);
+        o_smin = o_bmax + al(nblk * 4);
+        o_smax = o_smin + al(nsb * 4);
+        o_gmin = o_smax + al(nsb * 4);
+        o_gmax = o_gmin + al(nblk * 128);
+        total = o_gmax + al(nblk * 128);
+    }
+};
+
 }  // namespace
 
 extern "C" {
@@ -1082,7 +1283,7 @@ FZB_API size_t fzb_lorenzo_workspace_bytes(uint32_t n0, uint32_t n1, uint32_t n2
     const long long n = (long long)n0 * n1 * n2;
     if (n0 == 1 && n1 == 1) {
         const long long nblk = (n + BS1 - 1) / BS1, nsb = (nblk + 31) / 32, nch = (n + EVC - 1) / EVC;
-        const size_t enc = WS_HDR + (size_t)(nblk + nsb) * 8 + 1024;
+        const size_t enc = Walk1D(n).total;
         const size_t dec = WS_HDR + 1024 + (size_t)nch * 4 + (size_t)nch * 8 + fzscan::ws_bytes(nch) + 256 + (size_t)n * 8;
         return enc > dec ? enc : dec;
     }
@@ -1110,21 +1311,40 @@ FZB_API int fzb_lorenzo_encode_f32(const float* d_in, uint32_t n0, uint32_t n1, 
     if (n == 0) return 0;
     if (n0 == 1 && n1 == 1) {
         const long long nblk = (n + BS1 - 1) / BS1, nsb = (nblk + 31) / 32;
-        if (ws_bytes < WS_HDR + (size_t)(nblk + nsb) * 8) return FZB_E_WORKSPACE;
+        // every summary array 256-byte aligned (the walker bulk-prefetches them)
+        const Walk1D L(n);
+        if (ws_bytes < L.total) return FZB_E_WORKSPACE;
         invalidate_faces(d_ws, st);
-        float* bmin = reinterpret_cast<float*>(static_cast<unsigned char*>(d_ws) + WS_HDR);
-        float* bmax = bmin + nblk;
-        float* smin = bmax + nblk;
-        float* smax = smin + nsb;
-        lz1d_summary_kernel<<<kNumSMs * 8, 256, 0, st>>>(d_in, n, d_codes, (int)radius, bmin, bmax, nblk);
-        lz1d_super_kernel<<<kNumSMs * 2, 256, 0, st>>>(bmin, bmax, nblk, smin, smax, nsb);
-        // the summary pass streamed 4n bytes through L2: pull the (small) block summaries back in
-        lz1d_touch_kernel<<<kNumSMs * 4, 256, 0, st>>>(bmin, 2 * nblk);
-        const size_t wsm = nsb <= WALK_SMEM_SB ? (size_t)nsb * 8 : 0;
-        if (wsm > 48 * 1024) cudaFuncSetAttribute(lz1d_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
-        lz1d_walk_kernel<<<1, 32, wsm, st>>>(d_in, n, d_codes, d_bitmap, bmin, bmax, nblk, smin, smax, nsb, d_eb,
-                                             (int)radius);
-        return fzb_check_launch();
+        unsigned char* wb = static_cast<unsigned char*>(d_ws);
+        float* bmin = reinterpret_cast<float*>(wb + L.o_bmin);
+        float* bmax = reinterpret_cast<float*>(wb + L.o_bmax);
+        float* smin = reinterpret_cast<float*>(wb + L.o_smin);
+        float* smax = reinterpret_cast<float*>(wb + L.o_smax);
+        float* gmin = reinterpret_cast<float*>(wb + L.o_gmin);
+        float* gmax = reinterpret_cast<float*>(wb + L.o_gmax);
+        {
+            lz1d_summary2_kernel<<<kNumSMs * 8, 256, 0, st>>>(d_in, n, d_codes, (int)radius, bmin, bmax, gmin, gmax,
+                                                              nblk);
+            lz1d_super_kernel<<<kNumSMs * 2, 256, 0, st>>>(bmin, bmax, nblk, smin, smax, nsb);
+            const size_t wsm = nsb <= WALK_SMEM_SB ? (size_t)nsb * 8 : 0;
+            const bool vec = !(reinterpret_cast<uintptr_t>(d_in) & 15);
+            auto kfn = vec ? lz1d_walk3_kernel<true> : lz1d_walk3_kernel<false>;
+            cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
+            const char* pfe = getenv("FZB_WALK_PF");
+            const long long pf = pfe ? atoll(pfe) : PF_AHEAD;
+            long long* pos = reinterpret_cast<long long*>(wb + 24);   // header words 6-7: walker position
+            cudaMemsetAsync(pos, 0, 8, st);
+            kfn<<<2, 64, wsm, st>>>(d_in, n, d_codes, d_bitmap, bmin, bmax, nblk, smin, smax, nsb, gmin, gmax, d_eb,
+                                    (int)radius, pf, pos);
+#ifdef LZ7_TIMING
+            if (getenv("FZB_WALK_TWICE")) {
+                cudaMemsetAsync(pos, 0, 8, st);
+                kfn<<<2, 64, wsm, st>>>(d_in, n, d_codes, d_bitmap, bmin, bmax, nblk, smin, smax, nsb, gmin, gmax,
+                                        d_eb, (int)radius, pf, pos);
+            }
+#endif
+            return fzb_check_launch();
+        }
     }
     if (!use_v4(n2))
         return launch_v7<false>(d_in, nullptr, d_codes, d_bitmap, nullptr, n0, n1, n2, d_eb, (int)radius, d_ws, ws_bytes, st);
