@@ -1,32 +1,48 @@
 """Benchmark: FZModules hot path on B200 vs the CPU reference.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2|c1|c3|c4|c5|c5d]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c4|c1|c2|c3|c5|c5s] [--pipeline P] [--rel R] [--no-cpu] [--no-parity]
 
-Workload (default) = BASELINE.json configs[1]: FZMod-Speed (Lorenzo +
-bitshuffle) on a synthetic smooth_trig 512^3 f32 Nyx-shaped field at rel eb
-1e-3.  A "step" = one compress + decompress round trip of one field per GPU.
+Headline workload (default) = BASELINE.json configs[3], the largest
+single-GPU configuration: a HACC-shaped particle1d array of 280,953,867 f32
+values at rel eb 1e-4 through FZMod-Default (`value`), with FZMod-Speed and
+FZMod-Quality on the same bytes in `presets`.  A "step" = one compress +
+decompress round trip of one field per GPU.
 
-* value   : device-resident GB/s (input f32 bytes / step time), input in HBM
-            when the timed region starts; compress kernels -> one 32-byte size
-            read -> decompress kernels on the resident segments.
-* e2e     : the public API (compress(Field) -> Archive -> decompress(Archive)
-            -> Field) from pinned host memory, H2D/D2H inside the timed region.
-* roofline: dominant kernel, algorithmic bytes / CUDA-event duration vs the
-            measured HBM copy peak (MEASURED_PEAKS.json).
-* cpu_baseline: the C oracle (restated fzpipe; test infrastructure) on this
-            box's host cores over a bounded slab sample of the same field.
-Multi-GPU (torchrun): one field per rank (weak scaling); per step the ranks
-all-gather their compressed sizes (the container-offset collective);
-time = max over ranks.  L2 hygiene: every input/working set (537 MB + 268 MB
-codes) exceeds the 126 MB L2.
+* value    : device-resident GB/s (input f32 bytes / step time), the field in
+             HBM when the timed region starts: the compress DAG -> one
+             32-byte size read -> the decompress DAG on the resident segments,
+             replayed as two captured CUDA graphs (same kernels as the eager
+             path, checked bit-equal).
+* e2e      : the public API (compress(Field) -> archive bytes -> parse_archive
+             -> decompress -> Field) from pinned host memory; H2D/D2H inside.
+* parity   : the run's own archives and reconstructions against fzpipe's
+             SHA-256 at full size (tests/golden/fullsize.json, when the input
+             bytes equal fzpipe's data.generate output), else against the C
+             oracle on the same bytes; computed outside the timed region.
+* roofline : dominant kernel, algorithmic bytes / its CUDA-event
+             duration inside the timed replays, vs MEASURED_PEAKS.json.
+* cpu_baseline : the C oracle (fzpipe restated; test infrastructure) on the
+             host cores over a bounded sample of the same field.
+
+Multi-GPU: `--gpus N` without WORLD_SIZE re-launches itself under
+torch.distributed.run (one rank per GPU, NCCL).  Single-field workloads are
+replicas (weak scaling: one field per rank, per step an all-gather of the
+compressed sizes = the container-offset collective).  `--workload c5` is
+BASELINE configs[4]: 64 fields of 512^3 sharded over the ranks
+(shard.shard_range, strong scaling), each rank's fields through batched
+wavefronts of <= 8, then the size all-gather and container offsets; its e2e
+leg writes the rank's archives into its slice of the FZB1 container.
+Time = max over ranks of CUDA-event time.  L2: every working set exceeds
+the 126 MB L2 (no flush needed).
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -37,30 +53,34 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
+    "c4": dict(name="particle1d 280953867 (HACC-shaped) rel 1e-4, FZMod-Default (+Speed, Quality)",
+               pipeline="default", presets=("default", "speed", "quality"), dims=(280953867,), kind="particle",
+               rel=1e-4, golden="c4"),
     "c2": dict(name="FZMod-Speed smooth_trig 512x512x512 (Nyx-shaped) rel 1e-3", pipeline="speed",
-               dims=(512, 512, 512), kind="trig", rel=1e-3),
+               presets=("speed",), dims=(512, 512, 512), kind="trig", rel=1e-3, golden="c2"),
     "c1": dict(name="FZMod-Default smooth_trig 100x500x500 (Hurricane-shaped) rel 1e-4", pipeline="default",
-               dims=(100, 500, 500), kind="trig", rel=1e-4),
+               presets=("default", "speed", "quality"), dims=(100, 500, 500), kind="trig", rel=1e-4, golden="c1"),
     "c3": dict(name="FZMod-Quality smooth_trig 1800x3600 (CESM-shaped) rel 1e-4", pipeline="quality",
-               dims=(1800, 3600), kind="trig", rel=1e-4),
-    "c4": dict(name="FZMod-Default particle1d 280953867 (HACC-shaped) rel 1e-4", pipeline="default",
-               dims=(280953867,), kind="particle", rel=1e-4),
-    # C5 shard: 64 fields over 8 GPUs = 8 per GPU, all in flight at once (compress_batch)
-    "c5": dict(name="C5 shard: 8 x smooth_trig 512x512x512 per GPU (FZMod-Speed, batched) rel 1e-3",
-               pipeline="speed", dims=(512, 512, 512), kind="trig", rel=1e-3, fields=8),
-    "c5d": dict(name="C5 shard: 8 x smooth_trig 512x512x512 per GPU (FZMod-Default, batched) rel 1e-3",
-                pipeline="default", dims=(512, 512, 512), kind="trig", rel=1e-3, fields=8),
+               presets=("quality",), dims=(1800, 3600), kind="trig", rel=1e-4, golden="c3"),
+    # BASELINE configs[4]: 64 fields of 512^3 (34.4 GB) sharded over the ranks
+    "c5": dict(name="64 x smooth_trig 512x512x512 sharded over the GPUs, FZMod-Default, rel 1e-3",
+               pipeline="default", presets=("default",), dims=(512, 512, 512), kind="trig", rel=1e-3,
+               fields=64, golden="c2"),
+    "c5s": dict(name="64 x smooth_trig 512x512x512 sharded over the GPUs, FZMod-Speed, rel 1e-3",
+                pipeline="speed", presets=("speed",), dims=(512, 512, 512), kind="trig", rel=1e-3,
+                fields=64, golden="c2"),
 }
 METRIC = "compress/decompress GB/s per GPU & per box at fixed rel eb; CR+PSNR vs CPU ref"
+BATCH = 8   # fields per batched wavefront launch (C5)
 
 
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -111,6 +131,55 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+# ------------------------------------------------------------------ inputs
+
+def _golden(wl):
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "fullsize.json")) as f:
+            g = json.load(f).get(wl.get("golden"))
+    except Exception:
+        return None
+    if g and tuple(g["dims"]) == tuple(wl["dims"]) and abs(g["rel_eb"] - wl["rel"]) < 1e-15:
+        return g
+    return None
+
+
+def _sha(a) -> str:
+    return hashlib.sha256(memoryview(np.ascontiguousarray(a)).cast("B")).hexdigest()
+
+
+def _device_field(wl, seed, dev):
+    from paper_2509_20563_b200 import data
+    if wl["kind"] == "trig":
+        return data.smooth_trig_device(wl["dims"], seed, device=dev)
+    return data.particle1d_device(wl["dims"][0], seed, device=dev)
+
+
+def _host_field(wl, seed=0):
+    from paper_2509_20563_b200 import data
+    if wl["kind"] == "trig":
+        return data.smooth_trig_host(wl["dims"], seed)
+    return data.particle1d_host(wl["dims"][0], seed)
+
+
+def input_field(wl, dev):
+    """Field 0 of the workload on the device.  When fzpipe's full-size golden
+    exists, the bytes must be fzpipe's data.generate output: the device
+    generator is used when its SHA-256 matches, else the host generator."""
+    import torch
+    g = _golden(wl)
+    x = _device_field(wl, 0, dev).contiguous()
+    src = "device generator"
+    if g is not None:
+        h = x.cpu().numpy()
+        if _sha(h) != g["input_sha256"]:
+            h = _host_field(wl, 0)
+            src = "host generator (fzpipe data.generate restated)"
+            x = torch.from_numpy(h).to(dev)
+        src += ", sha256 == fzpipe's" if _sha(h) == g["input_sha256"] else ", sha256 != fzpipe's"
+    return x, src
+
+
 # ------------------------------------------------------------------ CPU side
 
 def cpu_roundtrip(x: np.ndarray, dims, pipeline: str, rel: float, threads: int, slab: int):
@@ -121,8 +190,7 @@ def cpu_roundtrip(x: np.ndarray, dims, pipeline: str, rel: float, threads: int, 
     O.build()
     nd = x.reshape(dims)
     lead = dims[0]
-    starts = [(t * slab) % max(lead - slab + 1, 1) for t in range(threads)] if len(dims) > 1 else \
-        [(t * slab) % max(lead - slab + 1, 1) for t in range(threads)]
+    starts = [(t * slab) % max(lead - slab + 1, 1) for t in range(threads)]
     jobs = [np.ascontiguousarray(nd[s:s + slab]) for s in starts]
     sub_dims = (slab,) + tuple(dims[1:])
 
@@ -143,31 +211,6 @@ def cpu_roundtrip(x: np.ndarray, dims, pipeline: str, rel: float, threads: int, 
     return nbytes / dt / 1e9, threads, dt, desc
 
 
-def run_reference(args, wl):
-    """--impl reference: the reference algorithm (C oracle port) on host cores."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    from paper_2509_20563_b200 import data
-    dims = wl["dims"]
-    x = _host_field(wl)
-    threads = min(os.cpu_count() or 1, 64)
-    slab = _slab(dims)
-    vals = []
-    for i in range(args.warmup + args.steps):
-        v, cores, dt, desc = cpu_roundtrip(x, dims, wl["pipeline"], wl["rel"], threads, slab)
-        if i >= args.warmup:
-            vals.append(v)
-    v = float(np.median(vals))
-    line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32 data, f64 predictor arithmetic", "data": "synthetic",
-            "config": {"workload": wl["name"], "pipeline": wl["pipeline"], "dims": list(dims), "rel_eb": wl["rel"]},
-            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "port", "sample": desc},
-            "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-
-
 def _slab(dims):
     if len(dims) == 3:
         return max(1, min(dims[0], 32))
@@ -176,279 +219,427 @@ def _slab(dims):
     return min(dims[0], 1 << 23)
 
 
-_HOST_CACHE = {}
+def run_reference(args, wl):
+    """--impl reference: the reference algorithm (C oracle port) on host cores."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    x = _host_field(wl, 0)
+    threads = min(os.cpu_count() or 1, 64)
+    slab = _slab(wl["dims"])
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, cores, dt, desc = cpu_roundtrip(x, wl["dims"], wl["pipeline"], wl["rel"], threads, slab)
+        if i >= args.warmup:
+            vals.append(v)
+    v = float(np.median(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "strong" if wl.get("fields") else "weak",
+            "vs_baseline": None, "dtype": "f32 data, f64 predictor arithmetic", "data": "synthetic",
+            "config": _config(wl, 1, 1),
+            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "port", "sample": desc},
+            "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
 
 
-def _host_field(wl):
-    key = (wl["dims"], wl["kind"])
-    if key not in _HOST_CACHE:
-        import torch
-        from paper_2509_20563_b200 import data
-        if torch.cuda.is_available():
-            x = _device_field(wl, 0).cpu().numpy()
-        else:
-            x = data.smooth_trig_host(wl["dims"], 0) if wl["kind"] == "trig" else data.particle1d_host(wl["dims"][0])
-        _HOST_CACHE[key] = x
-    return _HOST_CACHE[key]
-
-
-def _device_field(wl, seed):
-    from paper_2509_20563_b200 import data
-    if wl["kind"] == "trig":
-        return data.smooth_trig_device(wl["dims"], seed)
-    return data.particle1d_device(wl["dims"][0], seed)
+def _config(wl, world, fields_per_gpu):
+    return {"workload": wl["name"], "pipeline": wl["pipeline"], "dims": list(wl["dims"]), "rel_eb": wl["rel"],
+            "fields_total": wl.get("fields", world), "fields_per_gpu": fields_per_gpu,
+            "l2": "working set > 126 MB L2 (no flush needed)",
+            "parallelism": (f"64 fields sharded over {world} GPU(s)" if wl.get("fields")
+                            else f"whole-field replicas x{world}")}
 
 
 # ------------------------------------------------------------------ GPU side
 
-def run_ours(args, wl):
+ALGO = {  # algorithmic bytes per launch (SURVEY 8d), f(n, compressed size units)
+    "fzb_lorenzo_encode_f32": lambda n, s: 6 * n, "fzb_lorenzo_decode_f32": lambda n, s: 6 * n + n // 8,
+    "fzb_bitshuffle_encode": lambda n, s: 2 * n + n // 16 + 4 * s, "fzb_bitshuffle_decode": lambda n, s: 2 * n + n // 16 + 4 * s,
+    "fzb_huffman_encode": lambda n, s: 2 * n + (s + 7) // 8, "fzb_huffman_decode": lambda n, s: 2 * n + (s + 7) // 8,
+    "fzb_interp_encode_f32": lambda n, s: 6 * n, "fzb_interp_decode_f32": lambda n, s: 6 * n,
+    "fzb_histogram": lambda n, s: 2 * n, "fzb_minmax_f32": lambda n, s: 4 * n, "fzb_outlier_compact": lambda n, s: n // 8,
+}
+COMP_FNS = ("fzb_minmax_f32", "fzb_resolve_bound", "fzb_lorenzo_encode_f32", "fzb_lorenzo_encode_batch_f32",
+            "fzb_interp_encode_f32", "fzb_outlier_compact", "fzb_histogram", "fzb_huffman_build",
+            "fzb_huffman_encode", "fzb_bitshuffle_encode", "fzb_fill_u16")
+DEC_FNS = ("fzb_huffman_decode", "fzb_bitshuffle_decode", "fzb_outlier_scatter", "fzb_lorenzo_decode_f32",
+           "fzb_lorenzo_decode_batch_f32", "fzb_interp_decode_f32")
+
+
+def _allgather_sizes(nbytes, world, dev):
     import torch
     import torch.distributed as dist
+    if world > 1:
+        t = torch.tensor([nbytes], dtype=torch.int64, device=dev)
+        g = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(g, t)
 
-    import paper_2509_20563_b200 as fz
-    from paper_2509_20563_b200.core import ErrorBoundSpec, ErrorMode, Field
-    from paper_2509_20563_b200.device import default_engine
-    from paper_2509_20563_b200.metrics import quality_arrays
+
+def measure_field(x, wl, preset, steps, warmup, world, dev, full=True):
+    """Device-resident round trips of one field: traced eager pass (stage
+    times), then the timed CUDA-graph replays.  Returns a result dict."""
+    import torch
+    from paper_2509_20563_b200.device import default_engine, graph_engine
     from paper_2509_20563_b200.pipeline import get_pipeline
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    dims = wl["dims"]
+    dims, rel = wl["dims"], wl["rel"]
     n = int(np.prod(dims))
-    spec = get_pipeline(wl["pipeline"])
-    F = int(wl.get("fields", 1))
-    if F > 1:
-        X = torch.stack([_device_field(wl, seed=rank * F + f) for f in range(F)]).contiguous()
-        x = X[0]
-    else:
-        x = _device_field(wl, seed=rank).contiguous()
+    spec = get_pipeline(preset)
+    kw = dict(pipeline_id=spec.id, predictor=spec.predictor, codec=spec.primary_codec, radius=spec.radius())
     eng = default_engine()
     out = torch.empty(n, dtype=torch.float32, device=dev)
-    OUT = torch.empty(F, n, dtype=torch.float32, device=dev) if F > 1 else None
-    ebs = ErrorBoundSpec(ErrorMode.VALUE_RANGE_RELATIVE, wl["rel"])
-    kw = dict(pipeline_id=spec.id, predictor=spec.predictor, codec=spec.primary_codec, radius=spec.radius())
 
     def device_step():
-        if F > 1:
-            das = eng.compress_batch(X, dims, 1, wl["rel"], **kw)
-            szs = eng.sizes_batch(das)
-            eng.decompress_batch_resident(das, szs, [wl["rel"] * (z["hi"] - z["lo"]) for z in szs], OUT)
-            nbytes = sum(eng.compressed_bytes(d, z) for d, z in zip(das, szs))
-            da, sz = das[0], szs[0]
-        else:
-            da = eng.compress(x, dims, 1, wl["rel"], **kw)
-            sz = eng.sizes(da)
-            eb_abs = wl["rel"] * (sz["hi"] - sz["lo"])
-            eng.decompress_resident(da, sz, eb_abs, out)
-            nbytes = eng.compressed_bytes(da, sz)
-        if world > 1:
-            t = torch.tensor([nbytes], dtype=torch.int64, device=dev)
-            g = [torch.empty_like(t) for _ in range(world)]
-            dist.all_gather(g, t)
+        da = eng.compress(x, dims, 1, rel, **kw)
+        sz = eng.sizes(da)
+        eng.decompress_resident(da, sz, rel * (sz["hi"] - sz["lo"]), out)
+        _allgather_sizes(eng.compressed_bytes(da, sz), world, dev)
         return da, sz
 
-    def barrier():
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    # ---- warm-up + correctness of the measured path
-    for _ in range(max(args.warmup, 3)):
+    for _ in range(max(warmup, 3)):
         da, sz = device_step()
     torch.cuda.synchronize()
     assert sz["status"] == 0, f"device status {sz['status']:#x}"
     comp_bytes = eng.compressed_bytes(da, sz)
-    eb_abs = wl["rel"] * (sz["hi"] - sz["lo"])
-    maxerr = float(((OUT[0] if F > 1 else out).double() - x.double()).abs().max())
+    eb_abs = rel * (sz["hi"] - sz["lo"])
+    maxerr = float((out.double() - x.double()).abs().max())
     assert maxerr <= eb_abs, (maxerr, eb_abs)
-
-    # ---- the timed path.  One field per GPU: the round trip replays two
-    #      captured CUDA graphs (compress DAG, decompress DAG) -- the same
-    #      kernels as the eager path, checked bit-equal below, without the
-    #      per-call host cost; event-record nodes inside the graphs time every
-    #      kernel of every replay.  Batches (F > 1) run eagerly.
-    # per-stage times from one traced eager pass (two events around every
-    # C-ABI call); the timed region below times only the dominant entry point
+    # per-stage times: one traced eager round trip (two events around every C-ABI call)
     eng.trace = []
-    for _ in range(2):
-        device_step()
+    device_step()
     torch.cuda.synchronize()
     pre, eng.trace = eng.trace, None
     stage = {}
     for fn, e0, e1 in pre:
         stage.setdefault(fn, []).append(e0.elapsed_time(e1))
-    dom = max(stage, key=lambda k: np.mean(stage[k]))
-    run_eng, step = eng, device_step
-    if F == 1:
-        from paper_2509_20563_b200.device import graph_engine
-        geng = graph_engine()
-        geng.trace_only = {dom}
-        gout = torch.empty_like(out)
-        torch.cuda.synchronize()
+    dom = max(stage, key=lambda k: np.sum(stage[k]))
 
-        def graph_step():
-            gda = geng.compress_graphed(x, dims, 1, wl["rel"], **kw)
-            gsz = geng.sizes(gda)
-            geng.decompress_graphed(gda, gsz, wl["rel"] * (gsz["hi"] - gsz["lo"]), gout)
-            if world > 1:   # the container-offset collective, as in device_step
-                t = torch.tensor([geng.compressed_bytes(gda, gsz)], dtype=torch.int64, device=dev)
-                g = [torch.empty_like(t) for _ in range(world)]
-                dist.all_gather(g, t)
-            return gda, gsz
+    geng = graph_engine()
+    geng.trace_only = {dom}   # before the captures: a different set re-captures the graphs
+    gout = torch.empty_like(out)
 
-        for _ in range(max(args.warmup, 3)):
-            graph_step()
-        geng._sync()
-        assert torch.equal(gout.view(torch.int32), out.view(torch.int32)), "graph replay differs from the eager path"
-        run_eng, step = geng, graph_step
+    def graph_step():
+        gda = geng.compress_graphed(x, dims, 1, rel, **kw)
+        gsz = geng.sizes(gda)
+        geng.decompress_graphed(gda, gsz, rel * (gsz["hi"] - gsz["lo"]), gout)
+        _allgather_sizes(geng.compressed_bytes(gda, gsz), world, dev)
+        return gda, gsz
 
-    run_eng.launches = 0
-    run_eng.trace_only = {dom}
-    run_eng.trace = []
-    barrier()
+    for _ in range(max(warmup, 3)):
+        graph_step()
+    geng._sync()
+    assert torch.equal(gout.view(torch.int32), out.view(torch.int32)), "graph replay differs from the eager path"
+    geng.launches = 0
+    geng.trace = []
+    _barrier(world)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        t0.record(run_eng.stream)
-        for _ in range(args.steps):
-            step()
-        t1.record(run_eng.stream)
-        barrier()
-        run_eng._sync()
-    ms = t0.elapsed_time(t1) / args.steps
-    launches = run_eng.launches
-    trace, run_eng.trace = run_eng.trace, None
-    run_eng.trace_only = None
+    with ClockSampler(dev.index) as clk:
+        t0.record(geng.stream)
+        for _ in range(steps):
+            graph_step()
+        t1.record(geng.stream)
+        _barrier(world)
+        geng._sync()
+    ms = t0.elapsed_time(t1) / steps
+    launches = geng.launches
+    trace, geng.trace = geng.trace, None
+    geng.trace_only = None
     per_fn = {}
     for ent in trace:
         fn, v = (ent[0], ent[1]) if len(ent) == 2 else (ent[0], ent[1].elapsed_time(ent[2]))
         per_fn.setdefault(fn, []).append(v)
-    comp_ms = sum(np.sum(v) / 2 for k, v in stage.items() if k in (
-        "fzb_minmax_f32", "fzb_resolve_bound", "fzb_lorenzo_encode_f32", "fzb_lorenzo_encode_batch_f32",
-        "fzb_interp_encode_f32",
-        "fzb_outlier_compact", "fzb_histogram", "fzb_huffman_build", "fzb_huffman_encode", "fzb_bitshuffle_encode",
-        "fzb_fill_u16"))
-    dec_ms = sum(np.sum(v) / 2 for k, v in stage.items() if k in (
-        "fzb_huffman_decode", "fzb_bitshuffle_decode", "fzb_outlier_scatter", "fzb_lorenzo_decode_f32",
-        "fzb_lorenzo_decode_batch_f32",
-        "fzb_interp_decode_f32"))
-    eager = None
-    if F == 1:   # the same round trip issued call by call (reported beside it)
+    ms_max = _max_over_ranks(ms, world, dev)
+    res = {"ms": ms_max, "value": world * 4 * n / (ms_max / 1e3) / 1e9, "comp_bytes": comp_bytes,
+           "cr": 4 * n / comp_bytes, "max_abs_err": maxerr, "eb_abs": eb_abs, "launches": launches,
+           "clocks": clk.summary(), "stage": stage, "dom": dom, "size": sz["size"]}
+    comp_ms = sum(np.sum(v) for k, v in stage.items() if k in COMP_FNS)
+    dec_ms = sum(np.sum(v) for k, v in stage.items() if k in DEC_FNS)
+    res["compress_gbs"] = round(4 * n / (comp_ms / 1e3) / 1e9, 3) if comp_ms else None
+    res["decompress_gbs"] = round(4 * n / (dec_ms / 1e3) / 1e9, 3) if dec_ms else None
+    dom_ms = float(np.mean(per_fn[dom]))   # live, inside the timed region
+    if full:
+        # the same round trip issued call by call (reported beside it)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(eng.stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             device_step()
         e1.record(eng.stream)
         torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1) / args.steps
-        eager = {"ms_per_step": round(ems, 4), "value": round(world * 4 * n / (ems / 1e3) / 1e9, 3),
-                 "note": "same kernels launched one C-ABI call at a time (no CUDA graph)"}
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
-    value = world * F * 4 * n / (ms_max / 1e3) / 1e9
-
-    # ---- roofline of the dominant kernel
+        ems = e0.elapsed_time(e1) / steps
+        res["eager"] = {"ms_per_step": round(ems, 4), "value": round(world * 4 * n / (ems / 1e3) / 1e9, 3),
+                        "note": "same kernels launched one C-ABI call at a time (no CUDA graph)"}
     peak, peak_kind = _peaks()
-    algo = {"fzb_lorenzo_encode_f32": 6 * n, "fzb_lorenzo_decode_f32": 6 * n + n // 8,
-            "fzb_lorenzo_encode_batch_f32": F * 6 * n, "fzb_lorenzo_decode_batch_f32": F * (6 * n + n // 8),
-            "fzb_bitshuffle_encode": 2 * n + n // 16 + 4 * (sz["size"] if spec.primary_codec == "bitshuffle" else 0),
-            "fzb_bitshuffle_decode": 2 * n + n // 16 + 4 * (sz["size"] if spec.primary_codec == "bitshuffle" else 0),
-            "fzb_huffman_encode": 2 * n + (sz["size"] + 7) // 8, "fzb_huffman_decode": 2 * n + (sz["size"] + 7) // 8,
-            "fzb_interp_encode_f32": 10 * n, "fzb_interp_decode_f32": 8 * n, "fzb_histogram": 2 * n,
-            "fzb_minmax_f32": 4 * n, "fzb_outlier_compact": n // 8}
-    dom_ms = float(np.mean(per_fn[dom]))   # live, inside the timed region
-    achieved = algo.get(dom, 0) / (dom_ms / 1e3) / 1e9
-    traffic = None
+    algo = ALGO.get(dom, lambda n, s: 0)(n, sz["size"])
+    achieved = algo / (dom_ms / 1e3) / 1e9
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(dom)
+            tj = json.load(open(tp))
+            ent = tj.get("kernels", {}).get(wl.get("golden", "") + ":" + dom)
+            if ent:
+                traffic, traffic_src = ent["bytes"], tj.get("source")
         except Exception:
-            traffic = None
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
-                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                "algorithmic_bytes": int(algo.get(dom, 0)), "kernel_ms": round(dom_ms, 4),
-                "share_of_step": round(dom_ms / ms, 4),
-                "stage_ms": {k.replace("fzb_", ""): round(float(np.mean(v)), 4) for k, v in stage.items()},
-                "stage_ms_from": "one traced eager round trip before the timed region"}
+            pass
+    res["roofline"] = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+                       "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                       "traffic": traffic, "traffic_from": traffic_src, "algorithmic_bytes": int(algo),
+                       "kernel_ms": round(dom_ms, 4), "share_of_step": round(dom_ms / ms, 4),
+                       "stage_ms": {k.replace("fzb_", ""): round(float(np.sum(v)), 4) for k, v in stage.items()},
+                       "stage_ms_from": "one traced eager round trip before the timed region"}
+    return res
 
-    # ---- e2e through the public API from pinned host memory
-    hosts = []
-    for f in range(F):
-        xh = torch.empty(n, dtype=torch.float32, pin_memory=True)
-        xh.copy_(X[f] if F > 1 else x)
-        hosts.append(Field(dims, xh.numpy()))
-    field = hosts[0]
 
-    def e2e_step():
-        # the full container round trip: compress -> serialized archive bytes
-        # (archive_buffer: the pinned block the payloads were DMA'd into) ->
-        # parse_archive -> decompress
-        if F > 1:
-            arcs = fz.compress_batch(hosts, ebs, wl["pipeline"])
-            recs = fz.decompress_batch([fz.parse_archive(fz.archive_buffer(q)) for q in arcs])
-            return arcs[0], recs[0], arcs
-        a = fz.compress(field, ebs, wl["pipeline"])
-        return a, fz.decompress(fz.parse_archive(fz.archive_buffer(a))), [a]
+def _barrier(world):
+    import torch
+    import torch.distributed as dist
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def _max_over_ranks(v, world, dev):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def parity(wl, preset, a_bytes: bytes, recon: np.ndarray, xh: np.ndarray, golden_ok: bool):
+    """Archive + reconstruction of the run vs fzpipe's full-size SHA-256 (same
+    input bytes), else vs the C oracle on the same bytes."""
+    g = _golden(wl)
+    if golden_ok and g is not None and preset in g["archives"]:
+        want = g["archives"][preset]
+        ok = hashlib.sha256(a_bytes).hexdigest() == want["archive_sha256"] and _sha(recon) == want["recon_sha256"]
+        return ("bit-exact" if ok else "MISMATCH") + " vs fzpipe (sha256 of archive + reconstruction, " \
+                                                     "tests/golden/fullsize.json)"
+    from oracle import fzoracle as O
+    O.build()
+    want = O.compress(xh, wl["dims"], 1, wl["rel"], preset)
+    _, orec = O.decompress(want)
+    ok = want == a_bytes and orec.tobytes() == np.ascontiguousarray(recon).tobytes()
+    return ("bit-exact" if ok else "MISMATCH") + " vs the C oracle on the same bytes"
+
+
+def e2e_single(x, wl, preset, steps, world, dev):
+    """Public API round trip from pinned host memory (H2D/D2H in the timed region)."""
+    import torch
+    import paper_2509_20563_b200 as fz
+    n = int(np.prod(wl["dims"]))
+    ebs = fz.ErrorBoundSpec(fz.ErrorMode.VALUE_RANGE_RELATIVE, wl["rel"])
+    xh = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    xh.copy_(x)
+    field = fz.Field(wl["dims"], xh.numpy())
+
+    def step():
+        a = fz.compress(field, ebs, preset)
+        return a, fz.decompress(fz.parse_archive(fz.archive_buffer(a)))
 
     for _ in range(2):
-        a, r, arcs = e2e_step()
-    barrier()
-    e2e_times = []
-    for _ in range(max(1, min(args.steps, 5))):
+        a, r = step()
+    _barrier(world)
+    ts = []
+    for _ in range(max(1, min(steps, 5))):
         s0 = time.perf_counter()
-        a, r, arcs = e2e_step()
-        e2e_times.append(time.perf_counter() - s0)
-    e2e_s = torch.tensor([float(np.mean(e2e_times))], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-    e2e = world * F * 4 * n / float(e2e_s.item()) / 1e9
-    archive_bytes = len(fz.serialize_archive(a))
-    assert archive_bytes == comp_bytes, (archive_bytes, comp_bytes)
-    e2e_comp = sum(len(fz.serialize_archive(q)) for q in arcs)
-    q = quality_arrays(field.data, r.data, a.resolved_bound().eb_abs)
-    assert q.bound_satisfied
-    # the device-side metric (numpy-exact pairwise MSE) must agree bit for bit
-    from paper_2509_20563_b200.metrics import quality_device
-    q_dev = quality_device(torch.from_numpy(np.ascontiguousarray(field.data)).to(dev),
-                           torch.from_numpy(np.ascontiguousarray(r.data)).to(dev), dims, a.resolved_bound().eb_abs)
-    assert q_dev == q, (q_dev, q)
+        a, r = step()
+        ts.append(time.perf_counter() - s0)
+    s = _max_over_ranks(float(np.mean(ts)), world, dev)
+    comp = len(fz.serialize_archive(a))
+    return {"value": round(world * 4 * n / s / 1e9, 3), "unit": "GB/s",
+            "path": "compress(Field) -> archive bytes -> parse_archive -> decompress -> Field",
+            "h2d_bytes_per_step": 4 * n + comp, "d2h_bytes_per_step": 4 * n + comp}, a, r, field
 
-    line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32 data, f64 predictor arithmetic", "data": "synthetic",
-            "config": {"workload": wl["name"], "pipeline": wl["pipeline"], "dims": list(dims), "rel_eb": wl["rel"],
-                       "fields_per_gpu": F, "l2": "working set (805 MB per field) > 126 MB L2, no flush needed",
-                       "parallelism": f"whole-field shard x{world}"},
-            "compress_gbs": round(4 * n / (comp_ms / 1e3) / 1e9, 3) if comp_ms else None,
-            "decompress_gbs": round(4 * n / (dec_ms / 1e3) / 1e9, 3) if dec_ms else None,
-            "cr": round(4 * n / comp_bytes, 4), "psnr_db": round(q.psnr_db, 4), "max_abs_err": q.max_abs_err,
-            "quality_device_bit_identical": q_dev == q,
-            "eb_abs": a.resolved_bound().eb_abs,
-            "e2e": {"value": round(e2e, 3), "unit": "GB/s", "path": "compress(Field) -> archive bytes -> parse_archive -> decompress", "h2d_bytes_per_step": F * 4 * n + e2e_comp,
-                    "d2h_bytes_per_step": F * 4 * n + e2e_comp},
-            "roofline": roofline, "gpu_launches": launches, "clocks": clk.summary()}
-    if eager is not None:
-        line["config"]["timed_path"] = "CUDA-graph replays of the compress and decompress DAGs"
-        line["eager"] = eager
-    if rank == 0 and world == 1 and not args.no_cpu:
-        xs = x.cpu().numpy()
-        threads = min(os.cpu_count() or 1, 32)
-        v, cores, dt, desc = cpu_roundtrip(xs, dims, wl["pipeline"], wl["rel"], threads, _slab(dims))
-        line["cpu_baseline"] = {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "port",
-                                "sample": desc}
+
+def run_ours(args, wl):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if wl.get("fields"):
+        line = run_c5(args, wl, world, rank, dev)
+    else:
+        line = run_single(args, wl, world, rank, dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_single(args, wl, world, rank, dev):
+    import paper_2509_20563_b200 as fz
+    from paper_2509_20563_b200.metrics import quality_arrays, quality_device
+    import torch
+
+    x, src = input_field(wl, dev)
+    golden_ok = src.endswith("sha256 == fzpipe's")
+    n = int(np.prod(wl["dims"]))
+    head = wl["pipeline"]
+    presets = [head] + [p for p in wl["presets"] if p != head]
+    main = measure_field(x, wl, head, args.steps, args.warmup, world, dev, full=True)
+    e2e, a, r, field = e2e_single(x, wl, head, args.steps, world, dev)
+    assert len(fz.serialize_archive(a)) == main["comp_bytes"]
+    q = quality_arrays(field.data, r.data, a.resolved_bound().eb_abs)
+    assert q.bound_satisfied
+    q_dev = quality_device(x, torch.from_numpy(np.ascontiguousarray(r.data)).to(dev), wl["dims"],
+                           a.resolved_bound().eb_abs)
+    assert q_dev == q, (q_dev, q)
+    xh = field.data
+    par = {}
+    if not args.no_parity:
+        par[head] = parity(wl, head, bytes(fz.serialize_archive(a)), r.data, xh, golden_ok)
+    extra = {}
+    for p in presets[1:]:
+        m = measure_field(x, wl, p, max(3, min(args.steps, 10)), args.warmup, world, dev, full=False)
+        ent = {"value": round(m["value"], 3), "ms_per_step": round(m["ms"], 4), "cr": round(m["cr"], 4),
+               "compress_gbs": m["compress_gbs"], "decompress_gbs": m["decompress_gbs"],
+               "dominant_kernel": m["dom"], "dominant_frac": m["roofline"]["frac"]}
+        if not args.no_parity:
+            ap = fz.compress(field, fz.ErrorBoundSpec(fz.ErrorMode.VALUE_RANGE_RELATIVE, wl["rel"]), p)
+            rp = fz.decompress(ap)
+            ent["parity"] = parity(wl, p, bytes(fz.serialize_archive(ap)), rp.data, xh, golden_ok)
+            par[p] = ent["parity"]
+        extra[p] = ent
+    line = {"metric": METRIC, "value": round(main["value"], 3), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(main["ms"], 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 data, f64 predictor arithmetic", "data": f"synthetic ({src})",
+            "config": dict(_config(wl, world, 1), timed_path="CUDA-graph replays of the compress and decompress DAGs"),
+            "compress_gbs": main["compress_gbs"], "decompress_gbs": main["decompress_gbs"],
+            "cr": round(main["cr"], 4), "psnr_db": round(q.psnr_db, 4), "max_abs_err": q.max_abs_err,
+            "eb_abs": a.resolved_bound().eb_abs, "quality_device_bit_identical": q_dev == q,
+            "parity": par.get(head, "skipped (--no-parity)"), "presets": extra,
+            "e2e": e2e, "roofline": main["roofline"], "gpu_launches": main["launches"], "clocks": main["clocks"],
+            "eager": main["eager"]}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = min(os.cpu_count() or 1, 32)
+        v, cores, dt, desc = cpu_roundtrip(xh, wl["dims"], head, wl["rel"], threads, _slab(wl["dims"]))
+        line["cpu_baseline"] = {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+                                "sample": desc}
+    return line
+
+
+def run_c5(args, wl, world, rank, dev):
+    """BASELINE configs[4]: NF fields sharded over the ranks, batched wavefronts
+    of <= BATCH fields, size all-gather + container offsets per step."""
+    import torch
+    import paper_2509_20563_b200 as fz
+    from paper_2509_20563_b200 import shard
+    from paper_2509_20563_b200.device import default_engine
+    from paper_2509_20563_b200.pipeline import get_pipeline
+
+    NF, dims, rel = int(wl["fields"]), wl["dims"], wl["rel"]
+    n = int(np.prod(dims))
+    mine = list(shard.shard_range(NF, world, rank))
+    spec = get_pipeline(wl["pipeline"])
+    kw = dict(pipeline_id=spec.id, predictor=spec.predictor, codec=spec.primary_codec, radius=spec.radius())
+    X = torch.empty(len(mine), n, dtype=torch.float32, device=dev)
+    for i, f in enumerate(mine):
+        X[i].copy_(_device_field(wl, f, dev))
+    OUT = torch.empty_like(X)
+    eng = default_engine()
+    groups = [list(range(i, min(i + BATCH, len(mine)))) for i in range(0, len(mine), BATCH)]
+
+    def step():
+        local = []
+        for g in groups:
+            Xg = X[g[0]:g[-1] + 1]
+            das = eng.compress_batch(Xg, dims, 1, rel, **kw)
+            szs = eng.sizes_batch(das)
+            eng.decompress_batch_resident(das, szs, [rel * (z["hi"] - z["lo"]) for z in szs], OUT[g[0]:g[-1] + 1])
+            local += [eng.compressed_bytes(d, z) for d, z in zip(das, szs)]
+        sizes = shard.gather_sizes(local, NF, world, rank, device=dev)   # the one collective
+        return shard.container_offsets(sizes), sizes
+
+    for _ in range(max(args.warmup, 3)):
+        offs, sizes = step()
+    torch.cuda.synchronize()
+    maxerr = max(float((OUT[i].double() - X[i].double()).abs().max()) /
+                 (rel * (float(X[i].max().double()) - float(X[i].min().double()))) for i in range(len(mine)))
+    assert maxerr <= 1.0, maxerr
+    eng.launches = 0
+    _barrier(world)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        t0.record(eng.stream)
+        for _ in range(args.steps):
+            offs, sizes = step()
+        t1.record(eng.stream)
+        _barrier(world)
+    ms = _max_over_ranks(t0.elapsed_time(t1) / args.steps, world, dev)
+    launches = eng.launches
+    value = NF * 4 * n / (ms / 1e3) / 1e9
+
+    # e2e sample: this rank's first BATCH fields through the public batch API
+    # from pinned host memory, written into the rank's slice of the container
+    ebs = fz.ErrorBoundSpec(fz.ErrorMode.VALUE_RANGE_RELATIVE, rel)
+    samp = mine[:BATCH]
+    hosts = []
+    for i in range(len(samp)):
+        h = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        h.copy_(X[i])
+        hosts.append(fz.Field(dims, h.numpy()))
+    body = np.zeros(int(sum(sizes[f] for f in samp)), np.uint8)
+
+    def e2e_step():
+        arcs = fz.compress_batch(hosts, ebs, wl["pipeline"])
+        base = int(offs[samp[0]])
+        for f, a in zip(samp, arcs):
+            blob = fz.archive_buffer(a)
+            o = int(offs[f]) - base
+            body[o:o + len(blob)] = np.frombuffer(blob, np.uint8)
+        back = [fz.parse_archive(bytes(body[int(offs[f]) - base:int(offs[f]) - base + int(sizes[f])])) for f in samp]
+        return arcs, fz.decompress_batch(back)
+
+    for _ in range(2):
+        arcs, recs = e2e_step()
+    _barrier(world)
+    ts = []
+    for _ in range(max(1, min(args.steps, 3))):
+        s0 = time.perf_counter()
+        arcs, recs = e2e_step()
+        ts.append(time.perf_counter() - s0)
+    e2e_s = _max_over_ranks(float(np.mean(ts)), world, dev)
+    e2e_comp = int(sum(sizes[f] for f in samp))
+    for i in range(len(samp)):
+        assert np.abs(recs[i].data.astype(np.float64) - hosts[i].data).max() <= arcs[i].resolved_bound().eb_abs
+    par = "skipped (--no-parity)"
+    if not args.no_parity and rank == 0:
+        # field 0 of the batch, regenerated as fzpipe's bytes, through compress_batch with its neighbours
+        x0, src = input_field(wl, dev)
+        if src.endswith("sha256 == fzpipe's"):
+            f0 = fz.Field(dims, x0.cpu().numpy())
+            a0 = fz.compress_batch([f0] + hosts[1:], ebs, wl["pipeline"])[0]
+            r0 = fz.decompress_batch([a0] + arcs[1:])[0]
+            par = parity(wl, wl["pipeline"], bytes(fz.serialize_archive(a0)), r0.data, f0.data, True) + \
+                " (field 0, batched)"
+    cr = NF * 4 * n / float(np.sum(sizes))
+    line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 data, f64 predictor arithmetic", "data": "synthetic (device generator)",
+            "config": dict(_config(wl, world, len(mine)), batch=BATCH,
+                           timed_path="per step: every local field through batched wavefronts (compress -> sizes -> "
+                                      "resident decompress), then the NCCL all-gather of the 64 archive sizes and "
+                                      "the container offsets"),
+            "per_gpu_gbs": round(value / world, 3), "cr": round(cr, 4), "max_err_over_eb": maxerr,
+            "container_bytes": int(np.sum(sizes)) + 8 + 8 * (NF + 1), "parity": par,
+            "e2e": {"value": round(world * len(samp) * 4 * n / e2e_s / 1e9, 3), "unit": "GB/s",
+                    "path": f"compress_batch(Fields) -> archives written at their container offsets -> "
+                            f"parse_archive -> decompress_batch; a {len(samp)}-field sample per rank",
+                    "h2d_bytes_per_step": len(samp) * 4 * n + e2e_comp,
+                    "d2h_bytes_per_step": len(samp) * 4 * n + e2e_comp},
+            "gpu_launches": launches, "clocks": clk.summary()}
+    return line
 
 
 def main():
@@ -457,15 +648,26 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--pipeline", choices=["speed", "default", "quality"],
-                    help="override the workload's preset (SURVEY 8d: C4 on all three)")
+    ap.add_argument("--no-parity", action="store_true", help="skip the parity check (outside the timed region)")
+    ap.add_argument("--pipeline", choices=["speed", "default", "quality"], help="override the workload's preset")
     ap.add_argument("--rel", type=float, help="override the workload's relative error bound")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one rank per GPU: re-launch under torch.distributed.run
+        import socket
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
     wl = dict(WORKLOADS[args.workload])
     if args.pipeline or args.rel:
         wl["pipeline"] = args.pipeline or wl["pipeline"]
+        wl["presets"] = (wl["pipeline"],)
         wl["rel"] = args.rel or wl["rel"]
         wl["name"] = f"{wl['name']} [override: {wl['pipeline']} rel {wl['rel']:g}]"
     if args.impl == "reference":
