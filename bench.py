@@ -589,16 +589,14 @@ def run_c5(args, wl, world, rank, dev):
         h = torch.empty(n, dtype=torch.float32, pin_memory=True)
         h.copy_(X[i])
         hosts.append(fz.Field(dims, h.numpy()))
-    body = np.zeros(int(sum(sizes[f] for f in samp)), np.uint8)
+    srg = range(samp[0], samp[0] + len(samp))   # contiguous: the rank's first fields
+    body = np.zeros(shard.rank_slice(sizes, srg)[1], np.uint8)
 
     def e2e_step():
         arcs = fz.compress_batch(hosts, ebs, wl["pipeline"])
-        base = int(offs[samp[0]])
-        for f, a in zip(samp, arcs):
-            blob = fz.archive_buffer(a)
-            o = int(offs[f]) - base
-            body[o:o + len(blob)] = np.frombuffer(blob, np.uint8)
-        back = [fz.parse_archive(bytes(body[int(offs[f]) - base:int(offs[f]) - base + int(sizes[f])])) for f in samp]
+        part = shard.fill_slice(body, sizes, srg, [fz.archive_buffer(a) for a in arcs])   # the rank's container slice
+        o = shard.container_offsets(sizes) - shard.rank_slice(sizes, srg)[0]
+        back = [fz.parse_archive(bytes(part[int(o[f]):int(o[f]) + int(sizes[f])])) for f in srg]
         return arcs, fz.decompress_batch(back)
 
     for _ in range(2):

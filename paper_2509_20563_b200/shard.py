@@ -63,6 +63,37 @@ def container_offsets(sizes: np.ndarray) -> np.ndarray:
     return out
 
 
+def container_head(sizes) -> bytes:
+    """FZB1 header + offset table for archives of these sizes (the body follows)."""
+    sizes = np.asarray(sizes, np.int64)
+    offs = np.append(container_offsets(sizes), sizes.sum())
+    return MAGIC + struct.pack("<I", sizes.size) + offs.astype("<u8").tobytes()
+
+
+def rank_slice(sizes, rg: range) -> tuple:
+    """(start, length) of the container-body bytes that rank's fields `rg` own:
+    contiguous fields -> one contiguous slice, written with no coordination."""
+    sizes = np.asarray(sizes, np.int64)
+    start = int(container_offsets(sizes)[rg.start]) if len(rg) else int(sizes[: rg.start].sum())
+    return start, int(sizes[rg.start:rg.stop].sum())
+
+
+def fill_slice(out: np.ndarray, sizes, rg: range, blobs) -> np.ndarray:
+    """Write this rank's archives (fields `rg`, in order) into `out`, its slice
+    of the container body, at their offsets relative to the slice start."""
+    sizes = np.asarray(sizes, np.int64)
+    offs = container_offsets(sizes)
+    start, length = rank_slice(sizes, rg)
+    if out.size < length:
+        raise ValueError("slice buffer too small")
+    for f, blob in zip(rg, blobs):
+        if len(blob) != sizes[f]:
+            raise ValueError(f"field {f}: archive size {len(blob)} != gathered size {sizes[f]}")
+        o = int(offs[f]) - start
+        out[o:o + len(blob)] = np.frombuffer(blob, np.uint8)
+    return out[:length]
+
+
 def pack_container(archives: list) -> bytes:
     sizes = np.array([len(a) for a in archives], np.int64)
     offs = np.append(container_offsets(sizes), sizes.sum())

@@ -67,3 +67,47 @@ def test_container_round_trip():
     assert shard.unpack_container(blob) == arcs
     with pytest.raises(Exception):
         shard.unpack_container(blob[:-1])
+
+
+def _c5_worker(rank, world, port, nfields, q):
+    """The C5 host path of bench.py with the oracle as the per-field codec:
+    shard -> compress the rank's fields -> all-gather sizes -> offsets ->
+    write the rank's container slice -> gather slices -> rank 0 assembles."""
+    import torch.distributed as dist
+    from oracle import fzoracle as O
+    from paper_2509_20563_b200.data import smooth_trig_host
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dims = (8, 20, 24)
+    rg = shard.shard_range(nfields, world, rank)
+    blobs = [O.compress(smooth_trig_host(dims, f), dims, 1, 1e-3, "default") for f in rg]
+    sizes = shard.gather_sizes([len(b) for b in blobs], nfields, world, rank)
+    start, length = shard.rank_slice(sizes, rg)
+    part = shard.fill_slice(np.zeros(length, np.uint8), sizes, rg, blobs)
+    parts = [None] * world
+    dist.all_gather_object(parts, (start, part.tobytes()))
+    if rank == 0:
+        body = b"".join(p for _, p in sorted(parts))
+        q.put(shard.container_head(sizes) + body)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nfields", [7, 2])
+def test_gloo_c5_container_assembly(nfields, oracle):
+    from paper_2509_20563_b200.data import smooth_trig_host
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_c5_worker, args=(r, 2, port, nfields, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    blob = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    dims = (8, 20, 24)
+    want = [oracle.compress(smooth_trig_host(dims, f), dims, 1, 1e-3, "default") for f in range(nfields)]
+    assert blob == shard.pack_container(want)
+    assert shard.unpack_container(blob) == want
