@@ -21,6 +21,7 @@
 // look-back latency.  The decoder runs the same network backwards.
 #include "common.cuh"
 #include "scan.cuh"
+#include "lookback.cuh"
 
 namespace {
 
@@ -29,14 +30,9 @@ constexpr int BS_WARPS = BS_THREADS / 32;
 constexpr int BS_BPW = 4;                         // blocks per warp
 constexpr int BS_BPC = BS_WARPS * BS_BPW;         // blocks per CTA (32 -> 8192 codes)
 
-// decoupled look-back state per CTA: bits 62-63 flag (1 aggregate, 2 inclusive prefix), 0-61 value
-constexpr unsigned long long LB_AGG = 1ull << 62, LB_PRE = 2ull << 62, LB_VAL = (1ull << 62) - 1;
-
-FZB_DEV unsigned long long ld_volatile64(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
+using fzlb::LB_AGG;
+using fzlb::LB_PRE;
+using fzlb::lookback;
 
 FZB_DEV uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     uint32_t r;
@@ -155,129 +151,6 @@ FZB_DEV uint4 load_codes(const uint16_t* __restrict__ codes, uint64_t n, uint64_
     return make_uint4(c[0] | (c[1] << 16), c[2] | (c[3] << 16), c[4] | (c[5] << 16), c[6] | (c[7] << 16));
 }
 
-// CTA-wide exclusive prefix of `agg` by decoupled look-back (CTA ids from a
-// ticket, so every predecessor is resident or done).  Called by warp 0.
-FZB_DEV unsigned long long lookback(uint32_t cta, unsigned long long agg, unsigned long long* state) {
-    const int lane = threadIdx.x & 31;
-    unsigned long long excl = 0;
-    if (cta == 0) {
-        if (lane == 0) {
-            __threadfence();
-            atomicExch(state, LB_PRE | agg);
-        }
-        return 0;
-    }
-    long long base = (long long)cta - 1;
-    while (true) {
-        const long long p = base - lane;
-        unsigned long long v = LB_PRE;   // lanes before CTA 0 act as prefix 0
-        if (p >= 0) {
-            do { v = ld_volatile64(state + p); } while ((v >> 62) == 0);
-        }
-        const unsigned pre = __ballot_sync(0xffffffffu, (v >> 62) == 2);
-        const int stop = pre ? __ffs(pre) - 1 : 32;
-        unsigned long long add = (lane <= stop && p >= 0) ? (v & LB_VAL) : 0ull;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
-        excl += add;
-        if (pre) break;
-        base -= 32;
-    }
-    if (lane == 0) {
-        __threadfence();
-        atomicExch(state + cta, LB_PRE | (excl + agg));
-    }
-    return excl;
-}
-
-__global__ void __launch_bounds__(BS_THREADS) bs_enc3_kernel(const uint16_t* __restrict__ codes, uint64_t n,
-                                                             uint64_t nblocks, uint32_t* __restrict__ bitmap,
-                                                             uint32_t* __restrict__ payload,
-                                                             unsigned long long* __restrict__ state,
-                                                             uint32_t* __restrict__ ticket,
-                                                             unsigned long long* __restrict__ nwords) {
-    __shared__ uint32_t s_off[BS_BPC];
-    __shared__ unsigned long long s_agg, s_excl;
-    __shared__ uint32_t s_cta;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int gw = lane >> 2, gi = lane & 3;
-    const uint32_t xsel = (uint32_t)(gi | ((1 ^ gi) << 4) | ((2 ^ gi) << 8) | ((3 ^ gi) << 12));
-    if (threadIdx.x == 0) s_cta = atomicAdd(ticket, 1u);
-    __syncthreads();
-    const uint32_t cta = s_cta;
-    const uint64_t blk0 = (uint64_t)cta * BS_BPC + warp * BS_BPW;
-
-    // ---- loads + word counts (from 16-bit ORs); the CTA aggregate is
-    //      published before the transposes so they hide the look-back
-    uint4 r[BS_BPW];
-    uint32_t gor[BS_BPW];
-#pragma unroll
-    for (int q = 0; q < BS_BPW; q++) {
-        r[q] = (blk0 + q < nblocks) ? load_codes(codes, n, blk0 + q, lane) : make_uint4(0, 0, 0, 0);
-        gor[q] = group_or(r[q]);
-        uint32_t c = __popc(gor[q]);   // counted by each of the group's 4 lanes
-#pragma unroll
-        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        if (lane == 0) s_off[warp * BS_BPW + q] = c >> 2;
-    }
-    __syncthreads();
-    if (warp == 0) {
-        const uint32_t a = s_off[lane];   // BS_BPC == 32
-        uint32_t incl = a;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        s_off[lane] = incl - a;
-        if (lane == 31) {
-            s_agg = incl;
-            if (cta != 0) {
-                __threadfence();
-                atomicExch(state + cta, LB_AGG | (unsigned long long)incl);
-            }
-        }
-    }
-    // ---- bit-matrix transposes (independent of the offsets)
-    uint32_t Wd[BS_BPW][4];
-#pragma unroll
-    for (int q = 0; q < BS_BPW; q++) {
-        uint32_t E[4];
-        codes_to_planes(r[q], E);
-        planes_to_words(E, gi, xsel, Wd[q]);
-    }
-    __syncthreads();
-    if (warp == 0) {
-        const unsigned long long agg = s_agg;
-        const unsigned long long excl = lookback(cta, agg, state);
-        if (lane == 0) {
-            s_excl = excl;
-            if ((uint64_t)(cta + 1) * BS_BPC >= nblocks) *nwords = excl + agg;
-        }
-    }
-    __syncthreads();
-    // ---- bitmap + compacted payload
-#pragma unroll
-    for (int q = 0; q < BS_BPW; q++) {
-        const uint64_t blk = blk0 + q;
-        if (blk >= nblocks) break;
-        uint32_t BM[4];
-        block_bitmap(gor[q], gw, gi, BM);
-        if (lane < 4) bitmap[blk * 4 + lane] = sel4(BM, lane);
-        const unsigned long long base = s_excl + s_off[warp * BS_BPW + q];
-        uint32_t before = 0;
-#pragma unroll
-        for (int k = 0; k < 4; k++) before += (k < gi) ? __popc(BM[k]) : 0u;
-        const uint32_t bmi = sel4(BM, gi);
-#pragma unroll
-        for (int c = 0; c < 4; c++) {
-            if ((gor[q] >> (4 * gi + c)) & 1u) {
-                const uint32_t rank = before + __popc(bmi & ((1u << (8 * c + gw)) - 1u));
-                payload[base + rank] = Wd[q][c];
-            }
-        }
-    }
-}
 
 // Persistent variant: each CTA claims chunks of BS_BPC blocks by ticket (so
 // look-back predecessors are always claimed earlier) and issues the next
@@ -533,12 +406,7 @@ FZB_API int fzb_bitshuffle_encode(const uint16_t* d_codes, uint64_t n, uint8_t* 
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bs_enc4_kernel, BS_THREADS, 0);
         grid_cap = sms * (per > 0 ? per : 1);
     }
-    const char* e = getenv("FZB_BS_ENC");
-    if (e && e[0] == '3') {
-        bs_enc3_kernel<<<(unsigned)nc, BS_THREADS, 0, st>>>(d_codes, n, nb, reinterpret_cast<uint32_t*>(d_bitmap),
-                                                           d_payload, state, ticket,
-                                                           reinterpret_cast<unsigned long long*>(d_nwords));
-    } else {
+    {
         const unsigned grid = (unsigned)(nc < (uint64_t)grid_cap ? nc : (uint64_t)grid_cap);
         bs_enc4_kernel<<<grid, BS_THREADS, 0, st>>>(d_codes, n, nb, (uint32_t)nc, reinterpret_cast<uint32_t*>(d_bitmap),
                                                     d_payload, state, ticket,

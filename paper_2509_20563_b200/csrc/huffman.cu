@@ -26,6 +26,7 @@
 //    encode.py:299-316 exactly.
 #include "common.cuh"
 #include "scan.cuh"
+#include "lookback.cuh"
 
 #include <cooperative_groups.h>
 namespace cg = cooperative_groups;
@@ -485,17 +486,43 @@ FZB_DEV void load16(const uint16_t* __restrict__ codes, uint64_t n, uint64_t bas
     }
 }
 
+// Zero-code fast path: 16 codes that are all R (the common case at loose
+// bounds) contribute 16 copies of R's codeword; when that fits 64 bits it is
+// precomputed once (left-aligned in `pat`) and emitted with <= 3 word writes.
+FZB_DEV bool all_r(const uint32_t (&c)[HE_PER], uint32_t R) {
+    bool a = true;
+#pragma unroll
+    for (int e = 0; e < HE_PER; e++) a &= (c[e] == R);
+    return a;
+}
+FZB_DEV unsigned long long run_pattern(uint32_t cw, uint32_t len) {
+    unsigned long long p = 0;
+    if (len == 0 || len * HE_PER > 64) return 0;
+#pragma unroll
+    for (int i = 0; i < HE_PER; i++) p |= (unsigned long long)cw << (64 - (int)len * (i + 1));
+    return p;
+}
+
 __global__ void __launch_bounds__(HE_THREADS) hf_count_kernel(const uint16_t* __restrict__ codes, uint64_t n,
                                                               const uint8_t* __restrict__ lengths, uint32_t nsym,
-                                                              uint32_t* __restrict__ cta_bits) {
+                                                              uint32_t* __restrict__ cta_bits,
+                                                              uint8_t* __restrict__ all_r_chunk) {
     __shared__ unsigned long long tmp[33];
     const uint64_t base = ((uint64_t)blockIdx.x * HE_THREADS + threadIdx.x) * HE_PER;
     uint32_t c[HE_PER];
     load16(codes, n, base, c);
+    const uint32_t R = nsym >> 1;
     unsigned long long b = 0;
+    const bool ar = all_r(c, R);
+    if (__syncthreads_and(ar) && threadIdx.x == 0) all_r_chunk[blockIdx.x] = 1;
+    else if (threadIdx.x == 0) all_r_chunk[blockIdx.x] = 0;
+    if (ar) {
+        b = (unsigned long long)HE_PER * __ldg(lengths + R);
+    } else {
 #pragma unroll
-    for (int e = 0; e < HE_PER; e++)
-        if (c[e] < nsym) b += __ldg(lengths + c[e]);
+        for (int e = 0; e < HE_PER; e++)
+            if (c[e] < nsym) b += __ldg(lengths + c[e]);
+    }
     unsigned long long tot;
     block_exclusive_scan64(b, tmp, &tot);
     if (threadIdx.x == 0) cta_bits[blockIdx.x] = (uint32_t)tot;   // <= 32 * HE_CHUNK
@@ -533,34 +560,64 @@ __global__ void __launch_bounds__(HE_THREADS) hf_write2_kernel(const uint16_t* _
                                                                const unsigned long long* __restrict__ lc,
                                                                uint32_t nsym,
                                                                const unsigned long long* __restrict__ cta_off,
+                                                               const uint8_t* __restrict__ all_r_chunk,
                                                                uint32_t* __restrict__ out, uint64_t cap_words) {
     __shared__ unsigned long long tmp[33];
     __shared__ uint32_t buf[HE_WORDS + 1];
     const uint64_t base = ((uint64_t)blockIdx.x * HE_THREADS + threadIdx.x) * HE_PER;
     const unsigned long long G = __ldg(cta_off + blockIdx.x);   // issued early: read after the packing
+    const uint32_t R = nsym >> 1;
+    const unsigned long long vr = __ldg(lc + R);
+    const uint32_t lr = (uint32_t)vr & 0xFFu;
+    const unsigned long long pat = run_pattern((uint32_t)(vr >> 32), lr);
+    // a chunk the count pass saw as all R (and whose run fits the pattern):
+    // its bits are known without reading the codes again
+    const bool runs = lr != 0 && lr * HE_PER <= 64;   // R's run of HE_PER codewords fits `pat`
+    const bool chunk_r = runs && all_r_chunk[blockIdx.x];
     uint32_t c[HE_PER];
-    load16(codes, n, base, c);
+    bool fast = chunk_r;
+    if (!chunk_r) {
+        load16(codes, n, base, c);
+        fast = runs && all_r(c, R);
+    }
     uint32_t len[HE_PER], cwv[HE_PER];
     unsigned long long b = 0;
+    if (fast) {
+        b = (unsigned long long)HE_PER * lr;
+    } else {
 #pragma unroll
-    for (int e = 0; e < HE_PER; e++) {
-        len[e] = 0; cwv[e] = 0;
-        if (c[e] < nsym) {   // one 8-byte lookup: codeword << 32 | length
-            const unsigned long long v = __ldg(lc + c[e]);
-            len[e] = (uint32_t)v & 0xFFu;
-            cwv[e] = (uint32_t)(v >> 32);
+        for (int e = 0; e < HE_PER; e++) {
+            len[e] = 0; cwv[e] = 0;
+            if (c[e] < nsym) {   // one 8-byte lookup: codeword << 32 | length
+                const unsigned long long v = __ldg(lc + c[e]);
+                len[e] = (uint32_t)v & 0xFFu;
+                cwv[e] = (uint32_t)(v >> 32);
+            }
+            b += len[e];
         }
-        b += len[e];
     }
-    unsigned long long total;
-    const unsigned long long o = block_exclusive_scan64(b, tmp, &total);   // CTA-local bit offset (syncs)
+    unsigned long long total, o;
+    if (chunk_r) {   // uniform over the CTA: no scan needed
+        o = (unsigned long long)threadIdx.x * b;
+        total = (unsigned long long)HE_THREADS * b;
+    } else {
+        o = block_exclusive_scan64(b, tmp, &total);   // CTA-local bit offset (syncs)
+    }
     // clear only the words this CTA's bits occupy (low-entropy streams use a
     // small fraction of the worst-case buffer)
     for (uint32_t q = threadIdx.x; q <= (uint32_t)((total + 31) >> 5) && q <= (uint32_t)HE_WORDS; q += HE_THREADS)
         buf[q] = 0;
     __syncthreads();
     // pack this thread's bits into the shared buffer (bit 0 of the CTA = MSB of buf[0])
-    if (b) {
+    if (fast) {   // b <= 64 bits of the run pattern, starting at bit o: <= 3 words
+        const int f = (int)(o & 31);
+        const uint32_t w = (uint32_t)(o >> 5);
+        const unsigned long long hi = pat >> f;
+        const uint32_t lo = f ? (uint32_t)(pat << (64 - f) >> 32) : 0u;
+        atomicOr(buf + w, (uint32_t)(hi >> 32));
+        if (f + (int)b > 32) atomicOr(buf + w + 1, (uint32_t)hi);
+        if (f + (int)b > 64) atomicOr(buf + w + 2, lo);
+    } else if (b) {
         uint32_t w = (uint32_t)(o >> 5);
         int filled = (int)(o & 31);
         unsigned long long acc = 0;
@@ -1166,7 +1223,7 @@ FZB_API int fzb_huffman_build(const uint64_t* d_bins, uint32_t nsym, uint8_t* d_
 
 FZB_API size_t fzb_huffman_encode_workspace_bytes(uint64_t n) {
     const uint64_t nc = (n + HE_CHUNK - 1) / HE_CHUNK;
-    return 256 + 2 * align256(nc * 8) + align256(fzscan::ws_bytes(nc)) + align256(65536 * 8) + 256;
+    return 256 + 2 * align256(nc * 8) + align256(fzscan::ws_bytes(nc)) + align256(65536 * 8) + align256(nc) + 256;
 }
 
 FZB_API int fzb_huffman_encode(const uint16_t* d_codes, uint64_t n, const uint8_t* d_lengths,
@@ -1185,16 +1242,18 @@ FZB_API int fzb_huffman_encode(const uint16_t* d_codes, uint64_t n, const uint8_
     void* scan_ws = w + 256 + 2 * align256(nc * 8);
     unsigned long long* lc = reinterpret_cast<unsigned long long*>(w + 256 + 2 * align256(nc * 8) +
                                                                    align256(fzscan::ws_bytes(nc)));
+    uint8_t* all_r_chunk = w + 256 + 2 * align256(nc * 8) + align256(fzscan::ws_bytes(nc)) + align256(65536 * 8);
     const uint64_t cap_words = out_cap / 4;
     uint32_t* out = reinterpret_cast<uint32_t*>(d_out);
     const unsigned long long* want = reinterpret_cast<const unsigned long long*>(d_bit_count);
     hf_count_kernel<<<(unsigned)nc, HE_THREADS, 0, st>>>(d_codes, n, d_lengths, nsym,
-                                                        reinterpret_cast<uint32_t*>(cta_bits));
+                                                        reinterpret_cast<uint32_t*>(cta_bits), all_r_chunk);
     fzscan::exclusive(reinterpret_cast<uint32_t*>(cta_bits), nc, cta_off, tot, scan_ws, st);
     hf_check_kernel<<<1, 1, 0, st>>>(tot, want, d_status);
     hf_zero_kernel<<<kNumSMs * 4, 256, 0, st>>>(out, tot, cap_words);
     hf_pack_table_kernel<<<(nsym + 255) / 256, 256, 0, st>>>(d_lengths, d_codewords, nsym, lc);
-    hf_write2_kernel<<<(unsigned)nc, HE_THREADS, 0, st>>>(d_codes, n, lc, nsym, cta_off, out, cap_words);
+    hf_write2_kernel<<<(unsigned)nc, HE_THREADS, 0, st>>>(d_codes, n, lc, nsym, cta_off, all_r_chunk, out,
+                                                         cap_words);
     return fzb_check_launch();
 }
 

@@ -565,48 +565,63 @@ constexpr long long PF_CHUNK = 16;     // blocks per prefetch chunk (64 KB of x)
 __global__ void lz1d_summary2_kernel(const float* __restrict__ x, long long n, uint16_t* __restrict__ codes,
                                      int radius, float* __restrict__ bmin, float* __restrict__ bmax,
                                      float* __restrict__ gmin, float* __restrict__ gmax, long long nblk) {
-    // one warp per 1K block; lane l owns group l = elements [32 l, 32 l + 32)
+    // one warp per 1K block.  Row e = elements [128 e, 128 e + 128): lane l
+    // loads float4 (128 e + 4 l) -- one coalesced 512-byte access per row --
+    // so group g = 4 e + l / 8 is lanes 8(g & 3) .. +7 of row e (3 xor shuffles)
     const int lane = threadIdx.x & 31;
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
     const uint32_t rr = (uint32_t)radius | ((uint32_t)radius << 16);
+    const bool vec = !((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(codes)) & 15);
     for (long long blk = warp; blk < nblk; blk += nw) {
-        const long long g0 = blk * BS1 + 32 * lane;
-        float lo = INFINITY, hi = -INFINITY;
-        if (g0 + 32 <= n && !((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(codes)) & 15)) {
-            const float4* p = reinterpret_cast<const float4*>(x + g0);
-            float4 q[8];
+        const long long b0 = blk * BS1;
+        float4 q[8];
+        if (vec && b0 + BS1 <= n) {
 #pragma unroll
-            for (int e = 0; e < 8; e++) q[e] = __ldcs(p + e);
+            for (int e = 0; e < 8; e++) q[e] = __ldg(reinterpret_cast<const float4*>(x + b0) + e * 32 + lane);
+#pragma unroll
+            for (int e = 0; e < 4; e++)   // 1024 codes = 128 x 16 bytes
+                reinterpret_cast<uint4*>(codes + b0)[e * 32 + lane] = make_uint4(rr, rr, rr, rr);
+        } else {
 #pragma unroll
             for (int e = 0; e < 8; e++) {
-                lo = fminf(lo, fminf(fminf(q[e].x, q[e].y), fminf(q[e].z, q[e].w)));
-                hi = fmaxf(hi, fmaxf(fmaxf(q[e].x, q[e].y), fmaxf(q[e].z, q[e].w)));
-            }
-            uint4* c = reinterpret_cast<uint4*>(codes + g0);   // codes are 64-byte aligned per group
+                float v[4];
 #pragma unroll
-            for (int e = 0; e < 4; e++) c[e] = make_uint4(rr, rr, rr, rr);
-        } else {
-            for (int e = 0; e < 32; e++) {
-                const long long t = g0 + e;
-                if (t < n) {
-                    const float v = x[t];
-                    lo = fminf(lo, v);
-                    hi = fmaxf(hi, v);
-                    codes[t] = (uint16_t)radius;
+                for (int c = 0; c < 4; c++) {
+                    const long long t = b0 + 128 * e + 4 * lane + c;
+                    v[c] = t < n ? x[t] : NAN;
+                    if (t < n) codes[t] = (uint16_t)radius;
                 }
+                q[e] = make_float4(v[0], v[1], v[2], v[3]);
             }
         }
-        gmin[blk * 32 + lane] = lo;
-        gmax[blk * 32 + lane] = hi;
+        float blo = INFINITY, bhi = -INFINITY;
 #pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        for (int e = 0; e < 8; e++) {
+            // fminf/fmaxf drop the NaN padding of a partial block
+            float lo = fminf(fminf(q[e].x, q[e].y), fminf(q[e].z, q[e].w));
+            float hi = fmaxf(fmaxf(q[e].x, q[e].y), fmaxf(q[e].z, q[e].w));
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+                hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+            }
+            if ((lane & 7) == 0) {
+                const long long g = blk * 32 + 4 * e + (lane >> 3);
+                gmin[g] = isnan(lo) ? INFINITY : lo;   // an all-padding group stays empty
+                gmax[g] = isnan(hi) ? -INFINITY : hi;
+            }
+            blo = fminf(blo, lo);
+            bhi = fmaxf(bhi, hi);
+        }
+#pragma unroll
+        for (int o = 8; o < 32; o <<= 1) {
+            blo = fminf(blo, __shfl_xor_sync(0xffffffffu, blo, o));
+            bhi = fmaxf(bhi, __shfl_xor_sync(0xffffffffu, bhi, o));
         }
         if (lane == 0) {
-            bmin[blk] = lo;
-            bmax[blk] = hi;
+            bmin[blk] = isnan(blo) ? INFINITY : blo;
+            bmax[blk] = isnan(bhi) ? -INFINITY : bhi;
         }
     }
 }
@@ -995,6 +1010,7 @@ __global__ void lz1d_event_compact_kernel(const uint16_t* __restrict__ codes, co
     const int lane = threadIdx.x & 31;
     const long long ch = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (ch >= nch) return;
+    if (offs[ch + 1] == offs[ch]) return;   // no event in this chunk (sparse data: most chunks): no reload
     const long long base = ch * EVC + lane * 32;
     uint32_t m = event_mask(codes, bitmap, n, base, radius);
     uint32_t c = __popc(m), inc = c;
@@ -1056,6 +1072,58 @@ __global__ void lz1d_event_chain_kernel(const long long* __restrict__ evpos, con
     }
 }
 
+// Chain v2: one warp per segment (event 0 or an outlier, up to the next
+// outlier).  The warp gathers 32 events at a time (positions, flags, codes,
+// pre-scattered outlier values) and precomputes every 2eb*(code - R) in
+// parallel; only the reconstruction itself stays serial: per event
+// rec = RN32(RN64(0.0 + r) + c) -- one f32->f64 convert, two adds, one
+// convert back -- with the inputs broadcast by shuffles that do not depend
+// on r.  (v1: one thread per segment, ~180 cycles per event on long segments.)
+__global__ void __launch_bounds__(128) lz1d_chain2_kernel(const long long* __restrict__ evpos,
+                                                          const unsigned long long* __restrict__ nev_p,
+                                                          const uint16_t* __restrict__ codes,
+                                                          const uint32_t* __restrict__ bitmap,
+                                                          float* __restrict__ recon, const double* __restrict__ d_eb,
+                                                          int radius) {
+    const unsigned long long nev = *nev_p;
+    const int lane = threadIdx.x & 31;
+    const unsigned long long w0 = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nw = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    const QParams P = make_qparams(*d_eb, radius);
+    for (unsigned long long e = w0; e < nev; e += nw) {
+        const long long p0 = evpos[e];
+        const bool o0 = (__ldg(bitmap + (p0 >> 5)) >> (p0 & 31)) & 1u;
+        if (!(e == 0 || o0)) continue;   // warp-uniform: not a segment head
+        float r = 0.f;                   // state entering event 0 (every earlier element has code R)
+        for (unsigned long long b = e;; b += 32) {
+            const unsigned long long k = b + lane;
+            const bool valid = k < nev;
+            const long long pos = valid ? evpos[k] : 0;
+            const bool isout = valid && ((__ldg(bitmap + (pos >> 5)) >> (pos & 31)) & 1u);
+            const int code = valid ? (int)codes[pos] : radius;
+            const double c = __dmul_rn(P.two_eb, (double)(code - radius));
+            const float ov = isout ? recon[pos] : 0.f;
+            const unsigned stop = __ballot_sync(0xffffffffu, (isout && k != e) || !valid);
+            const int lim = stop ? __ffs(stop) - 1 : 32;
+            // RN64(0.0 + r) + c == RN64(r + c) for every c (the 0.0 + only turns -0 into +0,
+            // which no sum can tell apart), so one add per event
+            float mine = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; j++) {
+                const double cj = __shfl_sync(0xffffffffu, c, j);
+                const bool oj = __shfl_sync(0xffffffffu, isout, j);
+                const float ovj = __shfl_sync(0xffffffffu, ov, j);
+                if (j < lim) {
+                    r = oj ? ovj : __double2float_rn(__dadd_rn((double)r, cj));
+                    if (lane == j) mine = r;
+                }
+            }
+            if (lane < lim && !isout) recon[pos] = mine;
+            if (lim < 32) break;
+        }
+    }
+}
+
 __global__ void lz1d_fill_kernel(const uint16_t* __restrict__ codes, const uint32_t* __restrict__ bitmap, long long n,
                                  int radius, const unsigned long long* __restrict__ offs,
                                  const long long* __restrict__ evpos, float* __restrict__ recon, long long nch) {
@@ -1089,6 +1157,59 @@ __global__ void lz1d_fill_kernel(const uint16_t* __restrict__ codes, const uint3
         const uint32_t upto = mj & (0xFFFFFFFFu >> (31 - lane));   // events at positions <= lane
         const long long src = upto ? gb + 31 - __clz(upto) : cj;
         if (gb + lane < n && !((mj >> lane) & 1u)) recon[gb + lane] = src >= 0 ? recon[src] + 0.0f : 0.f;
+    }
+}
+
+// Fill without re-reading the codes: a chunk's events are evpos[offs[ch] ..
+// offs[ch+1]) (sorted); they set bits of a 1024-bit shared bitmap, and every
+// other element takes f32(0.0 + r) of the last event at or before it (the
+// chain pass wrote the event values into recon), -0 -> +0.  Traffic: the
+// 4n-byte recon write plus the (few) event positions and values.
+__global__ void __launch_bounds__(256) lz1d_fill2_kernel(const long long* __restrict__ evpos,
+                                                          const unsigned long long* __restrict__ offs,
+                                                          float* __restrict__ recon, long long n, long long nch) {
+    __shared__ uint32_t s_bm[8][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const long long ch = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (ch >= nch) return;
+    const long long base0 = ch * EVC;
+    const unsigned long long lo = offs[ch], hi = offs[ch + 1];
+    if (lo == hi && base0 + EVC <= n && !(reinterpret_cast<uintptr_t>(recon) & 15)) {
+        // no event in the chunk (most chunks of sparse data): one value, 16-byte stores
+        const float v = lo > 0 ? recon[evpos[lo - 1]] + 0.0f : 0.f;
+        const float4 q = make_float4(v, v, v, v);
+#pragma unroll
+        for (int e = 0; e < 8; e++) reinterpret_cast<float4*>(recon + base0)[e * 32 + lane] = q;
+        return;
+    }
+    uint32_t* bm = s_bm[wib];
+    bm[lane] = 0;
+    __syncwarp();
+    for (unsigned long long e = lo + lane; e < hi; e += 32) {
+        const int o = (int)(evpos[e] - base0);
+        atomicOr(bm + (o >> 5), 1u << (o & 31));
+    }
+    __syncwarp();
+    const uint32_t mw = bm[lane];   // lane j: events of row j
+    // last event strictly before row j: max over rows < j, else the previous chunk's last event
+    long long last = mw ? base0 + 32 * lane + 31 - __clz(mw) : -1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, last, o);
+        if (lane >= o) last = max(last, y);
+    }
+    long long carry = __shfl_up_sync(0xffffffffu, last, 1);
+    if (lane == 0 || carry < 0) carry = (lane == 0 || carry < 0) ? (lo > 0 ? evpos[lo - 1] : -1) : carry;
+    const float cval = carry >= 0 ? recon[carry] + 0.0f : 0.f;   // lane j: value entering row j
+    for (int j = 0; j < 32; j++) {
+        const long long gb = base0 + 32 * (long long)j;
+        if (gb >= n) break;
+        const uint32_t mj = __shfl_sync(0xffffffffu, mw, j);
+        const float cj = __shfl_sync(0xffffffffu, cval, j);
+        if (gb + lane < n && !((mj >> lane) & 1u)) {
+            const uint32_t upto = mj & (0xFFFFFFFFu >> (31 - lane));   // events at positions <= lane
+            recon[gb + lane] = upto ? recon[gb + 31 - __clz(upto)] + 0.0f : cj;
+        }
     }
 }
 
@@ -1284,7 +1405,7 @@ FZB_API size_t fzb_lorenzo_workspace_bytes(uint32_t n0, uint32_t n1, uint32_t n2
     if (n0 == 1 && n1 == 1) {
         const long long nblk = (n + BS1 - 1) / BS1, nsb = (nblk + 31) / 32, nch = (n + EVC - 1) / EVC;
         const size_t enc = Walk1D(n).total;
-        const size_t dec = WS_HDR + 1024 + (size_t)nch * 4 + (size_t)nch * 8 + fzscan::ws_bytes(nch) + 256 + (size_t)n * 8;
+        const size_t dec = WS_HDR + 2048 + (size_t)(nch + 1) * 12 + fzscan::ws_bytes(nch + 1) + (size_t)n * 8;
         return enc > dec ? enc : dec;
     }
     size_t w4;
@@ -1373,17 +1494,20 @@ FZB_API int fzb_lorenzo_decode_f32(const uint16_t* d_codes, const uint32_t* d_bi
         invalidate_faces(d_ws, st);
         unsigned char* w = static_cast<unsigned char*>(d_ws) + WS_HDR;
         auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+        // counts / offsets carry one extra entry (0 / the total) so offs[ch + 1] is always valid
         unsigned long long* nev = reinterpret_cast<unsigned long long*>(w);
         uint32_t* counts = reinterpret_cast<uint32_t*>(w + 256);
-        unsigned long long* offs = reinterpret_cast<unsigned long long*>(w + 256 + al(nch * 4));
-        void* sws = w + 256 + al(nch * 4) + al(nch * 8);
-        long long* evpos = reinterpret_cast<long long*>(w + 256 + al(nch * 4) + al(nch * 8) + al(fzscan::ws_bytes(nch)));
+        unsigned long long* offs = reinterpret_cast<unsigned long long*>(w + 256 + al((nch + 1) * 4));
+        void* sws = w + 256 + al((nch + 1) * 4) + al((nch + 1) * 8);
+        long long* evpos = reinterpret_cast<long long*>(w + 256 + al((nch + 1) * 4) + al((nch + 1) * 8) +
+                                                        al(fzscan::ws_bytes(nch + 1)));
         const unsigned blocks = (unsigned)((nch * 32 + 255) / 256);
+        cudaMemsetAsync(counts + nch, 0, 4, st);
         lz1d_event_count_kernel<<<blocks, 256, 0, st>>>(d_codes, d_bitmap, n, (int)radius, counts, nch);
-        fzscan::exclusive(counts, nch, offs, nev, sws, st);
+        fzscan::exclusive(counts, nch + 1, offs, nev, sws, st);
         lz1d_event_compact_kernel<<<blocks, 256, 0, st>>>(d_codes, d_bitmap, n, (int)radius, offs, evpos, nch);
-        lz1d_event_chain_kernel<<<kNumSMs * 4, 128, 0, st>>>(evpos, nev, d_codes, d_bitmap, d_recon, d_eb, (int)radius);
-        lz1d_fill_kernel<<<blocks, 256, 0, st>>>(d_codes, d_bitmap, n, (int)radius, offs, evpos, d_recon, nch);
+        lz1d_chain2_kernel<<<kNumSMs * 8, 128, 0, st>>>(evpos, nev, d_codes, d_bitmap, d_recon, d_eb, (int)radius);
+        lz1d_fill2_kernel<<<blocks, 256, 0, st>>>(evpos, offs, d_recon, n, nch);
         return fzb_check_launch();
     }
     if (!use_v4(n2))
