@@ -791,7 +791,11 @@ __global__ void __launch_bounds__(64) lz1d_walk3_kernel(const float* __restrict_
     }
     __syncthreads();
     if (warp == 1) return;
-    const QParams P = make_qparams(*d_eb, radius);
+    // the bound goes through an opaque move: otherwise ptxas rematerialises
+    // P's fields by re-loading *d_eb on the event chain (twice per event)
+    double ebr;
+    asm volatile("mov.f64 %0, %1;" : "=d"(ebr) : "d"(*d_eb));
+    const QParams P = make_qparams(ebr, radius);
 #ifdef LZ7_TIMING
     long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long c0 = clock64();
