@@ -649,7 +649,8 @@ def main():
     ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-parity", action="store_true", help="skip the parity check (outside the timed region)")
-    ap.add_argument("--pipeline", choices=["speed", "default", "quality"], help="override the workload's preset")
+    ap.add_argument("--pipeline", choices=["speed", "default", "quality", "dq-speed", "dq-default"],
+                    help="override the workload's preset (dq-*: the opt-in dual-quant pipelines 3/4)")
     ap.add_argument("--rel", type=float, help="override the workload's relative error bound")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:

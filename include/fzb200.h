@@ -149,6 +149,25 @@ FZB_API int fzb_bitshuffle_decode(const uint8_t *d_bitmap, const uint32_t *d_pay
 /* ---- utilities ----------------------------------------------------------- */
 FZB_API int fzb_fill_u16(uint16_t *d_dst, uint64_t n, uint16_t value, void *stream);
 
+/* ---- opt-in dual-quant Lorenzo (pipeline ids 3/4; no reference counterpart:
+ * north_star items 1 and 4).  p = rint(x / 2eb) with |x / 2eb| < 2^27 (else
+ * status bit 15), deltas = integer Lorenzo difference of p (zero padding),
+ * codes = delta + R or R for an outlier (|delta| >= R or |RN32(2eb p) - x| > eb,
+ * flag set in d_bitmap).  Decode = prefix sums along k, j, i. */
+FZB_API int fzb_dualquant_encode_f32(const float *d_in, uint32_t n0, uint32_t n1, uint32_t n2, const double *d_eb,
+                                     uint32_t radius, uint16_t *d_codes, uint32_t *d_bitmap, uint32_t *d_status,
+                                     void *stream);
+/* deltas of the *d_k compacted outliers (fzb_outlier_compact indices) */
+FZB_API int fzb_dualquant_outlier_deltas(const float *d_in, uint32_t n0, uint32_t n1, uint32_t n2,
+                                         const uint64_t *d_idx, const uint64_t *d_k, const double *d_eb,
+                                         uint32_t radius, int32_t *d_deltas, uint32_t *d_status, void *stream);
+FZB_API size_t fzb_dualquant_decode_workspace_bytes(uint32_t n0, uint32_t n1, uint32_t n2);
+/* codes + k outliers (indices, deltas, values) -> d_out; d_bitmap zeroed by the caller */
+FZB_API int fzb_dualquant_decode_f32(const uint16_t *d_codes, const uint64_t *d_idx, const int32_t *d_deltas,
+                                     const float *d_vals, uint64_t k, uint32_t n0, uint32_t n1, uint32_t n2,
+                                     const double *d_eb, uint32_t radius, uint32_t *d_bitmap, float *d_out,
+                                     void *d_ws, size_t ws_bytes, uint32_t *d_status, void *stream);
+
 /* ---- verification: metrics.quality (metrics.py:49-75) bit-identical ------ */
 /* Sums the leaves of numpy's pairwise-sum tree of d*d (d = f64(orig) -
  * f64(recon)); d_leaf_len <= 128.  d_red[0] = bits of max|d|, d_red[1] /

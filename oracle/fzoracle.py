@@ -29,10 +29,14 @@ MAGIC = b"FZM1"
 _HDR = struct.Struct("<4s4Bd2f3IIB")  # core.py:56 (41 bytes)
 _SEG = struct.Struct("<BQ")  # core.py:57
 SEG_HF_BOOK, SEG_HF_STREAM, SEG_OUT_IDX, SEG_OUT_VAL, SEG_BS_MAP, SEG_BS_PAY, SEG_ANCHOR = range(7)
+SEG_DQ_DELTAS = 8   # opt-in dual-quant pipelines only (this repo's own format, not the reference's)
 
-# preset table, pipeline.py:200-214: id -> (predictor, codec)
-PRESETS = {0: ("lorenzo", "huffman"), 1: ("lorenzo", "bitshuffle"), 2: ("interp", "huffman")}
-PRESET_NAMES = {"default": 0, "speed": 1, "quality": 2}
+# preset table, pipeline.py:200-214: id -> (predictor, codec); ids 3/4 are the
+# opt-in dual-quant pipelines of this repo (no reference counterpart; checked
+# against dq_quantize / dq_reconstruct below, a numpy statement of their spec)
+PRESETS = {0: ("lorenzo", "huffman"), 1: ("lorenzo", "bitshuffle"), 2: ("interp", "huffman"),
+           3: ("dualquant", "bitshuffle"), 4: ("dualquant", "huffman")}
+PRESET_NAMES = {"default": 0, "speed": 1, "quality": 2, "dq-speed": 3, "dq-default": 4}
 CUBIC = (-1 / 16, 9 / 16, 9 / 16, -1 / 16)  # predict.py:47
 
 
@@ -202,6 +206,42 @@ def interp_reconstruct(codes, idx, vals, anchors: bytes, dims, eb: float, radius
 
 # ------------------------------------------------------------------ codecs
 
+# ------------------------------------------------- dual-quant (opt-in ids 3/4)
+# Spec (paper_2509_20563_b200/csrc/dualquant.cu): p = rint(x * RN(1/2eb)) in f64
+# (|.| < 2^27), delta = Lorenzo difference of p with zero padding, code =
+# delta + R when |delta| < R and |RN32(2eb p) - x| <= eb, else an outlier
+# (code R; the archive keeps index, original value and delta).
+
+DQ_PMAX = 2.0 ** 27
+
+
+def dq_quantize(data: np.ndarray, dims, eb: float, radius: int = 512):
+    """-> (codes u32, outlier idx i64, values f32, deltas i32)."""
+    x = np.ascontiguousarray(data, np.float32).reshape(pad3(dims))
+    inv2eb = 1.0 / (2.0 * eb)
+    q = x.astype(np.float64) * inv2eb
+    if not (np.abs(q) < DQ_PMAX).all():
+        raise OracleError("DualQuantRange")
+    p = np.rint(q).astype(np.int64)
+    pp = np.pad(p, ((1, 0), (1, 0), (1, 0)))
+    d = (pp[1:, 1:, 1:] - pp[1:, :-1, 1:] - pp[1:, 1:, :-1] + pp[1:, :-1, :-1]
+         - pp[:-1, 1:, 1:] + pp[:-1, :-1, 1:] + pp[:-1, 1:, :-1] - pp[:-1, :-1, :-1])
+    rec = (2.0 * eb * p.astype(np.float64)).astype(np.float32)
+    ok = (np.abs(d) < radius) & (np.abs(rec.astype(np.float64) - x.astype(np.float64)) <= eb)
+    codes = np.where(ok, d + radius, radius).astype(np.uint32).reshape(-1)
+    idx = np.flatnonzero(~ok.reshape(-1)).astype(np.int64)
+    return codes, idx, x.reshape(-1)[idx].copy(), d.reshape(-1)[idx].astype(np.int32)
+
+
+def dq_reconstruct(codes, idx, vals, deltas, dims, eb: float, radius: int = 512) -> np.ndarray:
+    d = codes.astype(np.int64) - radius
+    d[idx] = deltas
+    p = d.reshape(pad3(dims)).cumsum(axis=2).cumsum(axis=1).cumsum(axis=0)
+    rec = (2.0 * eb * p.astype(np.float64)).astype(np.float32).reshape(-1)
+    rec[idx] = vals
+    return rec
+
+
 def histogram(codes, radius: int) -> np.ndarray:
     """encode.py:79-84 (and topk 87-111, bitwise identical)."""
     codes = np.ascontiguousarray(codes, np.uint32)
@@ -369,12 +409,18 @@ def compress(data: np.ndarray, dims, eb_mode: int, magnitude: float, pipeline,
     if lo == hi:
         return serialize(pid, eb_mode, magnitude, lo, hi, dims, radius, [])
     eb = resolve_eb(eb_mode, magnitude, lo, hi)
+    deltas = None
     if predictor == "interp":
         codes, idx, vals, _, anchors = interp_quantize(data, dims, eb, radius, anchor_stride)
+    elif predictor == "dualquant":
+        codes, idx, vals, deltas = dq_quantize(data, dims, eb, radius)
+        anchors = b""
     else:
         codes, idx, vals, _ = lorenzo_quantize(data, dims, eb, radius)
         anchors = b""
     segs = [(SEG_OUT_IDX, idx.astype("<u8").tobytes()), (SEG_OUT_VAL, vals.astype("<f4").tobytes())]
+    if deltas is not None:
+        segs.append((SEG_DQ_DELTAS, deltas.astype("<i4").tobytes()))
     if anchors:
         segs.append((SEG_ANCHOR, anchors))
     if codec == "huffman":
@@ -426,7 +472,12 @@ def decompress(archive: bytes, anchor_stride: int = 16):
     if idx.size and not (codes[idx] == radius).all():
         raise OracleError("MalformedCodes")
     anchors = segs.get(SEG_ANCHOR, b"")
-    if predictor == "interp":
+    if predictor == "dualquant":
+        db = segs.get(SEG_DQ_DELTAS)
+        if db is None or len(db) != 4 * idx.size:
+            raise OracleError("CorruptPayload")
+        rec = dq_reconstruct(codes, idx, vals, np.frombuffer(db, "<i4"), dims, eb, radius)
+    elif predictor == "interp":
         rec = interp_reconstruct(codes, idx, vals, anchors, dims, eb, radius, anchor_stride)
     else:
         rec = lorenzo_reconstruct(codes, idx, vals, dims, eb, radius)

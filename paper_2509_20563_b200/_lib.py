@@ -30,6 +30,7 @@ ERR_OUTLIER_CODE = 1 << 11
 ERR_HF_MISMATCH = 1 << 12
 ERR_HF_SYNC = 1 << 13
 ERR_BS_MISMATCH = 1 << 14
+ERR_DQ_RANGE = 1 << 15
 
 # (bit, exception factory), in the order the reference would raise them
 CODEC_ERRORS = [
@@ -99,6 +100,10 @@ def load():
         "fzb_bitshuffle_encode": (I, [P, U64, P, P, P, P, SZ, P]),
         "fzb_bitshuffle_decode": (I, [P, P, U64, U64, U32, P, P, SZ, P, P]),
         "fzb_fill_u16": (I, [P, U64, ctypes.c_uint16, P]),
+        "fzb_dualquant_encode_f32": (I, [P, U32, U32, U32, P, U32, P, P, P, P]),
+        "fzb_dualquant_outlier_deltas": (I, [P, U32, U32, U32, P, P, P, U32, P, P, P]),
+        "fzb_dualquant_decode_workspace_bytes": (SZ, [U32, U32, U32]),
+        "fzb_dualquant_decode_f32": (I, [P, P, P, P, U64, U32, U32, U32, P, U32, P, P, P, SZ, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -119,6 +124,8 @@ EXPORTED = [
     "fzb_histogram", "fzb_huffman_build_workspace_bytes", "fzb_huffman_build", "fzb_huffman_encode_workspace_bytes",
     "fzb_huffman_encode", "fzb_huffman_decode_workspace_bytes", "fzb_huffman_decode",
     "fzb_bitshuffle_workspace_bytes", "fzb_bitshuffle_encode", "fzb_bitshuffle_decode", "fzb_fill_u16",
+    "fzb_dualquant_encode_f32", "fzb_dualquant_outlier_deltas", "fzb_dualquant_decode_workspace_bytes",
+    "fzb_dualquant_decode_f32",
 ]
 
 

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 SO = os.path.join(HERE, "libfzb200.so")
-SOURCES = ["stream_ops.cu", "lorenzo.cu", "interp.cu", "bitshuffle.cu", "huffman.cu"]
+SOURCES = ["stream_ops.cu", "lorenzo.cu", "interp.cu", "bitshuffle.cu", "huffman.cu", "dualquant.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
          "-Xcompiler", "-fPIC,-fvisibility=hidden", "--expt-relaxed-constexpr", "-I", INCLUDE]

@@ -30,6 +30,7 @@ enum : uint32_t {
     FZB_ERR_HF_MISMATCH = 1u << 12,    // CorruptStream: histogram inconsistent (encode.py:289-290)
     FZB_ERR_HF_SYNC = 1u << 13,        // internal: decoder did not synchronise (retry)
     FZB_ERR_BS_MISMATCH = 1u << 14,    // BitmapPayloadMismatch: popcount != words (encode.py:372-375)
+    FZB_ERR_DQ_RANGE = 1u << 15,       // dual-quant (opt-in): |x / 2eb| >= 2^27
 };
 
 FZB_DEV void set_err(uint32_t* status, uint32_t bit) { atomicOr(status, bit); }

@@ -31,7 +31,7 @@ from . import _lib
 from . import errors as E
 from .core import HEADER as _HEADER, SEGMENT as _SEGMENT
 from .core import (
-    SEG_ANCHOR_GRID, SEG_BITSHUFFLE_BITMAP, SEG_BITSHUFFLE_PAYLOAD, SEG_HUFFMAN_BITSTREAM,
+    SEG_ANCHOR_GRID, SEG_BITSHUFFLE_BITMAP, SEG_BITSHUFFLE_PAYLOAD, SEG_DQ_DELTAS, SEG_HUFFMAN_BITSTREAM,
     SEG_HUFFMAN_CODEBOOK, SEG_OUTLIER_INDICES, SEG_OUTLIER_VALUES,
 )
 
@@ -259,7 +259,7 @@ class Engine:
             raise E.RadiusTooLarge(f"radius {radius} outside the 16-bit code range of the device path")
         n0, n1, n2 = pad3(dims)
         L, sp = self.lib, self.sp
-        if predictor not in ("lorenzo", "interp"):
+        if predictor not in ("lorenzo", "interp", "dualquant"):
             raise ValueError(f"unknown predictor '{predictor}'")
         use_anchors = predictor == "interp" and interp_applicable(dims, anchor_stride)
         if pre is None:
@@ -289,6 +289,9 @@ class Engine:
                        _p(bitmap), _p(anchors), sp, nk=1 + 3 * int(np.log2(a)))
             bufs["anchors"] = anchors
             bufs["n_anchors"] = na
+        elif predictor == "dualquant":
+            self._call("fzb_dualquant_encode_f32", _p(x), n0, n1, n2, _p(eb), radius, _p(codes), _p(bitmap),
+                       _p(status), sp)
         else:
             lzws = self.buf("lzws" + tag, L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
             self._call("fzb_lorenzo_encode_f32", _p(x), n0, n1, n2, _p(eb), radius, _p(codes), _p(bitmap),
@@ -302,6 +305,11 @@ class Engine:
         side = self._fork()
         self._call("fzb_outlier_compact", _p(bitmap), n, _p(x), _p(oidx), _p(oval), _p(ocount), _p(ocws),
                    ocws.numel(), ctypes.c_void_p(side.cuda_stream), nk=3, st=side)
+        if predictor == "dualquant":   # the outliers' deltas (the prefix-sum decode needs them)
+            odelta = self.buf("odelta" + tag, 4 * n)
+            self._call("fzb_dualquant_outlier_deltas", _p(x), n0, n1, n2, _p(oidx), _p(ocount), _p(eb), radius,
+                       _p(odelta), _p(status), ctypes.c_void_p(side.cuda_stream), st=side)
+            bufs["odelta"] = odelta
         self._mark("outliers_end", side)
         bufs.update(oidx=oidx, oval=oval, ocount=ocount)
         self._mark("predict_end")
@@ -364,11 +372,15 @@ class Engine:
         size = int(v[24:32].view(np.uint64)[0])
         if status & _lib.ERR_NONFINITE:
             raise ValueError("non-finite value in field")
+        if status & _lib.ERR_DQ_RANGE:
+            raise ValueError("dual-quant predictor: |x / 2eb| >= 2^27 (bound too tight for the value range)")
         if lo == hi:
             return lo, hi, [], None
         _lib.raise_codec_status(status)
         n = da.n
         parts = [("oidx", 8 * k), ("oval", 4 * k)]
+        if da.predictor == "dualquant":
+            parts.append(("odelta", 4 * k))
         if da.use_anchors:
             parts.append(("anchors", 4 * b["n_anchors"]))
         if da.codec == "huffman":
@@ -396,6 +408,9 @@ class Engine:
         blobs = [mv[o:o + sz] for o, sz in offs]
         segs = [(SEG_OUTLIER_INDICES, blobs[0]), (SEG_OUTLIER_VALUES, blobs[1])]
         q = 2
+        if da.predictor == "dualquant":
+            segs.append((SEG_DQ_DELTAS, blobs[q]))
+            q += 1
         if da.use_anchors:
             segs.append((SEG_ANCHOR_GRID, blobs[q]))
             q += 1
@@ -422,8 +437,9 @@ class Engine:
 
     def compressed_bytes(self, da: DeviceArchive, sz: dict) -> int:
         """Serialized archive length for these sizes (header + table + payloads)."""
-        nseg = 4 + (1 if da.use_anchors else 0)
-        body = 12 * sz["k"] + (4 * da.bufs["n_anchors"] if da.use_anchors else 0)
+        dq = da.predictor == "dualquant"
+        nseg = 4 + (1 if da.use_anchors else 0) + (1 if dq else 0)
+        body = (16 if dq else 12) * sz["k"] + (4 * da.bufs["n_anchors"] if da.use_anchors else 0)
         if da.codec == "huffman":
             body += 2 * da.radius + (sz["size"] + 7) // 8
         else:
@@ -447,7 +463,7 @@ class Engine:
             bitmap = batch["bitmap"]
         # outlier-scatter || codec decode (reference decompress graph, pipeline.py:490-580)
         side = self._fork()
-        if sz["k"]:
+        if sz["k"] and da.predictor != "dualquant":   # (the dual-quant decode scatters its own outliers)
             self._call("fzb_outlier_scatter", _p(b["oidx"]), _p(b["oval"]), sz["k"], n, None, da.radius,
                        _p(out), _p(bitmap), _p(status), ctypes.c_void_p(side.cuda_stream), st=side)
         if da.codec == "huffman":
@@ -467,7 +483,12 @@ class Engine:
             ebt[:8].view(torch.float64).fill_(eb_abs)
         if batch is not None:
             return out
-        if da.use_anchors:
+        if da.predictor == "dualquant":
+            dws = self.buf("ddqws" + tag, L.fzb_dualquant_decode_workspace_bytes(n0, n1, n2))
+            self._call("fzb_dualquant_decode_f32", _p(codes), _p(b["oidx"]), _p(b["odelta"]), _p(b["oval"]), sz["k"],
+                       n0, n1, n2, _p(ebt), da.radius, _p(bitmap), _p(out), _p(dws), dws.numel(), _p(status), sp,
+                       nk=8)
+        elif da.use_anchors:
             w = (ctypes.c_double * 4)(*CUBIC)
             self._call("fzb_interp_decode_f32", _p(codes), _p(bitmap), _p(b["anchors"]), _p(out), n0, n1, n2, _p(ebt),
                        da.radius, 16, w, sp, nk=13)
@@ -699,7 +720,7 @@ class Engine:
 
     def decompress_dag(self, codec: str, predictor: str, segs: dict, idx: np.ndarray, vals: np.ndarray,
                        anchors, dims, eb_abs: float, radius: int, anchor_stride: int = 16,
-                       stage: str | None = None) -> torch.Tensor:
+                       stage: str | None = None, deltas: np.ndarray | None = None) -> torch.Tensor:
         """The reference's four-task decompress graph (pipeline.py:490-580) on
         two streams: [side] outlier H2D + scatter (and the anchor grid H2D)
         || [main] codec H2D + decode, joined before the sentinel check and
@@ -717,11 +738,15 @@ class Engine:
         k = int(idx.size)
         side = self._fork()
         self._mark("decode-outliers", side)
+        dq = predictor == "dualquant"
         if k:
             di = self.upload("didx", np.ascontiguousarray(idx, np.uint64), st=side, stage=stage)
             dv = self.upload("dval", np.ascontiguousarray(vals, np.float32), st=side, stage=stage)
-            self._call("fzb_outlier_scatter", _p(di), _p(dv), k, n, None, radius, _p(recon), _p(bitmap), _p(status),
-                       ctypes.c_void_p(side.cuda_stream), st=side)
+            if dq:
+                dd = self.upload("ddelta", np.ascontiguousarray(deltas, np.int32), st=side, stage=stage)
+            else:
+                self._call("fzb_outlier_scatter", _p(di), _p(dv), k, n, None, radius, _p(recon), _p(bitmap),
+                           _p(status), ctypes.c_void_p(side.cuda_stream), st=side)
         use_anchors = predictor == "interp" and len(anchors)
         if use_anchors:
             danch = self.upload("danchors", anchors, st=side, stage=stage)
@@ -734,7 +759,12 @@ class Engine:
         self._mark("reconstruct")
         if k:
             self._call("fzb_outlier_check", _p(di), k, n, _p(codes), radius, _p(status), sp)
-        if use_anchors:
+        if dq:
+            dws = self.buf("ddqws", L.fzb_dualquant_decode_workspace_bytes(n0, n1, n2))
+            self._call("fzb_dualquant_decode_f32", _p(codes), _p(di) if k else None, _p(dd) if k else None,
+                       _p(dv) if k else None, k, n0, n1, n2, _p(ebt), radius, _p(bitmap), _p(recon), _p(dws),
+                       dws.numel(), _p(status), sp, nk=8)
+        elif use_anchors:
             w = (ctypes.c_double * 4)(*CUBIC)
             self._call("fzb_interp_decode_f32", _p(codes), _p(bitmap), _p(danch), _p(recon), n0, n1, n2, _p(ebt),
                        radius, anchor_stride, w, sp, nk=1 + 3 * int(np.log2(anchor_stride)))
@@ -745,7 +775,8 @@ class Engine:
         return recon
 
     def decompress_dag_graphed(self, codec: str, predictor: str, segs: dict, idx, vals, anchors, dims,
-                               eb_abs: float, radius: int, anchor_stride: int = 16) -> torch.Tensor:
+                               eb_abs: float, radius: int, anchor_stride: int = 16,
+                               deltas: np.ndarray | None = None) -> torch.Tensor:
         """decompress_dag as one CUDA-graph launch: the archive's payloads are
         copied into this shape's pinned staging buffers on the host, then the
         captured DAG (H2D nodes from those buffers, both branches, the join)
@@ -757,12 +788,12 @@ class Engine:
         key = ("dh", codec, predictor, tuple(dims), radius, anchor_stride, sizes, int(idx.size), len(anchors))
         stage = "gs%x:" % (hash(key) & 0xFFFFFFFF)
         run = lambda: self.decompress_dag(codec, predictor, segs, idx, vals, anchors, dims, eb_abs, radius,
-                                          anchor_stride, stage=stage)
+                                          anchor_stride, stage=stage, deltas=deltas)
         if key in self._graphs:   # stage this archive's payloads where the graph's H2D nodes read
-            self._stage_only(codec, segs, idx, vals, anchors, eb_abs, predictor, stage)
+            self._stage_only(codec, segs, idx, vals, anchors, eb_abs, predictor, stage, deltas)
         return self._graphed(key, run)
 
-    def _stage_only(self, codec, segs, idx, vals, anchors, eb_abs, predictor, stage):
+    def _stage_only(self, codec, segs, idx, vals, anchors, eb_abs, predictor, stage, deltas=None):
         def put(name, data):
             if isinstance(data, np.ndarray):
                 raw = np.ascontiguousarray(data).view(np.uint8).reshape(-1)
@@ -773,6 +804,8 @@ class Engine:
         if idx.size:
             put("didx", np.ascontiguousarray(idx, np.uint64))
             put("dval", np.ascontiguousarray(vals, np.float32))
+            if predictor == "dualquant":
+                put("ddelta", np.ascontiguousarray(deltas, np.int32))
         if predictor == "interp" and len(anchors):
             put("danchors", anchors)
         put("deb", np.array([eb_abs], np.float64))

@@ -24,8 +24,9 @@ import torch
 from . import errors as E
 from . import secondary
 from .core import (
-    SEG_ANCHOR_GRID, SEG_BITSHUFFLE_BITMAP, SEG_BITSHUFFLE_PAYLOAD, SEG_HUFFMAN_BITSTREAM, SEG_HUFFMAN_CODEBOOK,
-    SEG_OUTLIER_INDICES, SEG_OUTLIER_VALUES, SEG_SECONDARY_WRAPPED, Archive, ErrorBoundSpec, ErrorMode, Field,
+    SEG_ANCHOR_GRID, SEG_BITSHUFFLE_BITMAP, SEG_BITSHUFFLE_PAYLOAD, SEG_DQ_DELTAS, SEG_HUFFMAN_BITSTREAM,
+    SEG_HUFFMAN_CODEBOOK, SEG_OUTLIER_INDICES, SEG_OUTLIER_VALUES, SEG_SECONDARY_WRAPPED, Archive, ErrorBoundSpec,
+    ErrorMode, Field,
     ResolvedBound, attach_wire, eb_from_range, register_known_pipeline_id,
 )
 from .device import default_engine, graph_engine, interp_applicable
@@ -115,7 +116,7 @@ class PipelineSpec:
 
 
 _REGISTRY: dict[int, PipelineSpec] = {}
-PRESET_NAMES = {"default": 0, "speed": 1, "quality": 2}
+PRESET_NAMES = {"default": 0, "speed": 1, "quality": 2, "dq-speed": 3, "dq-default": 4}
 
 
 def register_pipeline(spec: PipelineSpec) -> PipelineSpec:
@@ -152,6 +153,13 @@ def _presets():
                                        S("encode", K.PRIMARY_CODEC, {"codec": "bitshuffle"}))))
     register_pipeline(PipelineSpec(2, (S("predict", K.PREDICT, {"predictor": "interp"}),
                                        S("histogram", K.ANALYSIS, {"method": "topk", "k": "16"}),
+                                       S("encode", K.PRIMARY_CODEC, {"codec": "huffman"}))))
+    # opt-in, this repo's own (no reference counterpart): dual-quant Lorenzo
+    # (north_star items 1 and 4; csrc/dualquant.cu), with bitshuffle / Huffman
+    register_pipeline(PipelineSpec(3, (S("predict", K.PREDICT, {"predictor": "dualquant"}),
+                                       S("encode", K.PRIMARY_CODEC, {"codec": "bitshuffle"}))))
+    register_pipeline(PipelineSpec(4, (S("predict", K.PREDICT, {"predictor": "dualquant"}),
+                                       S("histogram", K.ANALYSIS, {"method": "exact"}),
                                        S("encode", K.PRIMARY_CODEC, {"codec": "huffman"}))))
 
 
@@ -194,7 +202,7 @@ def _check_stage_params(spec: PipelineSpec):
         if st.kind == StageKind.PREPROCESS and st.param("op", "identity") != "identity":
             raise E.StageError(st.name, ValueError(f"unsupported preprocess op '{st.param('op')}'"))
     pst = spec.stage_of(StageKind.PREDICT)
-    if spec.predictor not in ("lorenzo", "interp"):
+    if spec.predictor not in ("lorenzo", "interp", "dualquant"):
         raise E.StageError(pst.name, ValueError(f"unknown predictor '{spec.predictor}'"))
     an = spec.stage_of(StageKind.ANALYSIS)
     if an is not None:
@@ -431,6 +439,12 @@ def _decompress_dev(a: Archive, pipeline=None, *, graph: bool = False, timings: 
         raise E.MalformedCodes("outlier indices not strictly increasing")
     anchors = segs.get(SEG_ANCHOR_GRID, b"")
     pred = spec.predictor
+    deltas = None
+    if pred == "dualquant":
+        db = segs.get(SEG_DQ_DELTAS)
+        if db is None or len(db) != 4 * idx.size:
+            raise E.StageError("decode-outliers", E.CorruptPayload("dual-quant delta segment missing or sized wrong"))
+        deltas = np.frombuffer(db, "<i4")
     stride = spec.interp_config().anchor_stride if pred == "interp" else 16
     if pred == "interp" and len(anchors):
         from .device import pad3
@@ -445,7 +459,8 @@ def _decompress_dev(a: Archive, pipeline=None, *, graph: bool = False, timings: 
     try:
         dag = eng.decompress_dag_graphed if graph else eng.decompress_dag
         try:
-            recon = dag(spec.primary_codec, pred, csegs, idx, vals, anchors, a.dims, bound.eb_abs, radius, stride)
+            recon = dag(spec.primary_codec, pred, csegs, idx, vals, anchors, a.dims, bound.eb_abs, radius, stride,
+                        deltas=deltas)
         except E.FZError as e:
             raise E.StageError("decode-codes", e) from e
         return eng, recon
