@@ -149,6 +149,11 @@ FZB_API int fzb_bitshuffle_decode(const uint8_t *d_bitmap, const uint32_t *d_pay
 /* ---- utilities ----------------------------------------------------------- */
 FZB_API int fzb_fill_u16(uint16_t *d_dst, uint64_t n, uint16_t value, void *stream);
 
+/* opt-in pipeline 5: sampled profiling of the G-Interp (anchor stride, weights)
+ * candidates (16|8) x (cubic, linear, natural cubic); u64 costs into d_scores[6] */
+FZB_API int fzb_interp_profile(const float *d_in, uint32_t n0, uint32_t n1, uint32_t n2, const double *d_eb,
+                               uint64_t *d_scores, void *stream);
+
 /* ---- opt-in dual-quant Lorenzo (pipeline ids 3/4; no reference counterpart:
  * north_star items 1 and 4).  p = rint(x / 2eb) with |x / 2eb| < 2^27 (else
  * status bit 15), deltas = integer Lorenzo difference of p (zero padding),

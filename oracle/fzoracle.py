@@ -30,13 +30,17 @@ _HDR = struct.Struct("<4s4Bd2f3IIB")  # core.py:56 (41 bytes)
 _SEG = struct.Struct("<BQ")  # core.py:57
 SEG_HF_BOOK, SEG_HF_STREAM, SEG_OUT_IDX, SEG_OUT_VAL, SEG_BS_MAP, SEG_BS_PAY, SEG_ANCHOR = range(7)
 SEG_DQ_DELTAS = 8   # opt-in dual-quant pipelines only (this repo's own format, not the reference's)
+SEG_INTERP_PROFILE = 9   # opt-in profiled G-Interp (pipeline 5): [anchor stride, weights id]
 
 # preset table, pipeline.py:200-214: id -> (predictor, codec); ids 3/4 are the
 # opt-in dual-quant pipelines of this repo (no reference counterpart; checked
 # against dq_quantize / dq_reconstruct below, a numpy statement of their spec)
 PRESETS = {0: ("lorenzo", "huffman"), 1: ("lorenzo", "bitshuffle"), 2: ("interp", "huffman"),
-           3: ("dualquant", "bitshuffle"), 4: ("dualquant", "huffman")}
-PRESET_NAMES = {"default": 0, "speed": 1, "quality": 2, "dq-speed": 3, "dq-default": 4}
+           3: ("dualquant", "bitshuffle"), 4: ("dualquant", "huffman"), 5: ("interp-profiled", "huffman")}
+PRESET_NAMES = {"default": 0, "speed": 1, "quality": 2, "dq-speed": 3, "dq-default": 4, "q-profiled": 5}
+# profiled G-Interp candidates (csrc/interp.cu interp_profile_kernel): c = 3 s + w
+PROFILE_STRIDES = (16, 8)
+PROFILE_WEIGHTS = ((-0.0625, 0.5625, 0.5625, -0.0625), (0.0, 0.5, 0.5, 0.0), (-0.075, 0.575, 0.575, -0.075))
 CUBIC = (-1 / 16, 9 / 16, 9 / 16, -1 / 16)  # predict.py:47
 
 
@@ -160,7 +164,7 @@ def interp_applicable(dims, anchor_stride: int = 16) -> bool:
     return all(d >= anchor_stride + 1 for d in dims)
 
 
-def interp_quantize(data, dims, eb: float, radius: int = 512, anchor_stride: int = 16):
+def interp_quantize(data, dims, eb: float, radius: int = 512, anchor_stride: int = 16, weights=CUBIC):
     """predict.py:270-306 -> (codes, idx, vals, recon, anchor bytes)."""
     data = np.ascontiguousarray(data, np.float32).reshape(-1)
     if not interp_applicable(dims, anchor_stride):
@@ -173,7 +177,7 @@ def interp_quantize(data, dims, eb: float, radius: int = 512, anchor_stride: int
     flags = np.zeros(data.size, np.uint8)
     anchors = np.ascontiguousarray(data.reshape(n0, n1, n2)[::a, ::a, ::a])
     recon.reshape(n0, n1, n2)[::a, ::a, ::a] = anchors
-    w = np.array(CUBIC, np.float64)
+    w = np.array(weights, np.float64)
     lib().fzo_interp_run(_p(data), _p(codes), _p(recon), _p(flags), n0, n1, n2, float(eb),
                          int(radius), a, _p(w), 1)
     idx = np.nonzero(flags)[0].astype(np.int64)
@@ -181,7 +185,7 @@ def interp_quantize(data, dims, eb: float, radius: int = 512, anchor_stride: int
 
 
 def interp_reconstruct(codes, idx, vals, anchors: bytes, dims, eb: float, radius: int = 512,
-                       anchor_stride: int = 16) -> np.ndarray:
+                       anchor_stride: int = 16, weights=CUBIC) -> np.ndarray:
     """predict.py:322-344."""
     if len(anchors) == 0:
         return lorenzo_reconstruct(codes, idx, vals, dims, eb, radius)
@@ -197,7 +201,7 @@ def interp_reconstruct(codes, idx, vals, anchors: bytes, dims, eb: float, radius
     recon[idx] = vals
     flags[idx] = 1
     recon.reshape(n0, n1, n2)[::a, ::a, ::a] = np.frombuffer(anchors, "<f4").reshape(adims)
-    w = np.array(CUBIC, np.float64)
+    w = np.array(weights, np.float64)
     empty = np.zeros(1, np.float32)
     lib().fzo_interp_run(_p(empty), _p(codes), _p(recon), _p(flags), n0, n1, n2, float(eb),
                          int(radius), a, _p(w), 0)
@@ -240,6 +244,68 @@ def dq_reconstruct(codes, idx, vals, deltas, dims, eb: float, radius: int = 512)
     rec = (2.0 * eb * p.astype(np.float64)).astype(np.float32).reshape(-1)
     rec[idx] = vals
     return rec
+
+
+def interp_profile(data: np.ndarray, dims, eb: float) -> np.ndarray:
+    """Sampled cost of the 6 (anchor stride, weights) candidates of pipeline 5
+    (spec: csrc/interp.cu interp_profile_kernel) -> u64[6]."""
+    n0, n1, n2 = pad3(dims)
+    x = np.ascontiguousarray(data, np.float32).reshape(n0, n1, n2)
+    inv2eb = 1.0 / (2.0 * eb)
+    axes = [np.arange(n) for n in (n0, n1, n2)]
+    sel = [a[((a >> 4) & 3) == 0] for a in axes]           # 16-cells whose cell coordinate is a multiple of 4
+    I, J, K = np.meshgrid(*sel, indexing="ij")
+    co = [I.reshape(-1), J.reshape(-1), K.reshape(-1)]
+    xv = x[co[0], co[1], co[2]].astype(np.float64)
+
+    def lowbit(c):
+        c = c.astype(np.int64)
+        out = np.full(c.shape, 62, np.int64)
+        nz = c != 0
+        out[nz] = np.log2(c[nz] & -c[nz]).astype(np.int64)
+        return out
+
+    lb = [lowbit(c) for c in co]
+    m = np.minimum(lb[0], np.minimum(lb[1], lb[2]))
+    ext = (n0, n1, n2)
+    flat = x.reshape(-1)
+    strides = (n1 * n2, n2, 1)
+    t = (co[0] * n1 + co[1]) * n2 + co[2]
+    scores = np.zeros(6, np.uint64)
+    for s, A in enumerate(PROFILE_STRIDES):
+        anchor = m >= int(np.log2(A))
+        for wi in range(3):
+            scores[3 * s + wi] += np.uint64(32 * int(anchor.sum()))
+        tgt = ~anchor
+        h = (1 << m[tgt]).astype(np.int64)
+        ax = np.where(lb[2][tgt] == m[tgt], 2, np.where(lb[1][tgt] == m[tgt], 1, 0))
+        c = np.choose(ax, [co[0][tgt], co[1][tgt], co[2][tgt]])
+        n = np.choose(ax, list(ext))
+        sh = h * np.choose(ax, list(strides))
+        tt = t[tgt]
+        cub = (c - 3 * h >= 0) & (c + 3 * h < n)
+        lin = ~cub & (c + h < n)
+        get = lambda off, ok: np.where(ok, flat[np.where(ok, tt + off, 0)], 0).astype(np.float64)
+        for wi, W in enumerate(PROFILE_WEIGHTS):
+            pc = W[0] * get(-3 * sh, cub)
+            pc = pc + W[1] * get(-sh, cub)
+            pc = pc + W[2] * get(sh, cub)
+            pc = pc + W[3] * get(3 * sh, cub)
+            pl = 0.5 * get(-sh, lin) + 0.5 * get(sh, lin)
+            pcp = flat[tt - sh].astype(np.float64)
+            pred = np.where(cub, pc, np.where(lin, pl, pcp))
+            e = np.minimum(np.abs(pred - xv[tgt]) * inv2eb, 1073741824.0)
+            iv = np.rint(e).astype(np.uint64)
+            bits = np.zeros(iv.shape, np.uint64)
+            nz = iv > 0
+            bits[nz] = np.floor(np.log2(iv[nz].astype(np.float64))).astype(np.uint64) + 1
+            scores[3 * s + wi] += np.uint64(int(bits.sum()))
+    return scores
+
+
+def profile_choice(scores) -> tuple:
+    c = int(np.argmin(np.asarray(scores, np.uint64)))   # ties: the lowest index
+    return PROFILE_STRIDES[c // 3], c % 3
 
 
 def histogram(codes, radius: int) -> np.ndarray:
@@ -410,8 +476,15 @@ def compress(data: np.ndarray, dims, eb_mode: int, magnitude: float, pipeline,
         return serialize(pid, eb_mode, magnitude, lo, hi, dims, radius, [])
     eb = resolve_eb(eb_mode, magnitude, lo, hi)
     deltas = None
+    prof = None
+    if predictor == "interp-profiled" and not interp_applicable(dims, 16):
+        predictor = "interp"   # (the reference's 1D / small-extent fallback to Lorenzo, no profile)
     if predictor == "interp":
         codes, idx, vals, _, anchors = interp_quantize(data, dims, eb, radius, anchor_stride)
+    elif predictor == "interp-profiled":
+        stride, wi = profile_choice(interp_profile(data, dims, eb))
+        prof = bytes([stride, wi])
+        codes, idx, vals, _, anchors = interp_quantize(data, dims, eb, radius, stride, PROFILE_WEIGHTS[wi])
     elif predictor == "dualquant":
         codes, idx, vals, deltas = dq_quantize(data, dims, eb, radius)
         anchors = b""
@@ -421,6 +494,8 @@ def compress(data: np.ndarray, dims, eb_mode: int, magnitude: float, pipeline,
     segs = [(SEG_OUT_IDX, idx.astype("<u8").tobytes()), (SEG_OUT_VAL, vals.astype("<f4").tobytes())]
     if deltas is not None:
         segs.append((SEG_DQ_DELTAS, deltas.astype("<i4").tobytes()))
+    if prof is not None:
+        segs.append((SEG_INTERP_PROFILE, prof))
     if anchors:
         segs.append((SEG_ANCHOR, anchors))
     if codec == "huffman":
@@ -477,8 +552,14 @@ def decompress(archive: bytes, anchor_stride: int = 16):
         if db is None or len(db) != 4 * idx.size:
             raise OracleError("CorruptPayload")
         rec = dq_reconstruct(codes, idx, vals, np.frombuffer(db, "<i4"), dims, eb, radius)
-    elif predictor == "interp":
-        rec = interp_reconstruct(codes, idx, vals, anchors, dims, eb, radius, anchor_stride)
+    elif predictor in ("interp", "interp-profiled"):
+        pb = segs.get(SEG_INTERP_PROFILE)
+        if predictor == "interp-profiled" and pb is not None:
+            if len(pb) != 2 or pb[0] not in PROFILE_STRIDES or pb[1] > 2:
+                raise OracleError("CorruptPayload")
+            rec = interp_reconstruct(codes, idx, vals, anchors, dims, eb, radius, pb[0], PROFILE_WEIGHTS[pb[1]])
+        else:
+            rec = interp_reconstruct(codes, idx, vals, anchors, dims, eb, radius, anchor_stride)
     else:
         rec = lorenzo_reconstruct(codes, idx, vals, dims, eb, radius)
     return dims, rec

@@ -100,6 +100,7 @@ def load():
         "fzb_bitshuffle_encode": (I, [P, U64, P, P, P, P, SZ, P]),
         "fzb_bitshuffle_decode": (I, [P, P, U64, U64, U32, P, P, SZ, P, P]),
         "fzb_fill_u16": (I, [P, U64, ctypes.c_uint16, P]),
+        "fzb_interp_profile": (I, [P, U32, U32, U32, P, P, P]),
         "fzb_dualquant_encode_f32": (I, [P, U32, U32, U32, P, U32, P, P, P, P]),
         "fzb_dualquant_outlier_deltas": (I, [P, U32, U32, U32, P, P, P, U32, P, P, P]),
         "fzb_dualquant_decode_workspace_bytes": (SZ, [U32, U32, U32]),
@@ -124,7 +125,7 @@ EXPORTED = [
     "fzb_histogram", "fzb_huffman_build_workspace_bytes", "fzb_huffman_build", "fzb_huffman_encode_workspace_bytes",
     "fzb_huffman_encode", "fzb_huffman_decode_workspace_bytes", "fzb_huffman_decode",
     "fzb_bitshuffle_workspace_bytes", "fzb_bitshuffle_encode", "fzb_bitshuffle_decode", "fzb_fill_u16",
-    "fzb_dualquant_encode_f32", "fzb_dualquant_outlier_deltas", "fzb_dualquant_decode_workspace_bytes",
+    "fzb_interp_profile", "fzb_dualquant_encode_f32", "fzb_dualquant_outlier_deltas", "fzb_dualquant_decode_workspace_bytes",
     "fzb_dualquant_decode_f32",
 ]
 

@@ -160,6 +160,84 @@ int run_passes(const float* orig, uint16_t* codes, float* recon, uint32_t* bitma
     return fzb_check_launch();
 }
 
+// ---- sampled profiling (opt-in pipeline 5, cuSZ-i / QoZ style) ----------
+// Candidates c = 3 s + w: anchor stride 16 (s = 0) or 8 (s = 1) x weights
+// cubic (-1, 9, 9, -1)/16, linear (0, 1, 1, 0)/2, natural cubic
+// (-3, 23, 23, -3)/40.  Sample = every point of the 16-cells whose cell
+// coordinates are multiples of 4 (1/64 of a 3D field); each is an anchor of
+// the candidate's lattice (32 bits) or the target of exactly one pass (level
+// h = lowest set bit of its coordinates, axis = the last axis with that bit)
+// and costs bitlen(rint(|pred - x| / 2eb)) with pred from ORIGINAL values
+// and the reference's cubic / linear / copy boundary rules.  Integer sums:
+// order-independent, so the CPU spec (oracle) reproduces the choice exactly.
+__constant__ double kProfW[3][4] = {{-0.0625, 0.5625, 0.5625, -0.0625},
+                                    {0.0, 0.5, 0.5, 0.0},
+                                    {-0.075, 0.575, 0.575, -0.075}};
+
+FZB_DEV int lowbit_of(long long c) { return c == 0 ? 62 : __ffsll(c) - 1; }
+
+__global__ void __launch_bounds__(256) interp_profile_kernel(const float* __restrict__ x, long long n0, long long n1,
+                                                              long long n2, const double* __restrict__ d_eb,
+                                                              unsigned long long* __restrict__ scores) {
+    const double inv2eb = __drcp_rn(__dmul_rn(2.0, *d_eb));
+    const long long C0 = (n0 + 15) / 16, C1 = (n1 + 15) / 16, C2 = (n2 + 15) / 16;
+    const long long S0 = (C0 + 3) / 4, S1 = (C1 + 3) / 4, S2 = (C2 + 3) / 4;
+    const long long total = S0 * S1 * S2 * 4096;
+    unsigned long long acc[6] = {0, 0, 0, 0, 0, 0};
+    const long long ext[3] = {n0, n1, n2};
+    const long long str[3] = {n1 * n2, n2, 1};
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+         q += (long long)gridDim.x * blockDim.x) {
+        const int u = (int)(q & 15), v = (int)((q >> 4) & 15), ww = (int)((q >> 8) & 15);
+        const long long cell = q >> 12;
+        const long long c2 = cell % S2, c1 = (cell / S2) % S1, c0 = cell / (S1 * S2);
+        const long long co[3] = {64 * c0 + ww, 64 * c1 + v, 64 * c2 + u};
+        if (co[0] >= n0 || co[1] >= n1 || co[2] >= n2) continue;
+        const long long t = (co[0] * n1 + co[1]) * n2 + co[2];
+        const double xv = (double)__ldg(x + t);
+        const int lb[3] = {lowbit_of(co[0]), lowbit_of(co[1]), lowbit_of(co[2])};
+        const int m = min(lb[0], min(lb[1], lb[2]));
+#pragma unroll
+        for (int s = 0; s < 2; s++) {
+            const int A = s == 0 ? 16 : 8;
+            if (m >= (s == 0 ? 4 : 3)) {   // an anchor of this lattice
+#pragma unroll
+                for (int wi = 0; wi < 3; wi++) acc[3 * s + wi] += 32;
+                continue;
+            }
+            const long long h = 1ll << m;
+            const int ax = lb[2] == m ? 2 : (lb[1] == m ? 1 : 0);
+            const long long c = co[ax], n = ext[ax], sh = h * str[ax];
+#pragma unroll
+            for (int wi = 0; wi < 3; wi++) {
+                double pred;
+                if (c - 3 * h >= 0 && c + 3 * h < n) {
+                    pred = __dmul_rn(kProfW[wi][0], (double)__ldg(x + t - 3 * sh));
+                    pred = __dadd_rn(pred, __dmul_rn(kProfW[wi][1], (double)__ldg(x + t - sh)));
+                    pred = __dadd_rn(pred, __dmul_rn(kProfW[wi][2], (double)__ldg(x + t + sh)));
+                    pred = __dadd_rn(pred, __dmul_rn(kProfW[wi][3], (double)__ldg(x + t + 3 * sh)));
+                } else if (c + h < n) {
+                    pred = __dadd_rn(__dmul_rn(0.5, (double)__ldg(x + t - sh)), __dmul_rn(0.5, (double)__ldg(x + t + sh)));
+                } else {
+                    pred = (double)__ldg(x + t - sh);
+                }
+                double e = __dmul_rn(fabs(__dsub_rn(pred, xv)), inv2eb);
+                e = e < 1073741824.0 ? e : 1073741824.0;
+                const unsigned int iv = (unsigned int)rint(e);
+                acc[3 * s + wi] += iv ? (unsigned long long)(32 - __clz(iv)) : 0ull;
+            }
+            (void)A;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 6; c++) {
+        unsigned long long v = acc[c];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(scores + c, v);
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -192,6 +270,17 @@ FZB_API int fzb_interp_decode_f32(const uint16_t* d_codes, const uint32_t* d_bit
     anchor_kernel<true><<<kNumSMs * 2, 256, 0, st>>>(nullptr, const_cast<float*>(d_anchors), d_recon, n1, n2, a, A0, A1, A2);
     return run_passes<true>(nullptr, const_cast<uint16_t*>(d_codes), d_recon, const_cast<uint32_t*>(d_bitmap), n0, n1,
                             n2, d_eb, radius, anchor_stride, h_weights4, st);
+}
+
+// Sampled profiling scores of the 6 (anchor stride, weights) candidates of
+// pipeline 5 into d_scores (u64[6], zeroed here).
+FZB_API int fzb_interp_profile(const float* d_in, uint32_t n0, uint32_t n1, uint32_t n2, const double* d_eb,
+                               uint64_t* d_scores, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaMemsetAsync(d_scores, 0, 6 * 8, st);
+    interp_profile_kernel<<<kNumSMs * 4, 256, 0, st>>>(d_in, n0, n1, n2, d_eb,
+                                                      reinterpret_cast<unsigned long long*>(d_scores));
+    return fzb_check_launch();
 }
 
 }  // extern "C"

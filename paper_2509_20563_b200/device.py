@@ -32,12 +32,15 @@ from . import errors as E
 from .core import HEADER as _HEADER, SEGMENT as _SEGMENT
 from .core import (
     SEG_ANCHOR_GRID, SEG_BITSHUFFLE_BITMAP, SEG_BITSHUFFLE_PAYLOAD, SEG_DQ_DELTAS, SEG_HUFFMAN_BITSTREAM,
-    SEG_HUFFMAN_CODEBOOK, SEG_OUTLIER_INDICES, SEG_OUTLIER_VALUES,
+    SEG_HUFFMAN_CODEBOOK, SEG_INTERP_PROFILE, SEG_OUTLIER_INDICES, SEG_OUTLIER_VALUES,
 )
 
 HEADER_SIZE, SEGMENT_SIZE = _HEADER.size, _SEGMENT.size
 
 CUBIC = (-1 / 16, 9 / 16, 9 / 16, -1 / 16)  # reference predict.py:47
+# opt-in profiled G-Interp (pipeline 5): candidates c = 3 s + w (csrc/interp.cu interp_profile_kernel)
+PROFILE_STRIDES = (16, 8)
+PROFILE_WEIGHTS = ((-0.0625, 0.5625, 0.5625, -0.0625), (0.0, 0.5, 0.5, 0.0), (-0.075, 0.575, 0.575, -0.075))
 
 
 def pad3(dims):
@@ -242,7 +245,8 @@ class Engine:
     # ----------------------------------------------------------- compress
     def compress(self, x: torch.Tensor, dims, eb_mode: int, magnitude: float, *, pipeline_id: int = 0,
                  predictor: str = "lorenzo", codec: str = "huffman", radius: int = 512,
-                 anchor_stride: int = 16, tag: str = "", pre: dict | None = None) -> DeviceArchive:
+                 anchor_stride: int = 16, tag: str = "", pre: dict | None = None,
+                 profile: bool = False) -> DeviceArchive:
         """Enqueue the whole compression of a device-resident f32 field.
 
         `tag` suffixes every cached buffer (several fields alive at once);
@@ -279,12 +283,23 @@ class Engine:
         if pre is not None:
             pass
         elif use_anchors:
+            weights = CUBIC
+            if profile:   # opt-in pipeline 5: sampled choice of (anchor stride, weights); one small sync
+                sc = self.buf("profile" + tag, 64)
+                self._call("fzb_interp_profile", _p(x), n0, n1, n2, _p(eb), _p(sc), sp)
+                hs = self.pinned("profile_h", 64)[:48]
+                with torch.cuda.stream(self.stream):
+                    hs.copy_(sc[:48], non_blocking=True)
+                self._sync()
+                c = int(np.argmin(hs.numpy().view(np.uint64)))
+                anchor_stride, weights = PROFILE_STRIDES[c // 3], PROFILE_WEIGHTS[c % 3]
+                bufs["profile"] = bytes([anchor_stride, c % 3])
             self._call("fzb_fill_u16", _p(codes), n, radius, sp)
             recon = self.buf("recon_ws" + tag, 4 * n)
             a = anchor_stride
             na = ((n0 - 1) // a + 1) * ((n1 - 1) // a + 1) * ((n2 - 1) // a + 1)
             anchors = self.buf("anchors" + tag, 4 * na)
-            w = (ctypes.c_double * 4)(*CUBIC)
+            w = (ctypes.c_double * 4)(*weights)
             self._call("fzb_interp_encode_f32", _p(x), n0, n1, n2, _p(eb), radius, a, w, _p(codes), _p(recon),
                        _p(bitmap), _p(anchors), sp, nk=1 + 3 * int(np.log2(a)))
             bufs["anchors"] = anchors
@@ -411,6 +426,8 @@ class Engine:
         if da.predictor == "dualquant":
             segs.append((SEG_DQ_DELTAS, blobs[q]))
             q += 1
+        if "profile" in b:
+            segs.append((SEG_INTERP_PROFILE, memoryview(b["profile"]).toreadonly()))
         if da.use_anchors:
             segs.append((SEG_ANCHOR_GRID, blobs[q]))
             q += 1
@@ -438,8 +455,9 @@ class Engine:
     def compressed_bytes(self, da: DeviceArchive, sz: dict) -> int:
         """Serialized archive length for these sizes (header + table + payloads)."""
         dq = da.predictor == "dualquant"
-        nseg = 4 + (1 if da.use_anchors else 0) + (1 if dq else 0)
-        body = (16 if dq else 12) * sz["k"] + (4 * da.bufs["n_anchors"] if da.use_anchors else 0)
+        pr = "profile" in da.bufs
+        nseg = 4 + (1 if da.use_anchors else 0) + (1 if dq else 0) + (1 if pr else 0)
+        body = (16 if dq else 12) * sz["k"] + (4 * da.bufs["n_anchors"] if da.use_anchors else 0) + (2 if pr else 0)
         if da.codec == "huffman":
             body += 2 * da.radius + (sz["size"] + 7) // 8
         else:
@@ -489,9 +507,11 @@ class Engine:
                        n0, n1, n2, _p(ebt), da.radius, _p(bitmap), _p(out), _p(dws), dws.numel(), _p(status), sp,
                        nk=8)
         elif da.use_anchors:
-            w = (ctypes.c_double * 4)(*CUBIC)
+            pf = b.get("profile")
+            stride, weights = (pf[0], PROFILE_WEIGHTS[pf[1]]) if pf else (16, CUBIC)
+            w = (ctypes.c_double * 4)(*weights)
             self._call("fzb_interp_decode_f32", _p(codes), _p(bitmap), _p(b["anchors"]), _p(out), n0, n1, n2, _p(ebt),
-                       da.radius, 16, w, sp, nk=13)
+                       da.radius, stride, w, sp, nk=1 + 3 * int(np.log2(stride)))
         else:
             lzws = self.buf("dlzws" + tag, L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
             self._call("fzb_lorenzo_decode_f32", _p(codes), _p(bitmap), _p(out), n0, n1, n2, _p(ebt), da.radius,
@@ -720,7 +740,8 @@ class Engine:
 
     def decompress_dag(self, codec: str, predictor: str, segs: dict, idx: np.ndarray, vals: np.ndarray,
                        anchors, dims, eb_abs: float, radius: int, anchor_stride: int = 16,
-                       stage: str | None = None, deltas: np.ndarray | None = None) -> torch.Tensor:
+                       stage: str | None = None, deltas: np.ndarray | None = None,
+                       weights=CUBIC) -> torch.Tensor:
         """The reference's four-task decompress graph (pipeline.py:490-580) on
         two streams: [side] outlier H2D + scatter (and the anchor grid H2D)
         || [main] codec H2D + decode, joined before the sentinel check and
@@ -765,7 +786,7 @@ class Engine:
                        _p(dv) if k else None, k, n0, n1, n2, _p(ebt), radius, _p(bitmap), _p(recon), _p(dws),
                        dws.numel(), _p(status), sp, nk=8)
         elif use_anchors:
-            w = (ctypes.c_double * 4)(*CUBIC)
+            w = (ctypes.c_double * 4)(*weights)
             self._call("fzb_interp_decode_f32", _p(codes), _p(bitmap), _p(danch), _p(recon), n0, n1, n2, _p(ebt),
                        radius, anchor_stride, w, sp, nk=1 + 3 * int(np.log2(anchor_stride)))
         else:
@@ -776,7 +797,7 @@ class Engine:
 
     def decompress_dag_graphed(self, codec: str, predictor: str, segs: dict, idx, vals, anchors, dims,
                                eb_abs: float, radius: int, anchor_stride: int = 16,
-                               deltas: np.ndarray | None = None) -> torch.Tensor:
+                               deltas: np.ndarray | None = None, weights=CUBIC) -> torch.Tensor:
         """decompress_dag as one CUDA-graph launch: the archive's payloads are
         copied into this shape's pinned staging buffers on the host, then the
         captured DAG (H2D nodes from those buffers, both branches, the join)
@@ -785,10 +806,11 @@ class Engine:
             sizes = (len(segs["codebook"]) if hasattr(segs["codebook"], "__len__") else 0, len(segs["stream"]))
         else:
             sizes = (len(segs["bitmap"]), len(segs["payload"]))
-        key = ("dh", codec, predictor, tuple(dims), radius, anchor_stride, sizes, int(idx.size), len(anchors))
+        key = ("dh", codec, predictor, tuple(dims), radius, anchor_stride, tuple(weights), sizes, int(idx.size),
+               len(anchors))
         stage = "gs%x:" % (hash(key) & 0xFFFFFFFF)
         run = lambda: self.decompress_dag(codec, predictor, segs, idx, vals, anchors, dims, eb_abs, radius,
-                                          anchor_stride, stage=stage, deltas=deltas)
+                                          anchor_stride, stage=stage, deltas=deltas, weights=weights)
         if key in self._graphs:   # stage this archive's payloads where the graph's H2D nodes read
             self._stage_only(codec, segs, idx, vals, anchors, eb_abs, predictor, stage, deltas)
         return self._graphed(key, run)

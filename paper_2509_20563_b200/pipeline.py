@@ -25,7 +25,7 @@ from . import errors as E
 from . import secondary
 from .core import (
     SEG_ANCHOR_GRID, SEG_BITSHUFFLE_BITMAP, SEG_BITSHUFFLE_PAYLOAD, SEG_DQ_DELTAS, SEG_HUFFMAN_BITSTREAM,
-    SEG_HUFFMAN_CODEBOOK, SEG_OUTLIER_INDICES, SEG_OUTLIER_VALUES, SEG_SECONDARY_WRAPPED, Archive, ErrorBoundSpec,
+    SEG_HUFFMAN_CODEBOOK, SEG_INTERP_PROFILE, SEG_OUTLIER_INDICES, SEG_OUTLIER_VALUES, SEG_SECONDARY_WRAPPED, Archive, ErrorBoundSpec,
     ErrorMode, Field,
     ResolvedBound, attach_wire, eb_from_range, register_known_pipeline_id,
 )
@@ -116,7 +116,7 @@ class PipelineSpec:
 
 
 _REGISTRY: dict[int, PipelineSpec] = {}
-PRESET_NAMES = {"default": 0, "speed": 1, "quality": 2, "dq-speed": 3, "dq-default": 4}
+PRESET_NAMES = {"default": 0, "speed": 1, "quality": 2, "dq-speed": 3, "dq-default": 4, "q-profiled": 5}
 
 
 def register_pipeline(spec: PipelineSpec) -> PipelineSpec:
@@ -160,6 +160,12 @@ def _presets():
                                        S("encode", K.PRIMARY_CODEC, {"codec": "bitshuffle"}))))
     register_pipeline(PipelineSpec(4, (S("predict", K.PREDICT, {"predictor": "dualquant"}),
                                        S("histogram", K.ANALYSIS, {"method": "exact"}),
+                                       S("encode", K.PRIMARY_CODEC, {"codec": "huffman"}))))
+    # opt-in: G-Interp whose anchor stride (16 | 8) and interpolation weights
+    # (cubic | linear | natural cubic) are chosen per field by sampled
+    # profiling (cuSZ-i / QoZ; north_star item 2; csrc/interp.cu)
+    register_pipeline(PipelineSpec(5, (S("predict", K.PREDICT, {"predictor": "interp", "profile": "1"}),
+                                       S("histogram", K.ANALYSIS, {"method": "topk", "k": "16"}),
                                        S("encode", K.PRIMARY_CODEC, {"codec": "huffman"}))))
 
 
@@ -250,12 +256,16 @@ def compress_device(x: torch.Tensor, dims, eb: ErrorBoundSpec, pipeline, *, grap
     if pred == "interp" and not interp_applicable(dims, cfg.anchor_stride):
         log.warning("interpolation needs a 2D or 3D field with every extent >= %d, got dims %s; "
                     "falling back to Lorenzo", cfg.anchor_stride + 1, tuple(dims))
+    prof = pred == "interp" and spec.stage_of(StageKind.PREDICT).param("profile", "0") == "1"
+    if prof and graph:   # the profiled choice is a host decision mid-DAG: run eagerly
+        eng, graph = default_engine(), False
     run = eng.compress_graphed if graph else eng.compress
     if timings is not None and not graph:
         eng.marks = {}
     try:
+        kwx = dict(profile=True) if prof else {}
         da = run(x, dims, int(eb.mode), float(eb.magnitude), pipeline_id=spec.id, predictor=pred,
-                 codec=spec.primary_codec, radius=spec.radius(), anchor_stride=cfg.anchor_stride if cfg else 16)
+                 codec=spec.primary_codec, radius=spec.radius(), anchor_stride=cfg.anchor_stride if cfg else 16, **kwx)
         return _archive_of(eng, da, spec, eb, dims, timings)
     finally:
         eng.marks = None
@@ -446,6 +456,13 @@ def _decompress_dev(a: Archive, pipeline=None, *, graph: bool = False, timings: 
             raise E.StageError("decode-outliers", E.CorruptPayload("dual-quant delta segment missing or sized wrong"))
         deltas = np.frombuffer(db, "<i4")
     stride = spec.interp_config().anchor_stride if pred == "interp" else 16
+    weights = None
+    pb = segs.get(SEG_INTERP_PROFILE)
+    if pred == "interp" and pb is not None:   # opt-in pipeline 5: the profiled choice
+        from .device import PROFILE_STRIDES, PROFILE_WEIGHTS
+        if len(pb) != 2 or pb[0] not in PROFILE_STRIDES or pb[1] > 2:
+            raise E.StageError("reconstruct", E.CorruptPayload("bad interpolation profile segment"))
+        stride, weights = pb[0], PROFILE_WEIGHTS[pb[1]]
     if pred == "interp" and len(anchors):
         from .device import pad3
         d3 = pad3(a.dims)
@@ -459,8 +476,9 @@ def _decompress_dev(a: Archive, pipeline=None, *, graph: bool = False, timings: 
     try:
         dag = eng.decompress_dag_graphed if graph else eng.decompress_dag
         try:
+            kwd = dict(weights=weights) if weights is not None else {}
             recon = dag(spec.primary_codec, pred, csegs, idx, vals, anchors, a.dims, bound.eb_abs, radius, stride,
-                        deltas=deltas)
+                        deltas=deltas, **kwd)
         except E.FZError as e:
             raise E.StageError("decode-codes", e) from e
         return eng, recon
