@@ -890,6 +890,20 @@ __global__ void __launch_bounds__(64) lz1d_walk3_kernel(const float* __restrict_
         if (t + 1 >= n) break;
         const double pr = __dadd_rn(0.0, (double)r);
         const long long gbase = (cb << 10) + 32 * cg;
+        // speculation: the window's exit block under the approximate bounds
+        // RN32(pr -/+ eb) -- its loads go out now and overlap the exact inner
+        // interval and the rest-of-block checks (they differ from the inner
+        // interval's choice only when a block summary falls in the ~eb 2^-20
+        // sliver, or when the exit is still in the current block)
+        long long sb;
+        {
+            const float alo = __double2float_rn(__dsub_rn(pr, P.eb)), ahi = __double2float_rn(__dadd_rn(pr, P.eb));
+            sb = window_first(alo, ahi);
+            if (sb >= 0) {
+                wait_buf(cur ^ 1);   // a stale speculative load may still write that buffer
+                issue(sb, cur ^ 1);
+            }
+        }
         float zlo, zhi;
         zinner(pr, P, zlo, zhi);
         WSTAMP3(1);
@@ -930,8 +944,13 @@ __global__ void __launch_bounds__(64) lz1d_walk3_kernel(const float* __restrict_
             fb = walk_far(cb + 1 + 32 * WIN1, nblk, bmin, bmax, smin, smax, nsb, zlo, zhi);
         }
         if (fb < 0) break;   // no further event: the rest keeps zero codes
-        wait_buf(cur ^ 1);
-        issue(fb, cur ^ 1);
+        if (fb != sb) {   // speculation missed (or was not taken)
+#ifdef LZ7_TIMING
+            ph[5]++;
+#endif
+            wait_buf(cur ^ 1);
+            issue(fb, cur ^ 1);
+        }
         cur ^= 1;
         commit();
         cb = fb;

@@ -9,5 +9,5 @@ for f in lorenzo huffman; do
         --expt-relaxed-constexpr -I ../include -c csrc/$f.cu -o _build/var/${f}_$1.o
 done
 nvcc -shared -gencode arch=compute_100a,code=sm_100a -o _build/var/libfzb200_$1.so _build/stream_ops.o \
-    _build/var/lorenzo_$1.o _build/interp.o _build/bitshuffle.o _build/var/huffman_$1.o -lcudart
+    _build/var/lorenzo_$1.o _build/interp.o _build/bitshuffle.o _build/var/huffman_$1.o _build/dualquant.o -lcudart
 rm -f _build/var/lorenzo_$1.o _build/var/huffman_$1.o
