@@ -1055,6 +1055,28 @@ FZB_DEV void put_chunk(uint16_t* __restrict__ out, unsigned long long base, unsi
     }
 }
 
+// 32 copies of `sym` appended at slot p of the thread's 8-symbol chunk
+// buffer: the rest of the current chunk, three whole 16-byte chunks, and p
+// slots of the next one (fixed cost, no per-symbol work)
+FZB_DEV void emit_run32(uint16_t* __restrict__ out, unsigned long long& base, int& from, int p,
+                        unsigned long long& lo, unsigned long long& hi, uint32_t sym) {
+    const unsigned long long e4 = (unsigned long long)sym * 0x0001000100010001ull;
+    const unsigned long long mlo = p >= 4 ? 0ull : (~0ull << (16 * p));          // slots p..3
+    const unsigned long long mhi = p <= 4 ? ~0ull : (~0ull << (16 * (p - 4)));   // slots max(p,4)..7
+    lo |= e4 & mlo;
+    hi |= e4 & mhi;
+    put_chunk(out, base, lo, hi, from, 8);
+    base += 8;
+    from = 0;
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+        put_chunk(out, base, e4, e4, 0, 8);
+        base += 8;
+    }
+    lo = e4 & ~mlo;
+    hi = e4 & ~mhi;
+}
+
 __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_t* __restrict__ stream,
                                                                    unsigned long long total_bits, uint64_t nsub,
                                                                    const DecTables* __restrict__ Tg,
@@ -1092,8 +1114,21 @@ __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_
     int from = (int)(o & 7);               // first slot of the chunk that is ours
     int p = from;                          // next free slot
     unsigned long long lo = 0, hi = 0;
+    // a 1-bit codeword "0" (or "1") makes a 32-bit window of zeros (ones) 32
+    // copies of its symbol: low-entropy streams (a dominant zero code) skip
+    // the per-window LUT walk
+    constexpr int LAST = (1 << LUT_BITS) - 1;
+    const bool z0 = (lm[0] & 7u) && ((lm[0] >> 7) & 15u) == 1u;
+    const bool z1 = (lm[LAST] & 7u) && ((lm[LAST] >> 7) & 15u) == 1u;
+    const uint32_t s0 = (uint32_t)(ls[0] & 0xFFFFu), s1 = (uint32_t)(ls[LAST] & 0xFFFFu);
     while (todo) {
         const uint32_t win = r.peek32();
+        if (todo >= 32 && ((z0 && win == 0u) || (z1 && win == 0xFFFFFFFFu))) {
+            emit_run32(out, base, from, p, lo, hi, win ? s1 : s0);
+            r.skip(32);
+            todo -= 32;
+            continue;
+        }
         const uint32_t idx = win >> (32 - LUT_BITS);
         const uint32_t md = lm[idx];
         int c = (int)(md & 7u);
