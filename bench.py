@@ -71,6 +71,7 @@ WORKLOADS = {
                 fields=64, golden="c2"),
 }
 METRIC = "compress/decompress GB/s per GPU & per box at fixed rel eb; CR+PSNR vs CPU ref"
+_COLL_CPU = False   # collectives on host tensors (gloo test hook)
 BATCH = 8   # fields per batched wavefront launch (C5)
 
 
@@ -270,7 +271,7 @@ def _allgather_sizes(nbytes, world, dev):
     import torch
     import torch.distributed as dist
     if world > 1:
-        t = torch.tensor([nbytes], dtype=torch.int64, device=dev)
+        t = torch.tensor([nbytes], dtype=torch.int64, device="cpu" if _COLL_CPU else dev)
         g = [torch.empty_like(t) for _ in range(world)]
         dist.all_gather(g, t)
 
@@ -403,7 +404,7 @@ def _barrier(world):
 def _max_over_ranks(v, world, dev):
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    t = torch.tensor([v], dtype=torch.float64, device="cpu" if _COLL_CPU else dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -462,10 +463,20 @@ def run_ours(args, wl):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one rank per GPU over NCCL.  FZB_BENCH_BACKEND=gloo (test hook) lets N
+    # ranks share the visible GPUs with host-side collectives, so the N > 1
+    # code path can be exercised on a single-GPU box.
+    global _COLL_CPU
+    backend = os.environ.get("FZB_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+            _COLL_CPU = True
     if wl.get("fields"):
         line = run_c5(args, wl, world, rank, dev)
     else:
@@ -558,7 +569,7 @@ def run_c5(args, wl, world, rank, dev):
             szs = eng.sizes_batch(das)
             eng.decompress_batch_resident(das, szs, [rel * (z["hi"] - z["lo"]) for z in szs], OUT[g[0]:g[-1] + 1])
             local += [eng.compressed_bytes(d, z) for d, z in zip(das, szs)]
-        sizes = shard.gather_sizes(local, NF, world, rank, device=dev)   # the one collective
+        sizes = shard.gather_sizes(local, NF, world, rank, device="cpu" if _COLL_CPU else dev)   # the one collective
         return shard.container_offsets(sizes), sizes
 
     for _ in range(max(args.warmup, 3)):
