@@ -10,7 +10,9 @@ rng = np.random.default_rng(0)
 cases = {"c1like_128": np.round(np.abs(rng.normal(0, 20, 128))).astype(np.uint64) + 1,
          "geo_79": rng.geometric(0.1, 79).astype(np.uint64),
          "ties_200": rng.integers(1, 4, 200).astype(np.uint64),
-         "wide_600": rng.geometric(0.01, 600).astype(np.uint64)}
+         "wide_600": rng.geometric(0.01, 600).astype(np.uint64),
+         "wide_1000": rng.geometric(0.005, 1000).astype(np.uint64),
+         "flat_1024": rng.integers(1000, 2000, 1024).astype(np.uint64)}
 for name, used in cases.items():
     bins = np.zeros(1024, np.uint64)
     bins[rng.choice(1024, used.size, replace=False)] = used
