@@ -9,6 +9,8 @@
 // pass, threads mapped to the innermost lattice axis for coalescing.  The
 // cubic/linear/copy stencils and the quantizer keep the reference's exact
 // f64 operation order (no FMA).
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace {
@@ -30,6 +32,13 @@ FastDiv fastdiv(uint32_t d) {
 }
 FZB_DEV uint32_t fdiv(uint32_t q, const FastDiv& f) {
     return (uint32_t)(((unsigned long long)__umulhi(f.m, q) + q) >> f.l);
+}
+FZB_DEV FastDiv fastdiv_dev(uint32_t d) {
+    FastDiv f;
+    f.d = d;
+    f.l = d > 1 ? 32 - __clz(d - 1) : 0;
+    f.m = (uint32_t)((((1ull << 32) * ((1ull << f.l) - d)) / d) + 1);
+    return f;
 }
 
 struct Pass {
@@ -54,6 +63,20 @@ FZB_DEV double interp_pred(const float* __restrict__ r, long long t, long long c
     if (c + h < n) return __dadd_rn(__dmul_rn(0.5, (double)r[t - sh]), __dmul_rn(0.5, (double)r[t + sh]));
     return (double)r[t - sh];
 }
+
+// interp_pred on a pointer to the target, 32-bit coordinates (shared-memory tiles)
+FZB_DEV double interp_pred_s(const float* r, int c, int n, int sh, int h, const double* w) {
+    if (c - 3 * h >= 0 && c + 3 * h < n) {
+        double acc = __dmul_rn(w[0], (double)r[-3 * sh]);
+        acc = __dadd_rn(acc, __dmul_rn(w[1], (double)r[-sh]));
+        acc = __dadd_rn(acc, __dmul_rn(w[2], (double)r[sh]));
+        acc = __dadd_rn(acc, __dmul_rn(w[3], (double)r[3 * sh]));
+        return acc;
+    }
+    if (c + h < n) return __dadd_rn(__dmul_rn(0.5, (double)r[-sh]), __dmul_rn(0.5, (double)r[sh]));
+    return (double)r[-sh];
+}
+
 
 template <int AXIS, bool DEC>
 __global__ void __launch_bounds__(256) interp_pass_kernel(const float* __restrict__ orig, uint16_t* __restrict__ codes,
@@ -142,8 +165,9 @@ void pad3(uint32_t& n0, uint32_t& n1, uint32_t& n2) { (void)n0; (void)n1; (void)
 
 template <bool DEC>
 int run_passes(const float* orig, uint16_t* codes, float* recon, uint32_t* bitmap, uint32_t n0, uint32_t n1,
-               uint32_t n2, const double* d_eb, uint32_t radius, uint32_t stride, const double* w, cudaStream_t st) {
-    for (long long h = stride / 2; h >= 1; h /= 2) {
+               uint32_t n2, const double* d_eb, uint32_t radius, uint32_t stride, const double* w, cudaStream_t st,
+               long long hmin = 1) {
+    for (long long h = stride / 2; h >= hmin; h /= 2) {
         for (int axis = 0; axis < 3; axis++) {
             const Pass p = make_pass(n0, n1, n2, h, axis);
             if (p.total == 0) continue;
@@ -158,6 +182,186 @@ int run_passes(const float* orig, uint16_t* codes, float* recon, uint32_t* bitma
         }
     }
     return fzb_check_launch();
+}
+
+// ---- 2D fields: all levels of a 128 x 128 tile in shared memory ----------
+// A target of pass (h, axis) reads points at +-h and +-3h along its axis, all
+// finished by earlier passes, so the values a tile needs form a region that
+// grows by 3h per axis going back through the passes:
+//   (1,k): tile   (1,j): +3 in k   (2,k): +3,+3   (2,j): +3,+9   (4,k): +9,+9
+//   (4,j): +9,+21 (8,k): +21,+21   (8,j): +21,+45 -> anchors within +-45.
+// One CTA loads the anchors of its tile +-45 (a 218 x 218 f32 region, 190 KB
+// of shared memory) and runs the eight passes over those shrinking regions
+// with the reference's exact stencil and quantizer: the halo is recomputed
+// (~20% extra work, nearly all of it at the coarse levels, which hold few
+// points) instead of eight grid-wide passes through HBM.  Only the tile's
+// own codes / outlier flags (encode) or reconstructions (decode) are written.
+
+struct Pass2 {
+    int h, axis, xj, xk;
+};
+struct Plan2 {
+    Pass2 p[8];
+    int np, halo;
+};
+Plan2 plan2(int htop) {
+    // passes in the reference order (levels h = htop .. 1, axis j then k);
+    // regions back from the last pass
+    Plan2 pl;
+    pl.np = 0;
+    for (int h = htop; h >= 1; h /= 2) {
+        pl.p[pl.np++] = {h, 1, 0, 0};
+        pl.p[pl.np++] = {h, 2, 0, 0};
+    }
+    int xj = 0, xk = 0;
+    for (int q = pl.np - 1; q >= 0; q--) {
+        pl.p[q].xj = xj;
+        pl.p[q].xk = xk;
+        if (pl.p[q].axis == 1) xj += 3 * pl.p[q].h; else xk += 3 * pl.p[q].h;
+    }
+    pl.halo = xj > xk ? xj : xk;
+    return pl;
+}
+
+// The kernel runs on the sub-lattice of every g-th point (n1 x n2 = its
+// extents, gn2 = the field's row pitch): g = 1 runs levels 2, 1 of the field;
+// g = 4 runs the field's levels 8, 4 as levels 2, 1 of the 4-lattice -- the
+// boundary rules only compare c +- 3h with the extent, which scales exactly.
+// Targets of one pass are independent (they read only earlier passes), so a
+// thread gathers IB of them at once -- their global operands (orig value,
+// or code + outlier bit) loaded back to back -- before computing any: one
+// memory latency per IB targets instead of per target.
+
+template <int T, int NT, int IB, int MINB, bool DEC>
+__global__ void __launch_bounds__(NT, MINB) interp2d_tile_kernel(const float* __restrict__ orig,
+                                                           const uint16_t* __restrict__ codes_in,
+                                                           uint16_t* __restrict__ codes, float* __restrict__ recon,
+                                                           uint32_t* __restrict__ bitmap, long long n1, long long n2,
+                                                           int g, long long gn2, Plan2 pl, const double* __restrict__ d_eb,
+                                                           int radius, double w0, double w1, double w2, double w3) {
+    extern __shared__ float Rs[];
+    const QParams P = make_qparams(*d_eb, radius);
+    const double w[4] = {w0, w1, w2, w3};
+    const int H = pl.halo, PW = T + 2 * H;   // region pitch
+    const long long j0 = (long long)blockIdx.y * T, k0 = (long long)blockIdx.x * T;
+    const long long rj0 = j0 - H, rk0 = k0 - H;   // region origin (global)
+    const int J0 = (int)j0, K0 = (int)k0, RJ0 = (int)rj0, RK0 = (int)rk0, N1 = (int)n1, N2 = (int)n2;
+    // the region's points of the levels above the tile's (lattice 2 * htop):
+    // anchors and coarse-level reconstructions, both already in `recon`
+    {
+        const int stride = 2 * pl.p[0].h;
+        const long long aj = ((max(rj0, 0ll) + stride - 1) / stride) * stride;
+        const long long ak = ((max(rk0, 0ll) + stride - 1) / stride) * stride;
+        const long long ej = min(rj0 + PW, n1), ek = min(rk0 + PW, n2);
+        const int cj = aj < ej ? (int)((ej - aj + stride - 1) / stride) : 0;
+        const int ck = ak < ek ? (int)((ek - ak + stride - 1) / stride) : 0;
+        for (int q = threadIdx.x; q < cj * ck; q += NT) {
+            const int qj = q / ck, qk = q - qj * ck;
+            const long long j = aj + (long long)qj * stride, k = ak + (long long)qk * stride;
+            Rs[(j - rj0) * PW + (k - rk0)] = recon[g * j * gn2 + g * k];
+        }
+    }
+    __syncthreads();
+    for (int pi = 0; pi < pl.np; pi++) {
+        const Pass2 ps = pl.p[pi];
+        const int h = ps.h;
+        // target lattice: axis j: j = h (mod 2h), k = 0 (mod 2h); axis k: j = 0 (mod h), k = h (mod 2h)
+        // all index math in 32 bits (run_tiles2d: n1, n2 < 2^30)
+        const int sj = ps.axis == 1 ? h : 0, dj = ps.axis == 1 ? 2 * h : h;
+        const int sk = ps.axis == 1 ? 0 : h, dk = 2 * h;
+        const int lj = max(J0 - ps.xj, 0), hj = min(J0 + T + ps.xj, N1);
+        const int lk = max(K0 - ps.xk, 0), hk = min(K0 + T + ps.xk, N2);
+        auto first = [](int lo, int st, int d) { return lo <= st ? st : st + ((lo - st + d - 1) / d) * d; };
+        const int fj = first(lj, sj, dj), fk = first(lk, sk, dk);
+        const int cj = fj < hj ? (hj - fj + dj - 1) / dj : 0;
+        const int ck = fk < hk ? (hk - fk + dk - 1) / dk : 0;
+        const int tot = cj * ck;
+        if (tot == 0) continue;   // uniform across the CTA
+        const FastDiv fck = fastdiv_dev((uint32_t)ck);
+        const int sh = ps.axis == 1 ? h * PW : h;
+        const int cn = ps.axis == 1 ? N1 : N2;
+        // local index of (fj, fk) and per-step deltas
+        const int l0 = (fj - RJ0) * PW + (fk - RK0), ldj = dj * PW;
+        for (int base = threadIdx.x; base < tot; base += NT * IB) {
+            int li[IB], cc[IB];
+            long long tt[IB];
+            float ov[IB];
+            int cv[IB];
+            bool ob[IB], own[IB];
+#pragma unroll
+            for (int u = 0; u < IB; u++) {
+                const int q = base + u * NT;
+                li[u] = -1;
+                if (q < tot) {
+                    const int qj = (int)fdiv((uint32_t)q, fck), qk = q - qj * ck;
+                    const int j = fj + qj * dj, k = fk + qk * dk;
+                    li[u] = l0 + qj * ldj + qk * dk;
+                    cc[u] = ps.axis == 1 ? j : k;
+                    own[u] = (unsigned)(j - J0) < (unsigned)T && (unsigned)(k - K0) < (unsigned)T;
+                    tt[u] = (long long)(g * j) * gn2 + (long long)g * k;
+                    if constexpr (DEC) {
+                        cv[u] = (int)codes_in[tt[u]];
+                        ob[u] = (bitmap[tt[u] >> 5] >> (tt[u] & 31)) & 1u;
+                        if (ob[u]) ov[u] = recon[tt[u]];   // pre-scattered outlier value
+                    } else {
+                        ov[u] = __ldg(orig + tt[u]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < IB; u++) {
+                if (li[u] < 0) continue;
+                const double pred = interp_pred_s(Rs + li[u], cc[u], cn, sh, h, w);
+                float rec;
+                const long long t = tt[u];
+                if constexpr (DEC) {
+                    rec = ob[u] ? ov[u] : dequantize(pred, cv[u], P);
+                    if (own[u] && !ob[u]) recon[t] = rec;
+                } else {
+                    bool outl;
+                    const int c = quantize((double)ov[u], pred, P, rec, outl);
+                    if (own[u]) {
+                        if (g > 1) recon[t] = rec;   // the field-level kernel reads the 4-lattice
+                        codes[t] = (uint16_t)c;
+                        if (outl) atomicOr(bitmap + (t >> 5), 1u << (t & 31));
+                    }
+                }
+                Rs[li[u]] = rec;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <int T, int NT, int IB, int MINB, bool DEC>
+int launch_tiles2d(const float* orig, uint16_t* codes, float* recon, uint32_t* bitmap, uint32_t n1, uint32_t n2,
+                   int g, const double* d_eb, uint32_t radius, int htop, const double* w, cudaStream_t st) {
+    const Plan2 pl = plan2(htop);
+    const int PW = T + 2 * pl.halo;
+    const size_t smem = (size_t)PW * PW * 4;
+    if (smem > 227 * 1024) return FZB_E_ARG;
+    auto kfn = interp2d_tile_kernel<T, NT, IB, MINB, DEC>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const uint32_t m1 = (n1 - 1) / g + 1, m2 = (n2 - 1) / g + 1;   // sub-lattice extents
+    const dim3 grid((m2 + T - 1) / T, (m1 + T - 1) / T);
+    kfn<<<grid, NT, smem, st>>>(orig, codes, codes, recon, bitmap, m1, m2, g, n2, pl, d_eb, (int)radius, w[0], w[1],
+                                w[2], w[3]);
+    return fzb_check_launch();
+}
+
+// 2D fields (anchor stride 4..64): levels stride/2 .. 4 as one tile kernel on
+// the 4-lattice, levels 2, 1 as one on the field -- two launches instead of
+// 2 log2(stride) grid-wide passes through HBM.
+template <bool DEC>
+int run_tiles2d(const float* orig, uint16_t* codes, float* recon, uint32_t* bitmap, uint32_t n1, uint32_t n2,
+                const double* d_eb, uint32_t radius, uint32_t stride, const double* w, cudaStream_t st) {
+    if (stride >= 8) {
+        const int rc = launch_tiles2d<32, 128, 2, 1, DEC>(orig, codes, recon, bitmap, n1, n2, 4, d_eb, radius,
+                                                          (int)stride / 8, w, st);
+        if (rc) return rc;
+    }
+    // (A/B on C3: 32-tiles 88/71 us, 48-tiles 63/55 us, 64-tiles 57/54 us enc/dec)
+    return launch_tiles2d<64, 128, 2, 7, DEC>(orig, codes, recon, bitmap, n1, n2, 1, d_eb, radius, 2, w, st);
 }
 
 // ---- sampled profiling (opt-in pipeline 5, cuSZ-i / QoZ style) ----------
@@ -254,6 +458,8 @@ FZB_API int fzb_interp_encode_f32(const float* d_in, uint32_t n0, uint32_t n1, u
     const long long a = anchor_stride;
     const long long A0 = (n0 - 1) / a + 1, A1 = (n1 - 1) / a + 1, A2 = (n2 - 1) / a + 1;
     anchor_kernel<false><<<kNumSMs * 2, 256, 0, st>>>(d_in, d_anchors, d_recon, n1, n2, a, A0, A1, A2);
+    if (n0 == 1 && n1 > 1 && n1 < (1u << 30) && n2 < (1u << 30) && anchor_stride <= 64 && !getenv("FZB_INTERP_PASSES"))   // 2D: every level of a tile in shared memory
+        return run_tiles2d<false>(d_in, d_codes, d_recon, d_bitmap, n1, n2, d_eb, radius, anchor_stride, h_weights4, st);
     return run_passes<false>(d_in, d_codes, d_recon, d_bitmap, n0, n1, n2, d_eb, radius, anchor_stride, h_weights4, st);
 }
 
@@ -268,6 +474,9 @@ FZB_API int fzb_interp_decode_f32(const uint16_t* d_codes, const uint32_t* d_bit
     const long long a = anchor_stride;
     const long long A0 = (n0 - 1) / a + 1, A1 = (n1 - 1) / a + 1, A2 = (n2 - 1) / a + 1;
     anchor_kernel<true><<<kNumSMs * 2, 256, 0, st>>>(nullptr, const_cast<float*>(d_anchors), d_recon, n1, n2, a, A0, A1, A2);
+    if (n0 == 1 && n1 > 1 && n1 < (1u << 30) && n2 < (1u << 30) && anchor_stride <= 64 && !getenv("FZB_INTERP_PASSES"))
+        return run_tiles2d<true>(nullptr, const_cast<uint16_t*>(d_codes), d_recon, const_cast<uint32_t*>(d_bitmap), n1,
+                                 n2, d_eb, radius, anchor_stride, h_weights4, st);
     return run_passes<true>(nullptr, const_cast<uint16_t*>(d_codes), d_recon, const_cast<uint32_t*>(d_bitmap), n0, n1,
                             n2, d_eb, radius, anchor_stride, h_weights4, st);
 }

@@ -72,6 +72,18 @@ def _align(n: int, a: int = 256) -> int:
     return (int(n) + a - 1) // a * a
 
 
+
+def _interp_nk(n0, n1, n2, stride):
+    """Kernels one fzb_interp_{en,de}code_f32 call launches (interp.cu):
+    2D = anchors + a shared-memory tile kernel on the 4-lattice (levels
+    stride/2..4) + one on the field (levels 2, 1) (run_tiles2d); otherwise
+    anchors + one pass per level and non-degenerate axis (run_passes)."""
+    levels = int(np.log2(stride))
+    if n0 == 1 and 1 < n1 < 1 << 30 and n2 < 1 << 30 and stride <= 64:
+        return 3 if stride >= 8 else 2
+    return 1 + levels * (3 if n0 > 1 else 1)
+
+
 class _NodeEvent:
     """A CUDA event recorded as an event-record node of a captured graph
     (torch.cuda.Event creates its handle lazily, at the first record)."""
@@ -301,7 +313,7 @@ class Engine:
             anchors = self.buf("anchors" + tag, 4 * na)
             w = (ctypes.c_double * 4)(*weights)
             self._call("fzb_interp_encode_f32", _p(x), n0, n1, n2, _p(eb), radius, a, w, _p(codes), _p(recon),
-                       _p(bitmap), _p(anchors), sp, nk=1 + 3 * int(np.log2(a)))
+                       _p(bitmap), _p(anchors), sp, nk=_interp_nk(n0, n1, n2, a))
             bufs["anchors"] = anchors
             bufs["n_anchors"] = na
         elif predictor == "dualquant":
@@ -511,7 +523,7 @@ class Engine:
             stride, weights = (pf[0], PROFILE_WEIGHTS[pf[1]]) if pf else (16, CUBIC)
             w = (ctypes.c_double * 4)(*weights)
             self._call("fzb_interp_decode_f32", _p(codes), _p(bitmap), _p(b["anchors"]), _p(out), n0, n1, n2, _p(ebt),
-                       da.radius, stride, w, sp, nk=1 + 3 * int(np.log2(stride)))
+                       da.radius, stride, w, sp, nk=_interp_nk(n0, n1, n2, stride))
         else:
             lzws = self.buf("dlzws" + tag, L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
             self._call("fzb_lorenzo_decode_f32", _p(codes), _p(bitmap), _p(out), n0, n1, n2, _p(ebt), da.radius,
@@ -731,7 +743,7 @@ class Engine:
             da = self.upload("danchors" + tag, anchors)
             w = (ctypes.c_double * 4)(*CUBIC)
             self._call("fzb_interp_decode_f32", _p(codes), _p(bitmap), _p(da), _p(recon), n0, n1, n2, _p(ebt), radius,
-                       anchor_stride, w, sp, nk=1 + 3 * int(np.log2(anchor_stride)))
+                       anchor_stride, w, sp, nk=_interp_nk(n0, n1, n2, anchor_stride))
         else:
             lzws = self.buf("dlzws" + tag, L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
             self._call("fzb_lorenzo_decode_f32", _p(codes), _p(bitmap), _p(recon), n0, n1, n2, _p(ebt), radius,
@@ -788,7 +800,7 @@ class Engine:
         elif use_anchors:
             w = (ctypes.c_double * 4)(*weights)
             self._call("fzb_interp_decode_f32", _p(codes), _p(bitmap), _p(danch), _p(recon), n0, n1, n2, _p(ebt),
-                       radius, anchor_stride, w, sp, nk=1 + 3 * int(np.log2(anchor_stride)))
+                       radius, anchor_stride, w, sp, nk=_interp_nk(n0, n1, n2, anchor_stride))
         else:
             lzws = self.buf("dlzws", L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
             self._call("fzb_lorenzo_decode_f32", _p(codes), _p(bitmap), _p(recon), n0, n1, n2, _p(ebt), radius,
