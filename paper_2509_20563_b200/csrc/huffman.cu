@@ -11,8 +11,10 @@
 //    item by rank search, with a prefix max over the packages' ranks so an
 //    unsorted package list still merges exactly as heapq.merge does, and
 //    the level loop stops at the fixed point (a level equal to the previous
-//    one repeats forever).  Larger alphabets use the whole CTA (parallel
-//    merge when the packages are sorted, serial two-head merge otherwise).
+//    one repeats forever).  Up to 2048 used symbols the whole CTA runs the
+//    same rank-search merge (8 packages per thread); beyond that, global
+//    memory with a parallel merge when the packages are sorted and a serial
+//    two-head merge otherwise.
 //  * encode: per-thread bit lengths -> CTA totals -> scan -> every thread
 //    writes its big-endian 32-bit words (interior words with plain stores,
 //    the two boundary words with atomicOr), i.e. the MSB-first byte stream
@@ -34,7 +36,7 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int MAXLEN = 32;
-constexpr int BT = 256;   // build threads (<= 255 registers: the small-alphabet path must not spill)
+constexpr int BT = 512;   // build threads (<= 128 registers; the small-alphabet path uses 128 of them)
 constexpr uint32_t SMEM_BUILD_SYMS = 2048;   // alphabets up to this size build in shared memory
 constexpr size_t SMEM_BUILD_BYTES = (size_t)SMEM_BUILD_SYMS * (8 + 8 + 16 + 4 + 4 + 8) + (size_t)MAXLEN * 2 * SMEM_BUILD_SYMS;
 
@@ -281,6 +283,244 @@ FZB_DEV void build_cta4(uint32_t m, uint32_t nsym, const unsigned long long* in_
     }
 }
 
+// ---- mid-size alphabets (WARP_BUILD_MAX < m <= SMEM_BUILD_SYMS): the whole
+// CTA runs build_cta4's algorithm (rank-search merge with the prefix max
+// over the packages' base ranks, fixed-point exit) on packed keys
+// weight << 16 | tiebreak symbol (one 64-bit compare per search step; needs
+// weights < 2^48) in explicitly shared arrays, BT / 32 warps.
+constexpr int MB_K = (int)(SMEM_BUILD_SYMS / BT);   // items per thread
+constexpr size_t MB_B = 0, MB_M = MB_B + 8 * SMEM_BUILD_SYMS, MB_LB = MB_M + 16 * SMEM_BUILD_SYMS,
+                 MB_IB = MB_LB + 4 * SMEM_BUILD_SYMS, MB_END = MB_IB + (size_t)MAXLEN * 2 * SMEM_BUILD_SYMS;
+static_assert(MB_END + 8 * (BT / 32) + 4 * MB_K * (BT / 32) + 4 * (BT / 32) * (MAXLEN + 1) + 4 <= SMEM_BUILD_BYTES,
+              "mid build layout");
+
+FZB_DEV bool build_mid(uint32_t m, uint32_t nsym, const unsigned long long* in_w, const uint32_t* in_s,
+                       uint8_t* __restrict__ lengths, uint32_t* __restrict__ cw,
+                       unsigned long long* __restrict__ bit_count, long long* s_nb, uint32_t* s_cnt,
+                       unsigned long long* s_first) {
+    extern __shared__ __align__(16) unsigned char sm_build[];
+    constexpr int NW = BT / 32;
+    // small arrays in the dynamic allocation past the lists (the static
+    // shared memory of all build paths plus SMEM_BUILD_BYTES must fit 227 KB)
+    unsigned long long* s_red = reinterpret_cast<unsigned long long*>(sm_build + MB_END);
+    uint32_t* s_ctot = reinterpret_cast<uint32_t*>(sm_build + MB_END + 8 * NW);
+    uint32_t(*s_lc)[MAXLEN + 1] = reinterpret_cast<uint32_t(*)[MAXLEN + 1]>(sm_build + MB_END + 8 * NW + 4 * MB_K * NW);
+    int* s_same_p = reinterpret_cast<int*>(sm_build + MB_END + 8 * NW + 4 * MB_K * NW + 4 * NW * (MAXLEN + 1));
+    int& s_same = *s_same_p;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    unsigned long long rk[MB_K];
+    bool big = false;
+#pragma unroll
+    for (int k = 0; k < MB_K; k++) {
+        const uint32_t q = k * BT + tid;
+        rk[k] = ~0ull;
+        if (q < m) {
+            big |= (in_w[q] >> 48) != 0;
+            rk[k] = (in_w[q] << 16) | in_s[q];
+        }
+    }
+    if (__syncthreads_or(big)) return false;   // (every read of the compacted base is done)
+    unsigned long long* B = reinterpret_cast<unsigned long long*>(sm_build + MB_B);
+    unsigned long long* M = reinterpret_cast<unsigned long long*>(sm_build + MB_M);
+    uint32_t* lbm = reinterpret_cast<uint32_t*>(sm_build + MB_LB);
+    uint8_t* IB = sm_build + MB_IB;
+    // 2. bitonic sort over the next power of two (pad = max key)
+    uint32_t np2 = 1;
+    while (np2 < m) np2 <<= 1;
+#pragma unroll
+    for (int k = 0; k < MB_K; k++) {
+        const uint32_t q = k * BT + tid;
+        if (q < np2) B[q] = rk[k];
+    }
+    __syncthreads();
+    for (uint32_t k2 = 2; k2 <= np2; k2 <<= 1)
+        for (uint32_t jj = k2 >> 1; jj > 0; jj >>= 1) {
+            for (uint32_t q = tid; q < np2; q += BT) {
+                const uint32_t ixj = q ^ jj;
+                if (ixj > q) {
+                    const unsigned long long x = B[q], y = B[ixj];
+                    if ((y < x) == ((q & k2) == 0)) { B[q] = y; B[ixj] = x; }
+                }
+            }
+            __syncthreads();
+        }
+    // 3. levels (see build_cta4)
+    for (uint32_t q = tid; q < m; q += BT) { M[q] = B[q]; IB[q] = 1; }
+    uint32_t mlen = m, pnpk = 0xFFFFFFFFu;
+    int lfix = MAXLEN - 1;
+    unsigned long long ppk[MB_K];
+#pragma unroll
+    for (int k = 0; k < MB_K; k++) ppk[k] = 0;
+    __syncthreads();
+    for (int l = 1; l < MAXLEN; l++) {
+        const uint32_t npk = mlen / 2;
+        unsigned long long pk[MB_K];
+        uint32_t lb[MB_K];
+        bool same = npk == pnpk;
+#pragma unroll
+        for (int k = 0; k < MB_K; k++) {
+            const uint32_t q = k * BT + tid;
+            pk[k] = 0;
+            lb[k] = 0;
+            if (q < npk) {
+                const unsigned long long x = M[2 * q], y = M[2 * q + 1];
+                pk[k] = (((x >> 16) + (y >> 16)) << 16) | (x & 0xFFFFull);
+                same &= pk[k] == ppk[k];
+            }
+        }
+        // lb = #{B < pk}
+#pragma unroll
+        for (int k = 0; k < MB_K; k++) {
+            if (k * BT + tid < npk) {
+                uint32_t lo = 0, hi = m;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (B[mid] < pk[k]) lo = mid + 1; else hi = mid;
+                }
+                lb[k] = lo;
+            }
+        }
+        uint32_t im[MB_K];
+#pragma unroll
+        for (int k = 0; k < MB_K; k++) {
+            const uint32_t q = k * BT + tid;
+            im[k] = warp_incl_max(q < npk ? lb[k] : 0u, lane);
+            if (lane == 31) s_ctot[k * NW + wid] = im[k];
+        }
+        if (tid == 0) s_same = 1;
+        __syncthreads();   // every read of M_{l-1} is done
+        if (!same) s_same = 0;
+        // exclusive prefix max over the MB_K * NW chunk totals (<= 64): two
+        // warp scans, chunk c's prefix read by shuffle
+        static_assert(MB_K * NW <= 64, "chunk scan");
+        const uint32_t c0 = lane < MB_K * NW ? s_ctot[lane] : 0u;
+        const uint32_t c1 = 32 + lane < MB_K * NW ? s_ctot[32 + lane] : 0u;
+        const uint32_t i0 = warp_incl_max(c0, lane);
+        const uint32_t i1 = max(warp_incl_max(c1, lane), __shfl_sync(0xffffffffu, i0, 31));
+        __syncthreads();
+        if (s_same) {      // P_l == P_{l-1}: M_l == M_{l-1} == every later level
+            lfix = l - 1;
+            break;
+        }
+        uint8_t* ib = IB + (size_t)l * 2 * m;
+#pragma unroll
+        for (int k = 0; k < MB_K; k++) {
+            const uint32_t q = k * BT + tid;
+            const int c = k * NW + wid;   // this item's chunk; prefix = incl[c - 1]
+            const uint32_t e0 = __shfl_sync(0xffffffffu, i0, (c - 1) & 31);
+            const uint32_t e1 = __shfl_sync(0xffffffffu, i1, (c - 1) & 31);
+            const uint32_t pre = c == 0 ? 0u : (c - 1 < 32 ? e0 : e1);
+            const uint32_t iv = max(im[k], pre);
+            if (q < npk) {
+                lbm[q] = iv;
+                M[iv + q] = pk[k];
+                ib[iv + q] = 0;
+            }
+            ppk[k] = pk[k];
+        }
+        __syncthreads();
+        for (uint32_t q = tid; q < m; q += BT) {   // base item q lands after the packages with i_j <= q
+            uint32_t lo = 0, hi = npk;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (lbm[mid] <= q) lo = mid + 1; else hi = mid;
+            }
+            M[q + lo] = B[q];
+            ib[q + lo] = 1;
+        }
+        pnpk = npk;
+        mlen = m + npk;
+        __syncthreads();
+    }
+    HB_STAMP(2);
+    // 4. selected prefixes, top level down
+    long long L = 2 * ((long long)m - 1);
+    for (int l = MAXLEN - 1; l >= 1; l--) {
+        const uint8_t* ib = IB + (size_t)min(l, lfix) * 2 * m;
+        uint32_t c = 0;
+        for (long long q = tid; q < L; q += BT) c += ib[q];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) s_ctot[wid] = c;
+        __syncthreads();
+        uint32_t tot = 0;
+#pragma unroll
+        for (int w = 0; w < NW; w++) tot += s_ctot[w];
+        __syncthreads();
+        if (tid == 0) s_nb[l] = tot;
+        L = 2 * (L - (long long)tot);
+    }
+    if (tid == 0) s_nb[0] = L;
+    if (tid <= MAXLEN) s_cnt[tid] = 0;
+    __syncthreads();
+    HB_STAMP(3);
+    // 5. lengths and bit count
+    unsigned long long bits = 0;
+    for (uint32_t q = tid; q < m; q += BT) {
+        int len = 0;
+        for (int l = 0; l < MAXLEN; l++) len += (long long)q < s_nb[l];
+        lengths[B[q] & 0xFFFFu] = (uint8_t)len;
+        bits += (B[q] >> 16) * (unsigned long long)len;
+        atomicAdd(&s_cnt[len], 1u);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) bits += __shfl_xor_sync(0xffffffffu, bits, o);
+    if (lane == 0) s_red[wid] = bits;
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < NW; w++) t += s_red[w];
+        *bit_count = t;
+        unsigned long long code = 0;
+        s_first[0] = 0;
+        for (int l = 1; l <= MAXLEN; l++) {
+            code = (code + (l > 1 ? s_cnt[l - 1] : 0)) << 1;
+            s_first[l] = code;
+        }
+    }
+    HB_STAMP(4);
+    // 6. canonical codewords by (length, symbol) (encode.py:155-171): warp w
+    // owns symbols [w * span, (w + 1) * span); pass 1 counts its lengths,
+    // an exclusive scan over the warps gives each warp's starting ranks,
+    // pass 2 assigns them in symbol order
+    const uint32_t span = ((nsym + NW - 1) / NW + 31) & ~31u;
+    const uint32_t s_lo = wid * span, s_hi = min(nsym, s_lo + span);
+    for (int l = lane; l <= MAXLEN; l += 32) s_lc[wid][l] = 0;
+    __syncwarp();
+    for (uint32_t s0 = s_lo; s0 < s_hi; s0 += 32) {
+        const uint32_t sy = s0 + lane;
+        const int len = sy < s_hi ? lengths[sy] : 0;
+        const unsigned peers = __match_any_sync(0xffffffffu, len);
+        if (len && __popc(peers & lanemask_lt()) == 0) s_lc[wid][len] += __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    if (tid <= MAXLEN) {   // exclusive scan over the warps, per length
+        uint32_t run = 0;
+        for (int w = 0; w < NW; w++) {
+            const uint32_t c = s_lc[w][tid];
+            s_lc[w][tid] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    for (uint32_t s0 = s_lo; s0 < s_hi; s0 += 32) {
+        const uint32_t sy = s0 + lane;
+        const int len = sy < s_hi ? lengths[sy] : 0;
+        const unsigned peers = __match_any_sync(0xffffffffu, len);
+        const uint32_t rank = __popc(peers & lanemask_lt());
+        if (len) cw[sy] = (uint32_t)(s_first[len] + s_lc[wid][len] + rank);
+        __syncwarp();
+        if (len && rank == 0) s_lc[wid][len] += __popc(peers);
+        __syncwarp();
+    }
+    HB_STAMP(5);
+#ifdef LZ7_TIMING
+    if (tid == 0) g_hf_build_stamp[7] = lfix;
+#endif
+    return true;
+}
+
 __global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long long* __restrict__ bins, uint32_t nsym,
                                                            uint8_t* __restrict__ lengths, uint32_t* __restrict__ cw,
                                                            unsigned long long* __restrict__ bit_count, BuildWS ws) {
@@ -307,6 +547,7 @@ __global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long l
         ws.isbase = p;   // MAXLEN * 2m bytes, m <= N2
     }
 
+    HB_STAMP(0);
     // 1. compact used symbols (symbol order) and zero outputs
     uint32_t carry = 0;
     for (uint32_t s0 = 0; s0 < nsym; s0 += NTH) {
@@ -337,6 +578,10 @@ __global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long l
         if (tid < CB) build_cta4(m, nsym, ws.bw, ws.bs, lengths, cw, bit_count, s_nb, s_cnt, s_first);
         return;
     }
+    HB_STAMP(1);
+    if (nsym <= SMEM_BUILD_SYMS && NTH == BT &&
+        build_mid(m, nsym, ws.bw, ws.bs, lengths, cw, bit_count, s_nb, s_cnt, s_first))
+        return;
     // 2. bitonic sort of (w, s) over the next power of two (pad = max key)
     uint32_t np2 = 1;
     while (np2 < m) np2 <<= 1;
@@ -359,9 +604,11 @@ __global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long l
             }
             __syncthreads();
         }
+    HB_STAMP(1);
     // 3. levels.  M_0 = base.
     for (uint32_t q = tid; q < m; q += NTH) { ws.mw[q] = ws.bw[q]; ws.mt[q] = ws.bs[q]; ws.isbase[q] = 1; }
     uint32_t mlen = m;
+    int lfix = MAXLEN - 1;
     __syncthreads();
     for (int l = 1; l < MAXLEN; l++) {
         const uint32_t npk = mlen / 2;
@@ -412,10 +659,11 @@ __global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long l
         mlen = m + npk;
         __syncthreads();
     }
+    HB_STAMP(2);
     // 4. selected prefixes, top level down
     long long L = 2 * ((long long)m - 1);
     for (int l = MAXLEN - 1; l >= 1; l--) {
-        const uint8_t* ib = ws.isbase + (size_t)l * 2 * m;
+        const uint8_t* ib = ws.isbase + (size_t)min(l, lfix) * 2 * m;
         uint32_t c = 0;
         for (long long q = tid; q < L; q += NTH) c += ib[q];
         uint32_t tot;
@@ -425,6 +673,7 @@ __global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long l
     }
     if (tid == 0) s_nb[0] = L;
     __syncthreads();
+    HB_STAMP(3);
     // 5. lengths and bit count
     unsigned long long bits = 0;
     for (uint32_t q = tid; q < m; q += NTH) {
@@ -437,6 +686,7 @@ __global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long l
     block_exclusive_scan64(bits, tmp64, &btot);
     if (tid == 0) *bit_count = btot;
     __syncthreads();
+    HB_STAMP(4);
     // 6. canonical codewords by (length, symbol)  (encode.py:155-171)
     if (tid <= MAXLEN) s_cnt[tid] = 0;
     __syncthreads();
@@ -466,6 +716,10 @@ __global__ void __launch_bounds__(BT) huffman_build_kernel(const unsigned long l
             __syncwarp();
         }
     }
+    HB_STAMP(5);
+#ifdef LZ7_TIMING
+    if (tid == 0) g_hf_build_stamp[7] = lfix;
+#endif
 }
 
 // ------------------------------------------------------------------ encode

@@ -171,3 +171,23 @@ def test_huffman_build_ties_vs_oracle(oracle, seed):
     cl, ostream, obits = oracle.huffman_encode(codes, h.bins)
     assert np.array_equal(cb.code_lengths, cl) and bits == obits and stream == ostream
     assert np.array_equal(enc.huffman_decode(cb, stream, codes.size), codes)
+
+
+@pytest.mark.parametrize("seed", range(15))
+def test_huffman_build_large_alphabets_vs_oracle(oracle, seed):
+    # 257..3000 used symbols: the whole-CTA rank-search merge (shared memory,
+    # up to 2048 symbols, including its fixed-point exit) and the global-
+    # memory path beyond; tie-heavy, power-of-two and geometric weights
+    rng = np.random.default_rng(100 + seed)
+    radius = (512, 1024, 2048)[seed % 3]
+    m = int(rng.integers(257, min(2 * radius, 3000)))
+    used = rng.choice(2 * radius, m, replace=False)
+    kind = (seed // 3) % 3
+    reps = (rng.integers(1, 4, m) if kind == 0 else
+            2 ** rng.integers(0, 10, m) if kind == 1 else rng.geometric(0.02, m))
+    codes = rng.permutation(np.repeat(used, reps)).astype(np.uint32)
+    h = enc.histogram_exact(codes, radius)
+    cb, stream, bits = enc.huffman_encode(codes, h)
+    cl, ostream, obits = oracle.huffman_encode(codes, h.bins)
+    assert np.array_equal(cb.code_lengths, cl) and bits == obits and stream == ostream
+    assert np.array_equal(enc.huffman_decode(cb, stream, codes.size), codes)
