@@ -98,6 +98,7 @@ FZB_DEV void build_cta4(uint32_t m, uint32_t nsym, const unsigned long long* in_
     __shared__ uint32_t s_tot[WARP_BUILD_MAX / 32];
     __shared__ int s_flag;
     const int tid = threadIdx.x, lane = tid & 31;
+    constexpr size_t IBS = 2 * WARP_BUILD_MAX;   // per-level leaf-mark stride (16-byte aligned)
     constexpr int KI = (int)(WARP_BUILD_MAX / CB);   // items per thread
     unsigned long long rw[KI];
     uint32_t rs[KI];
@@ -147,6 +148,7 @@ FZB_DEV void build_cta4(uint32_t m, uint32_t nsym, const unsigned long long* in_
             }
             cb_sync();
         }
+    HB_STAMP(1);
     // 3. levels.  M_0 = base.  A level's merge places every package and base
     // item by rank search; the prefix max over the packages' base ranks
     // reproduces heapq.merge (encode.py:196) for ANY package order: P[j] is
@@ -159,7 +161,7 @@ FZB_DEV void build_cta4(uint32_t m, uint32_t nsym, const unsigned long long* in_
     cb_sync();
     for (int l = 1; l < MAXLEN; l++) {
         const uint32_t npk = mlen / 2;
-        uint8_t* ib = ws.isbase + (size_t)l * 2 * m;
+        uint8_t* ib = ws.isbase + (size_t)l * IBS;
         unsigned long long* nw = (l & 1) ? mw2 : ws.mw;
         uint32_t* nt = (l & 1) ? mt2 : ws.mt;
         const unsigned long long* ow = (l & 1) ? ws.mw : mw2;
@@ -213,7 +215,7 @@ FZB_DEV void build_cta4(uint32_t m, uint32_t nsym, const unsigned long long* in_
         if (tid == 0) s_flag = 1;
         cb_sync();
         if (l >= 2 && mlen == plen) {
-            const uint8_t* pib = ib - 2 * m;
+            const uint8_t* pib = ib - IBS;
             bool same = true;
             for (uint32_t q = tid; q < mlen; q += CB) same &= nw[q] == ow[q] && nt[q] == ot[q] && ib[q] == pib[q];
             if (!same) s_flag = 0;
@@ -224,24 +226,36 @@ FZB_DEV void build_cta4(uint32_t m, uint32_t nsym, const unsigned long long* in_
             }
         }
     }
-    // 4. selected prefixes, top level down
+    HB_STAMP(2);
+    // 4. selected prefixes, top level down: L <= 2m - 2 <= 510 marks, so
+    // warp 0 counts a level with one 16-byte load per lane, no CTA barriers
     long long L = 2 * ((long long)m - 1);
-    for (int l = MAXLEN - 1; l >= 1; l--) {
-        const uint8_t* ib = ws.isbase + (size_t)min(l, lfix) * 2 * m;
-        uint32_t c = 0;
-        for (long long q = tid; q < L; q += CB) c += ib[q];
+    if (tid < 32) {
+        for (int l = MAXLEN - 1; l >= 1; l--) {
+            const uint8_t* ib = ws.isbase + (size_t)min(l, lfix) * IBS;   // 16-byte aligned
+            uint32_t c = 0;
+            const long long q0 = 16 * lane;
+            if (q0 < L) {
+                const uint4 v = *reinterpret_cast<const uint4*>(ib + q0);
+                const int keep = (int)min(16ll, L - q0);   // bytes of this lane below L
+                const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        if (lane == 0) s_tot[tid >> 5] = c;
-        cb_sync();
-        const uint32_t tot = s_tot[0] + s_tot[1] + s_tot[2] + s_tot[3];
-        cb_sync();
-        if (tid == 0) s_nb[l] = tot;
-        L = 2 * (L - (long long)tot);
+                for (int k = 0; k < 4; k++) {
+                    const int nb = min(4, max(0, keep - 4 * k));
+                    const uint32_t msk = nb >= 4 ? 0xFFFFFFFFu : ((1u << (8 * nb)) - 1u);
+                    c += ((wv[k] & msk) * 0x01010101u) >> 24;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            if (tid == 0) s_nb[l] = c;
+            L = 2 * (L - (long long)c);
+        }
     }
     if (tid == 0) s_nb[0] = L;
     if (tid <= MAXLEN) s_cnt[tid] = 0;
     cb_sync();
+    HB_STAMP(3);
     // 5. lengths and bit count
     unsigned long long bits = 0;
     for (uint32_t q = tid; q < m; q += CB) {
@@ -268,19 +282,43 @@ FZB_DEV void build_cta4(uint32_t m, uint32_t nsym, const unsigned long long* in_
     }
     __threadfence_block();
     cb_sync();
-    // 6. canonical codewords by (length, symbol)  (encode.py:155-171): one warp
-    if (tid < 32) {
-        for (uint32_t s0 = 0; s0 < nsym; s0 += 32) {
-            const uint32_t sy = s0 + lane;
-            const int len = sy < nsym ? lengths[sy] : 0;
-            const unsigned peers = __match_any_sync(0xffffffffu, len);
-            const uint32_t rank = __popc(peers & lanemask_lt());
-            if (len) cw[sy] = (uint32_t)(s_first[len] + s_cnt[len] + rank);
-            __syncwarp();
-            if (len && rank == 0) s_cnt[len] += __popc(peers);
-            __syncwarp();
+    HB_STAMP(4);
+    // 6. canonical codewords by (length, symbol)  (encode.py:155-171): the
+    // used symbols in symbol order are this thread's rs[k] (q = k * CB + tid);
+    // chunk c = 32 consecutive q: per-chunk length counts, an exclusive scan
+    // over the chunks, and a match_any rank inside the chunk
+    constexpr int NCH = KI * (CB / 32);
+    uint32_t(*s_cc)[MAXLEN + 1] = reinterpret_cast<uint32_t(*)[MAXLEN + 1]>(sm_build + WB_MW2 + 64);
+    for (int z = tid; z < NCH * (MAXLEN + 1); z += CB) s_cc[z / (MAXLEN + 1)][z % (MAXLEN + 1)] = 0;
+    cb_sync();
+    int lq[KI];
+#pragma unroll
+    for (int k = 0; k < KI; k++) {
+        const uint32_t q = k * CB + tid;
+        lq[k] = q < m ? lengths[rs[k]] : 0;
+        const unsigned peers = __match_any_sync(0xffffffffu, lq[k]);
+        if (lq[k] && __popc(peers & lanemask_lt()) == 0) s_cc[k * (CB / 32) + (tid >> 5)][lq[k]] = __popc(peers);
+    }
+    cb_sync();
+    if (tid <= MAXLEN) {
+        uint32_t run = (uint32_t)s_first[tid];
+        for (int c = 0; c < NCH; c++) {
+            const uint32_t v = s_cc[c][tid];
+            s_cc[c][tid] = run;
+            run += v;
         }
     }
+    cb_sync();
+#pragma unroll
+    for (int k = 0; k < KI; k++) {
+        const uint32_t q = k * CB + tid;
+        const unsigned peers = __match_any_sync(0xffffffffu, lq[k]);
+        if (q < m && lq[k]) cw[rs[k]] = s_cc[k * (CB / 32) + (tid >> 5)][lq[k]] + __popc(peers & lanemask_lt());
+    }
+    HB_STAMP(5);
+#ifdef LZ7_TIMING
+    if (tid == 0) g_hf_build_stamp[7] = lfix;
+#endif
 }
 
 // ---- mid-size alphabets (WARP_BUILD_MAX < m <= SMEM_BUILD_SYMS): the whole
