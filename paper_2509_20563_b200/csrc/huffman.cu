@@ -1338,8 +1338,9 @@ __global__ void __launch_bounds__(HD_THREADS) hf_sync_coop_kernel(const uint32_t
 // no block barriers.  The first true-path error with ordinal < n
 // (encode.py:299-310) is folded in with an atomicMin on (subsequence << 2 | kind).
 FZB_DEV void put_chunk(uint16_t* __restrict__ out, unsigned long long base, unsigned long long lo,
-                       unsigned long long hi, int from, int to) {
+                       unsigned long long hi, int from, int to, bool pre = false, unsigned long long e0 = 0) {
     if (from == 0 && to == 8) {
+        if (pre && lo == e0 && hi == e0) return;   // all s0: already in memory (hf_prefill_kernel)
         *reinterpret_cast<uint4*>(out + base) =
             make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32));
     } else {
@@ -1351,22 +1352,48 @@ FZB_DEV void put_chunk(uint16_t* __restrict__ out, unsigned long long base, unsi
 // buffer: the rest of the current chunk, three whole 16-byte chunks, and p
 // slots of the next one (fixed cost, no per-symbol work)
 FZB_DEV void emit_run32(uint16_t* __restrict__ out, unsigned long long& base, int& from, int p,
-                        unsigned long long& lo, unsigned long long& hi, uint32_t sym) {
+                        unsigned long long& lo, unsigned long long& hi, uint32_t sym, bool pre,
+                        unsigned long long e0) {
     const unsigned long long e4 = (unsigned long long)sym * 0x0001000100010001ull;
     const unsigned long long mlo = p >= 4 ? 0ull : (~0ull << (16 * p));          // slots p..3
     const unsigned long long mhi = p <= 4 ? ~0ull : (~0ull << (16 * (p - 4)));   // slots max(p,4)..7
     lo |= e4 & mlo;
     hi |= e4 & mhi;
-    put_chunk(out, base, lo, hi, from, 8);
+    put_chunk(out, base, lo, hi, from, 8, pre, e0);
     base += 8;
     from = 0;
+    if (!(pre && e4 == e0)) {
 #pragma unroll
-    for (int c = 0; c < 3; c++) {
-        put_chunk(out, base, e4, e4, 0, 8);
-        base += 8;
+        for (int c = 0; c < 3; c++) put_chunk(out, base + 8 * c, e4, e4, 0, 8);
     }
+    base += 24;
     lo = e4 & ~mlo;
     hi = e4 & ~mhi;
+}
+
+// Low-entropy streams whose 1-bit codeword "0" is symbol s0: the output is
+// first filled with s0 by coalesced 16-byte stores, and the write pass then
+// stores only the 8-symbol chunks that hold another symbol -- a thread's
+// stores of its own (contiguous, 512-byte-strided from its neighbours')
+// chunks are uncoalesced, 16 of every 32 bytes per sector.
+FZB_DEV bool zero_run_symbol(const unsigned long long* lut_s, const uint16_t* lut_m, uint32_t& s0) {
+    const uint32_t md = lut_m[0];
+    s0 = (uint32_t)(lut_s[0] & 0xFFFFu);
+    return (md & 7u) && ((md >> 7) & 15u) == 1u;
+}
+
+__global__ void hf_prefill_kernel(const unsigned long long* __restrict__ lut_s_g,
+                                  const uint16_t* __restrict__ lut_m_g, uint64_t n, uint16_t* __restrict__ out) {
+    uint32_t s0;
+    if (!zero_run_symbol(lut_s_g, lut_m_g, s0)) return;
+    const uint32_t w = s0 * 0x00010001u;
+    const uint4 v = make_uint4(w, w, w, w);
+    const uint64_t nch = n / 8;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nch; c += stride)
+        reinterpret_cast<uint4*>(out)[c] = v;
+    const uint64_t tail = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tail < n - nch * 8) out[nch * 8 + tail] = (uint16_t)s0;
 }
 
 __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_t* __restrict__ stream,
@@ -1413,10 +1440,12 @@ __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_
     const bool z0 = (lm[0] & 7u) && ((lm[0] >> 7) & 15u) == 1u;
     const bool z1 = (lm[LAST] & 7u) && ((lm[LAST] >> 7) & 15u) == 1u;
     const uint32_t s0 = (uint32_t)(ls[0] & 0xFFFFu), s1 = (uint32_t)(ls[LAST] & 0xFFFFu);
+    const bool pre = z0;   // output prefilled with s0 (hf_prefill_kernel: the same test)
+    const unsigned long long e0 = (unsigned long long)s0 * 0x0001000100010001ull;
     while (todo) {
         const uint32_t win = r.peek32();
         if (todo >= 32 && ((z0 && win == 0u) || (z1 && win == 0xFFFFFFFFu))) {
-            emit_run32(out, base, from, p, lo, hi, win ? s1 : s0);
+            emit_run32(out, base, from, p, lo, hi, win ? s1 : s0, pre, e0);
             r.skip(32);
             todo -= 32;
             continue;
@@ -1460,7 +1489,7 @@ __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_
         }
         p += c;
         if (p >= 8) {
-            put_chunk(out, base, lo, hi, from, 8);
+            put_chunk(out, base, lo, hi, from, 8, pre, e0);
             base += 8;
             from = 0;
             lo = spill;
@@ -1656,6 +1685,7 @@ FZB_API int fzb_huffman_decode(const uint8_t* d_stream, uint64_t nbytes, uint64_
     cudaLaunchCooperativeKernel((const void*)hf_sync_coop_kernel, dim3(gridc), dim3(HD_THREADS), kargs, 0, st);
     const int fin = 0;
     fzscan::exclusive(cn_[fin], nsub, offs, scal, scan_ws, st);
+    hf_prefill_kernel<<<kNumSMs * 8, 256, 0, st>>>(lut_s, lut_m, n, d_codes);
     hf_write_dec2_kernel<<<blocks, HD_THREADS, 0, st>>>(words, total_bits, nsub, T, lut_s, lut_m, sym_sorted,
                                                         st_[fin], cn_[fin], er_[fin], offs, n, d_codes, scal + 1,
                                                         scal + 4);

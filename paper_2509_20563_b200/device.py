@@ -500,7 +500,7 @@ class Engine:
             nbytes = (sz["size"] + 7) // 8
             hws = self.buf("hdws" + tag, L.fzb_huffman_decode_workspace_bytes(nbytes, nsym))
             self._call("fzb_huffman_decode", _p(b["hfout"]), nbytes, n, _p(b["lengths"]), nsym, _p(codes), _p(hws),
-                       hws.numel(), _p(status), sp, nk=10)
+                       hws.numel(), _p(status), sp, nk=11)
         else:
             bws = self.buf("dbsws" + tag, L.fzb_bitshuffle_workspace_bytes(n))
             self._call("fzb_bitshuffle_decode", _p(b["bsmap"]), _p(b["bspay"]), sz["size"], n, da.radius, _p(codes),
@@ -693,7 +693,7 @@ class Engine:
             s = self.upload("dstream" + tag, stream, pad=16, stage=stage)
             hws = self.buf("hdws" + tag, L.fzb_huffman_decode_workspace_bytes(len(stream), nsym))
             self._call("fzb_huffman_decode", _p(s), len(stream), n, _p(lengths), nsym, _p(codes), _p(hws),
-                       hws.numel(), _p(status), sp, nk=10)
+                       hws.numel(), _p(status), sp, nk=11)
         else:
             bitmap, payload = segs["bitmap"], segs["payload"]
             nb = (n + 255) // 256
