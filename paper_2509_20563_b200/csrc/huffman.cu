@@ -853,11 +853,10 @@ __global__ void __launch_bounds__(HE_THREADS) hf_write2_kernel(const uint16_t* _
                                                                uint32_t nsym,
                                                                const unsigned long long* __restrict__ cta_off,
                                                                const uint8_t* __restrict__ all_r_chunk,
-                                                               uint32_t* __restrict__ out, uint64_t cap_words) {
+                                                               uint32_t* __restrict__ out, uint64_t cap_words,
+                                                               uint64_t nc) {
     __shared__ unsigned long long tmp[33];
     __shared__ uint32_t buf[HE_WORDS + 1];
-    const uint64_t base = ((uint64_t)blockIdx.x * HE_THREADS + threadIdx.x) * HE_PER;
-    const unsigned long long G = __ldg(cta_off + blockIdx.x);   // issued early: read after the packing
     const uint32_t R = nsym >> 1;
     const unsigned long long vr = __ldg(lc + R);
     const uint32_t lr = (uint32_t)vr & 0xFFu;
@@ -865,7 +864,36 @@ __global__ void __launch_bounds__(HE_THREADS) hf_write2_kernel(const uint16_t* _
     // a chunk the count pass saw as all R (and whose run fits the pattern):
     // its bits are known without reading the codes again
     const bool runs = lr != 0 && lr * HE_PER <= 64;   // R's run of HE_PER codewords fits `pat`
-    const bool chunk_r = runs && all_r_chunk[blockIdx.x];
+    // grid-stride over the 4096-code chunks: on low-entropy fields nearly
+    // every chunk exits at once, and ~70K one-chunk CTAs cost more to launch
+    // than to run
+    // R's codeword all zero bits (the usual "0"): an all-R chunk writes only
+    // zeros into the zeroed stream (hf_zero_kernel) -- nothing to do.  The
+    // CTA reads the flags of its next HE_THREADS chunks at once (one per
+    // thread) and runs only the chunks left in the compacted list.
+    __shared__ uint32_t s_list[HE_THREADS];
+    __shared__ uint32_t s_wc[HE_THREADS / 32 + 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint64_t span = (uint64_t)gridDim.x * HE_THREADS;
+    for (uint64_t c0 = blockIdx.x; c0 < nc; c0 += span) {
+    const uint64_t mine = c0 + (uint64_t)threadIdx.x * gridDim.x;
+    const bool work = mine < nc && !(runs && pat == 0 && all_r_chunk[mine]);
+    const unsigned bal = __ballot_sync(0xffffffffu, work);
+    if (lane == 0) s_wc[wid] = __popc(bal);
+    __syncthreads();
+    uint32_t before = 0, nwork = 0;
+#pragma unroll
+    for (int w = 0; w < HE_THREADS / 32; w++) {
+        before += w < wid ? s_wc[w] : 0u;
+        nwork += s_wc[w];
+    }
+    if (work) s_list[before + __popc(bal & lanemask_lt())] = threadIdx.x;
+    __syncthreads();
+    for (uint32_t li = 0; li < nwork; li++) {
+    const uint64_t chunk = c0 + (uint64_t)s_list[li] * gridDim.x;
+    const uint64_t base = (chunk * HE_THREADS + threadIdx.x) * HE_PER;
+    const bool chunk_r = runs && all_r_chunk[chunk];
+    const unsigned long long G = __ldg(cta_off + chunk);
     uint32_t c[HE_PER];
     bool fast = chunk_r;
     if (!chunk_r) {
@@ -933,7 +961,8 @@ __global__ void __launch_bounds__(HE_THREADS) hf_write2_kernel(const uint16_t* _
         if (filled > 0) atomicOr(buf + w, (uint32_t)(acc >> 32));
     }
     __syncthreads();
-    if (total == 0) return;
+    if (total == 0) continue;   // uniform; buf is rewritten only after the next clear + barrier
+
     const int sh = (int)(G & 31);
     const uint64_t w0 = G >> 5, w1 = (G + total - 1) >> 5;   // global words touched
     const uint32_t nw = (uint32_t)(w1 - w0 + 1);
@@ -945,6 +974,10 @@ __global__ void __launch_bounds__(HE_THREADS) hf_write2_kernel(const uint16_t* _
         if (gw >= cap_words) continue;
         if (q == 0 || q == nw - 1) atomicOr(out + gw, bswap32(word));   // shared with the neighbouring CTAs
         else out[gw] = bswap32(word);
+    }
+    __syncthreads();   // buf is cleared by the next chunk
+    }
+    __syncthreads();   // s_list / s_wc are rewritten by the next span
     }
 }
 
@@ -1608,8 +1641,8 @@ FZB_API int fzb_huffman_encode(const uint16_t* d_codes, uint64_t n, const uint8_
     hf_check_kernel<<<1, 1, 0, st>>>(tot, want, d_status);
     hf_zero_kernel<<<kNumSMs * 4, 256, 0, st>>>(out, tot, cap_words);
     hf_pack_table_kernel<<<(nsym + 255) / 256, 256, 0, st>>>(d_lengths, d_codewords, nsym, lc);
-    hf_write2_kernel<<<(unsigned)nc, HE_THREADS, 0, st>>>(d_codes, n, lc, nsym, cta_off, all_r_chunk, out,
-                                                         cap_words);
+    hf_write2_kernel<<<(unsigned)(nc < (uint64_t)kNumSMs * 8 ? nc : (uint64_t)kNumSMs * 8), HE_THREADS, 0, st>>>(
+        d_codes, n, lc, nsym, cta_off, all_r_chunk, out, cap_words, nc);
     return fzb_check_launch();
 }
 
