@@ -113,6 +113,12 @@ FZB_API int fzb_outlier_check(const uint64_t *d_idx, uint64_t k, uint64_t n, con
 /* d_bins u64[nbins] is zeroed here; codes >= nbins set FZB_ERR_CODE_RANGE. */
 FZB_API int fzb_histogram(const uint16_t *d_codes, uint64_t n, uint32_t nbins, uint64_t *d_bins,
                           uint32_t *d_status, void *stream);
+/* Same, plus d_notr u8[ceil(n / FZB_HF_CHUNK)]: 1 iff that chunk of codes holds
+ * a code other than nbins / 2 (the zero-code R).  fzb_huffman_encode_chunks
+ * uses it to skip re-reading chunks that are all R (low-entropy fields). */
+#define FZB_HF_CHUNK 4096
+FZB_API int fzb_histogram_chunks(const uint16_t *d_codes, uint64_t n, uint32_t nbins, uint64_t *d_bins,
+                                 uint8_t *d_notr, uint32_t *d_status, void *stream);
 
 /* ---- a8: codebook (encode.py:118-217) ----------------------------------- */
 FZB_API size_t fzb_huffman_build_workspace_bytes(uint32_t nsym);
@@ -130,6 +136,12 @@ FZB_API int fzb_huffman_encode(const uint16_t *d_codes, uint64_t n, const uint8_
                                const uint32_t *d_codewords, uint32_t nsym, const uint64_t *d_bit_count,
                                uint8_t *d_out, uint64_t out_cap, void *d_ws, size_t ws_bytes, uint32_t *d_status,
                                void *stream);
+/* Same stream; d_notr from fzb_histogram_chunks over the same codes (NULL =
+ * read every chunk). */
+FZB_API int fzb_huffman_encode_chunks(const uint16_t *d_codes, uint64_t n, const uint8_t *d_lengths,
+                                      const uint32_t *d_codewords, uint32_t nsym, const uint64_t *d_bit_count,
+                                      const uint8_t *d_notr, uint8_t *d_out, uint64_t out_cap, void *d_ws,
+                                      size_t ws_bytes, uint32_t *d_status, void *stream);
 
 /* ---- a10: Huffman decode (encode.py:234-317) ----------------------------- */
 FZB_API size_t fzb_huffman_decode_workspace_bytes(uint64_t nbytes, uint32_t nsym);

@@ -26,6 +26,8 @@
 //    short-cuts the canonical first_code/limit walk of encode.py:234-276;
 //    truncation / invalid-code / trailing / padding checks reproduce
 //    encode.py:299-316 exactly.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "scan.cuh"
 #include "lookback.cuh"
@@ -820,6 +822,67 @@ __global__ void __launch_bounds__(HE_THREADS) hf_count_kernel(const uint16_t* __
     if (threadIdx.x == 0) cta_bits[blockIdx.x] = (uint32_t)tot;   // <= 32 * HE_CHUNK
 }
 
+// Count pass with the histogram's chunk flags (fzb_histogram_chunks): a full
+// chunk without a code != R is all R -- its bit total is HE_CHUNK * len(R)
+// and its codes are not read; persistent CTAs compact the rest (as in
+// hf_write2_kernel) and count them like hf_count_kernel.
+__global__ void __launch_bounds__(HE_THREADS) hf_count3_kernel(const uint16_t* __restrict__ codes, uint64_t n,
+                                                               const uint8_t* __restrict__ lengths, uint32_t nsym,
+                                                               const uint8_t* __restrict__ notr,
+                                                               uint32_t* __restrict__ cta_bits,
+                                                               uint8_t* __restrict__ all_r_chunk, uint64_t nc) {
+    __shared__ unsigned long long tmp[33];
+    __shared__ uint32_t s_list[HE_THREADS];
+    __shared__ uint32_t s_wc[HE_THREADS / 32 + 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t R = nsym >> 1;
+    const uint32_t lr = __ldg(lengths + R);
+    const uint64_t nfull = n / HE_CHUNK;
+    const uint64_t span = (uint64_t)gridDim.x * HE_THREADS;
+    for (uint64_t c0 = blockIdx.x; c0 < nc; c0 += span) {
+        const uint64_t mine = c0 + (uint64_t)threadIdx.x * gridDim.x;
+        const bool known = mine < nfull && !notr[mine];
+        if (known) {
+            cta_bits[mine] = (uint32_t)HE_CHUNK * lr;
+            all_r_chunk[mine] = 1;
+        }
+        const bool work = mine < nc && !known;
+        const unsigned bal = __ballot_sync(0xffffffffu, work);
+        if (lane == 0) s_wc[wid] = __popc(bal);
+        __syncthreads();
+        uint32_t before = 0, nwork = 0;
+#pragma unroll
+        for (int w = 0; w < HE_THREADS / 32; w++) {
+            before += w < wid ? s_wc[w] : 0u;
+            nwork += s_wc[w];
+        }
+        if (work) s_list[before + __popc(bal & lanemask_lt())] = threadIdx.x;
+        __syncthreads();
+        for (uint32_t li = 0; li < nwork; li++) {
+            const uint64_t chunk = c0 + (uint64_t)s_list[li] * gridDim.x;
+            const uint64_t base = (chunk * HE_THREADS + threadIdx.x) * HE_PER;
+            uint32_t c[HE_PER];
+            load16(codes, n, base, c);
+            unsigned long long b = 0;
+            const bool ar = all_r(c, R);
+            const bool all = __syncthreads_and(ar);
+            if (threadIdx.x == 0) all_r_chunk[chunk] = all ? 1 : 0;
+            if (ar) {
+                b = (unsigned long long)HE_PER * lr;
+            } else {
+#pragma unroll
+                for (int e = 0; e < HE_PER; e++)
+                    if (c[e] < nsym) b += __ldg(lengths + c[e]);
+            }
+            unsigned long long tot;
+            block_exclusive_scan64(b, tmp, &tot);
+            if (threadIdx.x == 0) cta_bits[chunk] = (uint32_t)tot;
+            __syncthreads();   // tmp is reused by the next chunk's scan
+        }
+        __syncthreads();   // s_list / s_wc are rewritten by the next span
+    }
+}
+
 __global__ void hf_zero_kernel(uint32_t* __restrict__ out, const unsigned long long* __restrict__ bits,
                                uint64_t cap_words) {
     uint64_t words = (*bits + 31) / 32;
@@ -1441,7 +1504,8 @@ __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_
                                                                    const unsigned long long* __restrict__ offs,
                                                                    uint64_t n, uint16_t* __restrict__ out,
                                                                    unsigned long long* __restrict__ end_pos,
-                                                                   unsigned long long* __restrict__ best) {
+                                                                   unsigned long long* __restrict__ best,
+                                                                   bool prefilled) {
     __shared__ unsigned long long ls[1 << LUT_BITS];
     __shared__ uint16_t lm[1 << LUT_BITS];
     __shared__ DecTables T;
@@ -1473,7 +1537,7 @@ __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_
     const bool z0 = (lm[0] & 7u) && ((lm[0] >> 7) & 15u) == 1u;
     const bool z1 = (lm[LAST] & 7u) && ((lm[LAST] >> 7) & 15u) == 1u;
     const uint32_t s0 = (uint32_t)(ls[0] & 0xFFFFu), s1 = (uint32_t)(ls[LAST] & 0xFFFFu);
-    const bool pre = z0;   // output prefilled with s0 (hf_prefill_kernel: the same test)
+    const bool pre = z0 && prefilled;   // output prefilled with s0 (hf_prefill_kernel: the same test)
     const unsigned long long e0 = (unsigned long long)s0 * 0x0001000100010001ull;
     while (todo) {
         const uint32_t win = r.peek32();
@@ -1619,6 +1683,15 @@ FZB_API int fzb_huffman_encode(const uint16_t* d_codes, uint64_t n, const uint8_
                                const uint32_t* d_codewords, uint32_t nsym, const uint64_t* d_bit_count,
                                uint8_t* d_out, uint64_t out_cap, void* d_ws, size_t ws_bytes, uint32_t* d_status,
                                void* stream) {
+    return fzb_huffman_encode_chunks(d_codes, n, d_lengths, d_codewords, nsym, d_bit_count, nullptr, d_out, out_cap,
+                                     d_ws, ws_bytes, d_status, stream);
+}
+
+FZB_API int fzb_huffman_encode_chunks(const uint16_t* d_codes, uint64_t n, const uint8_t* d_lengths,
+                                      const uint32_t* d_codewords, uint32_t nsym, const uint64_t* d_bit_count,
+                                      const uint8_t* d_notr, uint8_t* d_out, uint64_t out_cap, void* d_ws,
+                                      size_t ws_bytes, uint32_t* d_status, void* stream) {
+    static_assert(HE_CHUNK == FZB_HF_CHUNK, "chunk flags");
     cudaStream_t st = (cudaStream_t)stream;
     if (ws_bytes < fzb_huffman_encode_workspace_bytes(n)) return FZB_E_WORKSPACE;
     if ((reinterpret_cast<uintptr_t>(d_out) & 3) || (reinterpret_cast<uintptr_t>(d_codes) & 15)) return FZB_E_ARG;
@@ -1635,13 +1708,20 @@ FZB_API int fzb_huffman_encode(const uint16_t* d_codes, uint64_t n, const uint8_
     const uint64_t cap_words = out_cap / 4;
     uint32_t* out = reinterpret_cast<uint32_t*>(d_out);
     const unsigned long long* want = reinterpret_cast<const unsigned long long*>(d_bit_count);
-    hf_count_kernel<<<(unsigned)nc, HE_THREADS, 0, st>>>(d_codes, n, d_lengths, nsym,
-                                                        reinterpret_cast<uint32_t*>(cta_bits), all_r_chunk);
+    if (d_notr)
+        hf_count3_kernel<<<(unsigned)(nc < (uint64_t)kNumSMs * 32 ? nc : (uint64_t)kNumSMs * 32), HE_THREADS, 0, st>>>(
+            d_codes, n, d_lengths, nsym, d_notr, reinterpret_cast<uint32_t*>(cta_bits), all_r_chunk, nc);
+    else
+        hf_count_kernel<<<(unsigned)nc, HE_THREADS, 0, st>>>(d_codes, n, d_lengths, nsym,
+                                                            reinterpret_cast<uint32_t*>(cta_bits), all_r_chunk);
     fzscan::exclusive(reinterpret_cast<uint32_t*>(cta_bits), nc, cta_off, tot, scan_ws, st);
     hf_check_kernel<<<1, 1, 0, st>>>(tot, want, d_status);
     hf_zero_kernel<<<kNumSMs * 4, 256, 0, st>>>(out, tot, cap_words);
     hf_pack_table_kernel<<<(nsym + 255) / 256, 256, 0, st>>>(d_lengths, d_codewords, nsym, lc);
-    hf_write2_kernel<<<(unsigned)(nc < (uint64_t)kNumSMs * 8 ? nc : (uint64_t)kNumSMs * 8), HE_THREADS, 0, st>>>(
+    // persistent grid: 4 waves of 8 CTAs per SM (dense streams keep the
+    // per-chunk CTA turnover, sparse ones the few launches)
+    const uint64_t pgrid = (uint64_t)kNumSMs * 32;
+    hf_write2_kernel<<<(unsigned)(nc < pgrid ? nc : pgrid), HE_THREADS, 0, st>>>(
         d_codes, n, lc, nsym, cta_off, all_r_chunk, out, cap_words, nc);
     return fzb_check_launch();
 }
@@ -1718,10 +1798,15 @@ FZB_API int fzb_huffman_decode(const uint8_t* d_stream, uint64_t nbytes, uint64_
     cudaLaunchCooperativeKernel((const void*)hf_sync_coop_kernel, dim3(gridc), dim3(HD_THREADS), kargs, 0, st);
     const int fin = 0;
     fzscan::exclusive(cn_[fin], nsub, offs, scal, scan_ws, st);
-    hf_prefill_kernel<<<kNumSMs * 8, 256, 0, st>>>(lut_s, lut_m, n, d_codes);
+    // the s0 prefill pays when most 8-symbol chunks are all s0: at <= 1.125
+    // bits per symbol P(s0) >= 0.875 (any other codeword has >= 2 bits), so
+    // >= 34% of the chunks skip their uncoalesced store -- the break-even
+    // against one coalesced pass over the output
+    const bool prefill = total_bits * 8 <= 9ull * n;
+    if (prefill) hf_prefill_kernel<<<kNumSMs * 8, 256, 0, st>>>(lut_s, lut_m, n, d_codes);
     hf_write_dec2_kernel<<<blocks, HD_THREADS, 0, st>>>(words, total_bits, nsub, T, lut_s, lut_m, sym_sorted,
                                                         st_[fin], cn_[fin], er_[fin], offs, n, d_codes, scal + 1,
-                                                        scal + 4);
+                                                        scal + 4, prefill);
     hf_final2_kernel<<<1, 1, 0, st>>>(n, nbytes, d_stream, scal, scal + 1, scal + 4, d_status);
     return fzb_check_launch();
 }

@@ -161,8 +161,6 @@ Pass make_pass(long long n0, long long n1, long long n2, long long h, int axis) 
     return p;
 }
 
-void pad3(uint32_t& n0, uint32_t& n1, uint32_t& n2) { (void)n0; (void)n1; (void)n2; }
-
 template <bool DEC>
 int run_passes(const float* orig, uint16_t* codes, float* recon, uint32_t* bitmap, uint32_t n0, uint32_t n1,
                uint32_t n2, const double* d_eb, uint32_t radius, uint32_t stride, const double* w, cudaStream_t st,
@@ -403,7 +401,6 @@ __global__ void __launch_bounds__(256) interp_profile_kernel(const float* __rest
         const int m = min(lb[0], min(lb[1], lb[2]));
 #pragma unroll
         for (int s = 0; s < 2; s++) {
-            const int A = s == 0 ? 16 : 8;
             if (m >= (s == 0 ? 4 : 3)) {   // an anchor of this lattice
 #pragma unroll
                 for (int wi = 0; wi < 3; wi++) acc[3 * s + wi] += 32;
@@ -430,7 +427,6 @@ __global__ void __launch_bounds__(256) interp_profile_kernel(const float* __rest
                 const unsigned int iv = (unsigned int)rint(e);
                 acc[3 * s + wi] += iv ? (unsigned long long)(32 - __clz(iv)) : 0ull;
             }
-            (void)A;
         }
     }
 #pragma unroll

@@ -443,63 +443,12 @@ __global__ void lz1d_super_kernel(const float* __restrict__ bmin, const float* _
     }
 }
 
-// quantize(v, pred) == (radius, not outlier), with the chain cut short: a
-// zero code needs floor(|q|) == 0, so fr == |q| and the tie re-division only
-// matters near |q| == 0.5; the error check of s == 0 runs in parallel.
-// (40M randomised cases incl. ties and huge/tiny bounds agree with quantize.)
-FZB_DEV bool zero_code(double v, double pred, const QParams& P) {
-    const double d = __dsub_rn(v, pred);
-    double aq;
-    if (P.use_recip) {
-        aq = fabs(__dmul_rn(d, P.inv2eb));
-        const double tol = __dmul_rn(aq, 1.7763568394002505e-15) + 1e-300;
-        if (fabs(__dsub_rn(aq, 0.5)) <= tol) aq = fabs(__ddiv_rn(d, P.two_eb));
-    } else {
-        aq = fabs(__ddiv_rn(d, P.two_eb));
-    }
-    const float rc = __double2float_rn(__dadd_rn(pred, __dmul_rn(P.two_eb, 0.0)));
-    return aq < 0.5 && fabs(__dsub_rn((double)rc, v)) <= P.eb && P.radius > 0;
-}
 FZB_DEV uint32_t fkey(float f) {
     const uint32_t u = __float_as_uint(f);
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 FZB_DEV float kfloat(uint32_t k) { return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k); }
 
-// Exact bounds of the zero-code key interval that contains k0 = key(state).
-// The predicate is monotone on each side of k0 (true up to the bound, false
-// beyond), so 32-key windows started at the estimate c (key of r -/+ eb)
-// pin the transition, sliding until it lies inside the window.
-FZB_DEV bool zkey(long long k, double pred, const QParams& P) {
-    if (k < 0 || k > 0xFFFFFFFFll) return false;
-    const float f = kfloat((uint32_t)k);
-    return isfinite(f) && zero_code((double)f, pred, P);
-}
-// Both bounds at once: lanes 0-15 slide a 16-key window for the upper bound,
-// lanes 16-31 one for the lower bound.
-FZB_DEV void zbounds(long long k0, long long cu, long long cl, double pred, const QParams& P, uint32_t& khi,
-                     uint32_t& klo) {
-    const int lane = threadIdx.x & 31, h = lane >> 4, q = lane & 15;
-    long long wu = max(cu - 8, k0);      // upper window [wu, wu + 16)
-    long long el = min(cl + 7, k0);      // lower window (el - 16, el]
-    bool du = false, dl = false;
-    while (!(du && dl)) {
-        const long long key = h == 0 ? wu + q : el - 15 + q;
-        const bool z = zkey(key, pred, P);
-        const unsigned bal = __ballot_sync(0xffffffffu, z);
-        const unsigned mu = bal & 0xFFFFu, ml = bal >> 16;
-        if (!du) {
-            if (mu == 0xFFFFu) wu += 16;
-            else if (mu == 0) wu = max(wu - 16, k0);
-            else { khi = (uint32_t)(wu + __ffs(~mu) - 2); du = true; }   // trues occupy the low lanes
-        }
-        if (!dl) {
-            if (ml == 0xFFFFu) el -= 16;
-            else if (ml == 0) el = min(el + 16, k0);
-            else { klo = (uint32_t)(el - 15 + __ffs(ml) - 1); dl = true; }   // trues occupy the high lanes
-        }
-    }
-}
 
 // Superblock summaries live in shared memory (when they fit), and the
 // element loads of the current block are issued before the zero-interval
@@ -649,52 +598,15 @@ FZB_DEV int quantize_walk(double v, double pred, const QParams& P, float& rec, b
     return ok ? (int)(uint32_t)__double_as_longlong(tq) + P.radius : P.radius;
 }
 
-// Exact zero-code interval [zlo, zhi] of the state whose prediction is pred
-// (never -0.0).  One round: lanes 0-15 test the 16 keys around RN32(pred+eb),
-// lanes 16-31 the 16 around RN32(pred-eb), with zero_code's arithmetic and
-// the state's own RN32(pred) hoisted; the rare near-tie lanes re-divide (one
-// warp-uniform branch).  When a transition falls outside its window
-// (tiny / huge bounds), the sliding search (zbounds) takes over.
-FZB_DEV void zinterval(double pred, const QParams& P, float& zlo, float& zhi) {
-    const int lane = threadIdx.x & 31, q = lane & 15;
-    const float rp = __double2float_rn(pred);
-    const double rcd = (double)__double2float_rn(__dadd_rn(pred, __dmul_rn(P.two_eb, 0.0)));
-    const long long k0 = fkey(rp);
-    const long long cu = fkey(__double2float_rn(__dadd_rn(pred, P.eb)));
-    const long long cl = fkey(__double2float_rn(__dsub_rn(pred, P.eb)));
-    const long long wu = max(cu - 8, k0), el = min(cl + 7, k0);
-    const long long key = lane < 16 ? wu + q : el - 15 + q;
-    const bool valid = key >= 0 && key <= 0xFFFFFFFFll;
-    const float f = valid ? kfloat((uint32_t)key) : 0.f;
-    const double v = (double)f;
-    const double d = __dsub_rn(v, pred);
-    double aq = fabs(__dmul_rn(d, P.inv2eb));
-    const bool near = valid && (!P.use_recip || fabs(__dsub_rn(aq, 0.5)) <= __dmul_rn(aq, 1.7763568394002505e-15) + 1e-300);
-    if (__any_sync(0xffffffffu, near)) {   // rare: exact division for the lanes near a .5 tie
-        if (near) aq = fabs(__ddiv_rn(d, P.two_eb));
-    }
-    const bool z = valid && isfinite(f) && aq < 0.5 && fabs(__dsub_rn(rcd, v)) <= P.eb && P.radius > 0;
-    const unsigned bal = __ballot_sync(0xffffffffu, z);
-    const unsigned mu = bal & 0xFFFFu, ml = bal >> 16;
-    if (mu != 0xFFFFu && mu != 0 && ml != 0xFFFFu && ml != 0) {
-        zhi = kfloat((uint32_t)(wu + __ffs(~mu) - 2));      // trues occupy the low lanes
-        zlo = kfloat((uint32_t)(el - 15 + __ffs(ml) - 1));  // trues occupy the high lanes
-        return;
-    }
-    uint32_t khi = 0, klo = 0;
-    zbounds(k0, cu, cl, pred, P, khi, klo);
-    zlo = kfloat(klo);
-    zhi = kfloat(khi);
-}
 
 // An INNER zero-code interval: [ilo, ihi] with |v - pred| <= eb - m/2 for
 // every f32 v in it, m = eb 2^-20 + (|pred| + eb) 2^-44, which dominates the
 // rounding of the few f64 ops below.  Such a v has |q| < 0.5 - 2^-22 (no tie
 // re-division) and |RN32(pred) - v| <= eb, i.e. a zero code: the interval is
-// a subset of the exact one (zinterval), so a scan with it finds every event,
+// a subset of the exact zero-code set, so a scan with it finds every event,
 // plus -- when an element falls in the sliver between the two, width ~m --
 // a false candidate, which the event step quantizes to code R with the state
-// unchanged.  Six f64 ops instead of a ballot round of zero_code.
+// unchanged.  Six f64 ops instead of a ballot round over candidate keys.
 FZB_DEV void zinner(double pred, const QParams& P, float& ilo, float& ihi) {
     const double m = __dadd_rn(__dmul_rn(P.eb, 9.5367431640625e-07), __dmul_rn(__dadd_rn(fabs(pred), P.eb), 5.684341886080802e-14));
     const double w = __dsub_rn(P.eb, m);

@@ -84,6 +84,13 @@ def _interp_nk(n0, n1, n2, stride):
     return 1 + levels * (3 if n0 > 1 else 1)
 
 
+def _hf_decode_nk(nbytes, n):
+    """Kernels one fzb_huffman_decode call launches: tables, 3 sweeps, the
+    cooperative sweep, a 3-kernel scan, the write pass, the final check, and
+    the s0 prefill when the stream has <= 1.125 bits per symbol (huffman.cu)."""
+    return 10 + int(nbytes * 8 * 8 <= 9 * n)
+
+
 class _NodeEvent:
     """A CUDA event recorded as an event-record node of a captured graph
     (torch.cuda.Event creates its handle lazily, at the first record)."""
@@ -343,7 +350,8 @@ class Engine:
         nsym = 2 * radius
         if codec == "huffman":
             bins = self.buf("bins" + tag, 8 * nsym)
-            self._call("fzb_histogram", _p(codes), n, nsym, _p(bins), _p(status), sp)
+            notr = self.buf("notr" + tag, (n + 4095) // 4096)   # chunk flags for the encoder's count pass
+            self._call("fzb_histogram_chunks", _p(codes), n, nsym, _p(bins), _p(notr), _p(status), sp)
             self._mark("primary")
             lengths = self.buf("lengths" + tag, nsym)
             cw = self.buf("cw" + tag, 4 * nsym)
@@ -354,8 +362,8 @@ class Engine:
             cap = 4 * n + 16
             out = self.buf("hfout" + tag, cap)
             hws = self.buf("hews" + tag, L.fzb_huffman_encode_workspace_bytes(n))
-            self._call("fzb_huffman_encode", _p(codes), n, _p(lengths), _p(cw), nsym, _p(bitcount), _p(out), cap,
-                       _p(hws), hws.numel(), _p(status), sp, nk=5)
+            self._call("fzb_huffman_encode_chunks", _p(codes), n, _p(lengths), _p(cw), nsym, _p(bitcount), _p(notr),
+                       _p(out), cap, _p(hws), hws.numel(), _p(status), sp, nk=5)
             bufs.update(lengths=lengths, bitcount=bitcount, hfout=out)
         elif codec == "bitshuffle":
             self._mark("primary")
@@ -500,7 +508,7 @@ class Engine:
             nbytes = (sz["size"] + 7) // 8
             hws = self.buf("hdws" + tag, L.fzb_huffman_decode_workspace_bytes(nbytes, nsym))
             self._call("fzb_huffman_decode", _p(b["hfout"]), nbytes, n, _p(b["lengths"]), nsym, _p(codes), _p(hws),
-                       hws.numel(), _p(status), sp, nk=11)
+                       hws.numel(), _p(status), sp, nk=_hf_decode_nk(nbytes, n))
         else:
             bws = self.buf("dbsws" + tag, L.fzb_bitshuffle_workspace_bytes(n))
             self._call("fzb_bitshuffle_decode", _p(b["bsmap"]), _p(b["bspay"]), sz["size"], n, da.radius, _p(codes),
@@ -693,7 +701,7 @@ class Engine:
             s = self.upload("dstream" + tag, stream, pad=16, stage=stage)
             hws = self.buf("hdws" + tag, L.fzb_huffman_decode_workspace_bytes(len(stream), nsym))
             self._call("fzb_huffman_decode", _p(s), len(stream), n, _p(lengths), nsym, _p(codes), _p(hws),
-                       hws.numel(), _p(status), sp, nk=11)
+                       hws.numel(), _p(status), sp, nk=_hf_decode_nk(len(stream), n))
         else:
             bitmap, payload = segs["bitmap"], segs["payload"]
             nb = (n + 255) // 256

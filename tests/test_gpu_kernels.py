@@ -191,3 +191,52 @@ def test_huffman_build_large_alphabets_vs_oracle(oracle, seed):
     cl, ostream, obits = oracle.huffman_encode(codes, h.bins)
     assert np.array_equal(cb.code_lengths, cl) and bits == obits and stream == ostream
     assert np.array_equal(enc.huffman_decode(cb, stream, codes.size), codes)
+
+
+@pytest.mark.parametrize("n,seed", [(4096 * 5, 0), (4096 * 5 + 3, 1), (4096 * 7 + 4095, 2), (12345, 3), (8191, 4),
+                                    (4096 * 64, 5), (4096 * 64 + 8, 6)])
+def test_histogram_chunk_flags_and_flagged_encode(oracle, n, seed):
+    # fzb_histogram_chunks flags exactly the 4096-code chunks holding a code
+    # != R (incl. a chunk's first/last code and the partial tail), and the
+    # flag-driven count pass (fzb_huffman_encode_chunks) writes the same
+    # stream as the unflagged one and the oracle
+    from paper_2509_20563_b200.encode import _build, _fetch, _status, _upload_codes
+    from paper_2509_20563_b200.device import _p, default_engine
+    rng = np.random.default_rng(seed)
+    radius = 512
+    R = radius
+    c = np.full(n, R, np.uint16)
+    pos = list(rng.choice(n, min(n, 40), replace=False)) + [0, n - 1, min(n - 1, 4095), min(n - 1, 4096)]
+    c[pos] = rng.integers(R - 20, R + 20, len(pos)).astype(np.uint16)
+    c[min(n - 1, 8192 + 7)] = R   # may undo one of the above: flags must follow the final bytes
+    eng = default_engine()
+    nsym = 2 * radius
+    d = _upload_codes(eng, "t_codes", c)
+    bins = eng.buf("t_bins", 8 * nsym)
+    nc = (n + 4095) // 4096
+    notr = eng.buf("t_notr", nc)
+    st = eng.buf("dstatus", 8, zero=True)
+    eng._call("fzb_histogram_chunks", _p(d), n, nsym, _p(bins), _p(notr), _p(st), eng.sp)
+    got_bins = np.frombuffer(_fetch(eng, bins, 8 * nsym), np.uint64)
+    assert np.array_equal(got_bins, np.bincount(c, minlength=nsym).astype(np.uint64))
+    got_flags = np.frombuffer(_fetch(eng, notr, nc), np.uint8)
+    want_flags = np.array([np.any(c[4096 * k:4096 * (k + 1)] != R) for k in range(nc)], np.uint8)
+    assert np.array_equal(got_flags, want_flags)
+    lengths, cw, bc = _build(eng, got_bins.copy())
+    cap = 4 * n + 16
+    streams = []
+    for flagged in (False, True):
+        out = eng.buf(f"t_out{int(flagged)}", cap, zero=True)
+        ws = eng.buf("t_ws", eng.lib.fzb_huffman_encode_workspace_bytes(n))
+        if flagged:
+            eng._call("fzb_huffman_encode_chunks", _p(d), n, _p(lengths), _p(cw), nsym, _p(bc), _p(notr), _p(out), cap,
+                      _p(ws), ws.numel(), _p(st), eng.sp)
+        else:
+            eng._call("fzb_huffman_encode", _p(d), n, _p(lengths), _p(cw), nsym, _p(bc), _p(out), cap, _p(ws),
+                      ws.numel(), _p(st), eng.sp)
+        bits = int(np.frombuffer(_fetch(eng, bc, 8), np.uint64)[0])
+        streams.append(_fetch(eng, out, (bits + 7) // 8))
+    assert _status(eng) == 0
+    assert streams[0] == streams[1]
+    _, ostream, _ = oracle.huffman_encode(c.astype(np.uint32), got_bins.copy())
+    assert streams[1] == ostream

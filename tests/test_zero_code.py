@@ -1,6 +1,8 @@
-"""The 1D walker's short zero-code predicate (lorenzo.cu zero_code) against
-the full quantizer (common.cuh quantize, predict.py:93-115 semantics) on 40M
-randomised (value, prediction, bound) cases incl. ties and extreme bounds.
+"""The short zero-code predicate (a zero code needs floor(|q|) == 0, so only
+|q| near 0.5 needs the tie re-division) against the full quantizer
+(common.cuh quantize, predict.py:93-115 semantics) on 40M randomised (value,
+prediction, bound) cases incl. ties and extreme bounds -- the condition the
+1D walker's inner zero-code interval (lorenzo.cu zinner) is a subset of.
 Both are restated in plain C with the device's rounding (no FMA contraction)."""
 import os
 import shutil
