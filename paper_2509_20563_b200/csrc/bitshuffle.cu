@@ -212,19 +212,9 @@ __global__ void __launch_bounds__(BS_THREADS) bs_enc4_kernel(const uint16_t* __r
         uint32_t Wd[BS_BPW][4];
 #pragma unroll
         for (int q = 0; q < BS_BPW; q++) {
-            // a block of 256 equal codes v (low-entropy fields): word (p, w) is
-            // all ones iff bit p of v is set -- no transposes
-            const uint32_t u = r[q].x;
-            const bool same = r[q].y == u && r[q].z == u && r[q].w == u && (u >> 16) == (u & 0xFFFFu);
-            const uint32_t u0 = __shfl_sync(0xffffffffu, u, 0);   // (every lane: not inside the &&)
-            if (__all_sync(0xffffffffu, same && u == u0)) {
-#pragma unroll
-                for (int c = 0; c < 4; c++) Wd[q][c] = ((u >> (4 * gi + c)) & 1u) ? 0xFFFFFFFFu : 0u;
-            } else {
-                uint32_t E[4];
-                codes_to_planes(r[q], E);
-                planes_to_words(E, gi, xsel, Wd[q]);
-            }
+            uint32_t E[4];
+            codes_to_planes(r[q], E);
+            planes_to_words(E, gi, xsel, Wd[q]);
         }
         __syncthreads();   // (B) s_off prefix, s_agg, next ticket visible
         const uint32_t nxt = s_cta[(it + 1) & 1];
@@ -351,28 +341,9 @@ __global__ void __launch_bounds__(BS_THREADS) bs_dec3_kernel(const uint32_t* __r
     for (int q = 0; q < BS_BPW; q++) {
         const uint64_t blk = cblk + warp * BS_BPW + q;
         if (blk >= nblocks) break;
-        // every word 0 or all ones and the same for the 8 groups: a block of
-        // 256 equal codes (low-entropy fields) -- no transposes
-        bool full = true;
-        uint32_t nib = 0;
-#pragma unroll
-        for (int c = 0; c < 4; c++) {
-            full &= W[q][c] == 0u || W[q][c] == 0xFFFFFFFFu;
-            nib |= (W[q][c] != 0u ? 1u : 0u) << c;
-        }
-        uint4 rc;
-        const uint32_t nib0 = __shfl_sync(0xffffffffu, nib, gi);   // group 0's planes (every lane)
-        if (__all_sync(0xffffffffu, full && nib == nib0)) {
-            uint32_t v = 0;
-#pragma unroll
-            for (int k = 0; k < 4; k++) v |= __shfl_sync(0xffffffffu, nib, k) << (4 * k);
-            const uint32_t vv = v * 0x00010001u;
-            rc = make_uint4(vv, vv, vv, vv);
-        } else {
-            uint32_t E[4];
-            words_to_planes(W[q], gi, xsel, E);
-            rc = planes_to_codes(E);
-        }
+        uint32_t E[4];
+        words_to_planes(W[q], gi, xsel, E);
+        const uint4 rc = planes_to_codes(E);
         const uint64_t t0 = blk * 256 + 8 * lane;
         const uint32_t c8[8] = {rc.x & 0xFFFFu, rc.x >> 16, rc.y & 0xFFFFu, rc.y >> 16,
                                 rc.z & 0xFFFFu, rc.z >> 16, rc.w & 0xFFFFu, rc.w >> 16};

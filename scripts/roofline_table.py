@@ -18,7 +18,18 @@ ENTRY = {"lz1d_summary2": "fzb_lorenzo_encode_f32", "lz1d_super": "fzb_lorenzo_e
          "minmax": "fzb_minmax_f32", "interp_pass_kernel<0, 0>": "fzb_interp_encode_f32",
          "interp_pass_kernel<1, 0>": "fzb_interp_encode_f32", "interp_pass_kernel<2, 0>": "fzb_interp_encode_f32",
          "interp_pass_kernel<0, 1>": "fzb_interp_decode_f32", "interp_pass_kernel<1, 1>": "fzb_interp_decode_f32",
-         "interp_pass_kernel<2, 1>": "fzb_interp_decode_f32", "huffman_build": "fzb_huffman_build"}
+         "interp_pass_kernel<2, 1>": "fzb_interp_decode_f32", "huffman_build": "fzb_huffman_build",
+         "hf_prefill": "fzb_huffman_decode", "anchor_kernel<0>": "fzb_interp_encode_f32",
+         "anchor_kernel<1>": "fzb_interp_decode_f32"}
+
+
+def entry_of(name):
+    if name.startswith("interp2d_tile_kernel<"):   # last template argument = DEC
+        return "fzb_interp_decode_f32" if name.rstrip(">").endswith("1") else "fzb_interp_encode_f32"
+    for pre, ent in ENTRY.items():
+        if name.startswith(pre):
+            return ent
+    return None
 
 
 def load(path):
@@ -69,10 +80,9 @@ for cfg in ("c4", "c2", "c3"):
         gbs = (k["rd"] + k["wr"]) / (k["us"] * 1e3) if k["us"] > 0 else 0
         md.append(f"| {k['name'][:48]} | {k['us']:.1f} | {mbytes:.1f} | {gbs:.0f} | {100 * gbs / PEAK:.0f} | "
                   f"{k['issue']:.0f} | {k['warps']:.0f} |")
-        for pre, ent in ENTRY.items():
-            if k["name"].startswith(pre):
-                per_entry[ent] = per_entry.get(ent, 0) + k["rd"] + k["wr"]
-                break
+        ent = entry_of(k["name"])
+        if ent:
+            per_entry[ent] = per_entry.get(ent, 0) + k["rd"] + k["wr"]
     for ent, b in per_entry.items():
         traffic["kernels"][f"{cfg}:{ent}"] = {"bytes": int(b)}
 os.makedirs(dst, exist_ok=True)
