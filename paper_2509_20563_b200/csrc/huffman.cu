@@ -822,6 +822,26 @@ __global__ void __launch_bounds__(HE_THREADS) hf_count_kernel(const uint16_t* __
     if (threadIdx.x == 0) cta_bits[blockIdx.x] = (uint32_t)tot;   // <= 32 * HE_CHUNK
 }
 
+// Persistent chunk loops (hf_count3 / hf_write2): the CTA looks at its next
+// HE_THREADS chunks at once (chunk c0 + t * gridDim.x for thread t) and
+// compacts the ones whose `work` flag is set into s_list (thread indices, in
+// order); returns how many.  Both barriers are CTA-wide.
+FZB_DEV uint32_t chunk_worklist(bool work, uint32_t* s_list, uint32_t* s_wc) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned bal = __ballot_sync(0xffffffffu, work);
+    if (lane == 0) s_wc[wid] = __popc(bal);
+    __syncthreads();
+    uint32_t before = 0, nwork = 0;
+#pragma unroll
+    for (int w = 0; w < HE_THREADS / 32; w++) {
+        before += w < wid ? s_wc[w] : 0u;
+        nwork += s_wc[w];
+    }
+    if (work) s_list[before + __popc(bal & lanemask_lt())] = threadIdx.x;
+    __syncthreads();
+    return nwork;
+}
+
 // Count pass with the histogram's chunk flags (fzb_histogram_chunks): a full
 // chunk without a code != R is all R -- its bit total is HE_CHUNK * len(R)
 // and its codes are not read; persistent CTAs compact the rest (as in
@@ -834,7 +854,6 @@ __global__ void __launch_bounds__(HE_THREADS) hf_count3_kernel(const uint16_t* _
     __shared__ unsigned long long tmp[33];
     __shared__ uint32_t s_list[HE_THREADS];
     __shared__ uint32_t s_wc[HE_THREADS / 32 + 1];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t R = nsym >> 1;
     const uint32_t lr = __ldg(lengths + R);
     const uint64_t nfull = n / HE_CHUNK;
@@ -846,18 +865,7 @@ __global__ void __launch_bounds__(HE_THREADS) hf_count3_kernel(const uint16_t* _
             cta_bits[mine] = (uint32_t)HE_CHUNK * lr;
             all_r_chunk[mine] = 1;
         }
-        const bool work = mine < nc && !known;
-        const unsigned bal = __ballot_sync(0xffffffffu, work);
-        if (lane == 0) s_wc[wid] = __popc(bal);
-        __syncthreads();
-        uint32_t before = 0, nwork = 0;
-#pragma unroll
-        for (int w = 0; w < HE_THREADS / 32; w++) {
-            before += w < wid ? s_wc[w] : 0u;
-            nwork += s_wc[w];
-        }
-        if (work) s_list[before + __popc(bal & lanemask_lt())] = threadIdx.x;
-        __syncthreads();
+        const uint32_t nwork = chunk_worklist(mine < nc && !known, s_list, s_wc);
         for (uint32_t li = 0; li < nwork; li++) {
             const uint64_t chunk = c0 + (uint64_t)s_list[li] * gridDim.x;
             const uint64_t base = (chunk * HE_THREADS + threadIdx.x) * HE_PER;
@@ -936,22 +944,10 @@ __global__ void __launch_bounds__(HE_THREADS) hf_write2_kernel(const uint16_t* _
     // thread) and runs only the chunks left in the compacted list.
     __shared__ uint32_t s_list[HE_THREADS];
     __shared__ uint32_t s_wc[HE_THREADS / 32 + 1];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint64_t span = (uint64_t)gridDim.x * HE_THREADS;
     for (uint64_t c0 = blockIdx.x; c0 < nc; c0 += span) {
     const uint64_t mine = c0 + (uint64_t)threadIdx.x * gridDim.x;
-    const bool work = mine < nc && !(runs && pat == 0 && all_r_chunk[mine]);
-    const unsigned bal = __ballot_sync(0xffffffffu, work);
-    if (lane == 0) s_wc[wid] = __popc(bal);
-    __syncthreads();
-    uint32_t before = 0, nwork = 0;
-#pragma unroll
-    for (int w = 0; w < HE_THREADS / 32; w++) {
-        before += w < wid ? s_wc[w] : 0u;
-        nwork += s_wc[w];
-    }
-    if (work) s_list[before + __popc(bal & lanemask_lt())] = threadIdx.x;
-    __syncthreads();
+    const uint32_t nwork = chunk_worklist(mine < nc && !(runs && pat == 0 && all_r_chunk[mine]), s_list, s_wc);
     for (uint32_t li = 0; li < nwork; li++) {
     const uint64_t chunk = c0 + (uint64_t)s_list[li] * gridDim.x;
     const uint64_t base = (chunk * HE_THREADS + threadIdx.x) * HE_PER;

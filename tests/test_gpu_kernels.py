@@ -240,3 +240,24 @@ def test_histogram_chunk_flags_and_flagged_encode(oracle, n, seed):
     assert streams[0] == streams[1]
     _, ostream, _ = oracle.huffman_encode(c.astype(np.uint32), got_bins.copy())
     assert streams[1] == ostream
+
+
+@pytest.mark.parametrize("n,seed", [(4096 * 3 + 5, 0), (1000003, 1), (8 * 1024, 2), (4099, 3), (65536 + 1, 4)])
+def test_huffman_low_entropy_prefill_path(oracle, n, seed):
+    # a dominant zero code with the 1-bit codeword "0" at <= 1.125 bits per
+    # symbol takes the decoder's s0 prefill + skip-all-s0-chunk path: other
+    # symbols at 8-symbol chunk edges, at the ends, and n % 8 != 0
+    rng = np.random.default_rng(seed)
+    radius = 512
+    c = np.full(n, radius, np.uint32)
+    k = max(1, n // 200)
+    pos = np.unique(np.concatenate([rng.choice(n, k, replace=False), [0, n - 1],
+                                    np.arange(7, n, 4096)[:8], np.arange(8, n, 4096)[:8]]))
+    c[pos] = rng.integers(radius - 3, radius + 4, pos.size)
+    h = enc.histogram_exact(c, radius)
+    cb, stream, bits = enc.huffman_encode(c, h)
+    assert bits * 8 <= 9 * n                       # the prefill regime
+    assert cb.code_lengths[radius] == 1            # R has a 1-bit codeword
+    cl, ostream, obits = oracle.huffman_encode(c, h.bins)
+    assert np.array_equal(cb.code_lengths, cl) and stream == ostream
+    assert np.array_equal(enc.huffman_decode(cb, stream, n), c)
