@@ -1030,18 +1030,43 @@ __global__ void __launch_bounds__(128) lz1d_chain2_kernel(const long long* __res
         const bool o0 = (__ldg(bitmap + (p0 >> 5)) >> (p0 & 31)) & 1u;
         if (!(e == 0 || o0)) continue;   // warp-uniform: not a segment head
         float r = 0.f;                   // state entering event 0 (every earlier element has code R)
+        // one batch = 32 events, one per lane, software-pipelined: while batch
+        // b runs its serial loop, batch b + 32's code / outlier loads (their
+        // positions loaded one batch earlier) and batch b + 64's positions are
+        // in flight
+        struct Ev {
+            long long pos;
+            bool valid, isout;
+            int code;
+            float ov;
+        };
+        auto evp = [&](unsigned long long k) { return k < nev ? evpos[k] : 0ll; };
+        auto load = [&](unsigned long long k, long long pos) {
+            Ev v;
+            v.valid = k < nev;
+            v.pos = pos;
+            v.isout = v.valid && ((__ldg(bitmap + (pos >> 5)) >> (pos & 31)) & 1u);
+            v.code = v.valid ? (int)codes[pos] : radius;
+            v.ov = v.isout ? recon[pos] : 0.f;
+            return v;
+        };
+        Ev nx = load(e + lane, evp(e + lane));
+        long long pnn = evp(e + 32 + lane);
         for (unsigned long long b = e;; b += 32) {
             const unsigned long long k = b + lane;
-            const bool valid = k < nev;
-            const long long pos = valid ? evpos[k] : 0;
-            const bool isout = valid && ((__ldg(bitmap + (pos >> 5)) >> (pos & 31)) & 1u);
-            const int code = valid ? (int)codes[pos] : radius;
-            const double c = __dmul_rn(P.two_eb, (double)(code - radius));
-            const float ov = isout ? recon[pos] : 0.f;
+            const Ev cu = nx;
+            nx = load(k + 32, pnn);
+            pnn = evp(k + 64);
+            const long long pos = cu.pos;
+            const bool valid = cu.valid, isout = cu.isout;
+            const double c = __dmul_rn(P.two_eb, (double)(cu.code - radius));
+            const float ov = cu.ov;
             const unsigned stop = __ballot_sync(0xffffffffu, (isout && k != e) || !valid);
             const int lim = stop ? __ffs(stop) - 1 : 32;
             // RN64(0.0 + r) + c == RN64(r + c) for every c (the 0.0 + only turns -0 into +0,
-            // which no sum can tell apart), so one add per event
+            // which no sum can tell apart), so one add per event.  (RN32 as
+            // x + 1.5 * 2^(e+29) - that constant, off the XU pipe, made this
+            // chain slower: 148 -> 214 us on C4.)
             float mine = 0.f;
 #pragma unroll
             for (int j = 0; j < 32; j++) {
