@@ -1271,6 +1271,18 @@ FZB_DEV void setbits(uint32_t* bm, int rel, uint32_t m) {
     bm[w] |= m << o;
     if (o > 20) bm[w + 1] |= m >> (32 - o);
 }
+// 32-bit versions (rel + 32 <= SUB)
+FZB_DEV uint32_t bits32(const uint32_t* bm, int rel) {
+    const int w = rel >> 5, o = rel & 31;
+    uint32_t v = bm[w] >> o;
+    if (o) v |= bm[w + 1] << (32 - o);
+    return v;
+}
+FZB_DEV void setbits32(uint32_t* bm, int rel, uint32_t m) {
+    const int w = rel >> 5, o = rel & 31;
+    bm[w] |= m << o;
+    if (o) bm[w + 1] |= m >> (32 - o);
+}
 
 // One subsequence of one sweep (see hf_sync_coop_kernel): fresh = sweep 0
 // (start at the nominal offset), else restart at end[t-1] when it moved.
@@ -1300,9 +1312,26 @@ FZB_DEV void sync_one(uint64_t t, bool fresh, int slot, const uint32_t* __restri
         r.init(stream, s);
         uint32_t e = 0;
         int conv = -1;   // relative bit where the new path joins the previous one
+        // a 1-bit codeword "0" (12 codewords in the all-zero LUT window): a
+        // zero 32-bit window is 32 codeword starts (low-entropy streams)
+        const bool z0 = (lut2[0] & 15u) == (uint32_t)LUT_BITS;
         while (r.pos < stop) {
             const uint32_t win = r.peek32();
             const int rel = (int)(r.pos - base);
+            if (z0 && win == 0u && r.pos + 32 <= stop) {
+                if (!fresh) {
+                    const uint32_t common = bits32(ob, rel);
+                    if (common) {
+                        const int i = __ffs(common) - 1;
+                        if (i) setbits32(nb, rel, (1u << i) - 1u);
+                        conv = rel + i;
+                        break;
+                    }
+                }
+                setbits32(nb, rel, 0xFFFFFFFFu);
+                r.skip(32);
+                continue;
+            }
             const uint32_t me = lut2[win >> (32 - LUT_BITS)];
             const int c = (int)(me & 15u);
             if (c && r.pos + LUT_BITS <= stop) {   // every codeword of the window starts before lim
