@@ -62,6 +62,18 @@ FZB_API size_t fzb_lorenzo_workspace_bytes(uint32_t n0, uint32_t n1, uint32_t n2
 FZB_API int fzb_lorenzo_encode_f32(const float *d_in, uint32_t n0, uint32_t n1, uint32_t n2, const double *d_eb,
                                    uint32_t radius, uint16_t *d_codes, uint32_t *d_bitmap, void *d_ws,
                                    size_t ws_bytes, void *stream);
+/* 1D fields in two steps, so the field is read once before its bound is
+ * known (same result as fzb_lorenzo_encode_f32, which runs both):
+ * prepare writes the walker's min-max summaries into d_ws (workspace of
+ * fzb_lorenzo_workspace_bytes(1, 1, n)), fills d_codes with radius and, with
+ * d_lohi, stores the field's (min, max) and FZB_ERR_NONFINITE exactly as
+ * fzb_minmax_f32 (replaces pipeline.py:360-361's min/max pass); walk then
+ * runs the event walker with the resolved d_eb. */
+FZB_API int fzb_lorenzo1d_prepare_f32(const float *d_in, uint64_t n, uint32_t radius, uint16_t *d_codes,
+                                      float *d_lohi, void *d_ws, size_t ws_bytes, uint32_t *d_status,
+                                      void *stream);
+FZB_API int fzb_lorenzo1d_walk_f32(const float *d_in, uint64_t n, const double *d_eb, uint32_t radius,
+                                   uint16_t *d_codes, uint32_t *d_bitmap, void *d_ws, size_t ws_bytes, void *stream);
 /* d_recon holds the outlier values (fzb_outlier_scatter) and is completed in place. */
 FZB_API int fzb_lorenzo_decode_f32(const uint16_t *d_codes, const uint32_t *d_bitmap, float *d_recon, uint32_t n0,
                                    uint32_t n1, uint32_t n2, const double *d_eb, uint32_t radius, void *d_ws,

@@ -513,7 +513,11 @@ constexpr long long PF_CHUNK = 16;     // blocks per prefetch chunk (64 KB of x)
 
 __global__ void lz1d_summary2_kernel(const float* __restrict__ x, long long n, uint16_t* __restrict__ codes,
                                      int radius, float* __restrict__ bmin, float* __restrict__ bmax,
-                                     float* __restrict__ gmin, float* __restrict__ gmax, long long nblk) {
+                                     float* __restrict__ gmin, float* __restrict__ gmax, long long nblk,
+                                     uint32_t* __restrict__ status) {
+    // status (optional): FZB_ERR_NONFINITE for a NaN / inf element, as
+    // fzb_minmax_f32 reports it (fzb_lorenzo1d_prepare_f32 replaces that pass)
+    bool bad = false;
     // one warp per 1K block.  Row e = elements [128 e, 128 e + 128): lane l
     // loads float4 (128 e + 4 l) -- one coalesced 512-byte access per row --
     // so group g = 4 e + l / 8 is lanes 8(g & 3) .. +7 of row e (3 xor shuffles)
@@ -531,6 +535,14 @@ __global__ void lz1d_summary2_kernel(const float* __restrict__ x, long long n, u
 #pragma unroll
             for (int e = 0; e < 4; e++)   // 1024 codes = 128 x 16 bytes
                 reinterpret_cast<uint4*>(codes + b0)[e * 32 + lane] = make_uint4(rr, rr, rr, rr);
+            if (status) {
+#pragma unroll
+                for (int e = 0; e < 8; e++) {
+                    const uint32_t m = 0x7f800000u;
+                    bad |= ((__float_as_uint(q[e].x) & m) == m) | ((__float_as_uint(q[e].y) & m) == m) |
+                           ((__float_as_uint(q[e].z) & m) == m) | ((__float_as_uint(q[e].w) & m) == m);
+                }
+            }
         } else {
 #pragma unroll
             for (int e = 0; e < 8; e++) {
@@ -539,7 +551,10 @@ __global__ void lz1d_summary2_kernel(const float* __restrict__ x, long long n, u
                 for (int c = 0; c < 4; c++) {
                     const long long t = b0 + 128 * e + 4 * lane + c;
                     v[c] = t < n ? x[t] : NAN;
-                    if (t < n) codes[t] = (uint16_t)radius;
+                    if (t < n) {
+                        codes[t] = (uint16_t)radius;
+                        bad |= !isfinite(v[c]);
+                    }
                 }
                 q[e] = make_float4(v[0], v[1], v[2], v[3]);
             }
@@ -572,6 +587,35 @@ __global__ void lz1d_summary2_kernel(const float* __restrict__ x, long long n, u
             bmin[blk] = isnan(blo) ? INFINITY : blo;
             bmax[blk] = isnan(bhi) ? -INFINITY : bhi;
         }
+    }
+    if (status && __any_sync(0xffffffffu, bad) && lane == 0) set_err(status, FZB_ERR_NONFINITE);
+}
+
+// (min, max) of the field from its superblock summaries: the lohi of
+// fzb_minmax_f32 (fminf / fmaxf, NaN-free once the status is clear)
+__global__ void lz1d_lohi_kernel(const float* __restrict__ smin, const float* __restrict__ smax, long long nsb,
+                                 float* __restrict__ lohi) {
+    float lo = INFINITY, hi = -INFINITY;
+    for (long long q = threadIdx.x; q < nsb; q += blockDim.x) {
+        lo = fminf(lo, smin[q]);
+        hi = fmaxf(hi, smax[q]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    __shared__ float sl[32], sh[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) { sl[w] = lo; sh[w] = hi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int q = 1; q < (int)(blockDim.x >> 5); q++) {
+            lo = fminf(lo, sl[q]);
+            hi = fmaxf(hi, sh[q]);
+        }
+        lohi[0] = lo;
+        lohi[1] = hi;
     }
 }
 
@@ -1379,6 +1423,71 @@ FZB_API size_t fzb_lorenzo_workspace_bytes(uint32_t n0, uint32_t n1, uint32_t n2
     return w4 > w6 ? w4 : w6;
 }
 
+// 1D encode, step 1 (no error bound needed): the walker's group / block /
+// superblock min-max summaries into d_ws, codes filled with radius; with
+// d_lohi, also the field's (min, max) and FZB_ERR_NONFINITE exactly as
+// fzb_minmax_f32 -- so a 1D field is read once before its bound is known.
+FZB_API int fzb_lorenzo1d_prepare_f32(const float* d_in, uint64_t n, uint32_t radius, uint16_t* d_codes,
+                                      float* d_lohi, void* d_ws, size_t ws_bytes, uint32_t* d_status, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (radius == 0 || radius > 32768) return FZB_E_RADIUS;
+    if (n == 0) return d_lohi ? FZB_E_ARG : 0;
+    const long long nblk = ((long long)n + BS1 - 1) / BS1, nsb = (nblk + 31) / 32;
+    // every summary array 256-byte aligned (the walker bulk-prefetches them)
+    const Walk1D L((long long)n);
+    if (ws_bytes < L.total) return FZB_E_WORKSPACE;
+    invalidate_faces(d_ws, st);
+    unsigned char* wb = static_cast<unsigned char*>(d_ws);
+    float* bmin = reinterpret_cast<float*>(wb + L.o_bmin);
+    float* bmax = reinterpret_cast<float*>(wb + L.o_bmax);
+    float* smin = reinterpret_cast<float*>(wb + L.o_smin);
+    float* smax = reinterpret_cast<float*>(wb + L.o_smax);
+    lz1d_summary2_kernel<<<kNumSMs * 8, 256, 0, st>>>(d_in, (long long)n, d_codes, (int)radius, bmin, bmax,
+                                                      reinterpret_cast<float*>(wb + L.o_gmin),
+                                                      reinterpret_cast<float*>(wb + L.o_gmax), nblk,
+                                                      d_lohi ? d_status : nullptr);
+    lz1d_super_kernel<<<kNumSMs * 2, 256, 0, st>>>(bmin, bmax, nblk, smin, smax, nsb);
+    if (d_lohi) lz1d_lohi_kernel<<<1, 1024, 0, st>>>(smin, smax, nsb, d_lohi);
+    return fzb_check_launch();
+}
+
+// 1D encode, step 2: the event walker over the summaries of step 1 (same
+// d_in, n, radius, d_codes and d_ws) with the resolved bound.
+FZB_API int fzb_lorenzo1d_walk_f32(const float* d_in, uint64_t n, const double* d_eb, uint32_t radius,
+                                   uint16_t* d_codes, uint32_t* d_bitmap, void* d_ws, size_t ws_bytes, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (radius == 0 || radius > 32768) return FZB_E_RADIUS;
+    if (n == 0) return 0;
+    const long long nblk = ((long long)n + BS1 - 1) / BS1, nsb = (nblk + 31) / 32;
+    const Walk1D L((long long)n);
+    if (ws_bytes < L.total) return FZB_E_WORKSPACE;
+    unsigned char* wb = static_cast<unsigned char*>(d_ws);
+    float* bmin = reinterpret_cast<float*>(wb + L.o_bmin);
+    float* bmax = reinterpret_cast<float*>(wb + L.o_bmax);
+    float* smin = reinterpret_cast<float*>(wb + L.o_smin);
+    float* smax = reinterpret_cast<float*>(wb + L.o_smax);
+    float* gmin = reinterpret_cast<float*>(wb + L.o_gmin);
+    float* gmax = reinterpret_cast<float*>(wb + L.o_gmax);
+    const size_t wsm = nsb <= WALK_SMEM_SB ? (size_t)nsb * 8 : 0;
+    const bool vec = !(reinterpret_cast<uintptr_t>(d_in) & 15);
+    auto kfn = vec ? lz1d_walk3_kernel<true> : lz1d_walk3_kernel<false>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
+    const char* pfe = getenv("FZB_WALK_PF");
+    const long long pf = pfe ? atoll(pfe) : PF_AHEAD;
+    long long* pos = reinterpret_cast<long long*>(wb + 24);   // header words 6-7: walker position
+    cudaMemsetAsync(pos, 0, 8, st);
+    kfn<<<2, 64, wsm, st>>>(d_in, (long long)n, d_codes, d_bitmap, bmin, bmax, nblk, smin, smax, nsb, gmin, gmax,
+                            d_eb, (int)radius, pf, pos);
+#ifdef LZ7_TIMING
+    if (getenv("FZB_WALK_TWICE")) {
+        cudaMemsetAsync(pos, 0, 8, st);
+        kfn<<<2, 64, wsm, st>>>(d_in, (long long)n, d_codes, d_bitmap, bmin, bmax, nblk, smin, smax, nsb, gmin, gmax,
+                                d_eb, (int)radius, pf, pos);
+    }
+#endif
+    return fzb_check_launch();
+}
+
 // Reference: predict.py:93-115 (_lorenzo_encode) + the outlier flags of
 // predict.py:212-214.  codes: u16[n]; bitmap: u32[ceil(n/32)] zeroed by the
 // caller; receives one bit per outlier.
@@ -1391,41 +1500,10 @@ FZB_API int fzb_lorenzo_encode_f32(const float* d_in, uint32_t n0, uint32_t n1, 
     const long long n = (long long)n0 * n1 * n2;
     if (n == 0) return 0;
     if (n0 == 1 && n1 == 1) {
-        const long long nblk = (n + BS1 - 1) / BS1, nsb = (nblk + 31) / 32;
-        // every summary array 256-byte aligned (the walker bulk-prefetches them)
-        const Walk1D L(n);
-        if (ws_bytes < L.total) return FZB_E_WORKSPACE;
-        invalidate_faces(d_ws, st);
-        unsigned char* wb = static_cast<unsigned char*>(d_ws);
-        float* bmin = reinterpret_cast<float*>(wb + L.o_bmin);
-        float* bmax = reinterpret_cast<float*>(wb + L.o_bmax);
-        float* smin = reinterpret_cast<float*>(wb + L.o_smin);
-        float* smax = reinterpret_cast<float*>(wb + L.o_smax);
-        float* gmin = reinterpret_cast<float*>(wb + L.o_gmin);
-        float* gmax = reinterpret_cast<float*>(wb + L.o_gmax);
-        {
-            lz1d_summary2_kernel<<<kNumSMs * 8, 256, 0, st>>>(d_in, n, d_codes, (int)radius, bmin, bmax, gmin, gmax,
-                                                              nblk);
-            lz1d_super_kernel<<<kNumSMs * 2, 256, 0, st>>>(bmin, bmax, nblk, smin, smax, nsb);
-            const size_t wsm = nsb <= WALK_SMEM_SB ? (size_t)nsb * 8 : 0;
-            const bool vec = !(reinterpret_cast<uintptr_t>(d_in) & 15);
-            auto kfn = vec ? lz1d_walk3_kernel<true> : lz1d_walk3_kernel<false>;
-            cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
-            const char* pfe = getenv("FZB_WALK_PF");
-            const long long pf = pfe ? atoll(pfe) : PF_AHEAD;
-            long long* pos = reinterpret_cast<long long*>(wb + 24);   // header words 6-7: walker position
-            cudaMemsetAsync(pos, 0, 8, st);
-            kfn<<<2, 64, wsm, st>>>(d_in, n, d_codes, d_bitmap, bmin, bmax, nblk, smin, smax, nsb, gmin, gmax, d_eb,
-                                    (int)radius, pf, pos);
-#ifdef LZ7_TIMING
-            if (getenv("FZB_WALK_TWICE")) {
-                cudaMemsetAsync(pos, 0, 8, st);
-                kfn<<<2, 64, wsm, st>>>(d_in, n, d_codes, d_bitmap, bmin, bmax, nblk, smin, smax, nsb, gmin, gmax,
-                                        d_eb, (int)radius, pf, pos);
-            }
-#endif
-            return fzb_check_launch();
-        }
+        const int rc = fzb_lorenzo1d_prepare_f32(d_in, (uint64_t)n, radius, d_codes, nullptr, d_ws, ws_bytes, nullptr,
+                                                 stream);
+        if (rc) return rc;
+        return fzb_lorenzo1d_walk_f32(d_in, (uint64_t)n, d_eb, radius, d_codes, d_bitmap, d_ws, ws_bytes, stream);
     }
     if (!use_v4(n2))
         return launch_v7<false>(d_in, nullptr, d_codes, d_bitmap, nullptr, n0, n1, n2, d_eb, (int)radius, d_ws, ws_bytes, st);

@@ -285,15 +285,23 @@ class Engine:
         if predictor not in ("lorenzo", "interp", "dualquant"):
             raise ValueError(f"unknown predictor '{predictor}'")
         use_anchors = predictor == "interp" and interp_applicable(dims, anchor_stride)
+        # 1D Lorenzo: the walker's summary pass also yields the field's min / max
+        # (fzb_lorenzo1d_prepare_f32), so the field is read once before the bound
+        lz1d = predictor == "lorenzo" and pre is None and sum(d > 1 for d in (n0, n1, n2)) <= 1
         if pre is None:
             self._mark("bound")
             status = self.buf("status" + tag, 8, zero=True)
             lohi = self.buf("lohi" + tag, 8)
             eb = self.buf("eb" + tag, 8)
-            mmws = self.buf("mmws" + tag, L.fzb_minmax_workspace_bytes(n))
-            self._call("fzb_minmax_f32", _p(x), n, _p(lohi), _p(mmws), mmws.numel(), _p(status), sp, nk=2)
-            self._call("fzb_resolve_bound", _p(lohi), int(eb_mode), float(magnitude), _p(eb), sp)
             codes = self.buf("codes" + tag, 2 * n + 16)
+            if lz1d:
+                lzws = self.buf("lzws" + tag, L.fzb_lorenzo_workspace_bytes(1, 1, n), zero_new=True)
+                self._call("fzb_lorenzo1d_prepare_f32", _p(x), n, radius, _p(codes), _p(lohi), _p(lzws), lzws.numel(),
+                           _p(status), sp, nk=3)
+            else:
+                mmws = self.buf("mmws" + tag, L.fzb_minmax_workspace_bytes(n))
+                self._call("fzb_minmax_f32", _p(x), n, _p(lohi), _p(mmws), mmws.numel(), _p(status), sp, nk=2)
+            self._call("fzb_resolve_bound", _p(lohi), int(eb_mode), float(magnitude), _p(eb), sp)
             bitmap = self.buf("bitmap" + tag, 4 * ((n + 31) // 32), zero=True)
         else:
             status, lohi, eb, codes, bitmap = (pre[k] for k in ("status", "lohi", "eb", "codes", "bitmap"))
@@ -326,6 +334,9 @@ class Engine:
         elif predictor == "dualquant":
             self._call("fzb_dualquant_encode_f32", _p(x), n0, n1, n2, _p(eb), radius, _p(codes), _p(bitmap),
                        _p(status), sp)
+        elif lz1d:
+            self._call("fzb_lorenzo1d_walk_f32", _p(x), n, _p(eb), radius, _p(codes), _p(bitmap), _p(lzws),
+                       lzws.numel(), sp, nk=1)
         else:
             lzws = self.buf("lzws" + tag, L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
             self._call("fzb_lorenzo_encode_f32", _p(x), n0, n1, n2, _p(eb), radius, _p(codes), _p(bitmap),
