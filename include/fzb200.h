@@ -52,6 +52,10 @@ FZB_API int fzb_minmax_f32(const float *d_in, uint64_t n, float *d_lohi, void *d
 /* d_eb = eb_mode ? magnitude * (hi - lo) : magnitude, in f64 exactly as core.py:167. */
 FZB_API int fzb_resolve_bound(const float *d_lohi, int eb_mode, double magnitude, double *d_eb, void *stream);
 
+/* Codes per chunk of the encoder's "holds a code != R" flags (fzb_histogram_chunks,
+ * fzb_lorenzo1d_walk_f32, fzb_huffman_encode_chunks). */
+#define FZB_HF_CHUNK 4096
+
 /* ---- a2-a4: Lorenzo (predict.py:93-144, 221-253) ------------------------ */
 /* The workspace carries a launch epoch and tagged halo slots across calls:
  * zero-fill it once when it is allocated, then pass it unchanged (any later
@@ -72,8 +76,11 @@ FZB_API int fzb_lorenzo_encode_f32(const float *d_in, uint32_t n0, uint32_t n1, 
 FZB_API int fzb_lorenzo1d_prepare_f32(const float *d_in, uint64_t n, uint32_t radius, uint16_t *d_codes,
                                       float *d_lohi, void *d_ws, size_t ws_bytes, uint32_t *d_status,
                                       void *stream);
+/* d_notr (optional, u8[ceil(n / FZB_HF_CHUNK)]): zeroed here, then 1 for every
+ * chunk that gets a code != radius -- the flags of fzb_histogram_chunks. */
 FZB_API int fzb_lorenzo1d_walk_f32(const float *d_in, uint64_t n, const double *d_eb, uint32_t radius,
-                                   uint16_t *d_codes, uint32_t *d_bitmap, void *d_ws, size_t ws_bytes, void *stream);
+                                   uint16_t *d_codes, uint32_t *d_bitmap, uint8_t *d_notr, void *d_ws,
+                                   size_t ws_bytes, void *stream);
 /* d_recon holds the outlier values (fzb_outlier_scatter) and is completed in place. */
 FZB_API int fzb_lorenzo_decode_f32(const uint16_t *d_codes, const uint32_t *d_bitmap, float *d_recon, uint32_t n0,
                                    uint32_t n1, uint32_t n2, const double *d_eb, uint32_t radius, void *d_ws,
@@ -128,9 +135,13 @@ FZB_API int fzb_histogram(const uint16_t *d_codes, uint64_t n, uint32_t nbins, u
 /* Same, plus d_notr u8[ceil(n / FZB_HF_CHUNK)]: 1 iff that chunk of codes holds
  * a code other than nbins / 2 (the zero-code R).  fzb_huffman_encode_chunks
  * uses it to skip re-reading chunks that are all R (low-entropy fields). */
-#define FZB_HF_CHUNK 4096
 FZB_API int fzb_histogram_chunks(const uint16_t *d_codes, uint64_t n, uint32_t nbins, uint64_t *d_bins,
                                  uint8_t *d_notr, uint32_t *d_status, void *stream);
+/* Same bins from flags already known (fzb_lorenzo1d_walk_f32's): full
+ * chunks whose flag is clear are counted as FZB_HF_CHUNK codes R without
+ * being read. */
+FZB_API int fzb_histogram_flagged(const uint16_t *d_codes, uint64_t n, uint32_t nbins, uint64_t *d_bins,
+                                  const uint8_t *d_notr, uint32_t *d_status, void *stream);
 
 /* ---- a8: codebook (encode.py:118-217) ----------------------------------- */
 FZB_API size_t fzb_huffman_build_workspace_bytes(uint32_t nsym);

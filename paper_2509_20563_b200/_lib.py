@@ -91,7 +91,8 @@ def load():
         "fzb_quality_leaves": (I, [P, P, P, P, U64, P, P, P]),
         "fzb_histogram": (I, [P, U64, U32, P, P, P]),
         "fzb_lorenzo1d_prepare_f32": (I, [P, U64, U32, P, P, P, SZ, P, P]),
-        "fzb_lorenzo1d_walk_f32": (I, [P, U64, P, U32, P, P, P, SZ, P]),
+        "fzb_lorenzo1d_walk_f32": (I, [P, U64, P, U32, P, P, P, P, SZ, P]),
+        "fzb_histogram_flagged": (I, [P, U64, U32, P, P, P, P]),
         "fzb_histogram_chunks": (I, [P, U64, U32, P, P, P, P]),
         "fzb_huffman_build_workspace_bytes": (SZ, [U32]),
         "fzb_huffman_build": (I, [P, U32, P, P, P, P, SZ, P]),
@@ -126,7 +127,8 @@ EXPORTED = [
     "fzb_interp_decode_f32", "fzb_outlier_workspace_bytes", "fzb_outlier_compact", "fzb_outlier_scatter",
     "fzb_outlier_check",
     "fzb_quality_leaves",
-    "fzb_histogram", "fzb_histogram_chunks", "fzb_lorenzo1d_prepare_f32", "fzb_lorenzo1d_walk_f32", "fzb_huffman_encode_chunks", "fzb_huffman_build_workspace_bytes", "fzb_huffman_build", "fzb_huffman_encode_workspace_bytes",
+    "fzb_histogram", "fzb_histogram_chunks", "fzb_lorenzo1d_prepare_f32", "fzb_lorenzo1d_walk_f32",
+    "fzb_histogram_flagged", "fzb_huffman_encode_chunks", "fzb_huffman_build_workspace_bytes", "fzb_huffman_build", "fzb_huffman_encode_workspace_bytes",
     "fzb_huffman_encode", "fzb_huffman_decode_workspace_bytes", "fzb_huffman_decode",
     "fzb_bitshuffle_workspace_bytes", "fzb_bitshuffle_encode", "fzb_bitshuffle_decode", "fzb_fill_u16",
     "fzb_interp_profile", "fzb_dualquant_encode_f32", "fzb_dualquant_outlier_deltas", "fzb_dualquant_decode_workspace_bytes",

@@ -693,7 +693,8 @@ __global__ void __launch_bounds__(64) lz1d_walk3_kernel(const float* __restrict_
                                                          const float* __restrict__ smax_g, long long nsb,
                                                          const float* __restrict__ gmin, const float* __restrict__ gmax,
                                                          const double* __restrict__ d_eb, int radius,
-                                                         long long pf_ahead, long long* pos_slot) {
+                                                         long long pf_ahead, long long* pos_slot,
+                                                         uint8_t* __restrict__ notr) {
     extern __shared__ float s_sum[];
     __shared__ __align__(128) float s_blk[2][BS1];   // double-buffered exit blocks
     __shared__ __align__(8) uint64_t s_bar[2];
@@ -837,7 +838,10 @@ __global__ void __launch_bounds__(64) lz1d_walk3_kernel(const float* __restrict_
             bool outl;
             const int c = quantize_walk((double)xv, pred, P, rec, outl);
             if (lane == 0) {
-                if (c != radius) codes[t] = (uint16_t)c;
+                if (c != radius) {
+                    codes[t] = (uint16_t)c;
+                    if (notr) notr[t >> 12] = 1;   // this 4096-code chunk holds a code != R
+                }
                 if (outl) atomicOr(bitmap + (t >> 5), 1u << (t & 31));
             }
             r = rec;
@@ -1454,7 +1458,8 @@ FZB_API int fzb_lorenzo1d_prepare_f32(const float* d_in, uint64_t n, uint32_t ra
 // 1D encode, step 2: the event walker over the summaries of step 1 (same
 // d_in, n, radius, d_codes and d_ws) with the resolved bound.
 FZB_API int fzb_lorenzo1d_walk_f32(const float* d_in, uint64_t n, const double* d_eb, uint32_t radius,
-                                   uint16_t* d_codes, uint32_t* d_bitmap, void* d_ws, size_t ws_bytes, void* stream) {
+                                   uint16_t* d_codes, uint32_t* d_bitmap, uint8_t* d_notr, void* d_ws,
+                                   size_t ws_bytes, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (radius == 0 || radius > 32768) return FZB_E_RADIUS;
     if (n == 0) return 0;
@@ -1476,13 +1481,14 @@ FZB_API int fzb_lorenzo1d_walk_f32(const float* d_in, uint64_t n, const double* 
     const long long pf = pfe ? atoll(pfe) : PF_AHEAD;
     long long* pos = reinterpret_cast<long long*>(wb + 24);   // header words 6-7: walker position
     cudaMemsetAsync(pos, 0, 8, st);
+    if (d_notr) cudaMemsetAsync(d_notr, 0, (size_t)((n + FZB_HF_CHUNK - 1) / FZB_HF_CHUNK), st);
     kfn<<<2, 64, wsm, st>>>(d_in, (long long)n, d_codes, d_bitmap, bmin, bmax, nblk, smin, smax, nsb, gmin, gmax,
-                            d_eb, (int)radius, pf, pos);
+                            d_eb, (int)radius, pf, pos, d_notr);
 #ifdef LZ7_TIMING
     if (getenv("FZB_WALK_TWICE")) {
         cudaMemsetAsync(pos, 0, 8, st);
         kfn<<<2, 64, wsm, st>>>(d_in, (long long)n, d_codes, d_bitmap, bmin, bmax, nblk, smin, smax, nsb, gmin, gmax,
-                                d_eb, (int)radius, pf, pos);
+                                d_eb, (int)radius, pf, pos, d_notr);
     }
 #endif
     return fzb_check_launch();
@@ -1503,7 +1509,8 @@ FZB_API int fzb_lorenzo_encode_f32(const float* d_in, uint32_t n0, uint32_t n1, 
         const int rc = fzb_lorenzo1d_prepare_f32(d_in, (uint64_t)n, radius, d_codes, nullptr, d_ws, ws_bytes, nullptr,
                                                  stream);
         if (rc) return rc;
-        return fzb_lorenzo1d_walk_f32(d_in, (uint64_t)n, d_eb, radius, d_codes, d_bitmap, d_ws, ws_bytes, stream);
+        return fzb_lorenzo1d_walk_f32(d_in, (uint64_t)n, d_eb, radius, d_codes, d_bitmap, nullptr, d_ws, ws_bytes,
+                                      stream);
     }
     if (!use_v4(n2))
         return launch_v7<false>(d_in, nullptr, d_codes, d_bitmap, nullptr, n0, n1, n2, d_eb, (int)radius, d_ws, ws_bytes, st);

@@ -201,6 +201,75 @@ __global__ void __launch_bounds__(HIST_THREADS) hist_smem_kernel(const uint16_t*
     }
 }
 
+// Histogram with the chunk flags as INPUT (fzb_histogram_flagged): a full
+// 4096-code chunk whose flag is clear holds only R = nbins / 2 and is
+// counted without being read; one warp per flagged chunk, 16 coalesced
+// 16-byte loads per lane, run-merged into per-warp shared sub-histograms.
+__global__ void __launch_bounds__(HIST_THREADS) hist_flagged_kernel(const uint16_t* __restrict__ codes, uint64_t n,
+                                                                    uint32_t nbins, int nsub,
+                                                                    const uint8_t* __restrict__ notr,
+                                                                    unsigned long long* __restrict__ out,
+                                                                    uint32_t* __restrict__ status) {
+    extern __shared__ uint32_t sb[];
+    for (uint32_t q = threadIdx.x; q < nbins * (uint32_t)nsub; q += blockDim.x) sb[q] = 0;
+    __syncthreads();
+    uint32_t* mine = sb + (size_t)((threadIdx.x >> 5) % nsub) * nbins;
+    const uint32_t R = nbins / 2;
+    const int lane = threadIdx.x & 31;
+    uint32_t cur = 0xFFFFFFFFu, cnt = 0;
+    unsigned long long nr = 0;   // codes of unread (all-R) chunks
+    bool bad = false;
+    auto put = [&](uint32_t c) {
+        if (c == cur) {
+            cnt++;
+        } else {
+            if (cnt) {
+                if (cur < nbins) atomicAdd(mine + cur, cnt);
+                else bad = true;
+            }
+            cur = c;
+            cnt = 1;
+        }
+    };
+    const uint64_t nc = (n + 4095) / 4096, nfull = n / 4096;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t c = warp; c < nc; c += nw) {
+        if (c < nfull && !notr[c]) {   // warp-uniform
+            nr += 4096;
+            continue;
+        }
+        const uint64_t b0 = c * 4096;
+        if (c < nfull) {
+            const uint4* c8 = reinterpret_cast<const uint4*>(codes + b0);
+            uint4 v[16];
+#pragma unroll
+            for (int u = 0; u < 16; u++) v[u] = __ldcs(c8 + u * 32 + lane);
+#pragma unroll
+            for (int u = 0; u < 16; u++) {
+                put(v[u].x & 0xFFFFu); put(v[u].x >> 16);
+                put(v[u].y & 0xFFFFu); put(v[u].y >> 16);
+                put(v[u].z & 0xFFFFu); put(v[u].z >> 16);
+                put(v[u].w & 0xFFFFu); put(v[u].w >> 16);
+            }
+        } else {
+            for (uint64_t t = b0 + lane; t < n; t += 32) put(codes[t]);
+        }
+    }
+    if (cnt) {
+        if (cur < nbins) atomicAdd(mine + cur, cnt);
+        else bad = true;
+    }
+    if (bad) set_err(status, FZB_ERR_CODE_RANGE);
+    if (lane == 0 && nr) atomicAdd(out + R, nr);
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < nbins; q += blockDim.x) {
+        uint32_t t = 0;
+        for (int w = 0; w < nsub; w++) t += sb[(size_t)w * nbins + q];
+        if (t) atomicAdd(out + q, (unsigned long long)t);
+    }
+}
+
 __global__ void hist_global_kernel(const uint16_t* __restrict__ codes, uint64_t n, uint32_t nbins,
                                    unsigned long long* __restrict__ out, uint32_t* __restrict__ status,
                                    uint8_t* __restrict__ notr) {
@@ -435,6 +504,24 @@ FZB_API int fzb_fill_u16(uint16_t* d_dst, uint64_t n, uint16_t value, void* stre
 FZB_API int fzb_histogram(const uint16_t* d_codes, uint64_t n, uint32_t nbins, uint64_t* d_bins, uint32_t* d_status,
                           void* stream) {
     return fzb_histogram_chunks(d_codes, n, nbins, d_bins, nullptr, d_status, stream);
+}
+
+FZB_API int fzb_histogram_flagged(const uint16_t* d_codes, uint64_t n, uint32_t nbins, uint64_t* d_bins,
+                                  const uint8_t* d_notr, uint32_t* d_status, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (nbins == 0 || !d_notr) return FZB_E_ARG;
+    if (nbins > HIST_SMEM_BINS || (reinterpret_cast<uintptr_t>(d_codes) & 15))   // read everything
+        return fzb_histogram(d_codes, n, nbins, d_bins, d_status, stream);
+    cudaMemsetAsync(d_bins, 0, (size_t)nbins * 8, st);
+    if (n == 0) return fzb_check_launch();
+    int nsub = HIST_THREADS / 32;
+    while (nsub > 1 && (size_t)nsub * nbins * 4 > 64 * 1024) nsub >>= 1;
+    const size_t smem = (size_t)nbins * 4 * nsub;
+    cudaFuncSetAttribute(hist_flagged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    hist_flagged_kernel<<<kNumSMs * 4, HIST_THREADS, smem, st>>>(d_codes, n, nbins, nsub, d_notr,
+                                                                reinterpret_cast<unsigned long long*>(d_bins),
+                                                                d_status);
+    return fzb_check_launch();
 }
 
 FZB_API int fzb_histogram_chunks(const uint16_t* d_codes, uint64_t n, uint32_t nbins, uint64_t* d_bins,

@@ -335,8 +335,11 @@ class Engine:
             self._call("fzb_dualquant_encode_f32", _p(x), n0, n1, n2, _p(eb), radius, _p(codes), _p(bitmap),
                        _p(status), sp)
         elif lz1d:
-            self._call("fzb_lorenzo1d_walk_f32", _p(x), n, _p(eb), radius, _p(codes), _p(bitmap), _p(lzws),
-                       lzws.numel(), sp, nk=1)
+            # the walker flags the 4096-code chunks that get a code != R, so the
+            # histogram and the Huffman count pass skip the rest
+            notr = self.buf("notr" + tag, (n + 4095) // 4096) if codec == "huffman" else None
+            self._call("fzb_lorenzo1d_walk_f32", _p(x), n, _p(eb), radius, _p(codes), _p(bitmap), _p(notr),
+                       _p(lzws), lzws.numel(), sp, nk=1)
         else:
             lzws = self.buf("lzws" + tag, L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
             self._call("fzb_lorenzo_encode_f32", _p(x), n0, n1, n2, _p(eb), radius, _p(codes), _p(bitmap),
@@ -361,8 +364,11 @@ class Engine:
         nsym = 2 * radius
         if codec == "huffman":
             bins = self.buf("bins" + tag, 8 * nsym)
-            notr = self.buf("notr" + tag, (n + 4095) // 4096)   # chunk flags for the encoder's count pass
-            self._call("fzb_histogram_chunks", _p(codes), n, nsym, _p(bins), _p(notr), _p(status), sp)
+            if lz1d:   # flags from the walker
+                self._call("fzb_histogram_flagged", _p(codes), n, nsym, _p(bins), _p(notr), _p(status), sp)
+            else:      # flags from the histogram, for the encoder's count pass
+                notr = self.buf("notr" + tag, (n + 4095) // 4096)
+                self._call("fzb_histogram_chunks", _p(codes), n, nsym, _p(bins), _p(notr), _p(status), sp)
             self._mark("primary")
             lengths = self.buf("lengths" + tag, nsym)
             cw = self.buf("cw" + tag, 4 * nsym)
