@@ -259,10 +259,18 @@ ALGO = {  # algorithmic bytes per launch, f(n, compressed size units
     "fzb_huffman_encode": lambda n, s: 2 * n + (s + 7) // 8, "fzb_huffman_decode": lambda n, s: 2 * n + (s + 7) // 8,
     "fzb_interp_encode_f32": lambda n, s: 6 * n, "fzb_interp_decode_f32": lambda n, s: 6 * n,
     "fzb_histogram": lambda n, s: 2 * n, "fzb_minmax_f32": lambda n, s: 4 * n, "fzb_outlier_compact": lambda n, s: n // 8,
+    # 1D fields in two steps: the summary pass reads the field and writes the
+    # codes; the walker tests every element against the zero-code interval
+    # (through the summaries) -- its algorithmic input is the field
+    "fzb_lorenzo1d_prepare_f32": lambda n, s: 6 * n, "fzb_lorenzo1d_walk_f32": lambda n, s: 4 * n,
+    "fzb_histogram_chunks": lambda n, s: 2 * n, "fzb_histogram_flagged": lambda n, s: 2 * n,
+    "fzb_huffman_encode_chunks": lambda n, s: 2 * n + (s + 7) // 8,
 }
 COMP_FNS = ("fzb_minmax_f32", "fzb_resolve_bound", "fzb_lorenzo_encode_f32", "fzb_lorenzo_encode_batch_f32",
-            "fzb_interp_encode_f32", "fzb_outlier_compact", "fzb_histogram", "fzb_huffman_build",
-            "fzb_huffman_encode", "fzb_bitshuffle_encode", "fzb_fill_u16")
+            "fzb_lorenzo1d_prepare_f32", "fzb_lorenzo1d_walk_f32", "fzb_interp_encode_f32", "fzb_interp_profile",
+            "fzb_outlier_compact", "fzb_histogram", "fzb_histogram_chunks", "fzb_histogram_flagged",
+            "fzb_huffman_build", "fzb_huffman_encode", "fzb_huffman_encode_chunks", "fzb_bitshuffle_encode",
+            "fzb_fill_u16", "fzb_dualquant_encode_f32", "fzb_dualquant_outlier_deltas")
 DEC_FNS = ("fzb_huffman_decode", "fzb_bitshuffle_decode", "fzb_outlier_scatter", "fzb_lorenzo_decode_f32",
            "fzb_lorenzo_decode_batch_f32", "fzb_interp_decode_f32")
 

@@ -7,14 +7,15 @@ import csv, json, os, sys
 src, dst = sys.argv[1], sys.argv[2]
 PEAK = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6540.5
 # kernel name prefix -> C-ABI entry point (bench.py's `dom` keys)
-ENTRY = {"lz1d_summary2": "fzb_lorenzo_encode_f32", "lz1d_super": "fzb_lorenzo_encode_f32",
-         "lz1d_walk3": "fzb_lorenzo_encode_f32", "v6::lz7_kernel<4, 2, 0>": "fzb_lorenzo_encode_f32",
+ENTRY = {"lz1d_summary2": "fzb_lorenzo1d_prepare_f32", "lz1d_super": "fzb_lorenzo1d_prepare_f32",
+         "lz1d_lohi": "fzb_lorenzo1d_prepare_f32", "lz1d_walk3": "fzb_lorenzo1d_walk_f32",
+         "hist_flagged": "fzb_histogram_flagged", "v6::lz7_kernel<4, 2, 0>": "fzb_lorenzo_encode_f32",
          "v6::lz7_kernel<8, 1, 0>": "fzb_lorenzo_encode_f32", "v6::lz7_kernel<4, 2, 1>": "fzb_lorenzo_decode_f32",
          "v6::lz7_kernel<8, 1, 1>": "fzb_lorenzo_decode_f32", "lz1d_event": "fzb_lorenzo_decode_f32",
          "lz1d_chain2": "fzb_lorenzo_decode_f32", "lz1d_fill2": "fzb_lorenzo_decode_f32",
-         "bs_enc4": "fzb_bitshuffle_encode", "bs_dec": "fzb_bitshuffle_decode", "hf_count": "fzb_huffman_encode",
-         "hf_write2": "fzb_huffman_encode", "hf_zero": "fzb_huffman_encode", "hf_sync": "fzb_huffman_decode",
-         "hf_write_dec2": "fzb_huffman_decode", "hf_tables": "fzb_huffman_decode", "hist_smem": "fzb_histogram",
+         "bs_enc4": "fzb_bitshuffle_encode", "bs_dec": "fzb_bitshuffle_decode", "hf_count": "fzb_huffman_encode_chunks",
+         "hf_write2": "fzb_huffman_encode_chunks", "hf_zero": "fzb_huffman_encode_chunks", "hf_sync": "fzb_huffman_decode",
+         "hf_write_dec2": "fzb_huffman_decode", "hf_tables": "fzb_huffman_decode", "hist_smem": "fzb_histogram_chunks",
          "minmax": "fzb_minmax_f32", "interp_pass_kernel<0, 0>": "fzb_interp_encode_f32",
          "interp_pass_kernel<1, 0>": "fzb_interp_encode_f32", "interp_pass_kernel<2, 0>": "fzb_interp_encode_f32",
          "interp_pass_kernel<0, 1>": "fzb_interp_decode_f32", "interp_pass_kernel<1, 1>": "fzb_interp_decode_f32",
