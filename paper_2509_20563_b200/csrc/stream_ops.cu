@@ -234,11 +234,17 @@ __global__ void __launch_bounds__(HIST_THREADS) hist_flagged_kernel(const uint16
     const uint64_t nc = (n + 4095) / 4096, nfull = n / 4096;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t c = warp; c < nc; c += nw) {
-        if (c < nfull && !notr[c]) {   // warp-uniform
-            nr += 4096;
-            continue;
-        }
+    // the warp reads the flags of its next 32 chunks at once (one per lane)
+    // and visits only the flagged ones
+    for (uint64_t c0 = warp; c0 < nc; c0 += 32 * nw) {
+        const uint64_t mc = c0 + (uint64_t)lane * nw;
+        const bool skip = mc < nfull && !notr[mc];
+        if (skip) nr += 4096;
+        unsigned todo = __ballot_sync(0xffffffffu, mc < nc && !skip);
+        while (todo) {
+        const int j = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const uint64_t c = c0 + (uint64_t)j * nw;
         const uint64_t b0 = c * 4096;
         if (c < nfull) {
             const uint4* c8 = reinterpret_cast<const uint4*>(codes + b0);
@@ -255,12 +261,15 @@ __global__ void __launch_bounds__(HIST_THREADS) hist_flagged_kernel(const uint16
         } else {
             for (uint64_t t = b0 + lane; t < n; t += 32) put(codes[t]);
         }
+        }
     }
     if (cnt) {
         if (cur < nbins) atomicAdd(mine + cur, cnt);
         else bad = true;
     }
     if (bad) set_err(status, FZB_ERR_CODE_RANGE);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) nr += __shfl_xor_sync(0xffffffffu, nr, o);   // one atomic per warp
     if (lane == 0 && nr) atomicAdd(out + R, nr);
     __syncthreads();
     for (uint32_t q = threadIdx.x; q < nbins; q += blockDim.x) {
