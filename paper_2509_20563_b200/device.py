@@ -84,6 +84,13 @@ def _interp_nk(n0, n1, n2, stride):
     return 1 + levels * (3 if n0 > 1 else 1)
 
 
+def _lz_decode_nk(n0, n1, n2):
+    """Kernels one fzb_lorenzo_decode_f32 call launches: 1D = event count, a
+    3-kernel scan, compact, chain, fill; 2D/3D = prep, tile order, the
+    wavefront (+ face clear and scan on a layout change)."""
+    return 7 if sum(d > 1 for d in (n0, n1, n2)) <= 1 else 5
+
+
 def _hf_decode_nk(nbytes, n):
     """Kernels one fzb_huffman_decode call launches: tables, 3 sweeps, the
     cooperative sweep, a 3-kernel scan, the write pass, the final check, and
@@ -380,7 +387,7 @@ class Engine:
             out = self.buf("hfout" + tag, cap)
             hws = self.buf("hews" + tag, L.fzb_huffman_encode_workspace_bytes(n))
             self._call("fzb_huffman_encode_chunks", _p(codes), n, _p(lengths), _p(cw), nsym, _p(bitcount), _p(notr),
-                       _p(out), cap, _p(hws), hws.numel(), _p(status), sp, nk=5)
+                       _p(out), cap, _p(hws), hws.numel(), _p(status), sp, nk=8)
             bufs.update(lengths=lengths, bitcount=bitcount, hfout=out)
         elif codec == "bitshuffle":
             self._mark("primary")
@@ -552,7 +559,7 @@ class Engine:
         else:
             lzws = self.buf("dlzws" + tag, L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
             self._call("fzb_lorenzo_decode_f32", _p(codes), _p(bitmap), _p(out), n0, n1, n2, _p(ebt), da.radius,
-                       _p(lzws), lzws.numel(), sp, nk=5)
+                       _p(lzws), lzws.numel(), sp, nk=_lz_decode_nk(n0, n1, n2))
         return out
 
     # ------------------------------------------------------------- graphs
@@ -772,7 +779,7 @@ class Engine:
         else:
             lzws = self.buf("dlzws" + tag, L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
             self._call("fzb_lorenzo_decode_f32", _p(codes), _p(bitmap), _p(recon), n0, n1, n2, _p(ebt), radius,
-                       _p(lzws), lzws.numel(), sp, nk=5)
+                       _p(lzws), lzws.numel(), sp, nk=_lz_decode_nk(n0, n1, n2))
         return recon
 
     def decompress_dag(self, codec: str, predictor: str, segs: dict, idx: np.ndarray, vals: np.ndarray,
@@ -829,7 +836,7 @@ class Engine:
         else:
             lzws = self.buf("dlzws", L.fzb_lorenzo_workspace_bytes(n0, n1, n2), zero_new=True)
             self._call("fzb_lorenzo_decode_f32", _p(codes), _p(bitmap), _p(recon), n0, n1, n2, _p(ebt), radius,
-                       _p(lzws), lzws.numel(), sp, nk=5)
+                       _p(lzws), lzws.numel(), sp, nk=_lz_decode_nk(n0, n1, n2))
         return recon
 
     def decompress_dag_graphed(self, codec: str, predictor: str, segs: dict, idx, vals, anchors, dims,
