@@ -1540,13 +1540,15 @@ __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_
     }
     if (threadIdx.x == 0) T = *Tg;
     __syncthreads();
-    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= nsub) return;
+    // persistent: the 40 KB LUT is staged once per CTA, not once per 128
+    // subsequences (C4: 8.6K CTAs had moved 343 MB from L2 into shared memory)
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nsub;
+         t += (uint64_t)gridDim.x * blockDim.x) {
     const unsigned long long o = offs[t];
     const uint32_t c0 = cnt[t];
     const uint32_t er = err[t];
     if (er && o + c0 < n) atomicMin(best, (t << 2) | er);
-    if (o >= n) return;
+    if (o >= n) continue;
     uint32_t todo = (uint32_t)min((unsigned long long)c0, n - o);   // symbols this thread emits
     const bool last = todo && o + todo == n;   // emits symbol n-1: records where it ends
     BitReaderP r;
@@ -1621,6 +1623,7 @@ __global__ void __launch_bounds__(HD_THREADS) hf_write_dec2_kernel(const uint32_
     }
     if (p > from) put_chunk(out, base, lo, hi, from, p);
     if (last) *end_pos = r.pos;
+    }
 }
 
 // Remaining stream checks of encode.py:299-316 (one thread).
@@ -1829,7 +1832,9 @@ FZB_API int fzb_huffman_decode(const uint8_t* d_stream, uint64_t nbytes, uint64_
     // against one coalesced pass over the output
     const bool prefill = total_bits * 8 <= 9ull * n;
     if (prefill) hf_prefill_kernel<<<kNumSMs * 8, 256, 0, st>>>(lut_s, lut_m, n, d_codes);
-    hf_write_dec2_kernel<<<blocks, HD_THREADS, 0, st>>>(words, total_bits, nsub, T, lut_s, lut_m, sym_sorted,
+    const uint64_t wgrid = (uint64_t)kNumSMs * 16;   // dense streams keep one pass per thread
+    hf_write_dec2_kernel<<<(unsigned)(blocks < wgrid ? blocks : wgrid), HD_THREADS, 0, st>>>(
+                                                        words, total_bits, nsub, T, lut_s, lut_m, sym_sorted,
                                                         st_[fin], cn_[fin], er_[fin], offs, n, d_codes, scal + 1,
                                                         scal + 4, prefill);
     hf_final2_kernel<<<1, 1, 0, st>>>(n, nbytes, d_stream, scal, scal + 1, scal + 4, d_status);
